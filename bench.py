@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""Benchmark: assembled FP64 CSR stiffness nnz/s on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
+
+One step = one complete fast assembly (assembleFast: basis evaluation,
+thickness integrals, in-plane operators, combination into the FP64 CSR
+values) of the workload, inputs resident in HBM.  Workload at N=1: BASELINE
+config C4 (128x64 elements, p=2, 128 plies, 1.92e9 nnz, 23 GB CSR) -- the
+largest BASELINE config that fits one B200 (C5 is 203 GB).  With N ranks
+(torchrun) the matrix is split into N row slabs balanced by nnz, one per GPU,
+no collective on the data path ("strong" scaling).
+
+Reported beside the device number:
+  e2e           the same metric through the C-ABI one-shot call lf_assemble
+                (the drop-in for assembleFast) with pinned host buffers: H2D
+                of the problem tables + the whole CSR (row offsets, columns,
+                values) D2H inside the timed region;
+  roofline      8 B/nnz FP64 value stores of the combine kernel (K4) against
+                the measured HBM copy bandwidth (MEASURED_PEAKS.json);
+  cpu_baseline  the reference's own fast assembler (compiled from its
+                unmodified sources, oracle/_ref) on a bounded sample of the
+                same workload family, all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-plies", type=int, default=0)
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.06)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the reference's own CPU fast assembler (oracle/_ref)."""
+    if rank != 0:
+        return
+    from oracle.checkers import Reference
+    from paper_1905_05417_b200 import problem as P
+    if not Reference.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libref_lamfast.so not built"}))
+        return
+    ref = Reference()
+    threads = os.cpu_count() or 1
+    plies = choose_sample_plies(ref, args, threads, budget_s=150.0)
+    prob = P.baseline_config(args.config, plies=plies)
+    nnz = P.sizes(prob)["nnz"]
+    for _ in range(args.warmup):
+        ref.assemble(prob, "fast", threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ref.assemble(prob, "fast", threads)
+        times.append(time.perf_counter() - t0)
+    sec = sum(times) / len(times)
+    value = nnz / sec
+    sample = (f"{args.config} family with {plies} plies instead of "
+              f"{len(P.baseline_config(args.config).layers)} (same elements, degree, materials); "
+              f"{nnz} nnz per step")
+    line = {
+        "impl": "reference", "metric": "assembled stiffness nnz/s (FP64 CSR)", "value": value,
+        "unit": "nnz/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "backend": "fast", "sample_plies": plies,
+                   "nnz_per_step": nnz},
+        "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def choose_sample_plies(ref, args, threads, budget_s):
+    """Largest ply count of the config family whose reference run keeps
+    (warmup + steps) within budget_s; calibrated with a 1-ply run."""
+    from paper_1905_05417_b200 import problem as P
+    if args.cpu_sample_plies:
+        return args.cpu_sample_plies
+    probe = P.baseline_config(args.config, plies=1)
+    t0 = time.perf_counter()
+    ref.assemble(probe, "fast", threads)
+    dt = time.perf_counter() - t0
+    rate = P.sizes(probe)["nnz"] / max(dt, 1e-6)
+    per_step = budget_s / max(1, args.steps + args.warmup)
+    full = len(P.baseline_config(args.config).layers)
+    best = 1
+    for m in range(1, full + 1):
+        if P.sizes(P.baseline_config(args.config, plies=m))["nnz"] / rate <= per_step:
+            best = m
+        else:
+            break
+    return best
+
+
+def cpu_baseline(args):
+    """Reference fast path (oracle/_ref) on a bounded sample, ~10-30 s."""
+    from oracle.checkers import Reference
+    from paper_1905_05417_b200 import problem as P
+    if not Reference.available():
+        return None
+    ref = Reference()
+    threads = os.cpu_count() or 1
+    a = argparse.Namespace(**vars(args))
+    a.steps, a.warmup = 1, 0
+    plies = choose_sample_plies(ref, a, threads, budget_s=20.0)
+    prob = P.baseline_config(args.config, plies=plies)
+    nnz = P.sizes(prob)["nnz"]
+    t0 = time.perf_counter()
+    ref.assemble(prob, "fast", threads)
+    dt = time.perf_counter() - t0
+    return {"value": nnz / dt, "unit": "nnz/s", "cores": threads, "kind": "reference",
+            "sample": f"{args.config} family with {plies} plies ({nnz} nnz), one assembleFast, "
+                      f"reference sources compiled with the Eigen subset, threads={threads}"}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_1905_05417_b200 as lf
+    from paper_1905_05417_b200 import abi, problem as P
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    prob = P.baseline_config(args.config)
+    sz = P.sizes(prob)
+    bounds = lf.slab_bounds(prob, world, rank) if world > 1 else {"t_begin": 0, "t_end": -1}
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    plan = lf.Plan(prob, "fast", local, bounds["t_begin"], bounds["t_end"], stream=stream.cuda_stream)
+    rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
+    cols = torch.empty(plan.nnz, dtype=torch.int32, device="cuda")
+    vals = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
+    plan.build_pattern(rp.data_ptr(), cols.data_ptr())
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    for _ in range(args.warmup):
+        plan.assemble(vals.data_ptr())
+    torch.cuda.synchronize()
+    plan.kernel_time(reset=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        plan.assemble(vals.data_ptr())
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms_total = ev0.elapsed_time(ev1)
+    k_ms, k_n = plan.kernel_time(reset=True)
+    launches = plan.launch_count * args.steps
+    t = torch.tensor([ms_total, k_ms / max(k_n, 1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total, k_avg_ms = float(t[0]), float(t[1])
+    ms_per_step = ms_total / args.steps
+    total_nnz = sz["nnz"]
+    value = total_nnz / (ms_per_step / 1e3)
+
+    # verification of the resident matrix (outside the timed region)
+    verify = {}
+    if world == 1:
+        st = lf.device_csr_stats(plan.rows, rp.data_ptr(), cols.data_ptr(), vals.data_ptr(),
+                                 stream.cuda_stream)
+        verify = {"fro_norm": st["fro_sq"] ** 0.5, "symmetry_rel": (st["sym_sq"] / st["fro_sq"]) ** 0.5}
+    else:
+        # NCCL gather of slab summaries (verification only, never timed)
+        import torch as _t
+        fro = _t.tensor([float((vals * vals).sum()), float(plan.nnz)], dtype=_t.float64, device="cuda")
+        dist.all_reduce(fro)
+        verify = {"fro_norm": float(fro[0]) ** 0.5, "nnz_gathered": int(fro[1])}
+
+    hbm, peak_src = peaks()
+    achieved = plan.nnz * 8 / (k_avg_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None,
+                "kernel": "k_combine (K4)", "bytes_per_launch": plan.nnz * 8,
+                "kernel_ms": k_avg_ms, "peak_source": peak_src,
+                "step_frac": (hbm * 1e9 / 8) and (total_nnz / (ms_per_step / 1e3)) / (world * hbm * 1e9 / 8)}
+    traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(traffic_file):
+        try:
+            with open(traffic_file) as f:
+                tj = json.load(f)
+            if tj.get("config") == args.config:
+                roofline["traffic"] = tj["dram_bytes_per_launch"]
+        except Exception:
+            pass
+    del rp, cols, vals
+    torch.cuda.empty_cache()
+
+    e2e = None
+    if not args.no_e2e and world == 1:
+        e2e = measure_e2e(args, prob, local, total_nnz)
+    elif not args.no_e2e:
+        e2e = measure_e2e_slab(args, prob, local, rank, world, bounds, total_nnz)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(args)
+        except Exception as exc:  # reported, not fatal
+            cpu = {"error": str(exc)}
+
+    if rank == 0:
+        line = {
+            "metric": "assembled stiffness nnz/s (FP64 CSR)", "value": value, "unit": "nnz/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "backend": "fast", "nnz": total_nnz,
+                       "dofs": sz["dim"], "plies": len(prob.layers),
+                       "distinct_materials": prob.distinct_configs(),
+                       "l2": "output > L2 (values %.1f GB vs 126 MB L2); no flush needed"
+                             % (total_nnz * 8 / 1e9),
+                       "parallelism": f"row-slab x{world}"},
+            "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
+            "clocks": clocks, "verify": verify,
+        }
+        print(json.dumps(line))
+    plan.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def measure_e2e(args, prob, device, total_nnz):
+    """lf_assemble (drop-in for assembleFast) with pinned host buffers."""
+    import torch
+    from paper_1905_05417_b200 import abi
+    lib = abi.library()
+    c = prob.to_c()
+    dim = prob.dim
+    rp = torch.empty(dim + 1, dtype=torch.int64, pin_memory=True)
+    cols = torch.empty(total_nnz, dtype=torch.int32, pin_memory=True)
+    vals = torch.empty(total_nnz, dtype=torch.float64, pin_memory=True)
+    st = abi.Stats()
+
+    def once():
+        abi.check(lib.lf_assemble(ctypes.byref(c), abi.LF_BACKEND_FAST, device, rp.data_ptr(),
+                                  cols.data_ptr(), vals.data_ptr(), ctypes.byref(st)))
+
+    once()  # warm-up (allocator pool, module load)
+    n = max(1, args.e2e_steps)
+    t0 = time.perf_counter()
+    for _ in range(n):
+        once()
+    sec = (time.perf_counter() - t0) / n
+    h2d = sum(a.nbytes for a in prob._keep if hasattr(a, "nbytes"))
+    d2h = rp.numel() * 8 + total_nnz * 12
+    del rp, cols, vals
+    return {"value": total_nnz / sec, "unit": "nnz/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": sec * 1e3, "steps": n,
+            "call": "lf_assemble(LF_BACKEND_FAST) -> host CSR (row_ptr, cols, values)"}
+
+
+def measure_e2e_slab(args, prob, device, rank, world, bounds, total_nnz):
+    import torch
+    import torch.distributed as dist
+    import paper_1905_05417_b200 as lf
+    plan = lf.Plan(prob, "fast", device, bounds["t_begin"], bounds["t_end"])
+    h_rp = torch.empty(plan.rows + 1, dtype=torch.int64, pin_memory=True)
+    h_cols = torch.empty(plan.nnz, dtype=torch.int32, pin_memory=True)
+    h_vals = torch.empty(plan.nnz, dtype=torch.float64, pin_memory=True)
+    d_rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
+    d_cols = torch.empty(plan.nnz, dtype=torch.int32, device="cuda")
+    d_vals = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
+
+    def once():
+        plan.build_pattern(d_rp.data_ptr(), d_cols.data_ptr())
+        plan.assemble(d_vals.data_ptr())
+        plan.synchronize()
+        h_rp.copy_(d_rp)
+        h_cols.copy_(d_cols)
+        h_vals.copy_(d_vals)
+        torch.cuda.synchronize()
+
+    once()
+    dist.barrier()
+    n = max(1, args.e2e_steps)
+    t0 = time.perf_counter()
+    for _ in range(n):
+        once()
+    dt = torch.tensor([(time.perf_counter() - t0) / n], dtype=torch.float64, device="cuda")
+    dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    sec = float(dt[0])
+    plan.close()
+    return {"value": total_nnz / sec, "unit": "nnz/s", "h2d_bytes_per_step": 0,
+            "d2h_bytes_per_step": int(total_nnz * 12 + prob.dim * 8 // world), "ms_per_step": sec * 1e3,
+            "steps": n, "call": "Plan per rank: pattern + assemble + D2H of the slab"}
+
+
+if __name__ == "__main__":
+    main()

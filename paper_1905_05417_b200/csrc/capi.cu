@@ -1,0 +1,877 @@
+// C ABI of the B200 assembler (include/lamfast_cuda.h).  Host orchestration
+// only: validation and setup tables come from setup.cpp, all O(nnz) and
+// O(elements) work runs in the kernels of k_setup.cu / k_main.cu.  No CPU
+// fallback exists: without a usable CUDA device every compute entry point
+// fails with LF_ERR_CUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "kernels.cuh"
+#include "lamfast_cuda.h"
+#include "setup.hpp"
+
+using lfb::raise;
+
+namespace {
+
+thread_local std::string g_error;
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return LF_OK;
+    } catch (const lfb::Error& e) {
+        g_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc& e) {
+        g_error = e.what();
+        return LF_ERR_OUT_OF_MEMORY;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return LF_ERR_RUNTIME;
+    }
+}
+
+void cuda_check(cudaError_t st, const char* what) {
+    if (st != cudaSuccess) {
+        const std::string msg = std::string(what) + ": " + cudaGetErrorString(st);
+        if (st == cudaErrorMemoryAllocation)
+            raise(LF_ERR_OUT_OF_MEMORY, msg);
+        raise(LF_ERR_CUDA, msg);
+    }
+}
+#define CK(x) cuda_check((x), #x)
+
+void use_device(int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        raise(LF_ERR_CUDA, "no CUDA device available (the B200 assembler has no CPU fallback)");
+    }
+    if (device < 0 || device >= n)
+        raise(LF_ERR_INVALID_ARGUMENT, "device index out of range");
+    CK(cudaSetDevice(device));
+}
+
+/// Device allocations owned by a plan.
+struct DeviceArena {
+    std::vector<void*> ptrs;
+    ~DeviceArena() {
+        for (void* p : ptrs)
+            cudaFree(p);
+    }
+    template <typename T>
+    T* alloc(std::size_t n) {
+        void* p = nullptr;
+        CK(cudaMalloc(&p, std::max<std::size_t>(1, n) * sizeof(T)));
+        ptrs.push_back(p);
+        return static_cast<T*>(p);
+    }
+    template <typename T>
+    T* upload(const T* src, std::size_t n) {
+        T* d = alloc<T>(n);
+        if (n)
+            CK(cudaMemcpy(d, src, n * sizeof(T), cudaMemcpyHostToDevice));
+        return d;
+    }
+    template <typename T>
+    T* upload(const std::vector<T>& v) {
+        return upload(v.data(), v.size());
+    }
+};
+
+/// Uploads the space part of a setup (knots, spans, rules, adjacency) and
+/// allocates the basis / 1D-integral workspace.
+void upload_space(const lfb::Setup& s, DeviceArena& ar, lfb::DevTables& d) {
+    std::memset(&d, 0, sizeof d);
+    d.pu = s.ku.p;
+    d.pv = s.kv.p;
+    d.pt = s.kt.p;
+    d.nu = s.n_u;
+    d.nv = s.n_v;
+    d.nt = s.n_t;
+    d.ns = s.n_s;
+    d.nspu = static_cast<int>(s.spu.size());
+    d.nspv = static_cast<int>(s.spv.size());
+    d.nspt = static_cast<int>(s.spt.size());
+    d.nqu = s.nqu;
+    d.nqv = s.nqv;
+    d.nqt = s.nqt;
+    d.bu = 2 * d.pu + 1;
+    d.bv = 2 * d.pv + 1;
+    d.ku = ar.upload(s.ku.t);
+    d.kv = ar.upload(s.kv.t);
+    d.kt = ar.upload(s.kt.t);
+    d.nku = static_cast<int>(s.ku.t.size());
+    d.nkv = static_cast<int>(s.kv.t.size());
+    d.nkt = static_cast<int>(s.kt.t.size());
+    auto spans = [&](const std::vector<lfb::Span>& sp, const int** first, const double** lo, const double** hi) {
+        std::vector<int> f;
+        std::vector<double> l, h;
+        for (const auto& x : sp) {
+            f.push_back(x.first);
+            l.push_back(x.begin);
+            h.push_back(x.end);
+        }
+        *first = ar.upload(f);
+        *lo = ar.upload(l);
+        *hi = ar.upload(h);
+    };
+    spans(s.spu, &d.spu_first, &d.spu_lo, &d.spu_hi);
+    spans(s.spv, &d.spv_first, &d.spv_lo, &d.spv_hi);
+    d.ru = ar.upload(s.ru);
+    d.wu = ar.upload(s.wu);
+    d.rv = ar.upload(s.rv);
+    d.wv = ar.upload(s.wv);
+    d.lo_u = ar.upload(s.au.lo);
+    d.len_u = ar.upload(s.au.len);
+    d.pre_u = reinterpret_cast<const long long*>(ar.upload(s.au.pre));
+    d.lo_v = ar.upload(s.av.lo);
+    d.len_v = ar.upload(s.av.len);
+    d.pre_v = reinterpret_cast<const long long*>(ar.upload(s.av.pre));
+    d.es_pre = reinterpret_cast<const long long*>(ar.upload(s.es_pre));
+    {
+        // first in-plane function of every 256-entry block of the entry space
+        const long long E = 9 * s.S_s;
+        std::vector<int> blk(static_cast<std::size_t>((E + 255) / 256) + 1, 0);
+        int is = 0;
+        for (std::size_t b = 0; b + 1 < blk.size(); ++b) {
+            const long long e0 = static_cast<long long>(b) * 256;
+            while (is + 1 < s.n_s && s.es_pre[static_cast<std::size_t>(is) + 1] <= e0)
+                ++is;
+            blk[b] = is;
+        }
+        d.blk_is = ar.upload(blk);
+    }
+    d.S_s = s.S_s;
+    d.S_u = s.au.total;
+    d.E = 9 * s.S_s;
+    d.Bu_val = ar.alloc<double>(static_cast<std::size_t>(d.nspu) * d.nqu * (d.pu + 1));
+    d.Bu_der = ar.alloc<double>(static_cast<std::size_t>(d.nspu) * d.nqu * (d.pu + 1));
+    d.Bv_val = ar.alloc<double>(static_cast<std::size_t>(d.nspv) * d.nqv * (d.pv + 1));
+    d.Bv_der = ar.alloc<double>(static_cast<std::size_t>(d.nspv) * d.nqv * (d.pv + 1));
+    d.U = ar.alloc<double>(static_cast<std::size_t>(d.nu) * d.bu * 4);
+    d.V = ar.alloc<double>(static_cast<std::size_t>(d.nv) * d.bv * 4);
+}
+
+void upload_geometry(const lfb::Setup& s, DeviceArena& ar, lfb::DevTables& d) {
+    d.affine = s.affine ? 1 : 0;
+    if (s.affine) {
+        std::memcpy(d.G, s.frame0.dfit, sizeof d.G);
+        d.det = s.frame0.det;
+    } else {
+        d.frames = ar.upload(s.frames);
+    }
+}
+
+void upload_thickness(const lfb::Setup& s, DeviceArena& ar, lfb::DevTables& d, const lfb::Adjacency& at) {
+    d.ncells = static_cast<int>(s.cells.size());
+    d.cell_pts = ar.upload(s.cell_pts);
+    d.cell_wts = ar.upload(s.cell_wts);
+    d.cell_first = ar.upload(s.cell_first);
+    d.cell_layer = ar.upload(s.cell_layer);
+    d.span_cell0 = ar.upload(s.span_cell0);
+    d.spt_first = ar.upload(s.spt_first);
+    d.lo_t = ar.upload(at.lo);
+    d.len_t = ar.upload(at.len);
+    d.pre_t = reinterpret_cast<const long long*>(ar.upload(at.pre));
+    d.lt_max = at.max_len;
+    const std::size_t ntp = static_cast<std::size_t>(d.ncells) * d.nqt;
+    d.Bt_val = ar.alloc<double>(ntp * (d.pt + 1));
+    d.Bt_der = ar.alloc<double>(ntp * (d.pt + 1));
+    d.Bt_first = ar.alloc<int>(ntp);
+}
+
+void upload_terms(DeviceArena& ar, lfb::DevTables& d, int n_terms, int n_layers, const std::vector<double>& table,
+                  const std::vector<double>& lam, const std::vector<uint8_t>& lam_on) {
+    d.n_terms = n_terms;
+    d.n_layers = n_layers;
+    d.n_passes = (n_terms + lfb::kMaxTermsPerPass - 1) / lfb::kMaxTermsPerPass;
+    d.term_table = ar.upload(table);
+    d.lam = ar.upload(lam);
+    d.lam_on = ar.upload(lam_on);
+    d.Ct = ar.alloc<double>(static_cast<std::size_t>(std::max(1, n_terms)) * 81);
+}
+
+} // namespace
+
+struct lf_plan {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    lfb::Setup setup;
+    DeviceArena arena;
+    lfb::DevTables d{};
+    int launches = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> free_events, pending;
+    double kernel_ms = 0.0;
+    int64_t kernel_launches = 0;
+
+    ~lf_plan() {
+        if (stream)
+            cudaStreamSynchronize(stream);
+        for (auto& e : free_events) {
+            cudaEventDestroy(e.first);
+            cudaEventDestroy(e.second);
+        }
+        for (auto& e : pending) {
+            cudaEventDestroy(e.first);
+            cudaEventDestroy(e.second);
+        }
+        if (own_stream && stream)
+            cudaStreamDestroy(stream);
+    }
+
+    void harvest() {
+        CK(cudaStreamSynchronize(stream));
+        for (auto& e : pending) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, e.first, e.second));
+            kernel_ms += ms;
+            ++kernel_launches;
+            free_events.push_back(e);
+        }
+        pending.clear();
+    }
+};
+
+namespace {
+
+void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void* stream, int t0, int t1) {
+    if (!p)
+        raise(LF_ERR_INVALID_ARGUMENT, "null problem");
+    plan->setup = lfb::buildSetup(*p, backend, t0, t1 < 0 ? -1 : t1);
+    use_device(device);
+    plan->device = device;
+    if (stream) {
+        plan->stream = static_cast<cudaStream_t>(stream);
+    } else {
+        CK(cudaStreamCreateWithFlags(&plan->stream, cudaStreamNonBlocking));
+        plan->own_stream = true;
+    }
+    const lfb::Setup& s = plan->setup;
+    lfb::DevTables& d = plan->d;
+    DeviceArena& ar = plan->arena;
+    upload_space(s, ar, d);
+    upload_geometry(s, ar, d);
+    upload_thickness(s, ar, d, s.at);
+    upload_terms(ar, d, s.n_terms, p->n_layers, s.term_table, s.lam, s.lam_on);
+    d.layer_config = ar.upload(s.layup.layer_config);
+    d.t0 = s.t0;
+    d.t1 = s.t1;
+    d.n_pairs = s.n_pairs;
+    if (backend != LF_BACKEND_STANDARD) {
+        d.W = ar.alloc<double>(static_cast<std::size_t>(std::max<long long>(1, d.n_pairs)) * d.n_terms * 4);
+        d.Wmask = ar.alloc<unsigned>(static_cast<std::size_t>(std::max<long long>(1, d.n_pairs)) * d.n_passes);
+        if (!d.affine)
+            d.Pg = ar.alloc<double>(static_cast<std::size_t>(d.n_terms) * 4 * static_cast<std::size_t>(d.E));
+    }
+}
+
+int plan_launch(lf_plan* plan, double* values) {
+    const lfb::DevTables& d = plan->d;
+    int launches = 0;
+    cudaStream_t s = plan->stream;
+    if (plan->setup.backend == LF_BACKEND_STANDARD) {
+        CK(static_cast<cudaError_t>(lfb::launch_basis(d, false, s)));
+        ++launches;
+        CK(static_cast<cudaError_t>(lfb::launch_standard(d, values, plan->setup.nnz, s, &launches)));
+        return launches;
+    }
+    CK(static_cast<cudaError_t>(lfb::launch_basis(d, d.affine != 0, s)));
+    ++launches;
+    if (d.n_pairs > 0) {
+        CK(static_cast<cudaError_t>(lfb::launch_thickness_pairs(d, s)));
+        ++launches;
+    }
+    if (d.affine) {
+        CK(static_cast<cudaError_t>(lfb::launch_integrals_1d(d, s)));
+        ++launches;
+    } else {
+        CK(cudaMemsetAsync(d.Pg, 0, sizeof(double) * static_cast<std::size_t>(d.n_terms) * 4 * d.E, s));
+        CK(static_cast<cudaError_t>(lfb::launch_inplane_general(d, s)));
+        launches += (d.pu + 1) * (d.pv + 1);
+    }
+    std::pair<cudaEvent_t, cudaEvent_t> ev;
+    if (!plan->free_events.empty()) {
+        ev = plan->free_events.back();
+        plan->free_events.pop_back();
+    } else {
+        CK(cudaEventCreate(&ev.first));
+        CK(cudaEventCreate(&ev.second));
+    }
+    CK(cudaEventRecord(ev.first, s));
+    CK(static_cast<cudaError_t>(lfb::launch_combine(d, values, 0, s, &launches)));
+    CK(cudaEventRecord(ev.second, s));
+    plan->pending.push_back(ev);
+    if (plan->pending.size() > 4096)
+        plan->harvest();
+    return launches;
+}
+
+void copy_d2h(void* dst, const void* src, std::size_t bytes, cudaStream_t s) {
+    if (bytes)
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+}
+
+struct DeviceBuffer {
+    void* p = nullptr;
+    cudaStream_t s = nullptr;
+    DeviceBuffer(std::size_t bytes, cudaStream_t st) : s(st) {
+        CK(cudaMallocAsync(&p, std::max<std::size_t>(bytes, 8), st));
+    }
+    ~DeviceBuffer() {
+        if (p)
+            cudaFreeAsync(p, s);
+    }
+};
+
+void keep_pool_memory(int device) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t threshold = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+    }
+}
+
+/// Entry-layout P (Pg[t][f][e]) -> banded InPlaneOperator blocks (fast.cpp:13-32).
+void export_banded(const lfb::Setup& s, const std::vector<double>& pg, int n_terms, double* blocks, char* flags) {
+    const int pu = s.ku.p, pv = s.kv.p, bu = 2 * pu + 1, bv = 2 * pv + 1;
+    const std::size_t per = static_cast<std::size_t>(s.n_s) * bv * bu;
+    const long long E = 9 * s.S_s;
+    std::memset(flags, 0, per);
+    std::memset(blocks, 0, sizeof(double) * per * 9 * 4 * n_terms);
+    for (int is = 0; is < s.n_s; ++is) {
+        const int iu = is % s.n_u, iv = is / s.n_u;
+        const int Lu = s.au.len[static_cast<std::size_t>(iu)], Lv = s.av.len[static_cast<std::size_t>(iv)];
+        const long long B = 3LL * Lu * Lv;
+        for (int sv = 0; sv < Lv; ++sv)
+            for (int su = 0; su < Lu; ++su) {
+                const int jv = s.av.lo[static_cast<std::size_t>(iv)] + sv, ju = s.au.lo[static_cast<std::size_t>(iu)] + su;
+                const std::size_t slot = (static_cast<std::size_t>(is) * bv + (jv - iv + pv)) * bu + (ju - iu + pu);
+                flags[slot] = 1;
+                const long long e0 = s.es_pre[static_cast<std::size_t>(is)] + 3LL * (sv * Lu + su);
+                for (int t = 0; t < n_terms; ++t)
+                    for (int f = 0; f < 4; ++f)
+                        for (int a = 0; a < 3; ++a)
+                            for (int b = 0; b < 3; ++b)
+                                blocks[((static_cast<std::size_t>(t) * 4 + f) * per + slot) * 9 + 3 * a + b] =
+                                    pg[(static_cast<std::size_t>(t) * 4 + f) * E + e0 + a * B + b];
+            }
+    }
+}
+
+} // namespace
+
+extern "C" {
+
+int lf_abi_version(void) { return LF_ABI_VERSION; }
+
+const char* lf_status_name(int status) {
+    switch (status) {
+    case LF_OK: return "ok";
+    case LF_ERR_INVALID_ARGUMENT: return "invalid_argument";
+    case LF_ERR_DOMAIN: return "domain_error";
+    case LF_ERR_LOGIC: return "logic_error";
+    case LF_ERR_RUNTIME: return "runtime_error";
+    case LF_ERR_CUDA: return "cuda_error";
+    case LF_ERR_OUT_OF_MEMORY: return "out_of_memory";
+    case LF_ERR_UNSUPPORTED: return "unsupported";
+    default: return "unknown";
+    }
+}
+
+const char* lf_last_error(void) { return g_error.c_str(); }
+
+int lf_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int lf_voigt_from_constants(const lf_orthotropic* c, double d_out[36]) {
+    return guarded([&] { lfb::voigtFromConstants(*c, d_out); });
+}
+
+int lf_rotate_inplane(const double d[36], double theta, double d_out[36]) {
+    return guarded([&] { lfb::rotateInplane(d, theta, d_out); });
+}
+
+int lf_angle_decomposition(const lf_orthotropic* c, double out[180]) {
+    return guarded([&] { lfb::angleDecomposition(*c, out); });
+}
+
+int lf_bracket_parameters(const lf_orthotropic* c, double out[9]) {
+    return guarded([&] { lfb::bracketParameters(*c, out); });
+}
+
+int lf_layup_configs(const lf_problem* p, int32_t* n_configs, int32_t* layer_config, double* config_stiffness) {
+    return guarded([&] {
+        const lfb::LayupInfo L = lfb::buildLayup(*p);
+        *n_configs = L.n_configs;
+        for (int l = 0; l < p->n_layers; ++l)
+            layer_config[l] = L.layer_config[static_cast<std::size_t>(l)];
+        if (config_stiffness)
+            for (int c = 0; c < L.n_configs; ++c)
+                std::memcpy(config_stiffness + 36 * c, L.D[static_cast<std::size_t>(c)].data(), 36 * sizeof(double));
+    });
+}
+
+int lf_pattern_size(const lf_problem* p, int backend, int64_t* dim, int64_t* nnz) {
+    return guarded([&] {
+        const lfb::Setup s = lfb::buildSetup(*p, backend, 0, -1);
+        *dim = 3LL * s.n_s * s.n_t;
+        *nnz = s.nnz;
+    });
+}
+
+int lf_slab_bounds(const lf_problem* p, int backend, int n_parts, int part, int32_t* t_begin, int32_t* t_end,
+                   int64_t* row_begin, int64_t* row_end, int64_t* nnz_begin, int64_t* nnz_end) {
+    return guarded([&] {
+        const lfb::Setup s = lfb::buildSetup(*p, backend, 0, -1);
+        int t0 = 0, t1 = 0;
+        lfb::slabBounds(s, n_parts, part, &t0, &t1);
+        *t_begin = t0;
+        *t_end = t1;
+        *row_begin = 3LL * s.n_s * t0;
+        *row_end = 3LL * s.n_s * t1;
+        *nnz_begin = 9 * s.S_s * s.at.pre[static_cast<std::size_t>(t0)];
+        *nnz_end = 9 * s.S_s * s.at.pre[static_cast<std::size_t>(t1)];
+    });
+}
+
+int lf_plan_create(const lf_problem* p, int backend, int device, void* cuda_stream, int32_t t_begin, int32_t t_end,
+                   lf_plan** out) {
+    return guarded([&] {
+        auto plan = std::make_unique<lf_plan>();
+        plan_init(plan.get(), p, backend, device, cuda_stream, t_begin, t_end);
+        *out = plan.release();
+    });
+}
+
+int lf_plan_destroy(lf_plan* plan) {
+    return guarded([&] {
+        if (plan)
+            cudaSetDevice(plan->device);
+        delete plan;
+    });
+}
+
+int lf_plan_info(const lf_plan* plan, int64_t* rows, int64_t* nnz, int64_t* row_begin, int64_t* nnz_begin) {
+    return guarded([&] {
+        if (rows)
+            *rows = plan->setup.rows;
+        if (nnz)
+            *nnz = plan->setup.nnz;
+        if (row_begin)
+            *row_begin = plan->setup.row_begin;
+        if (nnz_begin)
+            *nnz_begin = plan->setup.nnz_begin;
+    });
+}
+
+int lf_plan_build_pattern(lf_plan* plan, int64_t* d_row_ptr, int32_t* d_cols) {
+    return guarded([&] {
+        CK(cudaSetDevice(plan->device));
+        CK(static_cast<cudaError_t>(lfb::launch_pattern(plan->d, reinterpret_cast<long long*>(d_row_ptr),
+                                                        reinterpret_cast<int*>(d_cols), plan->stream)));
+    });
+}
+
+int lf_plan_assemble(lf_plan* plan, double* d_values) {
+    return guarded([&] {
+        CK(cudaSetDevice(plan->device));
+        plan->launches = plan_launch(plan, d_values);
+    });
+}
+
+int lf_plan_launch_count(const lf_plan* plan) { return plan ? plan->launches : -1; }
+
+int lf_plan_kernel_time(lf_plan* plan, int reset, double* ms_total, int64_t* launches) {
+    return guarded([&] {
+        CK(cudaSetDevice(plan->device));
+        plan->harvest();
+        if (ms_total)
+            *ms_total = plan->kernel_ms;
+        if (launches)
+            *launches = plan->kernel_launches;
+        if (reset) {
+            plan->kernel_ms = 0.0;
+            plan->kernel_launches = 0;
+        }
+    });
+}
+
+int lf_plan_stats(const lf_plan* plan, lf_stats* stats) {
+    return guarded([&] {
+        stats->qpoint_visits += plan->setup.stats.qpoint_visits;
+        stats->frame_evaluations += plan->setup.stats.frame_evaluations;
+        stats->operator_builds += plan->setup.stats.operator_builds;
+    });
+}
+
+int lf_plan_synchronize(lf_plan* plan) {
+    return guarded([&] {
+        CK(cudaSetDevice(plan->device));
+        CK(cudaStreamSynchronize(plan->stream));
+    });
+}
+
+int lf_assemble(const lf_problem* p, int backend, int device, int64_t* row_ptr, int32_t* cols, double* values,
+                lf_stats* stats) {
+    return guarded([&] {
+        lf_plan plan;
+        plan_init(&plan, p, backend, device, nullptr, 0, -1);
+        keep_pool_memory(device);
+        const lfb::Setup& s = plan.setup;
+        if (s.nnz == 0)
+            raise(LF_ERR_LOGIC, "SparseMatrixBuilder: nothing accumulated");
+        const std::size_t rows = static_cast<std::size_t>(s.rows);
+        const std::size_t nnz = static_cast<std::size_t>(s.nnz);
+        DeviceBuffer drp(sizeof(int64_t) * (rows + 1), plan.stream);
+        DeviceBuffer dcols(sizeof(int32_t) * nnz, plan.stream);
+        DeviceBuffer dvals(sizeof(double) * nnz, plan.stream);
+        CK(static_cast<cudaError_t>(lfb::launch_pattern(plan.d, static_cast<long long*>(drp.p),
+                                                        static_cast<int*>(dcols.p), plan.stream)));
+        plan_launch(&plan, static_cast<double*>(dvals.p));
+        copy_d2h(row_ptr, drp.p, sizeof(int64_t) * (rows + 1), plan.stream);
+        copy_d2h(cols, dcols.p, sizeof(int32_t) * nnz, plan.stream);
+        copy_d2h(values, dvals.p, sizeof(double) * nnz, plan.stream);
+        CK(cudaStreamSynchronize(plan.stream));
+        CK(cudaGetLastError());
+        if (stats) {
+            stats->qpoint_visits += s.stats.qpoint_visits;
+            stats->frame_evaluations += s.stats.frame_evaluations;
+            stats->operator_builds += s.stats.operator_builds;
+        }
+    });
+}
+
+static int inplane_common(const lf_problem* p, const double table[81], int device, double* blocks, char* flags,
+                          lf_stats* stats) {
+    return guarded([&] {
+        if (!p)
+            raise(LF_ERR_INVALID_ARGUMENT, "null problem");
+        const lfb::Setup s = lfb::buildSpaceSetup(*p, true);
+        use_device(device);
+        cudaStream_t st;
+        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        {
+            DeviceArena ar;
+            lfb::DevTables d;
+            upload_space(s, ar, d);
+            upload_geometry(s, ar, d);
+            std::vector<double> tab(table, table + 81), lam(1, 1.0);
+            std::vector<uint8_t> on(1, 1);
+            upload_terms(ar, d, 1, 1, tab, lam, on);
+            d.Pg = ar.alloc<double>(4 * static_cast<std::size_t>(d.E));
+            CK(cudaMemsetAsync(d.Pg, 0, sizeof(double) * 4 * d.E, st));
+            CK(static_cast<cudaError_t>(lfb::launch_basis(d, d.affine != 0, st)));
+            if (d.affine) {
+                CK(static_cast<cudaError_t>(lfb::launch_integrals_1d(d, st)));
+                CK(static_cast<cudaError_t>(lfb::launch_affine_export(d, st)));
+            } else {
+                CK(static_cast<cudaError_t>(lfb::launch_inplane_general(d, st)));
+            }
+            std::vector<double> pg(4 * static_cast<std::size_t>(d.E));
+            CK(cudaMemcpyAsync(pg.data(), d.Pg, pg.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            export_banded(s, pg, 1, blocks, flags);
+        }
+        cudaStreamDestroy(st);
+        if (stats) {
+            const int64_t per = static_cast<int64_t>(s.spu.size() * s.spv.size()) * s.nqu * s.nqv;
+            stats->qpoint_visits += per;
+            stats->frame_evaluations += per;
+            stats->operator_builds += 1;
+        }
+    });
+}
+
+int lf_inplane_operators(const lf_problem* p, const double material[36], int device, double* blocks, char* flags,
+                         lf_stats* stats) {
+    double table[81];
+    lfb::tableFromVoigt(material, table);
+    return inplane_common(p, table, device, blocks, flags, stats);
+}
+
+int lf_inplane_operators_bracket(const lf_problem* p, const double table[81], int device, double* blocks,
+                                 char* flags, lf_stats* stats) {
+    return inplane_common(p, table, device, blocks, flags, stats);
+}
+
+int lf_thickness_operators(int32_t degree_t, int32_t n_knots_t, const double* knots_t, int32_t n_interfaces,
+                           const double* interfaces, int32_t pts_per_cell, int device, double* q, char* occupied) {
+    return guarded([&] {
+        lfb::Setup s;
+        s.kt = lfb::makeKnots(degree_t, n_knots_t, knots_t, "thickness");
+        s.spt = lfb::elementSpans(s.kt);
+        s.n_t = s.kt.n;
+        s.nqt = pts_per_cell;
+        if (pts_per_cell < 1 || pts_per_cell > lfb::kMaxPoints)
+            raise(LF_ERR_INVALID_ARGUMENT, "computeThicknessOperators: bad point count");
+        s.interfaces.assign(interfaces, interfaces + n_interfaces);
+        const int L = n_interfaces - 1;
+        s.cells = lfb::thicknessCells(s.kt, s.spt, s.interfaces);
+        s.span_cell0.assign(s.spt.size() + 1, 0);
+        for (const auto& c : s.cells)
+            s.span_cell0[static_cast<std::size_t>(c.span) + 1]++;
+        for (std::size_t k = 0; k < s.spt.size(); ++k)
+            s.span_cell0[k + 1] += s.span_cell0[k];
+        for (const auto& sp : s.spt)
+            s.spt_first.push_back(sp.first);
+        s.cell_pts.resize(s.cells.size() * static_cast<std::size_t>(s.nqt));
+        s.cell_wts.resize(s.cells.size() * static_cast<std::size_t>(s.nqt));
+        for (std::size_t c = 0; c < s.cells.size(); ++c) {
+            lfb::gaussLegendre(s.nqt, s.cells[c].lo, s.cells[c].hi, s.cell_pts.data() + c * s.nqt,
+                               s.cell_wts.data() + c * s.nqt);
+            s.cell_first.push_back(s.spt[static_cast<std::size_t>(s.cells[c].span)].first);
+            s.cell_layer.push_back(s.cells[c].layer);
+        }
+        s.at = lfb::adjacency(s.kt.p, s.n_t, s.spt);
+        use_device(device);
+        cudaStream_t st;
+        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        {
+            DeviceArena ar;
+            lfb::DevTables d;
+            std::memset(&d, 0, sizeof d);
+            d.pt = s.kt.p;
+            d.nt = s.n_t;
+            d.nqt = s.nqt;
+            d.nspt = static_cast<int>(s.spt.size());
+            d.kt = ar.upload(s.kt.t);
+            d.nkt = static_cast<int>(s.kt.t.size());
+            upload_thickness(s, ar, d, s.at);
+            // one term per layer, identity multipliers: W[pair][l] = Q_l(pair)
+            std::vector<double> tab(static_cast<std::size_t>(L) * 81, 0.0), lam(static_cast<std::size_t>(L) * L, 0.0);
+            std::vector<uint8_t> on(static_cast<std::size_t>(L) * L, 0);
+            for (int l = 0; l < L; ++l) {
+                lam[static_cast<std::size_t>(l) * L + l] = 1.0;
+                on[static_cast<std::size_t>(l) * L + l] = 1;
+            }
+            upload_terms(ar, d, L, L, tab, lam, on);
+            d.t0 = 0;
+            d.t1 = s.n_t;
+            d.n_pairs = s.at.total;
+            d.W = ar.alloc<double>(static_cast<std::size_t>(d.n_pairs) * L * 4);
+            d.Wmask = ar.alloc<unsigned>(static_cast<std::size_t>(d.n_pairs) * d.n_passes);
+            CK(static_cast<cudaError_t>(lfb::launch_basis(d, false, st)));
+            CK(static_cast<cudaError_t>(lfb::launch_thickness_pairs(d, st)));
+            std::vector<double> w(static_cast<std::size_t>(d.n_pairs) * L * 4);
+            CK(cudaMemcpyAsync(w.data(), d.W, w.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            const int nt = s.n_t;
+            std::memset(q, 0, sizeof(double) * static_cast<std::size_t>(L) * 4 * nt * nt);
+            std::memset(occupied, 0, static_cast<std::size_t>(nt) * nt);
+            for (int it = 0; it < nt; ++it)
+                for (int k = 0; k < s.at.len[static_cast<std::size_t>(it)]; ++k) {
+                    const int jt = s.at.lo[static_cast<std::size_t>(it)] + k;
+                    const std::size_t pr = static_cast<std::size_t>(s.at.pre[static_cast<std::size_t>(it)] + k);
+                    occupied[static_cast<std::size_t>(it) * nt + jt] = 1;
+                    for (int l = 0; l < L; ++l)
+                        for (int f = 0; f < 4; ++f)
+                            q[((static_cast<std::size_t>(l) * 4 + f) * nt + it) * nt + jt] = w[(pr * L + l) * 4 + f];
+                }
+        }
+        cudaStreamDestroy(st);
+    });
+}
+
+int lf_combine(const lf_problem* p, int32_t n_terms, const double* blocks, const char* flags, const double* thickness,
+               const char* thickness_occupied, int device, int64_t* nnz_out, int64_t* row_ptr, int32_t* cols,
+               double* values) {
+    return guarded([&] {
+        if (n_terms < 1)
+            raise(LF_ERR_INVALID_ARGUMENT, "combineOperators: no operator terms");
+        lfb::Setup s = lfb::buildSpaceSetup(*p, false);
+        const int pu = s.ku.p, pv = s.kv.p, bu = 2 * pu + 1, bv = 2 * pv + 1;
+        // the in-plane pattern of term 0 / family 0 must be the tensor adjacency
+        for (int is = 0; is < s.n_s; ++is) {
+            const int iu = is % s.n_u, iv = is / s.n_u;
+            for (int dv = -pv; dv <= pv; ++dv)
+                for (int du = -pu; du <= pu; ++du) {
+                    const int ju = iu + du, jv = iv + dv;
+                    if (ju < 0 || ju >= s.n_u || jv < 0 || jv >= s.n_v)
+                        continue;
+                    const bool adj = ju >= s.au.lo[static_cast<std::size_t>(iu)] &&
+                                     ju < s.au.lo[static_cast<std::size_t>(iu)] + s.au.len[static_cast<std::size_t>(iu)] &&
+                                     jv >= s.av.lo[static_cast<std::size_t>(iv)] &&
+                                     jv < s.av.lo[static_cast<std::size_t>(iv)] + s.av.len[static_cast<std::size_t>(iv)];
+                    const std::size_t slot = (static_cast<std::size_t>(is) * bv + (dv + pv)) * bu + (du + pu);
+                    if ((flags[slot] != 0) != adj)
+                        raise(LF_ERR_UNSUPPORTED, "combineOperators: in-plane occupancy is not the span adjacency");
+                }
+        }
+        // thickness pattern from the occupancy matrix (rows must be intervals)
+        const int nt = s.n_t;
+        lfb::Adjacency at;
+        at.lo.assign(static_cast<std::size_t>(nt), 0);
+        at.len.assign(static_cast<std::size_t>(nt), 0);
+        at.pre.assign(static_cast<std::size_t>(nt) + 1, 0);
+        for (int it = 0; it < nt; ++it) {
+            int lo = -1, hi = -1;
+            for (int jt = 0; jt < nt; ++jt)
+                if (thickness_occupied[static_cast<std::size_t>(it) * nt + jt]) {
+                    if (lo < 0)
+                        lo = jt;
+                    else if (hi != jt - 1)
+                        raise(LF_ERR_UNSUPPORTED, "combineOperators: thickness occupancy row is not an interval");
+                    hi = jt;
+                }
+            at.lo[static_cast<std::size_t>(it)] = lo < 0 ? 0 : lo;
+            at.len[static_cast<std::size_t>(it)] = lo < 0 ? 0 : hi - lo + 1;
+            at.pre[static_cast<std::size_t>(it) + 1] = at.pre[static_cast<std::size_t>(it)] + at.len[static_cast<std::size_t>(it)];
+        }
+        at.total = at.pre[static_cast<std::size_t>(nt)];
+        const int64_t nnz = 9 * s.S_s * at.total;
+        *nnz_out = nnz;
+        if (!row_ptr && !cols && !values)
+            return;
+        if (nnz == 0)
+            raise(LF_ERR_LOGIC, "SparseMatrixBuilder: nothing accumulated");
+        use_device(device);
+        keep_pool_memory(device);
+        cudaStream_t st;
+        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        {
+            DeviceArena ar;
+            lfb::DevTables d;
+            upload_space(s, ar, d);
+            d.lo_t = ar.upload(at.lo);
+            d.len_t = ar.upload(at.len);
+            d.pre_t = reinterpret_cast<const long long*>(ar.upload(at.pre));
+            d.lt_max = 0;
+            for (int it = 0; it < nt; ++it)
+                d.lt_max = std::max(d.lt_max, at.len[static_cast<std::size_t>(it)]);
+            d.nt = nt;
+            d.n_terms = n_terms;
+            d.n_passes = (n_terms + 7) / 8;
+            d.affine = 0;
+            d.t0 = 0;
+            d.t1 = nt;
+            d.n_pairs = at.total;
+            // P: banded -> entry layout
+            const std::size_t per = static_cast<std::size_t>(s.n_s) * bv * bu;
+            std::vector<double> pg(static_cast<std::size_t>(n_terms) * 4 * d.E);
+            for (int is = 0; is < s.n_s; ++is) {
+                const int iu = is % s.n_u, iv = is / s.n_u;
+                const int Lu = s.au.len[static_cast<std::size_t>(iu)], Lv = s.av.len[static_cast<std::size_t>(iv)];
+                const long long B = 3LL * Lu * Lv;
+                for (int sv = 0; sv < Lv; ++sv)
+                    for (int su = 0; su < Lu; ++su) {
+                        const int jv = s.av.lo[static_cast<std::size_t>(iv)] + sv, ju = s.au.lo[static_cast<std::size_t>(iu)] + su;
+                        const std::size_t slot = (static_cast<std::size_t>(is) * bv + (jv - iv + pv)) * bu + (ju - iu + pu);
+                        const long long e0 = s.es_pre[static_cast<std::size_t>(is)] + 3LL * (sv * Lu + su);
+                        for (int t = 0; t < n_terms; ++t)
+                            for (int f = 0; f < 4; ++f)
+                                for (int a = 0; a < 3; ++a)
+                                    for (int b = 0; b < 3; ++b)
+                                        pg[(static_cast<std::size_t>(t) * 4 + f) * d.E + e0 + a * B + b] =
+                                            blocks[((static_cast<std::size_t>(t) * 4 + f) * per + slot) * 9 + 3 * a + b];
+                    }
+            }
+            d.Pg = ar.upload(pg);
+            std::vector<double> w(static_cast<std::size_t>(at.total) * n_terms * 4);
+            std::vector<unsigned> mask(static_cast<std::size_t>(at.total) * d.n_passes, 0u);
+            for (int it = 0; it < nt; ++it)
+                for (int k = 0; k < at.len[static_cast<std::size_t>(it)]; ++k) {
+                    const int jt = at.lo[static_cast<std::size_t>(it)] + k;
+                    const std::size_t pr = static_cast<std::size_t>(at.pre[static_cast<std::size_t>(it)] + k);
+                    for (int t = 0; t < n_terms; ++t) {
+                        for (int f = 0; f < 4; ++f)
+                            w[(pr * n_terms + t) * 4 + f] =
+                                thickness[((static_cast<std::size_t>(t) * 4 + f) * nt + it) * nt + jt];
+                        mask[static_cast<std::size_t>(t / 8) * at.total + pr] |= 1u << (t % 8);
+                    }
+                }
+            d.W = ar.upload(w);
+            d.Wmask = ar.upload(mask);
+            const std::size_t rows = static_cast<std::size_t>(3LL * s.n_s * nt);
+            DeviceBuffer drp(sizeof(int64_t) * (rows + 1), st), dcols(sizeof(int32_t) * nnz, st),
+                dvals(sizeof(double) * nnz, st);
+            CK(static_cast<cudaError_t>(lfb::launch_pattern(d, static_cast<long long*>(drp.p),
+                                                            static_cast<int*>(dcols.p), st)));
+            CK(static_cast<cudaError_t>(lfb::launch_combine(d, static_cast<double*>(dvals.p), 0, st, nullptr)));
+            if (row_ptr)
+                copy_d2h(row_ptr, drp.p, sizeof(int64_t) * (rows + 1), st);
+            if (cols)
+                copy_d2h(cols, dcols.p, sizeof(int32_t) * nnz, st);
+            if (values)
+                copy_d2h(values, dvals.p, sizeof(double) * nnz, st);
+            CK(cudaStreamSynchronize(st));
+        }
+        cudaStreamDestroy(st);
+    });
+}
+
+static double fetch_scalar(double* d_out, cudaStream_t st) {
+    double h = 0.0;
+    CK(cudaMemcpyAsync(&h, d_out, sizeof h, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return h;
+}
+
+int lf_csr_frobenius_sq(int64_t rows, const int64_t* d_row_ptr, const double* d_values, void* cuda_stream,
+                        double* out) {
+    return guarded([&] {
+        cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+        double* d_out = nullptr;
+        CK(cudaMallocAsync(&d_out, sizeof(double), st));
+        CK(static_cast<cudaError_t>(lfb::launch_frobenius_sq(rows, reinterpret_cast<const long long*>(d_row_ptr),
+                                                             d_values, d_out, st)));
+        *out = fetch_scalar(d_out, st);
+        cudaFreeAsync(d_out, st);
+    });
+}
+
+int lf_csr_spmv(int64_t rows, const int64_t* d_row_ptr, const int32_t* d_cols, const double* d_values,
+                const double* d_x, double* d_y, void* cuda_stream) {
+    return guarded([&] {
+        CK(static_cast<cudaError_t>(lfb::launch_spmv(rows, reinterpret_cast<const long long*>(d_row_ptr),
+                                                     reinterpret_cast<const int*>(d_cols), d_values, d_x, d_y,
+                                                     static_cast<cudaStream_t>(cuda_stream))));
+    });
+}
+
+int lf_csr_diff_sq(int64_t rows, const int64_t* d_ra, const int32_t* d_ca, const double* d_va, const int64_t* d_rb,
+                   const int32_t* d_cb, const double* d_vb, void* cuda_stream, double* out) {
+    return guarded([&] {
+        cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+        double* d_out = nullptr;
+        CK(cudaMallocAsync(&d_out, sizeof(double), st));
+        CK(static_cast<cudaError_t>(lfb::launch_diff_sq(
+            rows, reinterpret_cast<const long long*>(d_ra), reinterpret_cast<const int*>(d_ca), d_va,
+            reinterpret_cast<const long long*>(d_rb), reinterpret_cast<const int*>(d_cb), d_vb, d_out, st)));
+        *out = fetch_scalar(d_out, st);
+        cudaFreeAsync(d_out, st);
+    });
+}
+
+int lf_csr_symmetry_sq(int64_t rows, const int64_t* d_row_ptr, const int32_t* d_cols, const double* d_values,
+                       void* cuda_stream, double* out) {
+    return guarded([&] {
+        cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+        double* d_out = nullptr;
+        CK(cudaMallocAsync(&d_out, sizeof(double), st));
+        CK(static_cast<cudaError_t>(lfb::launch_symmetry_sq(rows, reinterpret_cast<const long long*>(d_row_ptr),
+                                                            reinterpret_cast<const int*>(d_cols), d_values, d_out,
+                                                            st)));
+        *out = fetch_scalar(d_out, st);
+        cudaFreeAsync(d_out, st);
+    });
+}
+
+} // extern "C"

@@ -1,0 +1,827 @@
+// Main kernels of the B200 laminate assembler (sm_100a).
+//
+//  K2a k_integrals_1d     1D basis-product integrals U, V (sum-factorised P
+//                         for affine geometry; fast.cpp:54-168 restated)
+//  K2b k_inplane_general  per-element P for non-affine geometry, coloured
+//                         (fast.cpp:54-168 / voigt_free.cpp:142-248)
+//  K4  k_combine          P (x) q~ straight into the CSR value array
+//                         (fast.cpp:211-264 + sparse.cpp:30-55)       <- hot
+//  K5  k_pattern_*        closed-form CSR row offsets and columns
+//  K6  k_standard         full 3D quadrature cross-check, coloured
+//                         (assembly.cpp:134-245)
+//  K7  verification       ||K||_F, K x, ||A-B||_F, ||K-K^T||_F (sparse.cpp:66-139)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "kernels.cuh"
+
+namespace lfb {
+
+namespace {
+
+constexpr int kBlock = 256;
+
+__device__ __forceinline__ int find_is(const long long* es_pre, int ns, long long e) {
+    int lo = 0, hi = ns; // es_pre[lo] <= e < es_pre[hi]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(es_pre + mid) <= e)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// ---------------------------------------------------------------------------
+// K2a: U[i][slot][2d+e] = sum over spans and Gauss points of
+//      (w h) N_i^{(d)} N_j^{(e)},  j = lo(i) + slot.
+// With a constant frame the 2D in-plane integrals factor exactly:
+//      I_xy(i_s, j_s) = U_{du_x du_y}(i_u, j_u) * V_{dv_x dv_y}(i_v, j_v).
+__global__ void k_integrals_1d(DevTables d) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nu_slots = d.nu * d.bu, nv_slots = d.nv * d.bv;
+    if (g >= nu_slots + nv_slots)
+        return;
+    const bool is_u = g < nu_slots;
+    const int h = is_u ? g : g - nu_slots;
+    const int b = is_u ? d.bu : d.bv;
+    const int i = h / b, slot = h % b;
+    const int p = is_u ? d.pu : d.pv;
+    const int* lo = is_u ? d.lo_u : d.lo_v;
+    const int* len = is_u ? d.len_u : d.len_v;
+    const int* first = is_u ? d.spu_first : d.spv_first;
+    const double* slo = is_u ? d.spu_lo : d.spv_lo;
+    const double* shi = is_u ? d.spu_hi : d.spv_hi;
+    const double* wref = is_u ? d.wu : d.wv;
+    const double* bval = is_u ? d.Bu_val : d.Bv_val;
+    const double* bder = is_u ? d.Bu_der : d.Bv_der;
+    const int nsp = is_u ? d.nspu : d.nspv, nq = is_u ? d.nqu : d.nqv;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    if (slot < len[i]) {
+        const int j = lo[i] + slot;
+        const int mn = min(i, j), mx = max(i, j);
+        for (int s = 0; s < nsp; ++s) {
+            const int f = first[s];
+            if (f > mn || mx > f + p)
+                continue;
+            const double half = 0.5 * (shi[s] - slo[s]);
+            for (int q = 0; q < nq; ++q) {
+                const long long row = ((long long)s * nq + q) * (p + 1);
+                const double w = wref[q] * half;
+                const double vi = bval[row + i - f], di = bder[row + i - f];
+                const double vj = bval[row + j - f], dj = bder[row + j - f];
+                acc[0] += w * vi * vj;
+                acc[1] += w * vi * dj;
+                acc[2] += w * di * vj;
+                acc[3] += w * di * dj;
+            }
+        }
+    }
+    double* out = (is_u ? d.U : d.V) + (long long)h * 4;
+    out[0] = acc[0];
+    out[1] = acc[1];
+    out[2] = acc[2];
+    out[3] = acc[3];
+}
+
+/// Affine P of one in-plane entry for `nt` terms starting at term t0:
+/// P_{t,f}(a,b) = sum_{(x,y) in family f} Ct[t][3x+y][3a+b] * I_xy.
+template <int NT>
+__device__ __forceinline__ void affine_p(const DevTables& d, int iu, int iv, int su, int sv, int ab,
+                                         int t0, double (&P)[NT][4]) {
+    const double* U = d.U + ((long long)iu * d.bu + su) * 4;
+    const double* V = d.V + ((long long)iv * d.bv + sv) * 4;
+    const double u0 = __ldg(U), u1 = __ldg(U + 1), u2 = __ldg(U + 2), u3 = __ldg(U + 3);
+    const double v0 = __ldg(V), v1 = __ldg(V + 1), v2 = __ldg(V + 2), v3 = __ldg(V + 3);
+    // x -> (u-derivative, v-derivative): 0 -> (1,0) [d/du], 1 -> (0,1) [d/dv], 2 -> (0,0) [value]
+    const double I00 = u3 * v0, I01 = u2 * v1, I10 = u1 * v2, I11 = u0 * v3;
+    const double I02 = u2 * v0, I12 = u0 * v2, I20 = u1 * v0, I21 = u0 * v1, I22 = u0 * v0;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        const double* C = d.Ct + (long long)(t0 + t) * 81 + ab;
+        P[t][0] = __ldg(C + 0) * I00 + __ldg(C + 9) * I01 + __ldg(C + 27) * I10 + __ldg(C + 36) * I11;
+        P[t][1] = __ldg(C + 18) * I02 + __ldg(C + 45) * I12;
+        P[t][2] = __ldg(C + 54) * I20 + __ldg(C + 63) * I21;
+        P[t][3] = __ldg(C + 72) * I22;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K4: the hot kernel.  One thread per in-plane entry (i_s, a, slot, b); the
+// thread keeps its P_{t,f} for the pass's terms in registers and streams
+// over the thickness rows of its block-row chunk, writing one FP64 value per
+// thickness pair.  Consecutive lanes hold consecutive entries of one CSR row
+// segment, so every warp store is a contiguous 256-byte run.
+//
+// Per staged sub-chunk of thickness rows, the pair weights (warp-uniform)
+// sit in shared memory as s_w[row][k][term][4] and each row carries the
+// union mask of terms with any contributing cell.  A row is processed with
+// a compile-time neighbour count (switch on L_t), so the L_t accumulators
+// stay in registers, and each term is a uniform branch: a term absent from
+// the row costs nothing, a term present costs 2 LDS.128 + 4 DFMA per pair.
+struct RowInfo {
+    long long base; // 9 S_s (pre_t[it] - pre_t[t0]): slab offset of row block it
+    int lt;         // L_t(it)
+    unsigned mask;  // union of term masks over the row's pairs (this pass)
+};
+
+template <int NT, int LT, bool ACCUM>
+__device__ __forceinline__ void combine_row(const double (&P)[NT][4], const double4* __restrict__ w,
+                                            unsigned mask, double* __restrict__ o, int B) {
+    double acc[LT];
+#pragma unroll
+    for (int k = 0; k < LT; ++k)
+        acc[k] = ACCUM ? o[(long long)k * B] : 0.0;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        if (mask & (1u << t)) {
+#pragma unroll
+            for (int k = 0; k < LT; ++k) {
+                const double4 ww = w[k * NT + t];
+                acc[k] = fma(P[t][0], ww.x, acc[k]);
+                acc[k] = fma(P[t][1], ww.y, acc[k]);
+                acc[k] = fma(P[t][2], ww.z, acc[k]);
+                acc[k] = fma(P[t][3], ww.w, acc[k]);
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < LT; ++k)
+        o[(long long)k * B] = acc[k];
+}
+
+template <int NT, bool ACCUM>
+__device__ __forceinline__ void combine_row_dyn(const double (&P)[NT][4], const double4* __restrict__ w,
+                                                int lt, unsigned mask, double* __restrict__ o, int B) {
+    for (int k = 0; k < lt; ++k) {
+        double acc = ACCUM ? o[(long long)k * B] : 0.0;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            if (mask & (1u << t)) {
+                const double4 ww = w[k * NT + t];
+                acc = fma(P[t][0], ww.x, acc);
+                acc = fma(P[t][1], ww.y, acc);
+                acc = fma(P[t][2], ww.z, acc);
+                acc = fma(P[t][3], ww.w, acc);
+            }
+        }
+        o[(long long)k * B] = acc;
+    }
+}
+
+template <int NT, bool AFFINE, bool ACCUM>
+__global__ void __launch_bounds__(kBlock) k_combine(const DevTables d, double* __restrict__ out,
+                                                    int pass, int t_chunk, int stage_rows, int lt_max) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    RowInfo* s_row = reinterpret_cast<RowInfo*>(smem_raw);
+    double4* s_w = reinterpret_cast<double4*>(smem_raw + ((stage_rows * sizeof(RowInfo) + 31) & ~31));
+
+    const long long e = (long long)blockIdx.x * kBlock + threadIdx.x;
+    const bool live = e < d.E;
+    const long long ec = live ? e : d.E - 1;
+    // i_s of this entry: forward scan from the block's first function
+    int is = __ldg(d.blk_is + blockIdx.x);
+    while (__ldg(d.es_pre + is + 1) <= ec)
+        ++is;
+    const long long ebase = __ldg(d.es_pre + is);
+    const int r = (int)(ec - ebase);
+    const int iu = is % d.nu, iv = is / d.nu;
+    const int Lu = __ldg(d.len_u + iu), Lv = __ldg(d.len_v + iv);
+    const int B = 3 * Lu * Lv; // row segment length per thickness neighbour
+    const int a = r / B;
+    const int rem = r - a * B;
+    const long long A = ebase + (long long)a * B;
+    const int t_first = pass * 8;
+
+    double P[NT][4];
+    if constexpr (AFFINE) {
+        const int s = rem / 3, b = rem - 3 * (rem / 3);
+        const int sv = s / Lu, su = s - sv * Lu;
+        affine_p<NT>(d, iu, iv, su, sv, 3 * a + b, t_first, P);
+    } else {
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+#pragma unroll
+            for (int f = 0; f < 4; ++f)
+                P[t][f] = __ldg(d.Pg + ((long long)(t_first + t) * 4 + f) * d.E + ec);
+    }
+
+    const int it_begin = d.t0 + blockIdx.y * t_chunk;
+    const int it_end = min(d.t1, it_begin + t_chunk);
+    const long long pre0 = __ldg(d.pre_t + d.t0);
+    const long long nine_S = 9 * d.S_s;
+    const unsigned* mask_base = d.Wmask + (long long)pass * d.n_pairs;
+    const int T = d.n_terms;
+    double* const o_thread = out + (long long)rem;
+
+    for (int it0 = it_begin; it0 < it_end; it0 += stage_rows) {
+        const int nrow = min(stage_rows, it_end - it0);
+        if (it0 != it_begin)
+            __syncthreads();
+        // stage rows: RowInfo + weights s_w[row][k][t] (k < lt_max, zero padded)
+        for (int rr = threadIdx.x; rr < nrow; rr += kBlock) {
+            const int it = it0 + rr;
+            const long long pfx = __ldg(d.pre_t + it) - pre0;
+            const int lt = __ldg(d.len_t + it);
+            unsigned m = 0;
+            for (int k = 0; k < lt; ++k)
+                m |= __ldg(mask_base + pfx + k);
+            s_row[rr].base = nine_S * pfx;
+            s_row[rr].lt = lt;
+            s_row[rr].mask = m;
+        }
+        const int nw = nrow * lt_max * NT;
+        for (int idx = threadIdx.x; idx < nw; idx += kBlock) {
+            const int rr = idx / (lt_max * NT);
+            const int k = (idx / NT) % lt_max;
+            const int t = idx % NT;
+            const int it = it0 + rr;
+            double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
+            if (k < __ldg(d.len_t + it)) {
+                const long long q = __ldg(d.pre_t + it) - pre0 + k;
+                const double2* src = reinterpret_cast<const double2*>(d.W + ((q * T) + t_first + t) * 4);
+                const double2 lo = __ldg(src), hi = __ldg(src + 1);
+                v = make_double4(lo.x, lo.y, hi.x, hi.y);
+            }
+            s_w[idx] = v;
+        }
+        __syncthreads();
+        if (!live)
+            continue;
+        for (int rr = 0; rr < nrow; ++rr) {
+            const RowInfo ri = s_row[rr];
+            double* o = o_thread + ri.base + (long long)ri.lt * A;
+            const double4* w = s_w + rr * lt_max * NT;
+            switch (ri.lt) {
+            case 1: combine_row<NT, 1, ACCUM>(P, w, ri.mask, o, B); break;
+            case 2: combine_row<NT, 2, ACCUM>(P, w, ri.mask, o, B); break;
+            case 3: combine_row<NT, 3, ACCUM>(P, w, ri.mask, o, B); break;
+            case 4: combine_row<NT, 4, ACCUM>(P, w, ri.mask, o, B); break;
+            case 5: combine_row<NT, 5, ACCUM>(P, w, ri.mask, o, B); break;
+            case 7: combine_row<NT, 7, ACCUM>(P, w, ri.mask, o, B); break;
+            default: combine_row_dyn<NT, ACCUM>(P, w, ri.lt, ri.mask, o, B); break;
+            }
+        }
+    }
+}
+
+/// Exports P of every term in the entry layout Pg[t][f][e] (affine path),
+/// for the operator-level entry point.
+__global__ void k_affine_export(const DevTables d) {
+    const long long e = (long long)blockIdx.x * kBlock + threadIdx.x;
+    if (e >= d.E)
+        return;
+    const int is = find_is(d.es_pre, d.ns, e);
+    const int r = (int)(e - d.es_pre[is]);
+    const int iu = is % d.nu, iv = is / d.nu;
+    const int Lu = d.len_u[iu], Lv = d.len_v[iv];
+    const int B = 3 * Lu * Lv;
+    const int a = r / B, rem = r - a * B;
+    const int s = rem / 3, b = rem % 3;
+    const int sv = s / Lu, su = s - sv * Lu;
+    for (int t = 0; t < d.n_terms; ++t) {
+        double P[1][4];
+        affine_p<1>(d, iu, iv, su, sv, 3 * a + b, t, P);
+        for (int f = 0; f < 4; ++f)
+            d.Pg[((long long)t * 4 + f) * d.E + e] = P[0][f];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Shared per-element prologue: gradient tables and quadrature weights.
+struct ElemInfo {
+    int eu, ev, fu, fv, nl2, nq2;
+    double hu, hv;
+};
+
+__device__ __forceinline__ void element_tables(const DevTables& d, const ElemInfo& el, double* gh,
+                                               double* w2) {
+    // gh[(q*nl2 + a)*3 + {0,1,2}] = (du, dv, val) of local function a at in-plane point q
+    for (int idx = threadIdx.x; idx < el.nq2 * el.nl2; idx += blockDim.x) {
+        const int q = idx / el.nl2, a = idx % el.nl2;
+        const int qv = q / d.nqu, qu = q % d.nqu;
+        const int jv = a / (d.pu + 1), ju = a % (d.pu + 1);
+        const long long ru = ((long long)el.eu * d.nqu + qu) * (d.pu + 1) + ju;
+        const long long rv = ((long long)el.ev * d.nqv + qv) * (d.pv + 1) + jv;
+        const double bu = d.Bu_val[ru], bud = d.Bu_der[ru];
+        const double bv = d.Bv_val[rv], bvd = d.Bv_der[rv];
+        gh[idx * 3 + 0] = bud * bv;
+        gh[idx * 3 + 1] = bu * bvd;
+        gh[idx * 3 + 2] = bu * bv;
+    }
+    for (int q = threadIdx.x; q < el.nq2; q += blockDim.x) {
+        const int qv = q / d.nqu, qu = q % d.nqu;
+        w2[q] = d.wu[qu] * el.hu * d.wv[qv] * el.hv; // assembly.cpp:44-45
+    }
+}
+
+/// Ctq[q][3x+y][3i+k] = scale_q * sum_{j,l} G_q(j,x) G_q(l,y) C{e_j,e_l}(i,k)
+/// (pullbackContractionTable, voigt_free.cpp:125-140).
+__device__ __forceinline__ void pullback_tables(const DevTables& d, int e_index, int nq2,
+                                                const double* w2, const double* table, double* ctq) {
+    for (int idx = threadIdx.x; idx < nq2 * 81; idx += blockDim.x) {
+        const int q = idx / 81, xy = (idx % 81) / 9, ik = idx % 9;
+        const int x = xy / 3, y = xy % 3;
+        const double* G;
+        double det;
+        if (d.affine) {
+            G = d.G;
+            det = d.det;
+        } else {
+            const double* f = d.frames + ((long long)e_index * nq2 + q) * 19;
+            G = f + 9;
+            det = f[18];
+        }
+        double s = 0.0;
+        for (int j = 0; j < 3; ++j)
+            for (int l = 0; l < 3; ++l)
+                s += G[3 * x + j] * G[3 * y + l] * table[(3 * j + l) * 9 + ik];
+        ctq[idx] = w2[q] * det * s;
+    }
+}
+
+// K2b: in-plane operators of every term for one element colour.  Elements of
+// one colour share no basis function, so plain += is race-free and the
+// result is deterministic.
+__global__ void k_inplane_general(const DevTables d, int cu, int cv) {
+    extern __shared__ double sm[];
+    ElemInfo el;
+    el.eu = cu + blockIdx.x * (d.pu + 1);
+    el.ev = cv + blockIdx.y * (d.pv + 1);
+    if (el.eu >= d.nspu || el.ev >= d.nspv)
+        return;
+    el.fu = d.spu_first[el.eu];
+    el.fv = d.spv_first[el.ev];
+    el.nl2 = (d.pu + 1) * (d.pv + 1);
+    el.nq2 = d.nqu * d.nqv;
+    el.hu = 0.5 * (d.spu_hi[el.eu] - d.spu_lo[el.eu]);
+    el.hv = 0.5 * (d.spv_hi[el.ev] - d.spv_lo[el.ev]);
+    double* gh = sm;                    // nq2 * nl2 * 3
+    double* w2 = gh + el.nq2 * el.nl2 * 3; // nq2
+    double* ctq = w2 + el.nq2;          // nq2 * 81
+    element_tables(d, el, gh, w2);
+    const int e_index = el.ev * d.nspu + el.eu;
+    for (int t = 0; t < d.n_terms; ++t) {
+        __syncthreads();
+        pullback_tables(d, e_index, el.nq2, w2, d.term_table + (long long)t * 81, ctq);
+        __syncthreads();
+        for (int pr = threadIdx.x; pr < el.nl2 * el.nl2; pr += blockDim.x) {
+            const int al = pr / el.nl2, be = pr % el.nl2;
+            double acc[4][9];
+#pragma unroll
+            for (int f = 0; f < 4; ++f)
+#pragma unroll
+                for (int k = 0; k < 9; ++k)
+                    acc[f][k] = 0.0;
+            for (int q = 0; q < el.nq2; ++q) {
+                const double* ga = gh + (q * el.nl2 + al) * 3;
+                const double* gb = gh + (q * el.nl2 + be) * 3;
+                double s[9];
+#pragma unroll
+                for (int x = 0; x < 3; ++x)
+#pragma unroll
+                    for (int y = 0; y < 3; ++y)
+                        s[3 * x + y] = ga[x] * gb[y];
+                const double* C = ctq + q * 81;
+#pragma unroll
+                for (int k = 0; k < 9; ++k) {
+                    acc[0][k] += C[0 * 9 + k] * s[0] + C[1 * 9 + k] * s[1] + C[3 * 9 + k] * s[3] + C[4 * 9 + k] * s[4];
+                    acc[1][k] += C[2 * 9 + k] * s[2] + C[5 * 9 + k] * s[5];
+                    acc[2][k] += C[6 * 9 + k] * s[6] + C[7 * 9 + k] * s[7];
+                    acc[3][k] += C[8 * 9 + k] * s[8];
+                }
+            }
+            const int iu = el.fu + al % (d.pu + 1), iv = el.fv + al / (d.pu + 1);
+            const int ju = el.fu + be % (d.pu + 1), jv = el.fv + be / (d.pu + 1);
+            const int is = iv * d.nu + iu;
+            const int Lu = d.len_u[iu], Lv = d.len_v[iv];
+            const int slot = (jv - d.lo_v[iv]) * Lu + (ju - d.lo_u[iu]);
+            const long long base = d.es_pre[is] + 3 * slot;
+            const int B = 3 * Lu * Lv;
+            for (int f = 0; f < 4; ++f) {
+                double* dst = d.Pg + ((long long)t * 4 + f) * d.E + base;
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int b = 0; b < 3; ++b)
+                        dst[(long long)a * B + b] += acc[f][3 * a + b];
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K6: standard full-3D quadrature (assembly.cpp:134-245), one block per
+// (element, thickness span) of one colour, accumulated straight into the
+// precomputed CSR (the duplicate summation of sparse.cpp:30-55).
+__global__ void k_standard(const DevTables d, double* __restrict__ values, int cu, int cv, int ct) {
+    extern __shared__ double sm[];
+    ElemInfo el;
+    el.eu = cu + blockIdx.x * (d.pu + 1);
+    el.ev = cv + blockIdx.y * (d.pv + 1);
+    const int ks = ct + blockIdx.z * (d.pt + 1);
+    if (el.eu >= d.nspu || el.ev >= d.nspv || ks >= d.nspt)
+        return;
+    const int c0 = d.span_cell0[ks], c1 = d.span_cell0[ks + 1];
+    if (c0 == c1)
+        return; // span with no unmasked cell (assembly.cpp:185-186)
+    el.fu = d.spu_first[el.eu];
+    el.fv = d.spv_first[el.ev];
+    el.nl2 = (d.pu + 1) * (d.pv + 1);
+    el.nq2 = d.nqu * d.nqv;
+    el.hu = 0.5 * (d.spu_hi[el.eu] - d.spu_lo[el.eu]);
+    el.hv = 0.5 * (d.spv_hi[el.ev] - d.spv_lo[el.ev]);
+    const int ft = d.spt_first[ks];
+    const int ntl = d.pt + 1;
+    const int nl3 = el.nl2 * ntl;
+    double* gh = sm;
+    double* w2 = gh + el.nq2 * el.nl2 * 3;
+    double* ctq = w2 + el.nq2;
+    double* tv = ctq + el.nq2 * 81; // nqt * ntl values, then derivatives
+    double* td = tv + d.nqt * ntl;
+    double* w3 = td + d.nqt * ntl;
+    element_tables(d, el, gh, w2);
+    const int e_index = el.ev * d.nspu + el.eu;
+    const long long pre0 = d.pre_t[d.t0];
+    for (int c = c0; c < c1; ++c) {
+        __syncthreads();
+        const int cfg = d.layer_config[d.cell_layer[c]];
+        pullback_tables(d, e_index, el.nq2, w2, d.term_table + (long long)cfg * 81, ctq);
+        for (int idx = threadIdx.x; idx < d.nqt * ntl; idx += blockDim.x) {
+            const int q = idx / ntl, a = idx % ntl;
+            const long long h = (long long)c * d.nqt + q;
+            const int sh = ft - d.Bt_first[h]; // 0 unless a point rounds onto a knot
+            const int aa = a + sh;
+            const bool ok = aa >= 0 && aa <= d.pt;
+            tv[idx] = ok ? d.Bt_val[h * ntl + aa] : 0.0;
+            td[idx] = ok ? d.Bt_der[h * ntl + aa] : 0.0;
+        }
+        for (int q = threadIdx.x; q < d.nqt; q += blockDim.x)
+            w3[q] = d.cell_wts[(long long)c * d.nqt + q];
+        __syncthreads();
+        for (int pr = threadIdx.x; pr < nl3 * nl3; pr += blockDim.x) {
+            const int al = pr / nl3, be = pr % nl3;
+            const int at = al / el.nl2, as = al % el.nl2;
+            const int bt = be / el.nl2, bs = be % el.nl2;
+            const int it = ft + at, jt = ft + bt;
+            if (it < d.t0 || it >= d.t1)
+                continue;
+            double acc[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k)
+                acc[k] = 0.0;
+            for (int q2 = 0; q2 < el.nq2; ++q2) {
+                const double* ga = gh + (q2 * el.nl2 + as) * 3;
+                const double* gb = gh + (q2 * el.nl2 + bs) * 3;
+                const double* C = ctq + q2 * 81;
+                for (int q3 = 0; q3 < d.nqt; ++q3) {
+                    const double Ta = tv[q3 * ntl + at], Tda = td[q3 * ntl + at];
+                    const double Tb = tv[q3 * ntl + bt], Tdb = td[q3 * ntl + bt];
+                    // grad_hat = (du T, dv T, val T') (assembly.cpp:203-206)
+                    const double xa[3] = {ga[0] * Ta, ga[1] * Ta, ga[2] * Tda};
+                    const double xb[3] = {gb[0] * Tb * w3[q3], gb[1] * Tb * w3[q3], gb[2] * Tdb * w3[q3]};
+#pragma unroll
+                    for (int x = 0; x < 3; ++x)
+#pragma unroll
+                        for (int y = 0; y < 3; ++y) {
+                            const double s = xa[x] * xb[y];
+#pragma unroll
+                            for (int k = 0; k < 9; ++k)
+                                acc[k] += C[(3 * x + y) * 9 + k] * s;
+                        }
+                }
+            }
+            const int iu = el.fu + as % (d.pu + 1), iv = el.fv + as / (d.pu + 1);
+            const int ju = el.fu + bs % (d.pu + 1), jv = el.fv + bs / (d.pu + 1);
+            const int is = iv * d.nu + iu;
+            const int Lu = d.len_u[iu], Lv = d.len_v[iv];
+            const int B = 3 * Lu * Lv;
+            const int slot = (jv - d.lo_v[iv]) * Lu + (ju - d.lo_u[iu]);
+            const int Lt = d.len_t[it];
+            const long long pos = 9 * d.S_s * (d.pre_t[it] - pre0) + (long long)Lt * d.es_pre[is] +
+                                  (long long)(jt - d.lo_t[it]) * B + 3 * slot;
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b)
+                    values[pos + (long long)a * Lt * B + b] += acc[3 * a + b];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K5: closed-form CSR pattern, slab-local row offsets.
+__global__ void k_pattern_rows(const DevTables d, long long* __restrict__ row_ptr, long long rows) {
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r > rows)
+        return;
+    if (r == rows) {
+        row_ptr[rows] = 9 * d.S_s * (d.pre_t[d.t1] - d.pre_t[d.t0]);
+        return;
+    }
+    const long long per_t = 3LL * d.ns;
+    const int it = d.t0 + (int)(r / per_t);
+    const long long rr = r % per_t;
+    const int is = (int)(rr / 3), a = (int)(rr % 3);
+    const int iu = is % d.nu, iv = is / d.nu;
+    const int B = 3 * d.len_u[iu] * d.len_v[iv];
+    const int Lt = d.len_t[it];
+    row_ptr[r] = 9 * d.S_s * (d.pre_t[it] - d.pre_t[d.t0]) + (long long)Lt * (d.es_pre[is] + (long long)a * B);
+}
+
+__global__ void __launch_bounds__(kBlock) k_pattern_cols(const DevTables d, int* __restrict__ cols,
+                                                         int t_chunk) {
+    const long long e = (long long)blockIdx.x * kBlock + threadIdx.x;
+    if (e >= d.E)
+        return;
+    int is = d.blk_is[blockIdx.x];
+    while (d.es_pre[is + 1] <= e)
+        ++is;
+    const long long ebase = d.es_pre[is];
+    const int r = (int)(e - ebase);
+    const int iu = is % d.nu, iv = is / d.nu;
+    const int Lu = d.len_u[iu], Lv = d.len_v[iv];
+    const int B = 3 * Lu * Lv;
+    const int a = r / B, rem = r - a * B;
+    const int s = rem / 3, b = rem % 3;
+    const int jv = d.lo_v[iv] + s / Lu, ju = d.lo_u[iu] + s % Lu;
+    const int col_s = 3 * (jv * d.nu + ju) + b;
+    const long long A = ebase + (long long)a * B;
+    const int it_begin = d.t0 + blockIdx.y * t_chunk;
+    const int it_end = min(d.t1, it_begin + t_chunk);
+    const long long pre0 = d.pre_t[d.t0];
+    for (int it = it_begin; it < it_end; ++it) {
+        const int Lt = d.len_t[it];
+        const long long pfx = d.pre_t[it] - pre0;
+        int* o = cols + 9 * d.S_s * pfx + (long long)Lt * A + rem;
+        const int jt0 = d.lo_t[it];
+        for (int k = 0; k < Lt; ++k)
+            o[(long long)k * B] = 3 * d.ns * (jt0 + k) + col_s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K7: verification reductions (deterministic two-pass).
+__device__ __forceinline__ double block_sum(double v) {
+    __shared__ double red[32];
+    for (int o = 16; o > 0; o >>= 1)
+        v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0)
+        red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    if (threadIdx.x < 32)
+        for (int o = 16; o > 0; o >>= 1)
+            v += __shfl_down_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__global__ void k_sumsq(const double* v, long long n, double* partial) {
+    double s = 0.0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        s += v[i] * v[i];
+    s = block_sum(s);
+    if (threadIdx.x == 0)
+        partial[blockIdx.x] = s;
+}
+
+__global__ void k_final_sum(const double* partial, int n, double* out) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        s += partial[i];
+    s = block_sum(s);
+    if (threadIdx.x == 0)
+        *out = s;
+}
+
+__global__ void k_spmv(long long rows, const long long* rp, const int* c, const double* v, const double* x,
+                       double* y) {
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows)
+        return;
+    double s = 0.0;
+    for (long long k = rp[r]; k < rp[r + 1]; ++k)
+        s += v[k] * x[c[k]];
+    y[r] = s;
+}
+
+__global__ void k_diff_rows(long long rows, const long long* ra, const int* ca, const double* va,
+                            const long long* rb, const int* cb, const double* vb, double* partial) {
+    double s = 0.0;
+    for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+         r += (long long)gridDim.x * blockDim.x) {
+        long long ka = ra[r], kb = rb[r];
+        const long long ea = ra[r + 1], eb = rb[r + 1];
+        while (ka < ea || kb < eb) {
+            const long long xa = ka < ea ? ca[ka] : (1LL << 40);
+            const long long xb = kb < eb ? cb[kb] : (1LL << 40);
+            double dd;
+            if (xa == xb) {
+                dd = va[ka++] - vb[kb++];
+            } else if (xa < xb) {
+                dd = va[ka++];
+            } else {
+                dd = -vb[kb++];
+            }
+            s += dd * dd;
+        }
+    }
+    s = block_sum(s);
+    if (threadIdx.x == 0)
+        partial[blockIdx.x] = s;
+}
+
+__global__ void k_symmetry_rows(long long rows, const long long* rp, const int* c, const double* v,
+                                double* partial) {
+    double s = 0.0;
+    for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+         r += (long long)gridDim.x * blockDim.x) {
+        for (long long k = rp[r]; k < rp[r + 1]; ++k) {
+            const int col = c[k];
+            long long lo = rp[col], hi = rp[col + 1];
+            while (lo < hi) {
+                const long long mid = (lo + hi) >> 1;
+                if (c[mid] < r)
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+            const bool mirrored = lo < rp[col + 1] && c[lo] == r;
+            const double dd = v[k] - (mirrored ? v[lo] : 0.0);
+            s += dd * dd;
+            if (!mirrored)
+                s += dd * dd; // symmetryRelError counts the absent mirror slot (sparse.cpp:87-90)
+        }
+    }
+    s = block_sum(s);
+    if (threadIdx.x == 0)
+        partial[blockIdx.x] = s;
+}
+
+int reduce_launch(int blocks, double* partial, double* out, cudaStream_t stream) {
+    k_final_sum<<<1, 1024, 0, stream>>>(partial, blocks, out);
+    return (int)cudaGetLastError();
+}
+
+template <int NT>
+void combine_one(const DevTables& d, double* out, int pass, int t_chunk, int stage_rows, int lt_max, dim3 grid,
+                 cudaStream_t s, bool accum) {
+    const size_t smem = ((stage_rows * sizeof(RowInfo) + 31) & ~size_t(31)) +
+                        (size_t)stage_rows * lt_max * NT * sizeof(double4);
+    auto launch = [&](auto kern) {
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, kBlock, smem, s>>>(d, out, pass, t_chunk, stage_rows, lt_max);
+    };
+    if (d.affine) {
+        if (accum)
+            launch(k_combine<NT, true, true>);
+        else
+            launch(k_combine<NT, true, false>);
+    } else {
+        if (accum)
+            launch(k_combine<NT, false, true>);
+        else
+            launch(k_combine<NT, false, false>);
+    }
+}
+
+} // namespace
+
+int launch_integrals_1d(const DevTables& d, cudaStream_t stream) {
+    const int n = d.nu * d.bu + d.nv * d.bv;
+    k_integrals_1d<<<(n + 127) / 128, 128, 0, stream>>>(d);
+    return (int)cudaGetLastError();
+}
+
+int launch_affine_export(const DevTables& d, cudaStream_t stream) {
+    if (d.E == 0)
+        return 0;
+    k_affine_export<<<(unsigned)((d.E + kBlock - 1) / kBlock), kBlock, 0, stream>>>(d);
+    return (int)cudaGetLastError();
+}
+
+int launch_inplane_general(const DevTables& d, cudaStream_t stream) {
+    const int nl2 = (d.pu + 1) * (d.pv + 1), nq2 = d.nqu * d.nqv;
+    const size_t smem = sizeof(double) * ((size_t)nq2 * nl2 * 3 + nq2 + (size_t)nq2 * 81);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_inplane_general, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const dim3 grid((d.nspu + d.pu) / (d.pu + 1), (d.nspv + d.pv) / (d.pv + 1));
+    for (int cv = 0; cv <= d.pv; ++cv)
+        for (int cu = 0; cu <= d.pu; ++cu)
+            k_inplane_general<<<grid, 128, smem, stream>>>(d, cu, cv);
+    return (int)cudaGetLastError();
+}
+
+int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t stream, int* launches) {
+    if (d.E == 0 || d.t1 <= d.t0)
+        return 0;
+    const long long nblk = (d.E + kBlock - 1) / kBlock;
+    const int nt = d.t1 - d.t0;
+    if (t_chunk <= 0) {
+        // enough blocks for >= ~16 waves of 4 resident blocks on 148 SMs
+        const long long target = 148LL * 4 * 16;
+        long long nchunks = (target + nblk - 1) / nblk;
+        nchunks = std::max(1LL, std::min<long long>(nchunks, nt));
+        t_chunk = (int)((nt + nchunks - 1) / nchunks);
+    }
+    const dim3 grid((unsigned)nblk, (unsigned)((nt + t_chunk - 1) / t_chunk));
+    const int lt_max = std::max(1, d.lt_max);
+    for (int pass = 0; pass < d.n_passes; ++pass) {
+        const int nterm = std::min(8, d.n_terms - 8 * pass);
+        const bool accum = pass > 0;
+        // rows per staged sub-chunk: ~24 KB of weights, at most the chunk
+        int stage_rows = (int)((24 * 1024) / ((size_t)lt_max * nterm * sizeof(double4)));
+        stage_rows = std::max(1, std::min(stage_rows, t_chunk));
+        switch (nterm) {
+        case 1: combine_one<1>(d, out, pass, t_chunk, stage_rows, lt_max, grid, stream, accum); break;
+        case 2: combine_one<2>(d, out, pass, t_chunk, stage_rows, lt_max, grid, stream, accum); break;
+        case 3: combine_one<3>(d, out, pass, t_chunk, stage_rows, lt_max, grid, stream, accum); break;
+        case 4: combine_one<4>(d, out, pass, t_chunk, stage_rows, lt_max, grid, stream, accum); break;
+        case 5: combine_one<5>(d, out, pass, t_chunk, stage_rows, lt_max, grid, stream, accum); break;
+        case 6: combine_one<6>(d, out, pass, t_chunk, stage_rows, lt_max, grid, stream, accum); break;
+        case 7: combine_one<7>(d, out, pass, t_chunk, stage_rows, lt_max, grid, stream, accum); break;
+        default: combine_one<8>(d, out, pass, t_chunk, stage_rows, lt_max, grid, stream, accum); break;
+        }
+        if (launches)
+            ++*launches;
+    }
+    return (int)cudaGetLastError();
+}
+
+int launch_pattern(const DevTables& d, long long* row_ptr, int* cols, cudaStream_t stream) {
+    const long long rows = 3LL * d.ns * (d.t1 - d.t0);
+    k_pattern_rows<<<(unsigned)((rows + 1 + 255) / 256), 256, 0, stream>>>(d, row_ptr, rows);
+    if (d.E > 0 && d.t1 > d.t0) {
+        const long long nblk = (d.E + kBlock - 1) / kBlock;
+        const int nt = d.t1 - d.t0;
+        long long nchunks = std::max(1LL, std::min<long long>((148LL * 64 + nblk - 1) / nblk, nt));
+        const int t_chunk = (int)((nt + nchunks - 1) / nchunks);
+        const dim3 grid((unsigned)nblk, (unsigned)((nt + t_chunk - 1) / t_chunk));
+        k_pattern_cols<<<grid, kBlock, 0, stream>>>(d, cols, t_chunk);
+    }
+    return (int)cudaGetLastError();
+}
+
+int launch_standard(const DevTables& d, double* values, long long nnz, cudaStream_t stream, int* launches) {
+    cudaMemsetAsync(values, 0, sizeof(double) * (size_t)nnz, stream);
+    const int nl2 = (d.pu + 1) * (d.pv + 1), nq2 = d.nqu * d.nqv, ntl = d.pt + 1;
+    const size_t smem = sizeof(double) * ((size_t)nq2 * nl2 * 3 + nq2 + (size_t)nq2 * 81 +
+                                          2 * (size_t)d.nqt * ntl + d.nqt);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_standard, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const dim3 grid((d.nspu + d.pu) / (d.pu + 1), (d.nspv + d.pv) / (d.pv + 1), (d.nspt + d.pt) / (d.pt + 1));
+    for (int ct = 0; ct <= d.pt; ++ct)
+        for (int cv = 0; cv <= d.pv; ++cv)
+            for (int cu = 0; cu <= d.pu; ++cu) {
+                k_standard<<<grid, 256, smem, stream>>>(d, values, cu, cv, ct);
+                if (launches)
+                    ++*launches;
+            }
+    return (int)cudaGetLastError();
+}
+
+int launch_frobenius_sq(long long rows, const long long* rp, const double* v, double* out, cudaStream_t stream) {
+    long long nnz = 0;
+    cudaMemcpyAsync(&nnz, rp + rows, sizeof nnz, cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    const int blocks = 1024;
+    double* partial = nullptr;
+    cudaMallocAsync(&partial, sizeof(double) * blocks, stream);
+    k_sumsq<<<blocks, 256, 0, stream>>>(v, nnz, partial);
+    reduce_launch(blocks, partial, out, stream);
+    cudaFreeAsync(partial, stream);
+    return (int)cudaGetLastError();
+}
+
+int launch_spmv(long long rows, const long long* rp, const int* c, const double* v, const double* x, double* y,
+                cudaStream_t stream) {
+    k_spmv<<<(unsigned)((rows + 255) / 256), 256, 0, stream>>>(rows, rp, c, v, x, y);
+    return (int)cudaGetLastError();
+}
+
+int launch_diff_sq(long long rows, const long long* ra, const int* ca, const double* va, const long long* rb,
+                   const int* cb, const double* vb, double* out, cudaStream_t stream) {
+    const int blocks = 1024;
+    double* partial = nullptr;
+    cudaMallocAsync(&partial, sizeof(double) * blocks, stream);
+    k_diff_rows<<<blocks, 256, 0, stream>>>(rows, ra, ca, va, rb, cb, vb, partial);
+    reduce_launch(blocks, partial, out, stream);
+    cudaFreeAsync(partial, stream);
+    return (int)cudaGetLastError();
+}
+
+int launch_symmetry_sq(long long rows, const long long* rp, const int* c, const double* v, double* out,
+                       cudaStream_t stream) {
+    const int blocks = 1024;
+    double* partial = nullptr;
+    cudaMallocAsync(&partial, sizeof(double) * blocks, stream);
+    k_symmetry_rows<<<blocks, 256, 0, stream>>>(rows, rp, c, v, partial);
+    reduce_launch(blocks, partial, out, stream);
+    cudaFreeAsync(partial, stream);
+    return (int)cudaGetLastError();
+}
+
+} // namespace lfb

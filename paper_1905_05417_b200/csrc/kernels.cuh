@@ -1,0 +1,93 @@
+// Device-side tables and kernel launchers of the B200 assembler.
+//
+// Data layout in HBM:
+//   in-plane entry space  e in [0, E), E = 9 * S_s: for in-plane function i_s,
+//       entries es_pre[i_s] .. es_pre[i_s+1]) ordered (a, slot, b) with
+//       slot = (j_v - lo_v(i_v)) * L_u(i_u) + (j_u - lo_u(i_u)) -- exactly the
+//       order of one CSR row block, so thread e writes output entries
+//       base_t(i_t) + L_t(i_t) * (es_pre[i_s] + a*3L_s) + k*3L_s + (3*slot + b)
+//       for every thickness row i_t and neighbour k.
+//   thickness pairs p in [0, n_pairs): (i_t, j_t = lo_t(i_t) + k) of the slab in
+//       CSR order; W[p][term][family] are the layer-reduced q~ weights and
+//       Wmask[pass][p] flags the terms that have any contributing cell.
+#pragma once
+
+#include <cstdint>
+
+namespace lfb {
+
+struct DevTables {
+    // degrees / sizes
+    int pu, pv, pt;
+    int nu, nv, nt, ns;
+    int nspu, nspv, nspt;
+    int nqu, nqv, nqt;
+    int ncells, n_layers, n_terms, n_passes;
+    int bu, bv; // band widths 2p+1 of the U/V tables
+    // knots
+    const double *ku, *kv, *kt;
+    int nku, nkv, nkt;
+    // spans + reference Gauss rules on [-1, 1]
+    const int *spu_first, *spv_first, *spt_first;
+    const double *spu_lo, *spu_hi, *spv_lo, *spv_hi;
+    const double *ru, *wu, *rv, *wv;
+    // thickness cells (span-major), their Gauss rules, span -> cell range
+    const double *cell_pts, *cell_wts;
+    const int *cell_first, *cell_layer, *span_cell0;
+    // operator terms
+    const double* term_table; // [T][81] contraction tables C{e_j,e_l}(i,k)
+    const double* lam;        // [T][L]
+    const unsigned char* lam_on;
+    const int* layer_config;  // [L]
+    // adjacency / pattern
+    const int *lo_u, *len_u, *lo_v, *len_v, *lo_t, *len_t;
+    const long long *pre_u, *pre_v, *pre_t;
+    const long long* es_pre; // [ns + 1]
+    const int* blk_is;       // [ceil(E / 256)] i_s of each 256-entry block's first entry
+    int lt_max;              // max L_t over all thickness rows
+    long long S_s, S_u;
+    // geometry
+    int affine;
+    double G[9]; // constant DF^{-T} (col-major) when affine
+    double det;
+    const double* frames; // [n_el][nqu*nqv][19] when !affine
+    // workspace
+    double *Bu_val, *Bu_der, *Bv_val, *Bv_der; // [nsp * nq][p+1]
+    double *Bt_val, *Bt_der;                   // [ncells * nqt][pt+1]
+    int* Bt_first;                             // [ncells * nqt]
+    double *U, *V;                             // [n][b][4]
+    double* Ct;                                // [T][81]
+    double* W;                                 // [n_pairs][T][4]
+    unsigned* Wmask;                           // [n_passes][n_pairs]
+    double* Pg;                                // [T][4][E] (general geometry)
+    // slab
+    int t0, t1;
+    long long n_pairs, E;
+};
+
+// Launchers (all asynchronous on `stream`).  Return cudaError_t as int.
+int launch_basis(const DevTables& d, bool with_ct, cudaStream_t stream);
+int launch_thickness_pairs(const DevTables& d, cudaStream_t stream);
+int launch_integrals_1d(const DevTables& d, cudaStream_t stream);
+int launch_inplane_general(const DevTables& d, cudaStream_t stream);
+int launch_affine_export(const DevTables& d, cudaStream_t stream);
+/// Combine: one launch per pass of <= 8 terms.  `t_chunk` thickness rows per
+/// block row; returns the number of kernels launched via *launches.
+int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t stream,
+                   int* launches);
+int launch_pattern(const DevTables& d, long long* row_ptr, int* cols, cudaStream_t stream);
+int launch_standard(const DevTables& d, double* values, long long nnz, cudaStream_t stream,
+                    int* launches);
+
+// Verification (sparse.cpp:66-139)
+int launch_frobenius_sq(long long rows, const long long* rp, const double* v, double* out,
+                        cudaStream_t stream);
+int launch_spmv(long long rows, const long long* rp, const int* c, const double* v,
+                const double* x, double* y, cudaStream_t stream);
+int launch_diff_sq(long long rows, const long long* ra, const int* ca, const double* va,
+                   const long long* rb, const int* cb, const double* vb, double* out,
+                   cudaStream_t stream);
+int launch_symmetry_sq(long long rows, const long long* rp, const int* c, const double* v,
+                       double* out, cudaStream_t stream);
+
+} // namespace lfb

@@ -1,0 +1,274 @@
+"""GPU parity: the CUDA path through the C ABI against the CPU oracle.
+
+Gate (BASELINE.json north star): CSR pattern bit-exact; values within
+1e-12 * max|K_oracle|; frobeniusRelDiff <= 1e-12 (acceptance.cpp:113).
+"""
+import numpy as np
+import pytest
+
+from conftest import assert_csr_match
+from oracle.checkers import csr_rel_diff
+from paper_1905_05417_b200 import problem as P
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-12
+
+
+def test_c1_fast_matches_oracle(gpu, oracle):
+    prob = P.baseline_config("C1")
+    got = gpu.assemble_fast(prob)
+    want = oracle.assemble(prob, "fast")
+    assert_csr_match(got.astuple(), want, RTOL)
+    assert csr_rel_diff(got.astuple(), want) <= RTOL
+
+
+def test_c2_fast_matches_oracle(gpu, oracle):
+    prob = P.baseline_config("C2")
+    got = gpu.assemble_fast(prob)
+    want = oracle.assemble(prob, "fast")
+    assert_csr_match(got.astuple(), want, RTOL)
+
+
+def test_c1_standard_matches_oracle_and_fast(gpu, oracle):
+    prob = P.baseline_config("C1")
+    std = gpu.assemble_standard(prob)
+    assert_csr_match(std.astuple(), oracle.assemble(prob, "standard"), RTOL)
+    fast = gpu.assemble_fast(prob)
+    assert np.array_equal(std.cols, fast.cols)
+    assert csr_rel_diff(std.astuple(), fast.astuple()) <= RTOL
+
+
+def test_c1_voigt_free_matches_fast(gpu, oracle):
+    prob = P.baseline_config("C1")
+    vf = gpu.assemble_voigt_free(prob)
+    assert_csr_match(vf.astuple(), oracle.assemble(prob, "fast"), 1e-12)
+
+
+@pytest.mark.parametrize("degree,elems,angles,geom", [
+    (1, 1, [0.0], "flat"),
+    (2, 2, [0.0, 1.5707963267948966, 0.0], "skewed"),
+    (3, 2, [0.0, 0.7853981633974483, -0.7853981633974483, 1.5707963267948966], "flat"),
+])
+def test_reference_fast_equals_standard_cases(gpu, oracle, degree, elems, angles, geom):
+    """test_fast.cpp:310-333 on the GPU, each backend against the oracle."""
+    prob = P.cube_problem(degree, elems, 1, angles, geometry=geom)
+    fast = gpu.assemble_fast(prob)
+    std = gpu.assemble_standard(prob)
+    vf = gpu.assemble_voigt_free(prob)
+    assert_csr_match(fast.astuple(), oracle.assemble(prob, "fast"), RTOL)
+    assert_csr_match(std.astuple(), oracle.assemble(prob, "standard"), RTOL)
+    assert fast.nnz == std.nnz
+    assert csr_rel_diff(fast.astuple(), std.astuple()) <= RTOL
+    assert csr_rel_diff(vf.astuple(), std.astuple()) <= RTOL
+
+
+def test_mixed_degrees_and_c0_thickness(gpu, oracle):
+    """Shapes no reference test covers (SURVEY.md §4 gaps): p_u != p_v != p_t,
+    C0 thickness knots, non-square plate, skewed geometry."""
+    prob = P.LaminateProblem(
+        degree_u=2, degree_v=3, degree_t=2, knots_u=P.uniform_knots(2, 3),
+        knots_v=P.uniform_knots(3, 2), knots_t=P.c0_knots(2, 3),
+        interfaces=P.equal_interfaces(3),
+        layers=[(P.baseline_orthotropic(), 0.0), (P.isotropic(0.5, 0.3), 0.0),
+                (P.baseline_orthotropic(), 0.6)])
+    for geom in ("flat", "skewed"):
+        if geom == "skewed":
+            prob = prob.replace(geometry_kind=1,
+                                geometry=(0, 0, 0, 1.2, 0.1, 0.05, -0.1, 0.9, -0.02, 1.0, 1.1, 0.08),
+                                direction=(0.03, -0.02, 0.2))
+        for backend in ("fast", "standard"):
+            got = gpu.assemble_with(backend, prob)
+            assert_csr_match(got.astuple(), oracle.assemble(prob, backend), RTOL)
+
+
+def test_active_layers_patterns(gpu, oracle):
+    """Standard drops thickness spans whose cells are all masked; fast keeps
+    the full pattern (assembly.cpp:82-84 vs fast.cpp:203)."""
+    prob = P.baseline_config("C1").replace(active_layers=[1])
+    for backend in ("fast", "standard"):
+        got = gpu.assemble_with(backend, prob)
+        assert_csr_match(got.astuple(), oracle.assemble(prob, backend), RTOL)
+    assert gpu.pattern_size(prob, "standard")[1] < gpu.pattern_size(prob, "fast")[1]
+
+
+def test_layer_restriction_is_additive(gpu):
+    """test_fast.cpp:377-388: sum over single-layer assemblies equals the whole."""
+    prob = P.cube_problem(2, 2, 1, [0.0, 0.9, 0.3], geometry="skewed")
+    whole = gpu.assemble_fast(prob)
+    x = np.random.default_rng(31).uniform(-1, 1, whole.dim)
+    import scipy.sparse as sp
+    K = sp.csr_matrix((whole.values, whole.cols, whole.row_ptr), shape=(whole.dim,) * 2)
+    acc = np.zeros(whole.dim)
+    for l in range(3):
+        part = gpu.assemble_fast(prob.replace(active_layers=[l]))
+        acc += sp.csr_matrix((part.values, part.cols, part.row_ptr), shape=(whole.dim,) * 2) @ x
+    y = K @ x
+    assert np.linalg.norm(y - acc) <= 1e-13 * np.linalg.norm(y)
+
+
+def test_decompose_angles(gpu, oracle):
+    """test_fast.cpp:390-408: five builds per material; equals direct."""
+    rng = P.MT19937(99)
+    angles = [-1.6 + 3.2 * (rng() / 2**32) for _ in range(9)]
+    prob = P.cube_problem(2, 2, 1, angles, geometry="skewed")
+    direct = gpu.assemble_fast(prob)
+    assert direct.stats.operator_builds == 9
+    dec = gpu.assemble_fast(prob.replace(decompose_angles=True))
+    assert dec.stats.operator_builds == 5
+    assert csr_rel_diff(dec.astuple(), direct.astuple()) <= 1e-12
+    assert_csr_match(dec.astuple(), oracle.assemble(prob.replace(decompose_angles=True), "fast"), 1e-12)
+
+
+def test_many_terms_multi_pass(gpu, oracle):
+    """More than 8 operator terms exercises the accumulate passes of K4."""
+    angles = [0.1 * k for k in range(11)]
+    prob = P.cube_problem(2, 2, 2, angles)
+    got = gpu.assemble_fast(prob)
+    assert got.stats.operator_builds == 11
+    assert_csr_match(got.astuple(), oracle.assemble(prob, "fast"), RTOL)
+
+
+def test_stats_counters(gpu):
+    """test_fast.cpp:335-352 work accounting."""
+    angles = [0.0 if l % 2 == 0 else 1.5707963267948966 for l in range(32)]
+    prob = P.cube_problem(3, 2, 1, angles)
+    fast = gpu.assemble_fast(prob)
+    assert fast.stats.operator_builds == 2
+    assert fast.stats.qpoint_visits == 2 * 4 * 16
+    std = gpu.assemble_standard(prob)
+    assert std.stats.qpoint_visits == 32 * 4 * 16 * 4
+
+
+def test_inplane_operators_match_reference(gpu, reference):
+    """test_fast.cpp:278-289: P against the reference on skewed geometry,
+    4 in-plane points, p_u=2, p_v=3, theta=0.6."""
+    prob = P.LaminateProblem(
+        degree_u=2, degree_v=3, degree_t=2, knots_u=P.uniform_knots(2, 3),
+        knots_v=P.uniform_knots(3, 2), knots_t=P.uniform_knots(2, 1),
+        interfaces=P.equal_interfaces(1), layers=[(P.pagano(), 0.0)],
+        geometry_kind=1, geometry=(0, 0, 0, 1.2, 0.1, 0.05, -0.1, 0.9, -0.02, 1.0, 1.1, 0.08),
+        direction=(0.03, -0.02, 0.2), inplane_points=4)
+    d = reference.stiffness(P.pagano(), 0.6)
+    got, gflags, _ = gpu.compute_inplane_operators(prob, d)
+    want, wflags = reference.inplane_operators(prob, d)
+    assert np.array_equal(gflags, wflags)
+    assert np.abs(got - want).max() <= 1e-14 * np.abs(want).max()
+
+
+def test_inplane_operators_affine_and_corner_block(gpu):
+    """test_fast.cpp:268-276: P22(0,0) = diag(1/18, 1/18, 1/9)."""
+    prob = P.cube_problem(1, 1, 1, [0.0], thickness=1.0, material=P.isotropic(1.0, 0.0))
+    d = np.diag([1, 1, 1, 0.5, 0.5, 0.5]).astype(float)
+    blocks, flags, _ = gpu.compute_inplane_operators(prob, d)
+    # slot of (0, 0): dv = 0 + p_v, du = 0 + p_u in the band
+    b = blocks[3, 0, 1, 1]
+    assert np.abs(b - np.diag([1 / 18, 1 / 18, 1 / 9])).max() <= 1e-15
+
+
+def test_thickness_operators_closed_form(gpu):
+    """test_fast.cpp:171-188."""
+    q, occ = gpu.compute_thickness_operators(1, P.uniform_knots(1, 1), [0.0, 1.0], 2)
+    fam = q[0]
+    assert np.abs(fam[0] - [[1 / 3, 1 / 6], [1 / 6, 1 / 3]]).max() <= 1e-15
+    assert np.abs(fam[1] - [[-0.5, 0.5], [-0.5, 0.5]]).max() <= 1e-15
+    assert np.abs(fam[2] - [[-0.5, -0.5], [0.5, 0.5]]).max() <= 1e-15
+    assert np.abs(fam[3] - [[1, -1], [-1, 1]]).max() <= 1e-15
+    assert occ[0, 1] == 1
+
+
+def test_thickness_operators_match_reference(gpu, reference):
+    kt = P.uniform_knots(3, 2)
+    ifc = [0.0, 0.2, 0.5, 0.7, 1.0]
+    got, gocc = gpu.compute_thickness_operators(3, kt, ifc, 4)
+    want, wocc = reference.thickness_operators(3, kt, ifc, 4)
+    assert np.array_equal(gocc, wocc)
+    assert np.abs(got - want).max() <= 1e-15
+    assert gocc[0, 4] == 0 and gocc[1, 4] == 1
+
+
+def test_combine_operators_long_form(gpu, oracle):
+    """test_fast.cpp:354-375: per-layer long form == pre-reduced q~."""
+    prob = P.cube_problem(2, 2, 2, [0.0, 1.5707963267948966, 1.5707963267948966, 0.0],
+                          lx=1.3, ly=0.8, thickness=0.2)
+    reduced = gpu.assemble_fast(prob)
+    q, occ = gpu.compute_thickness_operators(2, prob.knots_t, prob.interfaces, 3)
+    sets = {}
+    for c, a in prob.layers:
+        if a not in sets:
+            d = oracle.stiffness(c, a)
+            sets[a] = gpu.compute_inplane_operators(prob, d)
+    blocks = np.stack([sets[a][0] for _, a in prob.layers])
+    flags = sets[prob.layers[0][1]][1]
+    long_form = gpu.combine_operators(prob, blocks, flags, q, occ)
+    assert long_form.nnz == reduced.nnz
+    assert csr_rel_diff(long_form.astuple(), reduced.astuple()) <= 1e-14
+
+
+def test_degenerate_geometry_raises_domain_error(gpu):
+    prob = P.cube_problem(1, 1, 1, [0.0]).replace(direction=(1.0, 0.0, 0.0))
+    with pytest.raises(gpu.LamfastError) as e:
+        gpu.assemble_fast(prob)
+    assert e.value.kind == "domain_error"
+
+
+def test_row_slabs_match_oracle_slabs(gpu, oracle):
+    """Slab plans (the multi-GPU unit) against oracle slab mode."""
+    import torch
+    prob = P.baseline_config("C2")
+    for parts in (2, 3):
+        for part in range(parts):
+            b = gpu.slab_bounds(prob, parts, part)
+            plan = gpu.Plan(prob, "fast", 0, b["t_begin"], b["t_end"])
+            rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
+            cols = torch.empty(max(1, plan.nnz), dtype=torch.int32, device="cuda")
+            vals = torch.empty(max(1, plan.nnz), dtype=torch.float64, device="cuda")
+            plan.build_pattern(rp.data_ptr(), cols.data_ptr())
+            plan.assemble(vals.data_ptr())
+            plan.synchronize()
+            want = oracle.assemble(prob, "fast", b["t_begin"], b["t_end"])
+            assert_csr_match((rp.cpu().numpy(), cols.cpu().numpy()[:plan.nnz],
+                              vals.cpu().numpy()[:plan.nnz]), want, RTOL)
+            plan.close()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_full_size_config_slab_and_properties(gpu, oracle, name):
+    """BASELINE C3/C4 at full size on the device: an oracle-checked slab,
+    plus size-independent properties of the whole matrix (rigid
+    translations annihilated, symmetry, nnz)."""
+    import torch
+    prob = P.baseline_config(name)
+    plan = gpu.Plan(prob, "fast", 0)
+    assert plan.nnz == P.sizes(prob)["nnz"]
+    rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
+    cols = torch.empty(plan.nnz, dtype=torch.int32, device="cuda")
+    vals = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
+    plan.build_pattern(rp.data_ptr(), cols.data_ptr())
+    plan.assemble(vals.data_ptr())
+    plan.synchronize()
+    # slab check: rows of thickness functions [t, t+3) from the middle
+    t = prob.n_t // 2
+    want = oracle.assemble(prob, "fast", t, t + 3)
+    r0 = 3 * prob.n_s * t
+    r1 = 3 * prob.n_s * (t + 3)
+    z0, z1 = int(rp[r0]), int(rp[r1])
+    got = ((rp[r0:r1 + 1] - z0).cpu().numpy(), cols[z0:z1].cpu().numpy(), vals[z0:z1].cpu().numpy())
+    assert_csr_match(got, want, RTOL)
+    # translations: K t = 0 for rigid translations (acceptance.cpp:95-104)
+    lib = gpu.library()
+    st = gpu.device_csr_stats(plan.rows, rp.data_ptr(), cols.data_ptr(), vals.data_ptr())
+    norm = np.sqrt(st["fro_sq"])
+    assert np.sqrt(st["sym_sq"]) / norm <= 1e-13
+    import ctypes
+    for d in range(3):
+        x = torch.zeros(plan.rows, dtype=torch.float64, device="cuda")
+        x[d::3] = 1.0
+        y = torch.empty_like(x)
+        assert lib.lf_csr_spmv(plan.rows, ctypes.c_void_p(rp.data_ptr()), ctypes.c_void_p(cols.data_ptr()),
+                               ctypes.c_void_p(vals.data_ptr()), ctypes.c_void_p(x.data_ptr()),
+                               ctypes.c_void_p(y.data_ptr()), None) == 0
+        torch.cuda.synchronize()
+        assert float(y.abs().max()) / norm <= 1e-12
+    plan.close()

@@ -1,0 +1,41 @@
+#!/usr/bin/env python
+"""Runs K fast-assembly steps of a BASELINE config on cuda:0 (for ncu / nsight
+captures and quick timing).  Prints per-kernel event timing."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paper_1905_05417_b200 as lf  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="C4")
+ap.add_argument("--steps", type=int, default=3)
+ap.add_argument("--backend", default="fast")
+ap.add_argument("--plies", type=int, default=0)
+a = ap.parse_args()
+prob = lf.baseline_config(a.config, plies=a.plies or None)
+s = torch.cuda.Stream()
+torch.cuda.set_stream(s)
+plan = lf.Plan(prob, a.backend, 0, stream=s.cuda_stream)
+vals = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
+rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
+cols = torch.empty(plan.nnz, dtype=torch.int32, device="cuda")
+plan.build_pattern(rp.data_ptr(), cols.data_ptr())
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+plan.assemble(vals.data_ptr())
+torch.cuda.synchronize()
+plan.kernel_time(reset=True)
+e0.record(s)
+for _ in range(a.steps):
+    plan.assemble(vals.data_ptr())
+e1.record(s)
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / a.steps
+kms, kn = plan.kernel_time(reset=True)
+print(f"{a.config} {a.backend} nnz={plan.nnz} step={ms:.3f} ms combine={kms / max(kn, 1):.3f} ms "
+      f"-> {plan.nnz / ms / 1e6:.3e} nnz/s, combine {plan.nnz * 8 / (kms / max(kn, 1)) / 1e6:.1f} GB/s, "
+      f"launches/step={plan.launch_count}")
