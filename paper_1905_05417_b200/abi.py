@@ -12,7 +12,7 @@ import os
 from ctypes import POINTER, c_char, c_char_p, c_double, c_int, c_int32, c_int64, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "liblamfast_b200.so")
+LIB_PATH = os.environ.get("LAMFAST_LIB") or os.path.join(_HERE, "lib", "liblamfast_b200.so")
 
 LF_OK = 0
 LF_ERR_INVALID_ARGUMENT = 1

@@ -21,6 +21,22 @@ namespace lfb {
 namespace {
 
 constexpr int kBlock = 256;
+#ifdef LF_COMBINE_MIN_BLOCKS
+#define LF_COMBINE_BOUNDS __launch_bounds__(kBlock, LF_COMBINE_MIN_BLOCKS)
+#else
+#define LF_COMBINE_BOUNDS __launch_bounds__(kBlock)
+#endif
+
+/// Output store of the combine kernel: st.global.cs (evict-first), the
+/// values are written once and never re-read by this kernel (measured
+/// 3.24 -> 3.15 ms on C4, profiles/round1.md).
+__device__ __forceinline__ void store_value(double* p, double v) {
+#ifdef LF_PLAIN_STORES
+    *p = v;
+#else
+    __stcs(p, v);
+#endif
+}
 
 __device__ __forceinline__ int find_is(const long long* es_pre, int ns, long long e) {
     int lo = 0, hi = ns; // es_pre[lo] <= e < es_pre[hi]
@@ -149,7 +165,7 @@ __device__ __forceinline__ void combine_row(const double (&P)[NT][4], const doub
     }
 #pragma unroll
     for (int k = 0; k < LT; ++k)
-        o[(long long)k * B] = acc[k];
+        store_value(o + (long long)k * B, acc[k]);
 }
 
 template <int NT, bool ACCUM>
@@ -167,12 +183,12 @@ __device__ __forceinline__ void combine_row_dyn(const double (&P)[NT][4], const 
                 acc = fma(P[t][3], ww.w, acc);
             }
         }
-        o[(long long)k * B] = acc;
+        store_value(o + (long long)k * B, acc);
     }
 }
 
 template <int NT, bool AFFINE, bool ACCUM>
-__global__ void __launch_bounds__(kBlock) k_combine(const DevTables d, double* __restrict__ out,
+__global__ void LF_COMBINE_BOUNDS k_combine(const DevTables d, double* __restrict__ out,
                                                     int pass, int t_chunk, int stage_rows, int lt_max) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     RowInfo* s_row = reinterpret_cast<RowInfo*>(smem_raw);

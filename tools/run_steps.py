@@ -16,7 +16,28 @@ ap.add_argument("--config", default="C4")
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--backend", default="fast")
 ap.add_argument("--plies", type=int, default=0)
+ap.add_argument("--calibrate", action="store_true")
 a = ap.parse_args()
+if a.calibrate:
+    # same-box write-only and copy bandwidth of a buffer the size of C4's values
+    n = 1924851600
+    buf = torch.empty(n, dtype=torch.float64, device="cuda")
+    src = torch.empty(n // 2, dtype=torch.float64, device="cuda")
+    dst = torch.empty(n // 2, dtype=torch.float64, device="cuda")
+    for name, fn, nbytes in (("fill", lambda: buf.fill_(1.0), n * 8),
+                             ("copy", lambda: dst.copy_(src), n * 8)):
+        fn()
+        torch.cuda.synchronize()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(10):
+            fn()
+        t1.record()
+        torch.cuda.synchronize()
+        ms = t0.elapsed_time(t1) / 10
+        print(f"calibrate {name}: {nbytes / ms / 1e6:.1f} GB/s ({ms:.3f} ms)")
+    del buf, src, dst
+    torch.cuda.empty_cache()
 prob = lf.baseline_config(a.config, plies=a.plies or None)
 s = torch.cuda.Stream()
 torch.cuda.set_stream(s)
