@@ -272,3 +272,45 @@ def test_full_size_config_slab_and_properties(gpu, oracle, name):
         torch.cuda.synchronize()
         assert float(y.abs().max()) / norm <= 1e-12
     plan.close()
+
+
+# ---- against the frozen outputs of the unmodified reference -------------------
+
+import json as _json
+import os as _os
+import sys as _sys
+
+_GOLD_DIR = _os.path.join(_os.path.dirname(_os.path.abspath(__file__)), "golden")
+_sys.path.insert(0, _GOLD_DIR)
+from cases import cases as _cases  # noqa: E402
+
+
+@pytest.mark.parametrize("name", list(_cases().keys()))
+def test_gpu_matches_reference_fixtures(gpu, name):
+    gold = np.load(_os.path.join(_GOLD_DIR, "ref_small.npz"))
+    with open(_os.path.join(_GOLD_DIR, "ref_summaries.json")) as f:
+        meta = _json.load(f)["small"]
+    prob, backends = _cases()[name]
+    for b in backends:
+        key = f"{name}__{b}"
+        want = (gold[key + "__row_ptr"], gold[key + "__cols"], gold[key + "__values"])
+        got = gpu.assemble_with(b, prob)
+        assert_csr_match(got.astuple(), want, RTOL)
+        assert csr_rel_diff(got.astuple(), want) <= RTOL
+        assert got.stats.qpoint_visits == meta[key]["qpoint_visits"]
+        assert got.stats.frame_evaluations == meta[key]["frame_evaluations"]
+        assert got.stats.operator_builds == meta[key]["operator_builds"]
+
+
+def test_gpu_matches_reference_c1_c2_summaries(gpu):
+    import hashlib
+    with open(_os.path.join(_GOLD_DIR, "ref_summaries.json")) as f:
+        summ = _json.load(f)["baseline"]
+    for key, s in summ.items():
+        name, b = key.split("__")
+        got = gpu.assemble_with(b, P.baseline_config(name))
+        assert hashlib.sha256(got.row_ptr.tobytes()).hexdigest() == s["row_ptr_sha256"]
+        assert hashlib.sha256(got.cols.tobytes()).hexdigest() == s["cols_sha256"]
+        assert np.sqrt(got.values @ got.values) == pytest.approx(s["fro"], rel=1e-13)
+        idx = np.asarray(s["sample_idx"])
+        assert np.abs(got.values[idx] - s["sample_values"]).max() <= RTOL * s["max_abs"]

@@ -1,0 +1,170 @@
+"""Host-side logic of the product library, CPU only (no compute calls):
+C-ABI exports, host setup mirrors, closed-form pattern sizes and slabs,
+error mapping, problem builders, and the no-fallback guarantee."""
+import ctypes
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1905_05417_b200 as lf
+from paper_1905_05417_b200 import abi
+from paper_1905_05417_b200 import problem as P
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+with open(os.path.join(ROOT, "tests", "golden", "ref_summaries.json")) as f:
+    SUMMARY = json.load(f)
+
+
+def declared_symbols():
+    text = open(os.path.join(ROOT, "include", "lamfast_cuda.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(lf_\w+)\(", text, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = lf.library()
+    names = declared_symbols()
+    assert len(names) >= 25
+    for n in names:
+        assert hasattr(lib, n), n
+    assert {n for n, _, _ in abi.SIGNATURES} == set(names)
+    assert lib.lf_abi_version() == 1
+    assert lib.lf_status_name(2) == b"domain_error"
+
+
+def test_compute_entry_points_fail_loudly_without_gpu():
+    lib = lf.library()
+    if lib.lf_device_count() > 0:
+        pytest.skip("a GPU is present")
+    with pytest.raises(lf.LamfastError) as e:
+        lf.assemble_fast(P.baseline_config("C1"))
+    assert "no CUDA device" in str(e.value) and e.value.status == abi.LF_ERR_CUDA
+
+
+def test_voigt_and_rotation_match_reference_known_answers(oracle):
+    lib = lf.library()
+    d = (ctypes.c_double * 36)()
+    assert lib.lf_voigt_from_constants(ctypes.byref(abi.Orthotropic(*P.pagano())), d) == 0
+    np.testing.assert_allclose(np.array(d).reshape(6, 6), SUMMARY["known_answers"]["pagano_D"],
+                               atol=1e-14)
+    r = (ctypes.c_double * 36)()
+    assert lib.lf_rotate_inplane(d, 0.6, r) == 0
+    np.testing.assert_allclose(np.array(r).reshape(6, 6), oracle.stiffness(P.pagano(), 0.6),
+                               atol=1e-14)
+
+
+def test_bracket_parameters_known_values():
+    """test_voigt_free.cpp:77-88."""
+    out = (ctypes.c_double * 9)()
+    assert lf.library().lf_bracket_parameters(ctypes.byref(abi.Orthotropic(*P.pagano())), out) == 0
+    b = np.array(out)
+    np.testing.assert_allclose(b[0], 0.07114093959731704, rtol=1e-11)
+    np.testing.assert_allclose(b[1], 0.5, rtol=1e-12)
+    np.testing.assert_allclose(b[2:], [24.767785234899335, -0.4, -0.3, 0, 0.2644295302013404,
+                                       0.2, -0.2], rtol=1e-11, atol=1e-12)
+    np.testing.assert_allclose(b, SUMMARY["known_answers"]["bracket_pagano"], rtol=1e-12, atol=1e-13)
+
+
+def test_angle_decomposition_matches_reference():
+    out = (ctypes.c_double * 180)()
+    assert lf.library().lf_angle_decomposition(ctypes.byref(abi.Orthotropic(*P.pagano())), out) == 0
+    np.testing.assert_allclose(np.array(out).reshape(5, 6, 6),
+                               SUMMARY["known_answers"]["angle_decomposition_pagano"], atol=1e-11)
+
+
+def test_layup_dedup():
+    """test_materials.cpp:170-224: cross-ply -> 2 configs, quad-ply -> 4."""
+    lib = lf.library()
+    for prob, want in ((P.baseline_config("C2"), 2), (P.baseline_config("C3"), 4),
+                       (P.baseline_config("C4"), 3), (P.baseline_config("C5"), 4)):
+        c = prob.to_c()
+        n = ctypes.c_int32()
+        ids = (ctypes.c_int32 * prob.n_layers)()
+        assert lib.lf_layup_configs(ctypes.byref(c), ctypes.byref(n), ids, None) == 0
+        assert n.value == want
+        # first-appearance order
+        seen = []
+        for l in range(prob.n_layers):
+            if prob.layers[l] not in seen:
+                seen.append(prob.layers[l])
+            assert ids[l] == seen.index(prob.layers[l])
+
+
+def test_baseline_sizes_match_survey():
+    """SURVEY.md Appendix A.1."""
+    want = {"C1": (2700, 574992), "C2": (114444, 31226256), "C3": (1737243, 964255833),
+            "C4": (6615180, 1924851600), "C5": (29317275, 16887368025)}
+    for name, (dim, nnz) in want.items():
+        prob = P.baseline_config(name)
+        assert lf.pattern_size(prob) == (dim, nnz)
+        assert P.sizes(prob)["nnz"] == nnz
+
+
+def test_pattern_size_matches_oracle_counts(oracle):
+    for prob in (P.baseline_config("C1"), P.cube_problem(3, 2, 1, [0.0, 0.5]),
+                 P.baseline_config("C1").replace(active_layers=[0, 3])):
+        for b in ("fast", "standard"):
+            rp, _, _ = oracle.assemble(prob, b)
+            assert lf.pattern_size(prob, b) == (prob.dim, int(rp[-1]))
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3, 4, 8])
+def test_slab_bounds_tile_rows_and_balance(parts):
+    prob = P.baseline_config("C5")
+    dim, nnz = lf.pattern_size(prob)
+    prev_t, prev_r, prev_z = 0, 0, 0
+    sizes = []
+    for k in range(parts):
+        b = lf.slab_bounds(prob, parts, k)
+        assert b["t_begin"] == prev_t and b["row_begin"] == prev_r and b["nnz_begin"] == prev_z
+        prev_t, prev_r, prev_z = b["t_end"], b["row_end"], b["nnz_end"]
+        sizes.append(b["nnz_end"] - b["nnz_begin"])
+    assert (prev_t, prev_r, prev_z) == (prob.n_t, dim, nnz)
+    assert max(sizes) / (nnz / parts) < 1.05
+
+
+def test_error_mapping():
+    bad_knots = P.baseline_config("C1").replace(knots_u=np.array([0.0, 0.5, 1.0, 1.0, 1.0, 1.0]))
+    with pytest.raises(lf.LamfastError) as e:
+        lf.pattern_size(bad_knots)
+    assert e.value.kind == "invalid_argument"
+    bad_ifc = P.baseline_config("C1").replace(interfaces=np.array([0.0, 0.5, 0.4, 0.9, 1.0]))
+    with pytest.raises(lf.LamfastError) as e:
+        lf.pattern_size(bad_ifc)
+    assert e.value.kind == "invalid_argument"
+    bad_mat = P.baseline_config("C1").replace(layers=[(P.orthotropic(-1, 1, 1, 1, 1, 1, 0, 0, 0), 0.0)] * 4)
+    with pytest.raises(lf.LamfastError) as e:
+        lf.pattern_size(bad_mat)
+    assert e.value.kind == "invalid_argument"
+    with pytest.raises(lf.LamfastError) as e:
+        lf.pattern_size(P.cube_problem(1, 1, 1, [0.0]).replace(direction=(1.0, 0.0, 0.0)))
+    assert e.value.kind == "domain_error"
+    with pytest.raises(lf.LamfastError) as e:
+        lf.pattern_size(P.baseline_config("C1").replace(knots_u=P.uniform_knots(7, 2), degree_u=7))
+    assert e.value.kind == "unsupported"
+
+
+def test_mt19937_matches_std():
+    """std::mt19937 default seed 5489: the 10000th output is 4123659995 (C++11 standard)."""
+    rng = P.MT19937(5489)
+    out = [rng() for _ in range(10000)]
+    assert out[0] == 3499211612
+    assert out[-1] == 4123659995
+
+
+def test_baseline_layups():
+    c4 = P.baseline_config("C4")
+    assert c4.distinct_configs() == 3 and c4.n_layers == 128
+    assert c4.layers[1][0] == P.isotropic(0.5, 0.3) and c4.layers[2][1] == P.DEG90
+    c5 = P.baseline_config("C5")
+    assert c5.distinct_configs() == 4 and c5.n_layers == 128
+    assert P.baseline_config("C2").layers[7][1] == P.DEG90 and P.baseline_config("C2").layers[8][1] == P.DEG90
+
+
+def test_c0_knots_align_with_interfaces():
+    kt = P.c0_knots(2, 128)
+    ifc = P.equal_interfaces(128)
+    interior = kt[3:-3:2]
+    assert np.array_equal(interior, ifc[1:-1])  # bit-identical: no sliver cells
