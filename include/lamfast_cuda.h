@@ -17,6 +17,9 @@
  *   lf_voigt_from_constants / lf_rotate_inplane / lf_angle_decomposition
  *                                              materials.hpp:55,62,68 (host setup, shared)
  *   lf_bracket_parameters                      bracketParameters  voigt_free.hpp:26
+ *   lf_contraction_table                       ContractionTable   voigt_free.hpp:41
+ *   lf_gauss_legendre / lf_basis_eval          gaussLegendre quadrature.hpp:20-23,
+ *                                              KnotVector::evaluate splines.hpp:45
  *   lf_csr_* (device verification)             StiffnessMatrix::{frobeniusNorm,symmetryRelError,apply},
  *                                              frobeniusRelDiff   sparse.hpp:45-69,83
  *
@@ -139,6 +142,14 @@ int lf_voigt_from_constants(const lf_orthotropic* c, double d_out[36]);
 int lf_rotate_inplane(const double d[36], double theta, double d_out[36]);
 int lf_angle_decomposition(const lf_orthotropic* c, double out[5 * 36]);
 int lf_bracket_parameters(const lf_orthotropic* c, double out[9]);
+/* gaussLegendre(n, a, b) (quadrature.cpp:9-57). */
+int lf_gauss_legendre(int32_t n, double a, double b, double* points, double* weights);
+/* KnotVector::evaluate (splines.cpp:53-101): p+1 values/derivatives at x. */
+int lf_basis_eval(int32_t degree, int32_t n_knots, const double* knots, double x,
+                  int32_t* first_active, double* values, double* derivs);
+/* ContractionTable(params, angle) entries, table[(3i+j)*9 + 3r + c]
+ * (voigt_free.cpp:89-123); params = lambda, mu, alpha[7]. */
+int lf_contraction_table(const double params[9], double angle, double table[81]);
 /* Distinct configurations of the layup: n_configs, per-layer config id,
  * rotated stiffness per config (row-major 6x6).  Arrays sized n_layers. */
 int lf_layup_configs(const lf_problem* p, int32_t* n_configs, int32_t* layer_config,

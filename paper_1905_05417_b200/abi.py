@@ -95,6 +95,10 @@ SIGNATURES = [
     ("lf_rotate_inplane", c_int, [_P(c_double), c_double, _P(c_double)]),
     ("lf_angle_decomposition", c_int, [_P(Orthotropic), _P(c_double)]),
     ("lf_bracket_parameters", c_int, [_P(Orthotropic), _P(c_double)]),
+    ("lf_gauss_legendre", c_int, [c_int32, c_double, c_double, _P(c_double), _P(c_double)]),
+    ("lf_basis_eval", c_int, [c_int32, c_int32, _P(c_double), c_double, _P(c_int32), _P(c_double),
+                              _P(c_double)]),
+    ("lf_contraction_table", c_int, [_P(c_double), c_double, _P(c_double)]),
     ("lf_layup_configs", c_int, [_P(Problem), _P(c_int32), _P(c_int32), _P(c_double)]),
     ("lf_pattern_size", c_int, [_P(Problem), c_int, _P(c_int64), _P(c_int64)]),
     ("lf_slab_bounds", c_int, [_P(Problem), c_int, c_int, c_int, _P(c_int32), _P(c_int32),

@@ -417,6 +417,22 @@ int lf_bracket_parameters(const lf_orthotropic* c, double out[9]) {
     return guarded([&] { lfb::bracketParameters(*c, out); });
 }
 
+int lf_gauss_legendre(int32_t n, double a, double b, double* points, double* weights) {
+    return guarded([&] { lfb::gaussLegendre(n, a, b, points, weights); });
+}
+
+int lf_basis_eval(int32_t degree, int32_t n_knots, const double* knots, double x, int32_t* first_active,
+                  double* values, double* derivs) {
+    return guarded([&] {
+        const lfb::Knots kv = lfb::makeKnots(degree, n_knots, knots, "evaluate");
+        *first_active = lfb::evaluateBasis(kv, x, values, derivs);
+    });
+}
+
+int lf_contraction_table(const double params[9], double angle, double table[81]) {
+    return guarded([&] { lfb::contractionTable(params, angle, table); });
+}
+
 int lf_layup_configs(const lf_problem* p, int32_t* n_configs, int32_t* layer_config, double* config_stiffness) {
     return guarded([&] {
         const lfb::LayupInfo L = lfb::buildLayup(*p);

@@ -99,6 +99,51 @@ Knots makeKnots(int degree, int n_knots, const double* knots, const char* which)
     return kv;
 }
 
+int evaluateBasis(const Knots& kv, double x, double* vals, double* ders) {
+    if (x < 0.0 || x > 1.0)
+        raise(LF_ERR_DOMAIN, "KnotVector: point outside [0,1]");
+    const int p = kv.p, n = kv.n;
+    const std::vector<double>& t = kv.t;
+    int span;
+    if (x >= 1.0) {
+        span = n - 1;
+        while (span > p && t[static_cast<std::size_t>(span)] >= 1.0)
+            --span;
+    } else {
+        span = static_cast<int>(std::upper_bound(t.begin() + p, t.begin() + n + 1, x) - t.begin()) - 1;
+    }
+    double low[kMaxDegree + 2] = {0}, left[kMaxDegree + 2] = {0}, right[kMaxDegree + 2] = {0};
+    for (int r = 0; r <= p; ++r)
+        vals[r] = 0.0;
+    vals[0] = 1.0;
+    for (int level = 1; level <= p; ++level) {
+        if (level == p)
+            for (int r = 0; r <= p; ++r)
+                low[r] = vals[r];
+        left[level] = x - t[static_cast<std::size_t>(span + 1 - level)];
+        right[level] = t[static_cast<std::size_t>(span + level)] - x;
+        double saved = 0.0;
+        for (int r = 0; r < level; ++r) {
+            const double denom = right[r + 1] + left[level - r];
+            const double tmp = denom > 0.0 ? vals[r] / denom : 0.0;
+            vals[r] = saved + right[r + 1] * tmp;
+            saved = left[level - r] * tmp;
+        }
+        vals[level] = saved;
+    }
+    const int first = span - p;
+    for (int r = 0; r <= p; ++r) {
+        const std::size_t i = static_cast<std::size_t>(first + r);
+        double d = 0.0;
+        if (r >= 1 && t[i + p] - t[i] > 0.0)
+            d += low[r - 1] / (t[i + p] - t[i]);
+        if (r <= p - 1 && t[i + p + 1] - t[i + 1] > 0.0)
+            d -= low[r] / (t[i + p + 1] - t[i + 1]);
+        ders[r] = p * d;
+    }
+    return first;
+}
+
 std::vector<Span> elementSpans(const Knots& kv) {
     std::vector<Span> s;
     for (int k = kv.p; k <= kv.n - 1; ++k)

@@ -37,6 +37,10 @@ struct Knots {
 /// KnotVector ctor checks (splines.cpp:10-25).
 Knots makeKnots(int degree, int n_knots, const double* knots, const char* which);
 
+/// KnotVector::findSpan + evaluate (splines.cpp:37-101) on the host; returns
+/// first_active.  Throws LF_ERR_DOMAIN outside [0, 1].
+int evaluateBasis(const Knots& kv, double x, double* vals, double* ders);
+
 struct Span {
     double begin, end;
     int first;
