@@ -125,103 +125,141 @@ __device__ __forceinline__ void affine_p(const DevTables& d, int iu, int iv, int
 }
 
 // ---------------------------------------------------------------------------
-// K4: the hot kernel.  One thread per in-plane entry (i_s, a, slot, b); the
-// thread keeps its P_{t,f} for the pass's terms in registers and streams
-// over the thickness rows of its block-row chunk, writing one FP64 value per
-// thickness pair.  Consecutive lanes hold consecutive entries of one CSR row
-// segment, so every warp store is a contiguous 256-byte run.
+// K4: the hot kernel.  Each thread owns EPT in-plane entries (i_s, a, slot, b)
+// (entries e and e + 256 of a 256*EPT block), keeps their P_{t,f} for the
+// pass's terms in registers and streams over the thickness rows of its
+// block-row chunk, writing one FP64 value per (entry, thickness pair).
+// Consecutive lanes hold consecutive entries of one CSR row segment, so every
+// warp store is a contiguous 256-byte run.
 //
-// Per staged sub-chunk of thickness rows, the pair weights (warp-uniform)
-// sit in shared memory as s_w[row][k][term][4] and each row carries the
-// union mask of terms with any contributing cell.  A row is processed with
-// a compile-time neighbour count (switch on L_t), so the L_t accumulators
-// stay in registers, and each term is a uniform branch: a term absent from
-// the row costs nothing, a term present costs 2 LDS.128 + 4 DFMA per pair.
+// Per staged sub-chunk of thickness rows, the pair weights (warp-uniform) sit
+// in shared memory as s_w[row][k][term][4]; each row carries the union mask of
+// its terms and, per term, the neighbour range [k_lo, k_hi) holding that
+// term's contributing pairs.  A row is processed with a compile-time
+// neighbour count (switch on L_t) so the accumulators stay in registers; a
+// term absent from the row is a skipped uniform branch, and pairs outside the
+// term's range are predicated off (no shared-memory wavefront, no FMA).  With
+// EPT = 2 every weight load feeds two outputs.
 struct RowInfo {
     long long base; // 9 S_s (pre_t[it] - pre_t[t0]): slab offset of row block it
     int lt;         // L_t(it)
     unsigned mask;  // union of term masks over the row's pairs (this pass)
 };
 
-template <int NT, int LT, bool ACCUM>
-__device__ __forceinline__ void combine_row(const double (&P)[NT][4], const double4* __restrict__ w,
-                                            unsigned mask, double* __restrict__ o, int B) {
-    double acc[LT];
+template <int NT, int EPT, int LT, bool ACCUM>
+__device__ __forceinline__ void combine_row(const double (&P)[EPT][NT][4], const double4* __restrict__ w,
+                                            unsigned mask, const unsigned char* __restrict__ kr,
+                                            double* const (&o)[EPT], const int (&B)[EPT], const bool (&live)[EPT]) {
+    double acc[EPT][LT];
 #pragma unroll
-    for (int k = 0; k < LT; ++k)
-        acc[k] = ACCUM ? o[(long long)k * B] : 0.0;
+    for (int x = 0; x < EPT; ++x)
+#pragma unroll
+        for (int k = 0; k < LT; ++k)
+            acc[x][k] = (ACCUM && live[x]) ? o[x][(long long)k * B[x]] : 0.0;
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
         if (mask & (1u << t)) {
+            const int klo = kr[2 * t], khi = kr[2 * t + 1];
 #pragma unroll
             for (int k = 0; k < LT; ++k) {
-                const double4 ww = w[k * NT + t];
-                acc[k] = fma(P[t][0], ww.x, acc[k]);
-                acc[k] = fma(P[t][1], ww.y, acc[k]);
-                acc[k] = fma(P[t][2], ww.z, acc[k]);
-                acc[k] = fma(P[t][3], ww.w, acc[k]);
+#ifdef LF_NO_KRANGE
+                if (true) {
+#else
+                if (k >= klo && k < khi) {
+#endif
+                    const double4 ww = w[k * NT + t];
+#pragma unroll
+                    for (int x = 0; x < EPT; ++x) {
+                        acc[x][k] = fma(P[x][t][0], ww.x, acc[x][k]);
+                        acc[x][k] = fma(P[x][t][1], ww.y, acc[x][k]);
+                        acc[x][k] = fma(P[x][t][2], ww.z, acc[x][k]);
+                        acc[x][k] = fma(P[x][t][3], ww.w, acc[x][k]);
+                    }
+                }
             }
         }
     }
 #pragma unroll
-    for (int k = 0; k < LT; ++k)
-        store_value(o + (long long)k * B, acc[k]);
+    for (int x = 0; x < EPT; ++x)
+        if (live[x])
+#pragma unroll
+            for (int k = 0; k < LT; ++k)
+                store_value(o[x] + (long long)k * B[x], acc[x][k]);
 }
 
-template <int NT, bool ACCUM>
-__device__ __forceinline__ void combine_row_dyn(const double (&P)[NT][4], const double4* __restrict__ w,
-                                                int lt, unsigned mask, double* __restrict__ o, int B) {
+template <int NT, int EPT, bool ACCUM>
+__device__ __forceinline__ void combine_row_dyn(const double (&P)[EPT][NT][4], const double4* __restrict__ w,
+                                                int lt, unsigned mask, double* const (&o)[EPT], const int (&B)[EPT],
+                                                const bool (&live)[EPT]) {
     for (int k = 0; k < lt; ++k) {
-        double acc = ACCUM ? o[(long long)k * B] : 0.0;
+        double acc[EPT];
+#pragma unroll
+        for (int x = 0; x < EPT; ++x)
+            acc[x] = (ACCUM && live[x]) ? o[x][(long long)k * B[x]] : 0.0;
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
             if (mask & (1u << t)) {
                 const double4 ww = w[k * NT + t];
-                acc = fma(P[t][0], ww.x, acc);
-                acc = fma(P[t][1], ww.y, acc);
-                acc = fma(P[t][2], ww.z, acc);
-                acc = fma(P[t][3], ww.w, acc);
+#pragma unroll
+                for (int x = 0; x < EPT; ++x) {
+                    acc[x] = fma(P[x][t][0], ww.x, acc[x]);
+                    acc[x] = fma(P[x][t][1], ww.y, acc[x]);
+                    acc[x] = fma(P[x][t][2], ww.z, acc[x]);
+                    acc[x] = fma(P[x][t][3], ww.w, acc[x]);
+                }
             }
         }
-        store_value(o + (long long)k * B, acc);
+#pragma unroll
+        for (int x = 0; x < EPT; ++x)
+            if (live[x])
+                store_value(o[x] + (long long)k * B[x], acc[x]);
     }
 }
 
-template <int NT, bool AFFINE, bool ACCUM>
-__global__ void LF_COMBINE_BOUNDS k_combine(const DevTables d, double* __restrict__ out,
-                                                    int pass, int t_chunk, int stage_rows, int lt_max) {
+template <int NT, int EPT, bool AFFINE, bool ACCUM>
+__global__ void LF_COMBINE_BOUNDS k_combine(const DevTables d, double* __restrict__ out, int pass, int t_chunk,
+                                            int stage_rows, int lt_max) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     RowInfo* s_row = reinterpret_cast<RowInfo*>(smem_raw);
-    double4* s_w = reinterpret_cast<double4*>(smem_raw + ((stage_rows * sizeof(RowInfo) + 31) & ~31));
+    unsigned char* s_kr = smem_raw + stage_rows * sizeof(RowInfo); // [row][NT][2]
+    double4* s_w = reinterpret_cast<double4*>(
+        smem_raw + ((stage_rows * (sizeof(RowInfo) + 2 * NT) + 31) & ~31));
 
-    const long long e = (long long)blockIdx.x * kBlock + threadIdx.x;
-    const bool live = e < d.E;
-    const long long ec = live ? e : d.E - 1;
-    // i_s of this entry: forward scan from the block's first function
-    int is = __ldg(d.blk_is + blockIdx.x);
-    while (__ldg(d.es_pre + is + 1) <= ec)
-        ++is;
-    const long long ebase = __ldg(d.es_pre + is);
-    const int r = (int)(ec - ebase);
-    const int iu = is % d.nu, iv = is / d.nu;
-    const int Lu = __ldg(d.len_u + iu), Lv = __ldg(d.len_v + iv);
-    const int B = 3 * Lu * Lv; // row segment length per thickness neighbour
-    const int a = r / B;
-    const int rem = r - a * B;
-    const long long A = ebase + (long long)a * B;
     const int t_first = pass * 8;
-
-    double P[NT][4];
-    if constexpr (AFFINE) {
-        const int s = rem / 3, b = rem - 3 * (rem / 3);
-        const int sv = s / Lu, su = s - sv * Lu;
-        affine_p<NT>(d, iu, iv, su, sv, 3 * a + b, t_first, P);
-    } else {
+    double P[EPT][NT][4];
+    double* o_thread[EPT];
+    long long A[EPT];
+    int B[EPT];
+    bool live[EPT];
 #pragma unroll
-        for (int t = 0; t < NT; ++t)
+    for (int x = 0; x < EPT; ++x) {
+        const int sub = blockIdx.x * EPT + x; // 256-entry sub-block
+        const long long e = (long long)sub * kBlock + threadIdx.x;
+        live[x] = e < d.E;
+        const long long ec = live[x] ? e : d.E - 1;
+        int is = __ldg(d.blk_is + min((long long)sub, (d.E - 1) / kBlock));
+        while (__ldg(d.es_pre + is + 1) <= ec)
+            ++is;
+        const long long ebase = __ldg(d.es_pre + is);
+        const int r = (int)(ec - ebase);
+        const int iu = is % d.nu, iv = is / d.nu;
+        const int Lu = __ldg(d.len_u + iu), Lv = __ldg(d.len_v + iv);
+        B[x] = 3 * Lu * Lv; // row segment length per thickness neighbour
+        const int a = r / B[x];
+        const int rem = r - a * B[x];
+        A[x] = ebase + (long long)a * B[x];
+        o_thread[x] = out + (long long)rem;
+        if constexpr (AFFINE) {
+            const int s = rem / 3, b = rem - 3 * (rem / 3);
+            const int sv = s / Lu, su = s - sv * Lu;
+            affine_p<NT>(d, iu, iv, su, sv, 3 * a + b, t_first, P[x]);
+        } else {
 #pragma unroll
-            for (int f = 0; f < 4; ++f)
-                P[t][f] = __ldg(d.Pg + ((long long)(t_first + t) * 4 + f) * d.E + ec);
+            for (int t = 0; t < NT; ++t)
+#pragma unroll
+                for (int f = 0; f < 4; ++f)
+                    P[x][t][f] = __ldg(d.Pg + ((long long)(t_first + t) * 4 + f) * d.E + ec);
+        }
     }
 
     const int it_begin = d.t0 + blockIdx.y * t_chunk;
@@ -230,23 +268,45 @@ __global__ void LF_COMBINE_BOUNDS k_combine(const DevTables d, double* __restric
     const long long nine_S = 9 * d.S_s;
     const unsigned* mask_base = d.Wmask + (long long)pass * d.n_pairs;
     const int T = d.n_terms;
-    double* const o_thread = out + (long long)rem;
+    bool any_live = false;
+#pragma unroll
+    for (int x = 0; x < EPT; ++x)
+        any_live |= live[x];
 
     for (int it0 = it_begin; it0 < it_end; it0 += stage_rows) {
         const int nrow = min(stage_rows, it_end - it0);
         if (it0 != it_begin)
             __syncthreads();
-        // stage rows: RowInfo + weights s_w[row][k][t] (k < lt_max, zero padded)
+        // stage rows: RowInfo, per-term neighbour ranges, weights s_w[row][k][t]
         for (int rr = threadIdx.x; rr < nrow; rr += kBlock) {
             const int it = it0 + rr;
             const long long pfx = __ldg(d.pre_t + it) - pre0;
             const int lt = __ldg(d.len_t + it);
             unsigned m = 0;
-            for (int k = 0; k < lt; ++k)
-                m |= __ldg(mask_base + pfx + k);
+            unsigned char lo[NT], hi[NT];
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                lo[t] = 255;
+                hi[t] = 0;
+            }
+            for (int k = 0; k < lt; ++k) {
+                const unsigned mk = __ldg(mask_base + pfx + k);
+                m |= mk;
+#pragma unroll
+                for (int t = 0; t < NT; ++t)
+                    if (mk & (1u << t)) {
+                        lo[t] = min((int)lo[t], k);
+                        hi[t] = (unsigned char)(k + 1);
+                    }
+            }
             s_row[rr].base = nine_S * pfx;
             s_row[rr].lt = lt;
             s_row[rr].mask = m;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                s_kr[(rr * NT + t) * 2] = lo[t] == 255 ? 0 : lo[t];
+                s_kr[(rr * NT + t) * 2 + 1] = hi[t];
+            }
         }
         const int nw = nrow * lt_max * NT;
         for (int idx = threadIdx.x; idx < nw; idx += kBlock) {
@@ -258,26 +318,30 @@ __global__ void LF_COMBINE_BOUNDS k_combine(const DevTables d, double* __restric
             if (k < __ldg(d.len_t + it)) {
                 const long long q = __ldg(d.pre_t + it) - pre0 + k;
                 const double2* src = reinterpret_cast<const double2*>(d.W + ((q * T) + t_first + t) * 4);
-                const double2 lo = __ldg(src), hi = __ldg(src + 1);
-                v = make_double4(lo.x, lo.y, hi.x, hi.y);
+                const double2 lo2 = __ldg(src), hi2 = __ldg(src + 1);
+                v = make_double4(lo2.x, lo2.y, hi2.x, hi2.y);
             }
             s_w[idx] = v;
         }
         __syncthreads();
-        if (!live)
+        if (!any_live)
             continue;
         for (int rr = 0; rr < nrow; ++rr) {
             const RowInfo ri = s_row[rr];
-            double* o = o_thread + ri.base + (long long)ri.lt * A;
+            double* o[EPT];
+#pragma unroll
+            for (int x = 0; x < EPT; ++x)
+                o[x] = o_thread[x] + ri.base + (long long)ri.lt * A[x];
             const double4* w = s_w + rr * lt_max * NT;
+            const unsigned char* kr = s_kr + rr * NT * 2;
             switch (ri.lt) {
-            case 1: combine_row<NT, 1, ACCUM>(P, w, ri.mask, o, B); break;
-            case 2: combine_row<NT, 2, ACCUM>(P, w, ri.mask, o, B); break;
-            case 3: combine_row<NT, 3, ACCUM>(P, w, ri.mask, o, B); break;
-            case 4: combine_row<NT, 4, ACCUM>(P, w, ri.mask, o, B); break;
-            case 5: combine_row<NT, 5, ACCUM>(P, w, ri.mask, o, B); break;
-            case 7: combine_row<NT, 7, ACCUM>(P, w, ri.mask, o, B); break;
-            default: combine_row_dyn<NT, ACCUM>(P, w, ri.lt, ri.mask, o, B); break;
+            case 1: combine_row<NT, EPT, 1, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
+            case 2: combine_row<NT, EPT, 2, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
+            case 3: combine_row<NT, EPT, 3, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
+            case 4: combine_row<NT, EPT, 4, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
+            case 5: combine_row<NT, EPT, 5, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
+            case 7: combine_row<NT, EPT, 7, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
+            default: combine_row_dyn<NT, EPT, ACCUM>(P, w, ri.lt, ri.mask, o, B, live); break;
             }
         }
     }
@@ -681,11 +745,20 @@ int reduce_launch(int blocks, double* partial, double* out, cudaStream_t stream)
     return (int)cudaGetLastError();
 }
 
+#ifndef LF_COMBINE_EPT
+#define LF_COMBINE_EPT 2 // two entries per thread for <= 3 terms (C4: 3.04 -> 2.82 ms); 4 terms spill
+#endif
+
 template <int NT>
-void combine_one(const DevTables& d, double* out, int pass, int t_chunk, int stage_rows, int lt_max, dim3 grid,
-                 cudaStream_t s, bool accum) {
-    const size_t smem = ((stage_rows * sizeof(RowInfo) + 31) & ~size_t(31)) +
+constexpr int entries_per_thread() { return NT <= 3 ? LF_COMBINE_EPT : 1; }
+
+template <int NT>
+void combine_one(const DevTables& d, double* out, int pass, int t_chunk, int stage_rows, int lt_max,
+                 unsigned nblk, unsigned nchunk, cudaStream_t s, bool accum) {
+    constexpr int EPT = entries_per_thread<NT>();
+    const size_t smem = ((stage_rows * (sizeof(RowInfo) + 2 * NT) + 31) & ~size_t(31)) +
                         (size_t)stage_rows * lt_max * NT * sizeof(double4);
+    const dim3 grid((nblk + EPT - 1) / EPT, nchunk);
     auto launch = [&](auto kern) {
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -693,14 +766,14 @@ void combine_one(const DevTables& d, double* out, int pass, int t_chunk, int sta
     };
     if (d.affine) {
         if (accum)
-            launch(k_combine<NT, true, true>);
+            launch(k_combine<NT, EPT, true, true>);
         else
-            launch(k_combine<NT, true, false>);
+            launch(k_combine<NT, EPT, true, false>);
     } else {
         if (accum)
-            launch(k_combine<NT, false, true>);
+            launch(k_combine<NT, EPT, false, true>);
         else
-            launch(k_combine<NT, false, false>);
+            launch(k_combine<NT, EPT, false, false>);
     }
 }
 
@@ -734,7 +807,7 @@ int launch_inplane_general(const DevTables& d, cudaStream_t stream) {
 int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t stream, int* launches) {
     if (d.E == 0 || d.t1 <= d.t0)
         return 0;
-    const long long nblk = (d.E + kBlock - 1) / kBlock;
+    const long long nblk = (d.E + kBlock - 1) / kBlock; // 256-entry sub-blocks
     const int nt = d.t1 - d.t0;
     if (t_chunk <= 0) {
         // enough blocks for >= ~16 waves of 4 resident blocks on 148 SMs
@@ -743,7 +816,7 @@ int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t st
         nchunks = std::max(1LL, std::min<long long>(nchunks, nt));
         t_chunk = (int)((nt + nchunks - 1) / nchunks);
     }
-    const dim3 grid((unsigned)nblk, (unsigned)((nt + t_chunk - 1) / t_chunk));
+    const unsigned nchunk = (unsigned)((nt + t_chunk - 1) / t_chunk);
     const int lt_max = std::max(1, d.lt_max);
     for (int pass = 0; pass < d.n_passes; ++pass) {
         const int nterm = std::min(8, d.n_terms - 8 * pass);
@@ -751,15 +824,16 @@ int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t st
         // rows per staged sub-chunk: ~24 KB of weights, at most the chunk
         int stage_rows = (int)((24 * 1024) / ((size_t)lt_max * nterm * sizeof(double4)));
         stage_rows = std::max(1, std::min(stage_rows, t_chunk));
+        const unsigned nb = (unsigned)nblk;
         switch (nterm) {
-        case 1: combine_one<1>(d, out, pass, t_chunk, stage_rows, lt_max, grid, stream, accum); break;
-        case 2: combine_one<2>(d, out, pass, t_chunk, stage_rows, lt_max, grid, stream, accum); break;
-        case 3: combine_one<3>(d, out, pass, t_chunk, stage_rows, lt_max, grid, stream, accum); break;
-        case 4: combine_one<4>(d, out, pass, t_chunk, stage_rows, lt_max, grid, stream, accum); break;
-        case 5: combine_one<5>(d, out, pass, t_chunk, stage_rows, lt_max, grid, stream, accum); break;
-        case 6: combine_one<6>(d, out, pass, t_chunk, stage_rows, lt_max, grid, stream, accum); break;
-        case 7: combine_one<7>(d, out, pass, t_chunk, stage_rows, lt_max, grid, stream, accum); break;
-        default: combine_one<8>(d, out, pass, t_chunk, stage_rows, lt_max, grid, stream, accum); break;
+        case 1: combine_one<1>(d, out, pass, t_chunk, stage_rows, lt_max, nb, nchunk, stream, accum); break;
+        case 2: combine_one<2>(d, out, pass, t_chunk, stage_rows, lt_max, nb, nchunk, stream, accum); break;
+        case 3: combine_one<3>(d, out, pass, t_chunk, stage_rows, lt_max, nb, nchunk, stream, accum); break;
+        case 4: combine_one<4>(d, out, pass, t_chunk, stage_rows, lt_max, nb, nchunk, stream, accum); break;
+        case 5: combine_one<5>(d, out, pass, t_chunk, stage_rows, lt_max, nb, nchunk, stream, accum); break;
+        case 6: combine_one<6>(d, out, pass, t_chunk, stage_rows, lt_max, nb, nchunk, stream, accum); break;
+        case 7: combine_one<7>(d, out, pass, t_chunk, stage_rows, lt_max, nb, nchunk, stream, accum); break;
+        default: combine_one<8>(d, out, pass, t_chunk, stage_rows, lt_max, nb, nchunk, stream, accum); break;
         }
         if (launches)
             ++*launches;
