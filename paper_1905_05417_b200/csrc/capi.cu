@@ -287,16 +287,17 @@ int plan_launch(lf_plan* plan, double* values) {
         CK(static_cast<cudaError_t>(lfb::launch_standard(d, values, plan->setup.nnz, s, &launches)));
         return launches;
     }
-    CK(static_cast<cudaError_t>(lfb::launch_basis(d, d.affine != 0, s)));
-    ++launches;
-    if (d.n_pairs > 0) {
-        CK(static_cast<cudaError_t>(lfb::launch_thickness_pairs(d, s)));
-        ++launches;
-    }
     if (d.affine) {
-        CK(static_cast<cudaError_t>(lfb::launch_integrals_1d(d, s)));
+        // one fused setup launch: U, V, thickness-pair weights, Ct
+        CK(static_cast<cudaError_t>(lfb::launch_prepare_affine(d, s)));
         ++launches;
     } else {
+        CK(static_cast<cudaError_t>(lfb::launch_basis(d, false, s)));
+        ++launches;
+        if (d.n_pairs > 0) {
+            CK(static_cast<cudaError_t>(lfb::launch_thickness_pairs(d, s)));
+            ++launches;
+        }
         CK(cudaMemsetAsync(d.Pg, 0, sizeof(double) * static_cast<std::size_t>(d.n_terms) * 4 * d.E, s));
         CK(static_cast<cudaError_t>(lfb::launch_inplane_general(d, s)));
         launches += (d.pu + 1) * (d.pv + 1);

@@ -210,7 +210,252 @@ __global__ void k_thickness_pairs(DevTables d) {
     }
 }
 
+/// Cox-de Boor on a known span (splines.cpp:53-101 after findSpan): the
+/// evaluation points of the fused setup are Gauss points strictly inside the
+/// span, so findSpan would return `span`.  Compile-time degree keeps every
+/// array in registers.  Returns values/derivatives of functions i and j
+/// (global indices); false when either is inactive on the span.
+template <int P>
+__device__ __forceinline__ bool eval_pair(const double* t, int span, double x, int i, int j, double& vi, double& di,
+                                          double& vj, double& dj) {
+    double vals[P + 1], low[P + 1], left[P + 1], right[P + 1];
+#pragma unroll
+    for (int r = 0; r <= P; ++r)
+        vals[r] = low[r] = left[r] = right[r] = 0.0;
+    vals[0] = 1.0;
+#pragma unroll
+    for (int level = 1; level <= P; ++level) {
+        if (level == P)
+#pragma unroll
+            for (int r = 0; r <= P; ++r)
+                low[r] = vals[r];
+        left[level] = x - t[span + 1 - level];
+        right[level] = t[span + level] - x;
+        double saved = 0.0;
+#pragma unroll
+        for (int r = 0; r < level; ++r) {
+            const double denom = right[r + 1] + left[level - r];
+            const double tmp = denom > 0.0 ? vals[r] / denom : 0.0;
+            vals[r] = saved + right[r + 1] * tmp;
+            saved = left[level - r] * tmp;
+        }
+        vals[level] = saved;
+    }
+    const int first = span - P;
+    const int a = i - first, b = j - first;
+    if (a < 0 || a > P || b < 0 || b > P)
+        return false;
+    vi = vj = di = dj = 0.0;
+#pragma unroll
+    for (int r = 0; r <= P; ++r) {
+        const int g = first + r;
+        double d = 0.0;
+        if (r >= 1) {
+            const double den = t[g + P] - t[g];
+            if (den > 0.0)
+                d += low[r - 1] / den;
+        }
+        if (r <= P - 1) {
+            const double den = t[g + P + 1] - t[g + 1];
+            if (den > 0.0)
+                d -= low[r] / den;
+        }
+        d = P * d;
+        if (r == a) {
+            vi = vals[r];
+            di = d;
+        }
+        if (r == b) {
+            vj = vals[r];
+            dj = d;
+        }
+    }
+    return true;
+}
+
+/// 1D in-plane integrals U/V of one (i, slot) (see k_integrals_1d).
+template <int P>
+__device__ void integral_1d(const double* kn, const int* first, const double* slo, const double* shi,
+                            const double* rref, const double* wref, int nsp, int nq, int i, int j, double* acc) {
+    const int mn = min(i, j), mx = max(i, j);
+    int s0 = 0, s1 = nsp; // first[] strictly increasing: spans with first in [mx - P, mn]
+    while (s0 < s1) {
+        const int m = (s0 + s1) >> 1;
+        if (first[m] < mx - P)
+            s0 = m + 1;
+        else
+            s1 = m;
+    }
+    for (int s = s0; s < nsp && first[s] <= mn; ++s) {
+        const double mid = 0.5 * (slo[s] + shi[s]), half = 0.5 * (shi[s] - slo[s]);
+        for (int q = 0; q < nq; ++q) {
+            double vi, di, vj, dj;
+            if (!eval_pair<P>(kn, first[s] + P, mid + half * rref[q], i, j, vi, di, vj, dj))
+                continue;
+            const double w = wref[q] * half;
+            acc[0] += w * vi * vj;
+            acc[1] += w * vi * dj;
+            acc[2] += w * di * vj;
+            acc[3] += w * di * dj;
+        }
+    }
+}
+
+/// Thickness integrals of one pair reduced per term (see k_thickness_pairs).
+template <int P>
+__device__ void thickness_pair(const DevTables& d, long long pp) {
+    const long long target = pp + d.pre_t[d.t0];
+    int lo = d.t0, hi = d.t1;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (d.pre_t[mid] <= target)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    const int it = lo;
+    const int jt = d.lo_t[it] + (int)(target - d.pre_t[it]);
+    const int mn = min(it, jt), mx = max(it, jt);
+    int s0 = 0, s1 = d.nspt;
+    while (s0 < s1) {
+        const int m = (s0 + s1) >> 1;
+        if (d.spt_first[m] < mx - P)
+            s0 = m + 1;
+        else
+            s1 = m;
+    }
+    int s_end = s0;
+    while (s_end < d.nspt && d.spt_first[s_end] <= mn)
+        ++s_end;
+    constexpr int kChunk = 8;
+    for (int t0 = 0; t0 < d.n_terms; t0 += kChunk) {
+        const int tn = min(kChunk, d.n_terms - t0);
+        double acc[kChunk][4];
+        unsigned on = 0;
+#pragma unroll
+        for (int t = 0; t < kChunk; ++t)
+            acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.0;
+        double ql[4] = {0.0, 0.0, 0.0, 0.0};
+        int cur = -1;
+        auto flush = [&](int layer) {
+            if (layer < 0)
+                return;
+#pragma unroll
+            for (int t = 0; t < kChunk; ++t) {
+                if (t >= tn)
+                    break;
+                const long long tl = (long long)(t0 + t) * d.n_layers + layer;
+                if (!d.lam_on[tl])
+                    continue;
+                const double w = d.lam[tl];
+                for (int f = 0; f < 4; ++f)
+                    acc[t][f] += w * ql[f];
+                on |= 1u << t;
+            }
+        };
+        for (int s = s0; s < s_end; ++s) {
+            const int span = d.spt_first[s] + P;
+            for (int c = d.span_cell0[s]; c < d.span_cell0[s + 1]; ++c) {
+                const int layer = d.cell_layer[c];
+                if (layer != cur) {
+                    flush(cur);
+                    cur = layer;
+                    ql[0] = ql[1] = ql[2] = ql[3] = 0.0;
+                }
+                for (int q = 0; q < d.nqt; ++q) {
+                    const long long hq = (long long)c * d.nqt + q;
+                    double va, da, vb, db;
+                    if (!eval_pair<P>(d.kt, span, d.cell_pts[hq], it, jt, va, da, vb, db))
+                        continue;
+                    const double wq = d.cell_wts[hq];
+                    ql[0] += wq * va * vb;
+                    ql[1] += wq * va * db;
+                    ql[2] += wq * da * vb;
+                    ql[3] += wq * da * db;
+                }
+            }
+        }
+        flush(cur);
+#pragma unroll
+        for (int t = 0; t < kChunk; ++t)
+            if (t < tn)
+                for (int f = 0; f < 4; ++f)
+                    d.W[(pp * d.n_terms + t0 + t) * 4 + f] = acc[t][f];
+        d.Wmask[(long long)(t0 / kChunk) * d.n_pairs + pp] = on;
+    }
+}
+
+#define LF_DISPATCH_P(p, CALL)                                  \
+    switch (p) {                                                \
+    case 1: { constexpr int PP = 1; CALL; } break;              \
+    case 2: { constexpr int PP = 2; CALL; } break;              \
+    case 3: { constexpr int PP = 3; CALL; } break;              \
+    case 4: { constexpr int PP = 4; CALL; } break;              \
+    case 5: { constexpr int PP = 5; CALL; } break;              \
+    default: { constexpr int PP = 6; CALL; } break;             \
+    }
+
+/// Fused setup of the affine fast path: one launch computes, one thread per
+/// item,
+///   [0, nU)            U[i][slot][4]   1D in-plane integrals, u direction
+///   [nU, nU+nV)        V[i][slot][4]   v direction
+///   [.., +n_pairs)     W / Wmask       thickness integrals reduced per term
+///   [.., +T*81)        Ct              constant-frame pulled-back tables
+/// with the same arithmetic as k_integrals_1d / k_thickness_pairs / k_basis.
+__global__ void __launch_bounds__(64) k_prepare_affine(DevTables d) {
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long nU = (long long)d.nu * d.bu, nV = (long long)d.nv * d.bv;
+    if (g < nU + nV) {
+        const bool is_u = g < nU;
+        const int h = (int)(is_u ? g : g - nU);
+        const int b = is_u ? d.bu : d.bv;
+        const int i = h / b, slot = h % b;
+        const int* lo = is_u ? d.lo_u : d.lo_v;
+        const int* len = is_u ? d.len_u : d.len_v;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        if (slot < len[i]) {
+            const int j = lo[i] + slot;
+            if (is_u) {
+                LF_DISPATCH_P(d.pu, (integral_1d<PP>(d.ku, d.spu_first, d.spu_lo, d.spu_hi, d.ru, d.wu, d.nspu,
+                                                     d.nqu, i, j, acc)))
+            } else {
+                LF_DISPATCH_P(d.pv, (integral_1d<PP>(d.kv, d.spv_first, d.spv_lo, d.spv_hi, d.rv, d.wv, d.nspv,
+                                                     d.nqv, i, j, acc)))
+            }
+        }
+        double* out = (is_u ? d.U : d.V) + (long long)h * 4;
+        out[0] = acc[0];
+        out[1] = acc[1];
+        out[2] = acc[2];
+        out[3] = acc[3];
+        return;
+    }
+    long long h = g - nU - nV;
+    if (h < d.n_pairs) {
+        LF_DISPATCH_P(d.pt, (thickness_pair<PP>(d, h)))
+        return;
+    }
+    h -= d.n_pairs;
+    if (h < (long long)d.n_terms * 81) {
+        const int t = (int)(h / 81), xy = (int)(h % 81) / 9, ik = (int)(h % 9);
+        const int x = xy / 3, y = xy % 3;
+        const double* tab = d.term_table + (long long)t * 81;
+        double s = 0.0;
+        for (int j = 0; j < 3; ++j)
+            for (int l = 0; l < 3; ++l)
+                s += d.G[3 * x + j] * d.G[3 * y + l] * tab[(3 * j + l) * 9 + ik];
+        d.Ct[(long long)t * 81 + xy * 9 + ik] = d.det * s;
+    }
+}
+
 } // namespace
+
+int launch_prepare_affine(const DevTables& d, cudaStream_t stream) {
+    const long long n = (long long)d.nu * d.bu + (long long)d.nv * d.bv + d.n_pairs + (long long)d.n_terms * 81;
+    const int block = 64; // few items: spread them over more SMs
+    k_prepare_affine<<<(unsigned)((n + block - 1) / block), block, 0, stream>>>(d);
+    return (int)cudaGetLastError();
+}
 
 int launch_basis(const DevTables& d, bool with_ct, cudaStream_t stream) {
     const long long n = (long long)d.nspu * d.nqu + (long long)d.nspv * d.nqv +

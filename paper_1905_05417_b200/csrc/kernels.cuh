@@ -68,6 +68,8 @@ struct DevTables {
 // Launchers (all asynchronous on `stream`).  Return cudaError_t as int.
 int launch_basis(const DevTables& d, bool with_ct, cudaStream_t stream);
 int launch_thickness_pairs(const DevTables& d, cudaStream_t stream);
+/// Affine fast path: U, V, thickness pairs and Ct in one launch.
+int launch_prepare_affine(const DevTables& d, cudaStream_t stream);
 int launch_integrals_1d(const DevTables& d, cudaStream_t stream);
 int launch_inplane_general(const DevTables& d, cudaStream_t stream);
 int launch_affine_export(const DevTables& d, cudaStream_t stream);
