@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-plies", type=int, default=0)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo only to exercise the multi-rank path on fewer GPUs than ranks")
     return ap.parse_args()
 
 
@@ -207,89 +209,141 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_1905_05417_b200 as lf
-    from paper_1905_05417_b200 import abi, problem as P
+    from paper_1905_05417_b200 import problem as P
 
-    torch.cuda.set_device(local)
+    device = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(device)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        else:
+            dist.init_process_group(args.dist_backend)
     prob = P.baseline_config(args.config)
     sz = P.sizes(prob)
-    bounds = lf.slab_bounds(prob, world, rank) if world > 1 else {"t_begin": 0, "t_end": -1}
+    bounds = lf.slab_bounds(prob, world, rank) if world > 1 else {"t_begin": 0, "t_end": prob.n_t}
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    plan = lf.Plan(prob, "fast", local, bounds["t_begin"], bounds["t_end"], stream=stream.cuda_stream)
-    rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
-    cols = torch.empty(plan.nnz, dtype=torch.int32, device="cuda")
-    vals = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
-    plan.build_pattern(rp.data_ptr(), cols.data_ptr())
+
+    # this rank's slab; split into sequential sub-slab passes when its values
+    # do not fit in HBM next to the workspace (C5: 135 GB of values)
+    free, _ = torch.cuda.mem_get_info()
+    full = lf.Plan(prob, "fast", device, bounds["t_begin"], bounds["t_end"], stream=stream.cuda_stream)
+    # one pass when values + columns + row offsets fit; else values-only sub-slabs
+    if full.nnz * 12 + full.rows * 8 <= int(0.85 * free):
+        passes = 1
+    else:
+        passes = max(2, -(-full.nnz * 8 // int(0.8 * free)))
+    if passes == 1:
+        plans = [full]
+    else:
+        full.close()
+        nt = bounds["t_end"] - bounds["t_begin"]
+        cuts = [bounds["t_begin"] + (nt * k) // passes for k in range(passes + 1)]
+        plans = [lf.Plan(prob, "fast", device, cuts[k], cuts[k + 1], stream=stream.cuda_stream)
+                 for k in range(passes)]
+    vals = torch.empty(max(p.nnz for p in plans), dtype=torch.float64, device="cuda")
+    rp = cols = None
+    if passes == 1:
+        plan = plans[0]
+        rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
+        cols = torch.empty(plan.nnz, dtype=torch.int32, device="cuda")
+        plan.build_pattern(rp.data_ptr(), cols.data_ptr())
     torch.cuda.synchronize()
 
-    sampler = ClockSampler(local)
+    def step():
+        for p in plans:
+            p.assemble(vals.data_ptr())
+
+    sampler = ClockSampler(device)
     sampler.start()
     for _ in range(args.warmup):
-        plan.assemble(vals.data_ptr())
+        step()
     torch.cuda.synchronize()
-    plan.kernel_time(reset=True)
+    for p in plans:
+        p.kernel_time(reset=True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for _ in range(args.steps):
-        plan.assemble(vals.data_ptr())
+        step()
     ev1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
     ms_total = ev0.elapsed_time(ev1)
-    k_ms, k_n = plan.kernel_time(reset=True)
-    launches = plan.launch_count * args.steps
-    t = torch.tensor([ms_total, k_ms / max(k_n, 1)], dtype=torch.float64, device="cuda")
+    k_ms = k_n = 0
+    for p in plans:
+        a, b = p.kernel_time(reset=True)
+        k_ms += a
+        k_n += b
+    launches = sum(p.launch_count for p in plans) * args.steps
+    rank_nnz = sum(p.nnz for p in plans)
+    # combine kernel: average duration of one launch over all sub-slabs -> bytes/s
+    k_avg_ms = k_ms / max(k_n, 1)
+    k_bytes = rank_nnz * 8 / len(plans)
+    t = torch.tensor([ms_total, k_ms / max(args.steps, 1)], dtype=torch.float64, device="cuda")
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_total, k_avg_ms = float(t[0]), float(t[1])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX) if args.dist_backend == "nccl" else None
+        if args.dist_backend != "nccl":
+            tc = t.cpu()
+            dist.all_reduce(tc, op=dist.ReduceOp.MAX)
+            t = tc
+    ms_total = float(t[0])
     ms_per_step = ms_total / args.steps
     total_nnz = sz["nnz"]
     value = total_nnz / (ms_per_step / 1e3)
 
     # verification of the resident matrix (outside the timed region)
     verify = {}
-    if world == 1:
-        st = lf.device_csr_stats(plan.rows, rp.data_ptr(), cols.data_ptr(), vals.data_ptr(),
+    if world == 1 and passes == 1:
+        st = lf.device_csr_stats(plans[0].rows, rp.data_ptr(), cols.data_ptr(), vals.data_ptr(),
                                  stream.cuda_stream)
         verify = {"fro_norm": st["fro_sq"] ** 0.5, "symmetry_rel": (st["sym_sq"] / st["fro_sq"]) ** 0.5}
-    else:
-        # NCCL gather of slab summaries (verification only, never timed)
-        import torch as _t
-        fro = _t.tensor([float((vals * vals).sum()), float(plan.nnz)], dtype=_t.float64, device="cuda")
-        dist.all_reduce(fro)
-        verify = {"fro_norm": float(fro[0]) ** 0.5, "nnz_gathered": int(fro[1])}
+    elif world > 1 and passes == 1:
+        # gather of slab summaries (verification only, never timed)
+        from paper_1905_05417_b200 import distributed as D
+        s = D.slab_summary(rp, cols, vals[:plans[0].nnz])
+        parts = D.gather_summaries(s.cuda() if args.dist_backend == "nccl" else s)
+        tot = D.combine_summaries(parts)
+        verify = {"fro_norm": tot["fro_sq"] ** 0.5, "nnz_gathered": int(tot["nnz"]),
+                  "rows_gathered": int(tot["rows"])}
 
     hbm, peak_src = peaks()
-    achieved = plan.nnz * 8 / (k_avg_ms / 1e3) / 1e9
+    achieved = k_bytes / (k_avg_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": None,
-                "kernel": "k_combine (K4)", "bytes_per_launch": plan.nnz * 8,
+                "kernel": "k_combine (K4)", "bytes_per_launch": k_bytes,
                 "kernel_ms": k_avg_ms, "peak_source": peak_src,
-                "step_frac": (hbm * 1e9 / 8) and (total_nnz / (ms_per_step / 1e3)) / (world * hbm * 1e9 / 8)}
+                "step_frac": value * 8 / (world * hbm * 1e9)}
     traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(traffic_file):
         try:
             with open(traffic_file) as f:
-                tj = json.load(f)
-            if tj.get("config") == args.config:
+                tj = json.load(f).get(args.config)
+            if tj:
                 roofline["traffic"] = tj["dram_bytes_per_launch"]
+                roofline["traffic_source"] = tj["source"]
         except Exception:
             pass
     del rp, cols, vals
+    for p in plans:
+        p.close()
     torch.cuda.empty_cache()
 
     e2e = None
-    if not args.no_e2e and world == 1:
-        e2e = measure_e2e(args, prob, local, total_nnz)
-    elif not args.no_e2e:
-        e2e = measure_e2e_slab(args, prob, local, rank, world, bounds, total_nnz)
+    if args.no_e2e:
+        e2e = None
+    elif passes > 1:
+        e2e = {"value": None, "unit": "nnz/s",
+               "unavailable": f"the {args.config} CSR ({total_nnz * 12 / 1e9:.0f} GB) does not fit one "
+                              f"device for a one-shot host-buffer call"}
+    elif world == 1:
+        e2e = measure_e2e(args, prob, device, total_nnz)
+    else:
+        e2e = measure_e2e_slab(args, prob, device, rank, world, bounds, total_nnz)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -309,12 +363,11 @@ def main():
                        "distinct_materials": prob.distinct_configs(),
                        "l2": "output > L2 (values %.1f GB vs 126 MB L2); no flush needed"
                              % (total_nnz * 8 / 1e9),
-                       "parallelism": f"row-slab x{world}"},
+                       "parallelism": f"row-slab x{world}", "slab_passes_per_gpu": passes},
             "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
             "clocks": clocks, "verify": verify,
         }
         print(json.dumps(line))
-    plan.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -376,7 +429,9 @@ def measure_e2e_slab(args, prob, device, rank, world, bounds, total_nnz):
     t0 = time.perf_counter()
     for _ in range(n):
         once()
-    dt = torch.tensor([(time.perf_counter() - t0) / n], dtype=torch.float64, device="cuda")
+    dt = torch.tensor([(time.perf_counter() - t0) / n], dtype=torch.float64)
+    if args.dist_backend == "nccl":
+        dt = dt.cuda()
     dist.all_reduce(dt, op=dist.ReduceOp.MAX)
     sec = float(dt[0])
     plan.close()

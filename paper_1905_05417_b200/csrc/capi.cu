@@ -281,10 +281,25 @@ int plan_launch(lf_plan* plan, double* values) {
     const lfb::DevTables& d = plan->d;
     int launches = 0;
     cudaStream_t s = plan->stream;
+    auto events = [&]() {
+        std::pair<cudaEvent_t, cudaEvent_t> ev;
+        if (!plan->free_events.empty()) {
+            ev = plan->free_events.back();
+            plan->free_events.pop_back();
+        } else {
+            CK(cudaEventCreate(&ev.first));
+            CK(cudaEventCreate(&ev.second));
+        }
+        return ev;
+    };
     if (plan->setup.backend == LF_BACKEND_STANDARD) {
         CK(static_cast<cudaError_t>(lfb::launch_basis(d, false, s)));
         ++launches;
+        const auto ev = events(); // brackets the coloured standard kernels
+        CK(cudaEventRecord(ev.first, s));
         CK(static_cast<cudaError_t>(lfb::launch_standard(d, values, plan->setup.nnz, s, &launches)));
+        CK(cudaEventRecord(ev.second, s));
+        plan->pending.push_back(ev);
         return launches;
     }
     if (d.affine) {
@@ -302,14 +317,7 @@ int plan_launch(lf_plan* plan, double* values) {
         CK(static_cast<cudaError_t>(lfb::launch_inplane_general(d, s)));
         launches += (d.pu + 1) * (d.pv + 1);
     }
-    std::pair<cudaEvent_t, cudaEvent_t> ev;
-    if (!plan->free_events.empty()) {
-        ev = plan->free_events.back();
-        plan->free_events.pop_back();
-    } else {
-        CK(cudaEventCreate(&ev.first));
-        CK(cudaEventCreate(&ev.second));
-    }
+    const auto ev = events();
     CK(cudaEventRecord(ev.first, s));
     CK(static_cast<cudaError_t>(lfb::launch_combine(d, values, 0, s, &launches)));
     CK(cudaEventRecord(ev.second, s));
