@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -151,6 +152,43 @@ void upload_space(const lfb::Setup& s, DeviceArena& ar, lfb::DevTables& d) {
             blk[b] = is;
         }
         d.blk_is = ar.upload(blk);
+        // group-aligned blocks for the TMA-bulk combine: whole row segments
+        // (a, slot, b) of one i_s, packed greedily up to `cap` entries
+        for (int which = 0; which < 2; ++which) {
+            const long long cap = which == 0 ? 512 : 256;
+            std::vector<long long> e0;
+            std::vector<int> is0;
+            long long cur = -1;
+            bool ok = true;
+            for (int is = 0; is < s.n_s && ok; ++is) {
+                const long long B = 3LL * s.au.len[static_cast<std::size_t>(is % s.n_u)] *
+                                    s.av.len[static_cast<std::size_t>(is / s.n_u)];
+                if (B > cap)
+                    ok = false;
+                for (int a = 0; a < 3 && ok; ++a) {
+                    const long long g0 = s.es_pre[static_cast<std::size_t>(is)] + a * B;
+                    if (cur < 0 || g0 + B - cur > cap) {
+                        e0.push_back(g0);
+                        is0.push_back(is);
+                        cur = g0;
+                    }
+                }
+            }
+            e0.push_back(E);
+            const int n = ok ? static_cast<int>(e0.size()) - 1 : 0;
+            if (which == 0) {
+                d.n_gb2 = n;
+                d.gb2_e0 = reinterpret_cast<const long long*>(ar.upload(e0));
+                d.gb2_is = ar.upload(is0);
+            } else {
+                d.n_gb1 = n;
+                d.gb1_e0 = reinterpret_cast<const long long*>(ar.upload(e0));
+                d.gb1_is = ar.upload(is0);
+            }
+        }
+        // TMA-bulk combine is an opt-in experiment: slower than direct stores so far
+        // (profiles/r1_tma_bulk_experiment.md)
+        d.no_bulk = std::getenv("LAMFAST_BULK") == nullptr;
     }
     d.S_s = s.S_s;
     d.S_u = s.au.total;

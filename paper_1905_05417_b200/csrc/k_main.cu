@@ -156,6 +156,10 @@ __device__ __forceinline__ void combine_row(const double (&P)[EPT][NT][4], const
 #pragma unroll
         for (int k = 0; k < LT; ++k)
             acc[x][k] = (ACCUM && live[x]) ? o[x][(long long)k * B[x]] : 0.0;
+#ifdef LF_STORE_ONLY
+    // diagnostic build: identical store pattern, no weight loads / FMAs
+    mask = 0;
+#endif
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
         if (mask & (1u << t)) {
@@ -345,6 +349,254 @@ __global__ void LF_COMBINE_BOUNDS k_combine(const DevTables d, double* __restric
             }
         }
     }
+}
+
+// K4 (TMA variant): same arithmetic as k_combine, but every block owns whole
+// CSR row-segment groups (all entries (a, slot, b) of a row segment of i_s),
+// so its output for one thickness row is ONE contiguous range of
+// L_t * (#entries) values.  Threads write their values into a shared-memory
+// copy of that range (lanes -> consecutive words, conflict-free), and one
+// elected thread streams it out with a single cp.async.bulk (TMA bulk store):
+// full 128-byte lines instead of 256-byte warp pieces at 8-byte alignment.
+// Three staging buffers rotate so that the bulk store of row r overlaps the
+// arithmetic of rows r+1, r+2 with one block barrier per row.
+__device__ __forceinline__ void bulk_store(double* gdst, const double* ssrc, unsigned bytes) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(ssrc));
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst), "r"(s),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
+}
+constexpr int kBulkBuffers = 3; // staging ring: the store of row r is awaited at row r + 1
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+template <int NT, int EPT, int LT>
+__device__ __forceinline__ void combine_row_smem(const double (&P)[EPT][NT][4], const double4* __restrict__ w,
+                                                 unsigned mask, const unsigned char* __restrict__ kr, double* sbuf,
+                                                 const int (&loc)[EPT], const int (&rem)[EPT], const int (&B)[EPT],
+                                                 const bool (&live)[EPT]) {
+    double acc[EPT][LT];
+#pragma unroll
+    for (int x = 0; x < EPT; ++x)
+#pragma unroll
+        for (int k = 0; k < LT; ++k)
+            acc[x][k] = 0.0;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        if (mask & (1u << t)) {
+            const int klo = kr[2 * t], khi = kr[2 * t + 1];
+#pragma unroll
+            for (int k = 0; k < LT; ++k) {
+                if (k >= klo && k < khi) {
+                    const double4 ww = w[k * NT + t];
+#pragma unroll
+                    for (int x = 0; x < EPT; ++x) {
+                        acc[x][k] = fma(P[x][t][0], ww.x, acc[x][k]);
+                        acc[x][k] = fma(P[x][t][1], ww.y, acc[x][k]);
+                        acc[x][k] = fma(P[x][t][2], ww.z, acc[x][k]);
+                        acc[x][k] = fma(P[x][t][3], ww.w, acc[x][k]);
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int x = 0; x < EPT; ++x)
+        if (live[x])
+#pragma unroll
+            for (int k = 0; k < LT; ++k)
+                sbuf[LT * loc[x] + k * B[x] + rem[x]] = acc[x][k];
+}
+
+template <int NT, int EPT>
+__device__ __forceinline__ void combine_row_smem_dyn(const double (&P)[EPT][NT][4], const double4* __restrict__ w,
+                                                     int lt, unsigned mask, double* sbuf, const int (&loc)[EPT],
+                                                     const int (&rem)[EPT], const int (&B)[EPT],
+                                                     const bool (&live)[EPT]) {
+    for (int k = 0; k < lt; ++k) {
+        double acc[EPT];
+#pragma unroll
+        for (int x = 0; x < EPT; ++x)
+            acc[x] = 0.0;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            if (mask & (1u << t)) {
+                const double4 ww = w[k * NT + t];
+#pragma unroll
+                for (int x = 0; x < EPT; ++x) {
+                    acc[x] = fma(P[x][t][0], ww.x, acc[x]);
+                    acc[x] = fma(P[x][t][1], ww.y, acc[x]);
+                    acc[x] = fma(P[x][t][2], ww.z, acc[x]);
+                    acc[x] = fma(P[x][t][3], ww.w, acc[x]);
+                }
+            }
+        }
+#pragma unroll
+        for (int x = 0; x < EPT; ++x)
+            if (live[x])
+                sbuf[lt * loc[x] + k * B[x] + rem[x]] = acc[x];
+    }
+}
+
+template <int NT, int EPT, bool AFFINE>
+__global__ void __launch_bounds__(kBlock, 2) k_combine_bulk(const DevTables d, double* __restrict__ out, int t_chunk,
+                                                 int stage_rows, int lt_max) {
+    constexpr int kCap = kBlock * EPT; // entries per block at most
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    // [kBulkBuffers staging buffers of lt_max * kCap + 2 doubles][weights][RowInfo][kr]
+    const int buf_len = lt_max * kCap + 2;
+    double* s_out = reinterpret_cast<double*>(smem_raw);
+    double4* s_w = reinterpret_cast<double4*>(smem_raw + (size_t)kBulkBuffers * buf_len * sizeof(double) + 16);
+    s_w = reinterpret_cast<double4*>((reinterpret_cast<size_t>(s_w) + 31) & ~size_t(31));
+    RowInfo* s_row = reinterpret_cast<RowInfo*>(s_w + stage_rows * lt_max * NT);
+    unsigned char* s_kr = reinterpret_cast<unsigned char*>(s_row + stage_rows);
+
+    const long long* gb_e0 = EPT == 2 ? d.gb2_e0 : d.gb1_e0;
+    const int* gb_is = EPT == 2 ? d.gb2_is : d.gb1_is;
+    const long long e0 = __ldg(gb_e0 + blockIdx.x), e1 = __ldg(gb_e0 + blockIdx.x + 1);
+    const int ne = (int)(e1 - e0);
+
+    const int t_first = 0;
+    double P[EPT][NT][4];
+    int loc[EPT], rem[EPT], B[EPT];
+    bool live[EPT];
+    int is = __ldg(gb_is + blockIdx.x);
+#pragma unroll
+    for (int x = 0; x < EPT; ++x) {
+        const long long e = e0 + x * kBlock + threadIdx.x;
+        live[x] = e < e1;
+        const long long ec = live[x] ? e : e1 - 1;
+        while (__ldg(d.es_pre + is + 1) <= ec)
+            ++is;
+        const long long ebase = __ldg(d.es_pre + is);
+        const int r = (int)(ec - ebase);
+        const int iu = is % d.nu, iv = is / d.nu;
+        const int Lu = __ldg(d.len_u + iu), Lv = __ldg(d.len_v + iv);
+        B[x] = 3 * Lu * Lv;
+        const int a = r / B[x];
+        rem[x] = r - a * B[x];
+        // (row, k) position inside the block's range: L_t * loc + k * B + rem
+        loc[x] = (int)(ebase + (long long)a * B[x] - e0);
+        if constexpr (AFFINE) {
+            const int s = rem[x] / 3, b = rem[x] - 3 * (rem[x] / 3);
+            const int sv = s / Lu, su = s - sv * Lu;
+            affine_p<NT>(d, iu, iv, su, sv, 3 * a + b, t_first, P[x]);
+        } else {
+#pragma unroll
+            for (int t = 0; t < NT; ++t)
+#pragma unroll
+                for (int f = 0; f < 4; ++f)
+                    P[x][t][f] = __ldg(d.Pg + ((long long)(t_first + t) * 4 + f) * d.E + ec);
+        }
+    }
+
+    const int it_begin = d.t0 + blockIdx.y * t_chunk;
+    const int it_end = min(d.t1, it_begin + t_chunk);
+    const long long pre0 = __ldg(d.pre_t + d.t0);
+    const long long nine_S = 9 * d.S_s;
+    const unsigned* mask_base = d.Wmask;
+    const int T = d.n_terms;
+    int row_counter = 0;
+
+    for (int it0 = it_begin; it0 < it_end; it0 += stage_rows) {
+        const int nrow = min(stage_rows, it_end - it0);
+        // all threads past the previous sub-chunk's rows before the weights are overwritten
+        __syncthreads();
+        for (int rr = threadIdx.x; rr < nrow; rr += kBlock) {
+            const int it = it0 + rr;
+            const long long pfx = __ldg(d.pre_t + it) - pre0;
+            const int lt = __ldg(d.len_t + it);
+            unsigned m = 0;
+            unsigned char lo[NT], hi[NT];
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                lo[t] = 255;
+                hi[t] = 0;
+            }
+            for (int k = 0; k < lt; ++k) {
+                const unsigned mk = __ldg(mask_base + pfx + k);
+                m |= mk;
+#pragma unroll
+                for (int t = 0; t < NT; ++t)
+                    if (mk & (1u << t)) {
+                        lo[t] = min((int)lo[t], k);
+                        hi[t] = (unsigned char)(k + 1);
+                    }
+            }
+            s_row[rr].base = nine_S * pfx;
+            s_row[rr].lt = lt;
+            s_row[rr].mask = m;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                s_kr[(rr * NT + t) * 2] = lo[t] == 255 ? 0 : lo[t];
+                s_kr[(rr * NT + t) * 2 + 1] = hi[t];
+            }
+        }
+        const int nw = nrow * lt_max * NT;
+        for (int idx = threadIdx.x; idx < nw; idx += kBlock) {
+            const int rr = idx / (lt_max * NT);
+            const int k = (idx / NT) % lt_max;
+            const int t = idx % NT;
+            const int it = it0 + rr;
+            double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
+            if (k < __ldg(d.len_t + it)) {
+                const long long q = __ldg(d.pre_t + it) - pre0 + k;
+                const double2* src = reinterpret_cast<const double2*>(d.W + ((q * T) + t_first + t) * 4);
+                const double2 lo2 = __ldg(src), hi2 = __ldg(src + 1);
+                v = make_double4(lo2.x, lo2.y, hi2.x, hi2.y);
+            }
+            s_w[idx] = v;
+        }
+        __syncthreads();
+        for (int rr = 0; rr < nrow; ++rr, ++row_counter) {
+            const RowInfo ri = s_row[rr];
+            // destination of this block's contiguous range for row it, in doubles
+            const long long dst = ri.base + (long long)ri.lt * e0;
+            const int shift = (int)(dst & 1); // keep the bulk source 16-byte aligned
+            double* sbuf = s_out + (size_t)(row_counter % kBulkBuffers) * buf_len + shift;
+            const double4* w = s_w + rr * lt_max * NT;
+            const unsigned char* kr = s_kr + rr * NT * 2;
+            switch (ri.lt) {
+            case 1: combine_row_smem<NT, EPT, 1>(P, w, ri.mask, kr, sbuf, loc, rem, B, live); break;
+            case 2: combine_row_smem<NT, EPT, 2>(P, w, ri.mask, kr, sbuf, loc, rem, B, live); break;
+            case 3: combine_row_smem<NT, EPT, 3>(P, w, ri.mask, kr, sbuf, loc, rem, B, live); break;
+            case 4: combine_row_smem<NT, EPT, 4>(P, w, ri.mask, kr, sbuf, loc, rem, B, live); break;
+            case 5: combine_row_smem<NT, EPT, 5>(P, w, ri.mask, kr, sbuf, loc, rem, B, live); break;
+            case 7: combine_row_smem<NT, EPT, 7>(P, w, ri.mask, kr, sbuf, loc, rem, B, live); break;
+            default: combine_row_smem_dyn<NT, EPT>(P, w, ri.lt, ri.mask, sbuf, loc, rem, B, live); break;
+            }
+            fence_proxy_async_smem();
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                long long n = (long long)ri.lt * ne; // doubles in the range
+                double* g = out + dst;
+                const double* s = sbuf;
+                if (shift) { // odd start: one plain store, bulk from the next (aligned) element
+                    g[0] = s[0];
+                    ++g;
+                    ++s;
+                    --n;
+                }
+                if (n & 1) { // odd length: last element plain
+                    g[n - 1] = s[n - 1];
+                    --n;
+                }
+                if (n > 0)
+                    bulk_store(g, s, (unsigned)(n * sizeof(double)));
+                bulk_commit();
+                bulk_wait_read<kBulkBuffers - 2>(); // older stores have left their buffers
+            }
+        }
+    }
+    if (threadIdx.x == 0)
+        bulk_wait_all();
 }
 
 /// Exports P of every term in the entry layout Pg[t][f][e] (affine path),
@@ -752,10 +1004,32 @@ int reduce_launch(int blocks, double* partial, double* out, cudaStream_t stream)
 template <int NT>
 constexpr int entries_per_thread() { return NT <= 3 ? LF_COMBINE_EPT : 1; }
 
+/// TMA-bulk variant for a first pass; false when it does not apply (group
+/// wider than a block, or staging buffers too large for two blocks per SM).
+template <int NT>
+bool combine_bulk(const DevTables& d, double* out, int t_chunk, int stage_rows, int lt_max, unsigned nchunk,
+                  cudaStream_t s) {
+    constexpr int EPT = NT <= 4 ? 2 : 1; // 512-entry group packing keeps ~87% of lanes live
+    const int nblk = EPT == 2 ? d.n_gb2 : d.n_gb1;
+    if (nblk <= 0 || d.no_bulk)
+        return false;
+    const size_t buf_len = (size_t)lt_max * kBlock * EPT + 2;
+    const size_t smem = kBulkBuffers * buf_len * sizeof(double) + 16 + 32 + (size_t)stage_rows * lt_max * NT * sizeof(double4) +
+                        (size_t)stage_rows * (sizeof(RowInfo) + 2 * NT) + 64;
+    if (smem > 200 * 1024)
+        return false;
+    auto kern = d.affine ? k_combine_bulk<NT, EPT, true> : k_combine_bulk<NT, EPT, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<dim3((unsigned)nblk, nchunk), kBlock, smem, s>>>(d, out, t_chunk, stage_rows, lt_max);
+    return true;
+}
+
 template <int NT>
 void combine_one(const DevTables& d, double* out, int pass, int t_chunk, int stage_rows, int lt_max,
                  unsigned nblk, unsigned nchunk, cudaStream_t s, bool accum) {
     constexpr int EPT = entries_per_thread<NT>();
+    if (!accum && pass == 0 && d.n_passes == 1 && combine_bulk<NT>(d, out, t_chunk, stage_rows, lt_max, nchunk, s))
+        return;
     const size_t smem = ((stage_rows * (sizeof(RowInfo) + 2 * NT) + 31) & ~size_t(31)) +
                         (size_t)stage_rows * lt_max * NT * sizeof(double4);
     const dim3 grid((nblk + EPT - 1) / EPT, nchunk);

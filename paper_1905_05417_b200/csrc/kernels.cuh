@@ -45,6 +45,12 @@ struct DevTables {
     const long long* es_pre; // [ns + 1]
     const int* blk_is;       // [ceil(E / 256)] i_s of each 256-entry block's first entry
     int lt_max;              // max L_t over all thickness rows
+    // blocks of whole row-segment groups for the TMA-bulk combine
+    // (<= 512 / <= 256 entries): first entry (n+1 values) and first i_s
+    const long long *gb2_e0, *gb1_e0;
+    const int *gb2_is, *gb1_is;
+    int n_gb2, n_gb1;
+    int no_bulk; // 1 unless LAMFAST_BULK is set: direct-store combine
     long long S_s, S_u;
     // geometry
     int affine;
