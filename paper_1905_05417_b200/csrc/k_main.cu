@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -1084,11 +1085,20 @@ int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t st
     const long long nblk = (d.E + kBlock - 1) / kBlock; // 256-entry sub-blocks
     const int nt = d.t1 - d.t0;
     if (t_chunk <= 0) {
-        // enough blocks for >= ~16 waves of 4 resident blocks on 148 SMs
-        const long long target = 148LL * 4 * 16;
-        long long nchunks = (target + nblk - 1) / nblk;
-        nchunks = std::max(1LL, std::min<long long>(nchunks, nt));
-        t_chunk = (int)((nt + nchunks - 1) / nchunks);
+        if (const char* env = std::getenv("LAMFAST_TCHUNK"))
+            t_chunk = std::atoi(env);
+    }
+    if (t_chunk <= 0) {
+        // 64 thickness rows per block amortise the per-block prologue (P in
+        // registers, entry decode, staging); shorter chunks (down to 32) only
+        // while the grid is under ~4 waves of 2 resident blocks on 148 SMs.
+        // Measured sweep: profiles/r1_tchunk_sweep.txt.
+        const long long blocks_x = (nblk + 1) / 2; // two entries per thread for <= 3 terms
+        t_chunk = std::min(nt, 64);
+        while (t_chunk > 32 && blocks_x * ((nt + t_chunk - 1) / t_chunk) < 148LL * 2 * 4)
+            t_chunk /= 2;
+        const int nchunks = (nt + t_chunk - 1) / t_chunk; // balance, in multiples of 16 rows
+        t_chunk = std::min(nt, ((nt + nchunks - 1) / nchunks + 15) / 16 * 16);
     }
     const unsigned nchunk = (unsigned)((nt + t_chunk - 1) / t_chunk);
     const int lt_max = std::max(1, d.lt_max);

@@ -1,5 +1,3 @@
-python tools/run_steps.py --config C4 --steps 3 --calibrate | head -2
-for v in A SO A SO; do
-  if [ $v = A ]; then L=paper_1905_05417_b200/lib/liblamfast_b200.so; else L=build/var$v/lib.so; fi
-  for c in C4 C3; do echo -n "$v "; LAMFAST_LIB=$L python tools/run_steps.py --config $c --steps 20; done
+for c in C2 C3 C4; do
+  for tc in 0 4 8 16 32 64 129 257; do echo -n "tchunk=$tc "; LAMFAST_TCHUNK=$tc python tools/run_steps.py --config $c --steps 20; done
 done
