@@ -760,6 +760,8 @@ __global__ void k_standard(const DevTables d, double* __restrict__ values, int c
     const int c0 = d.span_cell0[ks], c1 = d.span_cell0[ks + 1];
     if (c0 == c1)
         return; // span with no unmasked cell (assembly.cpp:185-186)
+    if (d.spt_first[ks] + d.pt < d.t0 || d.spt_first[ks] >= d.t1)
+        return; // no row of this span lies in the slab
     el.fu = d.spu_first[el.eu];
     el.fv = d.spv_first[el.ev];
     el.nl2 = (d.pu + 1) * (d.pv + 1);

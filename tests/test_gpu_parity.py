@@ -314,3 +314,59 @@ def test_gpu_matches_reference_c1_c2_summaries(gpu):
         assert np.sqrt(got.values @ got.values) == pytest.approx(s["fro"], rel=1e-13)
         idx = np.asarray(s["sample_idx"])
         assert np.abs(got.values[idx] - s["sample_values"]).max() <= RTOL * s["max_abs"]
+
+
+def _device_csr(gpu, prob, backend, t0=0, t1=-1):
+    import torch
+    plan = gpu.Plan(prob, backend, 0, t0, t1)
+    rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
+    cols = torch.empty(max(1, plan.nnz), dtype=torch.int32, device="cuda")
+    vals = torch.empty(max(1, plan.nnz), dtype=torch.float64, device="cuda")
+    plan.build_pattern(rp.data_ptr(), cols.data_ptr())
+    plan.assemble(vals.data_ptr())
+    plan.synchronize()
+    rows = plan.rows
+    plan.close()
+    return rows, rp, cols, vals
+
+
+def _device_rel_diff(gpu, a, b):
+    import ctypes
+    lib = gpu.library()
+    d2, fa, fb = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    ptr = lambda t: ctypes.c_void_p(t.data_ptr())
+    assert lib.lf_csr_diff_sq(a[0], ptr(a[1]), ptr(a[2]), ptr(a[3]), ptr(b[1]), ptr(b[2]), ptr(b[3]),
+                              None, ctypes.byref(d2)) == 0
+    assert lib.lf_csr_frobenius_sq(a[0], ptr(a[1]), ptr(a[3]), None, ctypes.byref(fa)) == 0
+    assert lib.lf_csr_frobenius_sq(b[0], ptr(b[1]), ptr(b[3]), None, ctypes.byref(fb)) == 0
+    return (d2.value / max(fa.value, fb.value)) ** 0.5
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_full_size_fast_equals_standard_on_device(gpu, name):
+    """The paper's equivalence at BASELINE size: fast (sum-factorised P,
+    Kronecker combination) vs standard (full 3D quadrature, coloured
+    scatter) -- two independent device paths -- frobeniusRelDiff <= 1e-12 and
+    identical patterns."""
+    import torch
+    prob = P.baseline_config(name)
+    fast = _device_csr(gpu, prob, "fast")
+    std = _device_csr(gpu, prob, "standard")
+    assert torch.equal(fast[1], std[1]) and torch.equal(fast[2], std[2])
+    assert _device_rel_diff(gpu, fast, std) <= RTOL
+    del fast, std
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+def test_c5_slab_fast_equals_standard_on_device(gpu):
+    """C5 (203 GB CSR) cannot be resident; check a middle row slab of the
+    fast path against the standard path's slab."""
+    import torch
+    prob = P.baseline_config("C5")
+    t0 = prob.n_t // 2
+    fast = _device_csr(gpu, prob, "fast", t0, t0 + 4)
+    std = _device_csr(gpu, prob, "standard", t0, t0 + 4)
+    assert torch.equal(fast[1], std[1]) and torch.equal(fast[2], std[2])
+    assert _device_rel_diff(gpu, fast, std) <= RTOL

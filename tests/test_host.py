@@ -168,3 +168,17 @@ def test_c0_knots_align_with_interfaces():
     ifc = P.equal_interfaces(128)
     interior = kt[3:-3:2]
     assert np.array_equal(interior, ifc[1:-1])  # bit-identical: no sliver cells
+
+
+def test_report_format_round_trip():
+    """Reference report shape (bench.cpp:245-299), extended columns appended."""
+    from paper_1905_05417_b200 import report as R
+    rep = R.Report([R.Record("fast", 2, 8, 4, 2, 1.5e-5, 574992, 1e-16, 256, 8, 3.8e10, 0.05),
+                    R.Record("standard", 2, 8, 4, 2, 1e-3, 574992, None, 6912, 8, 5.7e8, 0.0007)],
+                   ["C9 backend=fast: boom"], 1)
+    csv = R.emit_csv(rep)
+    lines = csv.strip().splitlines()
+    assert lines[0] == "backend,p,elements,m,m_bar,time_s,nnz,rel_diff,qpoints,elements_y,nnz_per_s,hbm_frac"
+    assert lines[2].split(",")[7] == ""  # empty rel_diff cell when unavailable
+    back = R.parse_json(R.emit_json(rep))
+    assert back == rep
