@@ -186,9 +186,11 @@ void upload_space(const lfb::Setup& s, DeviceArena& ar, lfb::DevTables& d) {
                 d.gb1_is = ar.upload(is0);
             }
         }
-        // TMA-bulk combine is an opt-in experiment: slower than direct stores so far
-        // (profiles/r1_tma_bulk_experiment.md)
-        d.no_bulk = std::getenv("LAMFAST_BULK") == nullptr;
+        // combine store mode (profiles/r1_store_modes.md): direct stores by default;
+        // staged (aligned copy) and TMA bulk are slower so far and stay opt-in
+        d.store_mode = 0;
+        if (const char* m = std::getenv("LAMFAST_STORE"))
+            d.store_mode = std::strcmp(m, "staged") == 0 ? 1 : std::strcmp(m, "tma") == 0 ? 2 : 0;
     }
     d.S_s = s.S_s;
     d.S_u = s.au.total;

@@ -372,7 +372,6 @@ template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
     asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
 }
-constexpr int kBulkBuffers = 3; // staging ring: the store of row r is awaited at row r + 1
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -446,9 +445,13 @@ __device__ __forceinline__ void combine_row_smem_dyn(const double (&P)[EPT][NT][
     }
 }
 
-template <int NT, int EPT, bool AFFINE>
+template <int NT, int EPT, bool AFFINE, bool TMA>
 __global__ void __launch_bounds__(kBlock, 2) k_combine_bulk(const DevTables d, double* __restrict__ out, int t_chunk,
                                                  int stage_rows, int lt_max) {
+    // TMA: one elected thread issues cp.async.bulk per row (3 buffers);
+    // otherwise all warps copy the staged range out with 128-byte aligned
+    // 16-byte vector stores (2 buffers, one block barrier per row).
+    constexpr int kBulkBuffers = TMA ? 3 : 2;
     constexpr int kCap = kBlock * EPT; // entries per block at most
     extern __shared__ __align__(128) unsigned char smem_raw[];
     // [kBulkBuffers staging buffers of lt_max * kCap + 2 doubles][weights][RowInfo][kr]
@@ -573,31 +576,50 @@ __global__ void __launch_bounds__(kBlock, 2) k_combine_bulk(const DevTables d, d
             case 7: combine_row_smem<NT, EPT, 7>(P, w, ri.mask, kr, sbuf, loc, rem, B, live); break;
             default: combine_row_smem_dyn<NT, EPT>(P, w, ri.lt, ri.mask, sbuf, loc, rem, B, live); break;
             }
-            fence_proxy_async_smem();
+            if constexpr (TMA)
+                fence_proxy_async_smem();
             __syncthreads();
-            if (threadIdx.x == 0) {
-                long long n = (long long)ri.lt * ne; // doubles in the range
+            if constexpr (TMA) {
+                if (threadIdx.x == 0) {
+                    long long n = (long long)ri.lt * ne; // doubles in the range
+                    double* g = out + dst;
+                    const double* s = sbuf;
+                    if (shift) { // odd start: one plain store, bulk from the next (aligned) element
+                        g[0] = s[0];
+                        ++g;
+                        ++s;
+                        --n;
+                    }
+                    if (n & 1) { // odd length: last element plain
+                        g[n - 1] = s[n - 1];
+                        --n;
+                    }
+                    if (n > 0)
+                        bulk_store(g, s, (unsigned)(n * sizeof(double)));
+                    bulk_commit();
+                    bulk_wait_read<kBulkBuffers - 2>(); // older stores have left their buffers
+                }
+            } else {
+                // cooperative aligned copy: element j of the range is sbuf[j], global dst + j;
+                // scalar head up to the first 128-byte boundary, then 16-byte vectors
+                const int n = ri.lt * ne;
                 double* g = out + dst;
-                const double* s = sbuf;
-                if (shift) { // odd start: one plain store, bulk from the next (aligned) element
-                    g[0] = s[0];
-                    ++g;
-                    ++s;
-                    --n;
-                }
-                if (n & 1) { // odd length: last element plain
-                    g[n - 1] = s[n - 1];
-                    --n;
-                }
-                if (n > 0)
-                    bulk_store(g, s, (unsigned)(n * sizeof(double)));
-                bulk_commit();
-                bulk_wait_read<kBulkBuffers - 2>(); // older stores have left their buffers
+                const int head = (int)min((long long)n, (16 - (dst & 15)) & 15);
+                if ((int)threadIdx.x < head)
+                    __stcs(g + threadIdx.x, sbuf[threadIdx.x]);
+                const int body = (n - head) >> 1;
+                const double2* sv = reinterpret_cast<const double2*>(sbuf + head);
+                double2* gv = reinterpret_cast<double2*>(g + head);
+                for (int v = threadIdx.x; v < body; v += kBlock)
+                    __stcs(gv + v, sv[v]);
+                if (((n - head) & 1) && threadIdx.x == kBlock - 1)
+                    __stcs(g + n - 1, sbuf[n - 1]);
             }
         }
     }
-    if (threadIdx.x == 0)
-        bulk_wait_all();
+    if constexpr (TMA)
+        if (threadIdx.x == 0)
+            bulk_wait_all();
 }
 
 /// Exports P of every term in the entry layout Pg[t][f][e] (affine path),
@@ -1009,19 +1031,25 @@ constexpr int entries_per_thread() { return NT <= 3 ? LF_COMBINE_EPT : 1; }
 
 /// TMA-bulk variant for a first pass; false when it does not apply (group
 /// wider than a block, or staging buffers too large for two blocks per SM).
+/// Staged-store variant for a first pass; false when it does not apply (row
+/// segment wider than a block, or staging buffers too large for two blocks
+/// per SM).  store_mode: 1 = cooperative aligned copy, 2 = TMA bulk.
 template <int NT>
 bool combine_bulk(const DevTables& d, double* out, int t_chunk, int stage_rows, int lt_max, unsigned nchunk,
                   cudaStream_t s) {
     constexpr int EPT = NT <= 4 ? 2 : 1; // 512-entry group packing keeps ~87% of lanes live
     const int nblk = EPT == 2 ? d.n_gb2 : d.n_gb1;
-    if (nblk <= 0 || d.no_bulk)
+    if (nblk <= 0 || d.store_mode == 0)
         return false;
+    const bool tma = d.store_mode == 2;
     const size_t buf_len = (size_t)lt_max * kBlock * EPT + 2;
-    const size_t smem = kBulkBuffers * buf_len * sizeof(double) + 16 + 32 + (size_t)stage_rows * lt_max * NT * sizeof(double4) +
+    const size_t smem = (tma ? 3 : 2) * buf_len * sizeof(double) + 16 + 32 +
+                        (size_t)stage_rows * lt_max * NT * sizeof(double4) +
                         (size_t)stage_rows * (sizeof(RowInfo) + 2 * NT) + 64;
-    if (smem > 200 * 1024)
+    if (smem > 110 * 1024)
         return false;
-    auto kern = d.affine ? k_combine_bulk<NT, EPT, true> : k_combine_bulk<NT, EPT, false>;
+    auto kern = d.affine ? (tma ? k_combine_bulk<NT, EPT, true, true> : k_combine_bulk<NT, EPT, true, false>)
+                         : (tma ? k_combine_bulk<NT, EPT, false, true> : k_combine_bulk<NT, EPT, false, false>);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<dim3((unsigned)nblk, nchunk), kBlock, smem, s>>>(d, out, t_chunk, stage_rows, lt_max);
     return true;

@@ -50,7 +50,7 @@ struct DevTables {
     const long long *gb2_e0, *gb1_e0;
     const int *gb2_is, *gb1_is;
     int n_gb2, n_gb1;
-    int no_bulk; // 1 unless LAMFAST_BULK is set: direct-store combine
+    int store_mode; // combine stores: 0 direct, 1 staged aligned copy, 2 TMA bulk (LAMFAST_STORE)
     long long S_s, S_u;
     // geometry
     int affine;

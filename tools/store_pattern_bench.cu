@@ -1,0 +1,82 @@
+// Microbenchmark: HBM write bandwidth of the combine kernel's store pattern vs
+// simpler patterns, 15.4 GB buffer (C4 values).  Build:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o build/store_bench tools/store_pattern_bench.cu
+// Variants:
+//   fill        warp w writes 256 B at 256*w (grid-stride)             -- ideal
+//   pattern     thread = entry of a row segment of length B; per row it writes
+//               L_t values at base + L_t*A + k*B + rem (the combine layout),
+//               B = 75 (C4 interior), L_t alternating 3 / 5
+//   pattern96   same with B = 96 (every warp piece 256-byte aligned)
+//   pattern_cs  'pattern' with st.global.cs
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void fill(double* out, long long n) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        out[i] = 1.0;
+}
+
+template <bool CS>
+__global__ void pattern(double* out, long long E, int B, int nrows, int chunk) {
+    const long long e = (long long)blockIdx.x * 256 + threadIdx.x;
+    if (e >= E)
+        return;
+    const long long A = e / B * B;
+    const int rem = (int)(e - A);
+    const int r0 = blockIdx.y * chunk, r1 = min(nrows, r0 + chunk);
+    // row r has L_t = 3 (odd) or 5 (even); base = 8*E per pair-row prefix
+    for (int r = r0; r < r1; ++r) {
+        const int lt = (r & 1) ? 3 : 5;
+        const long long pfx = (long long)(r / 2) * 8 + ((r & 1) ? 5 : 0);
+        double* o = out + pfx * E + (long long)lt * A + rem;
+        for (int k = 0; k < lt; ++k) {
+            if (CS)
+                __stcs(o + (long long)k * B, 1.0);
+            else
+                o[(long long)k * B] = 1.0;
+        }
+    }
+}
+
+int main() {
+    const int nrows = 257;
+    long long E = 1884000; // ~C4 entry count
+    const long long pairs = (long long)(nrows / 2) * 8 + 5;
+    double* buf;
+    const long long n = pairs * E;
+    if (cudaMalloc(&buf, n * sizeof(double)) != cudaSuccess) {
+        printf("alloc failed\n");
+        return 1;
+    }
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    auto timeit = [&](const char* name, auto launch) {
+        launch();
+        cudaDeviceSynchronize();
+        cudaEventRecord(a);
+        for (int i = 0; i < 10; ++i)
+            launch();
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        ms /= 10;
+        printf("%-12s %8.3f ms  %7.1f GB/s  (%s)\n", name, ms, n * 8.0 / ms / 1e6,
+               cudaGetErrorString(cudaGetLastError()));
+    };
+    timeit("fill", [&] { fill<<<148 * 16, 256>>>(buf, n); });
+    for (int B : {75, 96}) {
+        const long long EB = E / B * B;
+        dim3 grid((unsigned)((EB + 255) / 256), 5);
+        const int chunk = (nrows + 4) / 5;
+        char nm[32];
+        snprintf(nm, sizeof nm, "pattern%d", B);
+        timeit(nm, [&] { pattern<false><<<grid, 256>>>(buf, EB, B, nrows, chunk); });
+        snprintf(nm, sizeof nm, "pattern%d_cs", B);
+        timeit(nm, [&] { pattern<true><<<grid, 256>>>(buf, EB, B, nrows, chunk); });
+    }
+    cudaFree(buf);
+    return 0;
+}
