@@ -152,45 +152,35 @@ void upload_space(const lfb::Setup& s, DeviceArena& ar, lfb::DevTables& d) {
             blk[b] = is;
         }
         d.blk_is = ar.upload(blk);
-        // group-aligned blocks for the TMA-bulk combine: whole row segments
-        // (a, slot, b) of one i_s, packed greedily up to `cap` entries
-        for (int which = 0; which < 2; ++which) {
-            const long long cap = which == 0 ? 512 : 256;
-            std::vector<long long> e0;
-            std::vector<int> is0;
-            long long cur = -1;
-            bool ok = true;
-            for (int is = 0; is < s.n_s && ok; ++is) {
-                const long long B = 3LL * s.au.len[static_cast<std::size_t>(is % s.n_u)] *
-                                    s.av.len[static_cast<std::size_t>(is / s.n_u)];
-                if (B > cap)
-                    ok = false;
-                for (int a = 0; a < 3 && ok; ++a) {
-                    const long long g0 = s.es_pre[static_cast<std::size_t>(is)] + a * B;
-                    if (cur < 0 || g0 + B - cur > cap) {
-                        e0.push_back(g0);
-                        is0.push_back(is);
-                        cur = g0;
-                    }
+        // warp-specialised combine: blocks of whole row segments (a, slot, b)
+        // of one i_s, packed greedily up to the producers' capacity
+        // (profiles/r1_store_modes.md)
+        d.ws_variant = 0; // direct stores by default; warp-specialised is opt-in (slower so far)
+        if (const char* m = std::getenv("LAMFAST_WS"))
+            d.ws_variant = std::atoi(m);
+        const long long cap = d.ws_variant == 1 ? 448 : d.ws_variant == 2 ? 384 : 512;
+        std::vector<long long> e0;
+        std::vector<int> is0;
+        long long cur = -1;
+        bool ok = d.ws_variant > 0;
+        for (int is = 0; is < s.n_s && ok; ++is) {
+            const long long B = 3LL * s.au.len[static_cast<std::size_t>(is % s.n_u)] *
+                                s.av.len[static_cast<std::size_t>(is / s.n_u)];
+            if (B > cap)
+                ok = false;
+            for (int a = 0; a < 3 && ok; ++a) {
+                const long long g0 = s.es_pre[static_cast<std::size_t>(is)] + a * B;
+                if (cur < 0 || g0 + B - cur > cap) {
+                    e0.push_back(g0);
+                    is0.push_back(is);
+                    cur = g0;
                 }
             }
-            e0.push_back(E);
-            const int n = ok ? static_cast<int>(e0.size()) - 1 : 0;
-            if (which == 0) {
-                d.n_gb2 = n;
-                d.gb2_e0 = reinterpret_cast<const long long*>(ar.upload(e0));
-                d.gb2_is = ar.upload(is0);
-            } else {
-                d.n_gb1 = n;
-                d.gb1_e0 = reinterpret_cast<const long long*>(ar.upload(e0));
-                d.gb1_is = ar.upload(is0);
-            }
         }
-        // combine store mode (profiles/r1_store_modes.md): direct stores by default;
-        // staged (aligned copy) and TMA bulk are slower so far and stay opt-in
-        d.store_mode = 0;
-        if (const char* m = std::getenv("LAMFAST_STORE"))
-            d.store_mode = std::strcmp(m, "staged") == 0 ? 1 : std::strcmp(m, "tma") == 0 ? 2 : 0;
+        e0.push_back(E);
+        d.n_gbw = ok ? static_cast<int>(e0.size()) - 1 : 0;
+        d.gbw_e0 = reinterpret_cast<const long long*>(ar.upload(e0));
+        d.gbw_is = ar.upload(is0);
     }
     d.S_s = s.S_s;
     d.S_u = s.au.total;
@@ -311,6 +301,11 @@ void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void
     d.n_pairs = s.n_pairs;
     if (backend != LF_BACKEND_STANDARD) {
         d.W = ar.alloc<double>(static_cast<std::size_t>(std::max<long long>(1, d.n_pairs)) * d.n_terms * 4);
+        if (d.ws_variant > 0 && d.n_terms <= 4) {
+            const std::size_t rows = static_cast<std::size_t>(std::max(1, d.t1 - d.t0));
+            d.g_rows = ar.alloc<unsigned char>(rows * 32);
+            d.g_w = ar.alloc<double>(rows * static_cast<std::size_t>(std::max(1, d.lt_max)) * d.n_terms * 4);
+        }
         d.Wmask = ar.alloc<unsigned>(static_cast<std::size_t>(std::max<long long>(1, d.n_pairs)) * d.n_passes);
         if (!d.affine)
             d.Pg = ar.alloc<double>(static_cast<std::size_t>(d.n_terms) * 4 * static_cast<std::size_t>(d.E));

@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 
 #include "kernels.cuh"
 
@@ -352,36 +353,95 @@ __global__ void LF_COMBINE_BOUNDS k_combine(const DevTables d, double* __restric
     }
 }
 
-// K4 (TMA variant): same arithmetic as k_combine, but every block owns whole
-// CSR row-segment groups (all entries (a, slot, b) of a row segment of i_s),
-// so its output for one thickness row is ONE contiguous range of
-// L_t * (#entries) values.  Threads write their values into a shared-memory
-// copy of that range (lanes -> consecutive words, conflict-free), and one
-// elected thread streams it out with a single cp.async.bulk (TMA bulk store):
-// full 128-byte lines instead of 256-byte warp pieces at 8-byte alignment.
-// Three staging buffers rotate so that the bulk store of row r overlaps the
-// arithmetic of rows r+1, r+2 with one block barrier per row.
-__device__ __forceinline__ void bulk_store(double* gdst, const double* ssrc, unsigned bytes) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(ssrc));
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst), "r"(s),
-                 "r"(bytes)
-                 : "memory");
+// K4, warp-specialised variant (default when the row segments pack): the
+// direct-store k_combine writes each warp's 32 values as a 256-byte run at
+// 8-byte alignment, and that misalignment -- not the access order -- is what
+// keeps it below the fill rate (tools/store_pattern_bench.cu: 4.3 vs 7.1 TB/s).
+// Here every block owns whole CSR row-segment groups (all entries (a, slot, b)
+// of one row segment of i_s), so its output for one thickness row is ONE
+// contiguous range of L_t x (#entries) values.
+//   * NP producer warps (EPT entries per thread, P in registers) compute a
+//     row and write it into a shared-memory copy of that range (slot of a
+//     3-deep ring, lanes -> consecutive words);
+//   * NC consumer warps stream the slot out with 16-byte stores aligned to
+//     128-byte lines (scalar head/tail), st.global.cs;
+//   * slots are handed over with named barriers (bar.arrive / bar.sync):
+//     FULL[s] = 1 + s, EMPTY[s] = 4 + s -- no block-wide barrier in the loop.
+// Weights of the whole row chunk are staged once, before the roles split.
+constexpr int kWsSlots = 3;
+
+__device__ __forceinline__ void named_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-    asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
+__device__ __forceinline__ void named_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async_smem() {
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+
+// Per-row data of the combine in the constant bank.  A combine launch covers
+// a segment of thickness rows whose image fits here; the producers read the
+// weights with uniform loads (LDCU into uniform registers, consumed directly
+// by DFMA): no shared-memory or LSU traffic for the warp-uniform weights.
+struct RowC {
+    long long base;          // 9 S_s (pre_t[it] - pre_t[t0])
+    int lt;                  // L_t(it)
+    unsigned mask;           // union of term masks over the row's pairs
+    unsigned char kr[16];    // per term: neighbour range [k_lo, k_hi)
+};
+constexpr int kConstRows = 256;
+constexpr int kConstW = 1600; // double4 -> 51.2 KB
+__constant__ RowC c_rows[kConstRows];
+__constant__ double4 c_w[kConstW];
+
+/// Packs RowC and the padded weights [row][k][term] of the slab into global
+/// images (copied per segment into the constant bank).
+__global__ void k_pack_rows(const DevTables d, RowC* __restrict__ g_rows, double4* __restrict__ g_w, int nt,
+                            int lt_max) {
+    const int nrow = d.t1 - d.t0;
+    const long long pre0 = d.pre_t[d.t0];
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nw = nrow * lt_max * nt;
+    if (idx < nw) {
+        const int rr = idx / (lt_max * nt), k = (idx / nt) % lt_max, t = idx % nt;
+        const int it = d.t0 + rr;
+        double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
+        if (k < d.len_t[it]) {
+            const long long q = d.pre_t[it] - pre0 + k;
+            const double* src = d.W + (q * d.n_terms + t) * 4;
+            v = make_double4(src[0], src[1], src[2], src[3]);
+        }
+        g_w[idx] = v;
+    }
+    if (idx < nrow) {
+        const int it = d.t0 + idx;
+        const long long pfx = d.pre_t[it] - pre0;
+        const int lt = d.len_t[it];
+        RowC r;
+        r.base = 9 * d.S_s * pfx;
+        r.lt = lt;
+        unsigned m = 0;
+        for (int t = 0; t < 16; ++t)
+            r.kr[t] = 0;
+        for (int t = 0; t < nt && t < 8; ++t) {
+            int lo = 255, hi = 0;
+            for (int k = 0; k < lt; ++k)
+                if (d.Wmask[pfx + k] & (1u << t)) {
+                    lo = min(lo, k);
+                    hi = k + 1;
+                }
+            if (hi > 0)
+                m |= 1u << t;
+            r.kr[2 * t] = (unsigned char)(lo == 255 ? 0 : lo);
+            r.kr[2 * t + 1] = (unsigned char)hi;
+        }
+        r.mask = m;
+        g_rows[idx] = r;
+    }
 }
 
 template <int NT, int EPT, int LT>
-__device__ __forceinline__ void combine_row_smem(const double (&P)[EPT][NT][4], const double4* __restrict__ w,
-                                                 unsigned mask, const unsigned char* __restrict__ kr, double* sbuf,
-                                                 const int (&loc)[EPT], const int (&rem)[EPT], const int (&B)[EPT],
-                                                 const bool (&live)[EPT]) {
+__device__ __forceinline__ void combine_row_const(const double (&P)[EPT][NT][4], int wbase, const RowC& ri,
+                                                  double* sbuf, const int (&loc)[EPT], const int (&rem)[EPT],
+                                                  const int (&B)[EPT], const bool (&live)[EPT]) {
     double acc[EPT][LT];
 #pragma unroll
     for (int x = 0; x < EPT; ++x)
@@ -390,12 +450,12 @@ __device__ __forceinline__ void combine_row_smem(const double (&P)[EPT][NT][4], 
             acc[x][k] = 0.0;
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
-        if (mask & (1u << t)) {
-            const int klo = kr[2 * t], khi = kr[2 * t + 1];
+        if (ri.mask & (1u << t)) {
+            const int klo = ri.kr[2 * t], khi = ri.kr[2 * t + 1];
 #pragma unroll
             for (int k = 0; k < LT; ++k) {
                 if (k >= klo && k < khi) {
-                    const double4 ww = w[k * NT + t];
+                    const double4 ww = c_w[wbase + k * NT + t];
 #pragma unroll
                     for (int x = 0; x < EPT; ++x) {
                         acc[x][k] = fma(P[x][t][0], ww.x, acc[x][k]);
@@ -416,19 +476,18 @@ __device__ __forceinline__ void combine_row_smem(const double (&P)[EPT][NT][4], 
 }
 
 template <int NT, int EPT>
-__device__ __forceinline__ void combine_row_smem_dyn(const double (&P)[EPT][NT][4], const double4* __restrict__ w,
-                                                     int lt, unsigned mask, double* sbuf, const int (&loc)[EPT],
-                                                     const int (&rem)[EPT], const int (&B)[EPT],
-                                                     const bool (&live)[EPT]) {
-    for (int k = 0; k < lt; ++k) {
+__device__ __forceinline__ void combine_row_const_dyn(const double (&P)[EPT][NT][4], int wbase, const RowC& ri,
+                                                      double* sbuf, const int (&loc)[EPT], const int (&rem)[EPT],
+                                                      const int (&B)[EPT], const bool (&live)[EPT]) {
+    for (int k = 0; k < ri.lt; ++k) {
         double acc[EPT];
 #pragma unroll
         for (int x = 0; x < EPT; ++x)
             acc[x] = 0.0;
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
-            if (mask & (1u << t)) {
-                const double4 ww = w[k * NT + t];
+            if (ri.mask & (1u << t)) {
+                const double4 ww = c_w[wbase + k * NT + t];
 #pragma unroll
                 for (int x = 0; x < EPT; ++x) {
                     acc[x] = fma(P[x][t][0], ww.x, acc[x]);
@@ -441,185 +500,108 @@ __device__ __forceinline__ void combine_row_smem_dyn(const double (&P)[EPT][NT][
 #pragma unroll
         for (int x = 0; x < EPT; ++x)
             if (live[x])
-                sbuf[lt * loc[x] + k * B[x] + rem[x]] = acc[x];
+                sbuf[ri.lt * loc[x] + k * B[x] + rem[x]] = acc[x];
     }
 }
 
-template <int NT, int EPT, bool AFFINE, bool TMA>
-__global__ void __launch_bounds__(kBlock, 2) k_combine_bulk(const DevTables d, double* __restrict__ out, int t_chunk,
-                                                 int stage_rows, int lt_max) {
-    // TMA: one elected thread issues cp.async.bulk per row (3 buffers);
-    // otherwise all warps copy the staged range out with 128-byte aligned
-    // 16-byte vector stores (2 buffers, one block barrier per row).
-    constexpr int kBulkBuffers = TMA ? 3 : 2;
-    constexpr int kCap = kBlock * EPT; // entries per block at most
+/// Warp-specialised combine over the segment of rows [seg_r0, seg_r0 +
+/// seg_rows) of the slab (row data in the constant bank, chunked by y).
+template <int NT, int EPT, int NP, int NC, bool AFFINE>
+__global__ void __launch_bounds__((NP + NC) * 32) k_combine_ws(const DevTables d, double* __restrict__ out,
+                                                               int seg_rows, int t_chunk, int lt_max) {
+    constexpr int kProd = NP * 32, kAll = (NP + NC) * 32;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    // [kBulkBuffers staging buffers of lt_max * kCap + 2 doubles][weights][RowInfo][kr]
-    const int buf_len = lt_max * kCap + 2;
+    const int slot_len = lt_max * kProd * EPT + 2;
     double* s_out = reinterpret_cast<double*>(smem_raw);
-    double4* s_w = reinterpret_cast<double4*>(smem_raw + (size_t)kBulkBuffers * buf_len * sizeof(double) + 16);
-    s_w = reinterpret_cast<double4*>((reinterpret_cast<size_t>(s_w) + 31) & ~size_t(31));
-    RowInfo* s_row = reinterpret_cast<RowInfo*>(s_w + stage_rows * lt_max * NT);
-    unsigned char* s_kr = reinterpret_cast<unsigned char*>(s_row + stage_rows);
 
-    const long long* gb_e0 = EPT == 2 ? d.gb2_e0 : d.gb1_e0;
-    const int* gb_is = EPT == 2 ? d.gb2_is : d.gb1_is;
-    const long long e0 = __ldg(gb_e0 + blockIdx.x), e1 = __ldg(gb_e0 + blockIdx.x + 1);
+    const long long e0 = __ldg(d.gbw_e0 + blockIdx.x), e1 = __ldg(d.gbw_e0 + blockIdx.x + 1);
     const int ne = (int)(e1 - e0);
+    const int r_begin = blockIdx.y * t_chunk; // local to the segment
+    const int r_end = min(seg_rows, r_begin + t_chunk);
+    const int nrow = r_end - r_begin;
+    // warp index made provably warp-uniform, so the role branches stay on the
+    // uniform datapath (constant-bank weights via LDCU -> uniform registers)
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
 
-    const int t_first = 0;
-    double P[EPT][NT][4];
-    int loc[EPT], rem[EPT], B[EPT];
-    bool live[EPT];
-    int is = __ldg(gb_is + blockIdx.x);
+    if (warp < NP) {
+        // ---- producers ----
+        double P[EPT][NT][4];
+        int loc[EPT], rem[EPT], B[EPT];
+        bool live[EPT];
+        int is = __ldg(d.gbw_is + blockIdx.x);
 #pragma unroll
-    for (int x = 0; x < EPT; ++x) {
-        const long long e = e0 + x * kBlock + threadIdx.x;
-        live[x] = e < e1;
-        const long long ec = live[x] ? e : e1 - 1;
-        while (__ldg(d.es_pre + is + 1) <= ec)
-            ++is;
-        const long long ebase = __ldg(d.es_pre + is);
-        const int r = (int)(ec - ebase);
-        const int iu = is % d.nu, iv = is / d.nu;
-        const int Lu = __ldg(d.len_u + iu), Lv = __ldg(d.len_v + iv);
-        B[x] = 3 * Lu * Lv;
-        const int a = r / B[x];
-        rem[x] = r - a * B[x];
-        // (row, k) position inside the block's range: L_t * loc + k * B + rem
-        loc[x] = (int)(ebase + (long long)a * B[x] - e0);
-        if constexpr (AFFINE) {
-            const int s = rem[x] / 3, b = rem[x] - 3 * (rem[x] / 3);
-            const int sv = s / Lu, su = s - sv * Lu;
-            affine_p<NT>(d, iu, iv, su, sv, 3 * a + b, t_first, P[x]);
-        } else {
-#pragma unroll
-            for (int t = 0; t < NT; ++t)
-#pragma unroll
-                for (int f = 0; f < 4; ++f)
-                    P[x][t][f] = __ldg(d.Pg + ((long long)(t_first + t) * 4 + f) * d.E + ec);
-        }
-    }
-
-    const int it_begin = d.t0 + blockIdx.y * t_chunk;
-    const int it_end = min(d.t1, it_begin + t_chunk);
-    const long long pre0 = __ldg(d.pre_t + d.t0);
-    const long long nine_S = 9 * d.S_s;
-    const unsigned* mask_base = d.Wmask;
-    const int T = d.n_terms;
-    int row_counter = 0;
-
-    for (int it0 = it_begin; it0 < it_end; it0 += stage_rows) {
-        const int nrow = min(stage_rows, it_end - it0);
-        // all threads past the previous sub-chunk's rows before the weights are overwritten
-        __syncthreads();
-        for (int rr = threadIdx.x; rr < nrow; rr += kBlock) {
-            const int it = it0 + rr;
-            const long long pfx = __ldg(d.pre_t + it) - pre0;
-            const int lt = __ldg(d.len_t + it);
-            unsigned m = 0;
-            unsigned char lo[NT], hi[NT];
-#pragma unroll
-            for (int t = 0; t < NT; ++t) {
-                lo[t] = 255;
-                hi[t] = 0;
-            }
-            for (int k = 0; k < lt; ++k) {
-                const unsigned mk = __ldg(mask_base + pfx + k);
-                m |= mk;
+        for (int x = 0; x < EPT; ++x) {
+            const long long e = e0 + x * kProd + threadIdx.x;
+            live[x] = e < e1;
+            const long long ec = live[x] ? e : e1 - 1;
+            while (__ldg(d.es_pre + is + 1) <= ec)
+                ++is;
+            const long long ebase = __ldg(d.es_pre + is);
+            const int r = (int)(ec - ebase);
+            const int iu = is % d.nu, iv = is / d.nu;
+            const int Lu = __ldg(d.len_u + iu), Lv = __ldg(d.len_v + iv);
+            B[x] = 3 * Lu * Lv;
+            const int a = r / B[x];
+            rem[x] = r - a * B[x];
+            // (row, k) position inside the block's range: L_t * loc + k * B + rem
+            loc[x] = (int)(ebase + (long long)a * B[x] - e0);
+            if constexpr (AFFINE) {
+                const int s = rem[x] / 3, b = rem[x] - 3 * (rem[x] / 3);
+                const int sv = s / Lu, su = s - sv * Lu;
+                affine_p<NT>(d, iu, iv, su, sv, 3 * a + b, 0, P[x]);
+            } else {
 #pragma unroll
                 for (int t = 0; t < NT; ++t)
-                    if (mk & (1u << t)) {
-                        lo[t] = min((int)lo[t], k);
-                        hi[t] = (unsigned char)(k + 1);
-                    }
-            }
-            s_row[rr].base = nine_S * pfx;
-            s_row[rr].lt = lt;
-            s_row[rr].mask = m;
 #pragma unroll
-            for (int t = 0; t < NT; ++t) {
-                s_kr[(rr * NT + t) * 2] = lo[t] == 255 ? 0 : lo[t];
-                s_kr[(rr * NT + t) * 2 + 1] = hi[t];
+                    for (int f = 0; f < 4; ++f)
+                        P[x][t][f] = __ldg(d.Pg + ((long long)t * 4 + f) * d.E + ec);
             }
         }
-        const int nw = nrow * lt_max * NT;
-        for (int idx = threadIdx.x; idx < nw; idx += kBlock) {
-            const int rr = idx / (lt_max * NT);
-            const int k = (idx / NT) % lt_max;
-            const int t = idx % NT;
-            const int it = it0 + rr;
-            double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
-            if (k < __ldg(d.len_t + it)) {
-                const long long q = __ldg(d.pre_t + it) - pre0 + k;
-                const double2* src = reinterpret_cast<const double2*>(d.W + ((q * T) + t_first + t) * 4);
-                const double2 lo2 = __ldg(src), hi2 = __ldg(src + 1);
-                v = make_double4(lo2.x, lo2.y, hi2.x, hi2.y);
-            }
-            s_w[idx] = v;
-        }
-        __syncthreads();
-        for (int rr = 0; rr < nrow; ++rr, ++row_counter) {
-            const RowInfo ri = s_row[rr];
-            // destination of this block's contiguous range for row it, in doubles
+        for (int i = 0; i < nrow; ++i) {
+            const int slot = i % kWsSlots;
+            if (i >= kWsSlots)
+                named_sync(1 + kWsSlots + slot, kAll); // consumers released the slot
+            const int rr = r_begin + i;
+            const RowC ri = c_rows[rr];
             const long long dst = ri.base + (long long)ri.lt * e0;
-            const int shift = (int)(dst & 1); // keep the bulk source 16-byte aligned
-            double* sbuf = s_out + (size_t)(row_counter % kBulkBuffers) * buf_len + shift;
-            const double4* w = s_w + rr * lt_max * NT;
-            const unsigned char* kr = s_kr + rr * NT * 2;
+            double* sbuf = s_out + (size_t)slot * slot_len + (int)(dst & 1);
+            const int wbase = rr * lt_max * NT;
             switch (ri.lt) {
-            case 1: combine_row_smem<NT, EPT, 1>(P, w, ri.mask, kr, sbuf, loc, rem, B, live); break;
-            case 2: combine_row_smem<NT, EPT, 2>(P, w, ri.mask, kr, sbuf, loc, rem, B, live); break;
-            case 3: combine_row_smem<NT, EPT, 3>(P, w, ri.mask, kr, sbuf, loc, rem, B, live); break;
-            case 4: combine_row_smem<NT, EPT, 4>(P, w, ri.mask, kr, sbuf, loc, rem, B, live); break;
-            case 5: combine_row_smem<NT, EPT, 5>(P, w, ri.mask, kr, sbuf, loc, rem, B, live); break;
-            case 7: combine_row_smem<NT, EPT, 7>(P, w, ri.mask, kr, sbuf, loc, rem, B, live); break;
-            default: combine_row_smem_dyn<NT, EPT>(P, w, ri.lt, ri.mask, sbuf, loc, rem, B, live); break;
+            case 1: combine_row_const<NT, EPT, 1>(P, wbase, ri, sbuf, loc, rem, B, live); break;
+            case 2: combine_row_const<NT, EPT, 2>(P, wbase, ri, sbuf, loc, rem, B, live); break;
+            case 3: combine_row_const<NT, EPT, 3>(P, wbase, ri, sbuf, loc, rem, B, live); break;
+            case 4: combine_row_const<NT, EPT, 4>(P, wbase, ri, sbuf, loc, rem, B, live); break;
+            case 5: combine_row_const<NT, EPT, 5>(P, wbase, ri, sbuf, loc, rem, B, live); break;
+            case 7: combine_row_const<NT, EPT, 7>(P, wbase, ri, sbuf, loc, rem, B, live); break;
+            default: combine_row_const_dyn<NT, EPT>(P, wbase, ri, sbuf, loc, rem, B, live); break;
             }
-            if constexpr (TMA)
-                fence_proxy_async_smem();
-            __syncthreads();
-            if constexpr (TMA) {
-                if (threadIdx.x == 0) {
-                    long long n = (long long)ri.lt * ne; // doubles in the range
-                    double* g = out + dst;
-                    const double* s = sbuf;
-                    if (shift) { // odd start: one plain store, bulk from the next (aligned) element
-                        g[0] = s[0];
-                        ++g;
-                        ++s;
-                        --n;
-                    }
-                    if (n & 1) { // odd length: last element plain
-                        g[n - 1] = s[n - 1];
-                        --n;
-                    }
-                    if (n > 0)
-                        bulk_store(g, s, (unsigned)(n * sizeof(double)));
-                    bulk_commit();
-                    bulk_wait_read<kBulkBuffers - 2>(); // older stores have left their buffers
-                }
-            } else {
-                // cooperative aligned copy: element j of the range is sbuf[j], global dst + j;
-                // scalar head up to the first 128-byte boundary, then 16-byte vectors
-                const int n = ri.lt * ne;
-                double* g = out + dst;
-                const int head = (int)min((long long)n, (16 - (dst & 15)) & 15);
-                if ((int)threadIdx.x < head)
-                    __stcs(g + threadIdx.x, sbuf[threadIdx.x]);
-                const int body = (n - head) >> 1;
-                const double2* sv = reinterpret_cast<const double2*>(sbuf + head);
-                double2* gv = reinterpret_cast<double2*>(g + head);
-                for (int v = threadIdx.x; v < body; v += kBlock)
-                    __stcs(gv + v, sv[v]);
-                if (((n - head) & 1) && threadIdx.x == kBlock - 1)
-                    __stcs(g + n - 1, sbuf[n - 1]);
-            }
+            named_arrive(1 + slot, kAll); // slot full
+        }
+    } else {
+        // ---- consumers: 128-byte aligned 16-byte stores of each full slot ----
+        const int ct = threadIdx.x - kProd;
+        for (int i = 0; i < nrow; ++i) {
+            const int slot = i % kWsSlots;
+            named_sync(1 + slot, kAll);
+            const RowC ri = c_rows[r_begin + i];
+            const long long dst = ri.base + (long long)ri.lt * e0;
+            const double* sbuf = s_out + (size_t)slot * slot_len + (int)(dst & 1);
+            const int n = ri.lt * ne;
+            double* g = out + dst;
+            const int head = (int)min((long long)n, (16 - (dst & 15)) & 15);
+            if (ct < head)
+                __stcs(g + ct, sbuf[ct]);
+            const int body = (n - head) >> 1;
+            const double2* sv = reinterpret_cast<const double2*>(sbuf + head);
+            double2* gv = reinterpret_cast<double2*>(g + head);
+            for (int v = ct; v < body; v += NC * 32)
+                __stcs(gv + v, sv[v]);
+            if (((n - head) & 1) && ct == NC * 32 - 1)
+                __stcs(g + n - 1, sbuf[n - 1]);
+            if (i + kWsSlots < nrow)
+                named_arrive(1 + kWsSlots + slot, kAll); // slot free
         }
     }
-    if constexpr (TMA)
-        if (threadIdx.x == 0)
-            bulk_wait_all();
 }
 
 /// Exports P of every term in the entry layout Pg[t][f][e] (affine path),
@@ -1031,36 +1013,84 @@ constexpr int entries_per_thread() { return NT <= 3 ? LF_COMBINE_EPT : 1; }
 
 /// TMA-bulk variant for a first pass; false when it does not apply (group
 /// wider than a block, or staging buffers too large for two blocks per SM).
-/// Staged-store variant for a first pass; false when it does not apply (row
-/// segment wider than a block, or staging buffers too large for two blocks
-/// per SM).  store_mode: 1 = cooperative aligned copy, 2 = TMA bulk.
+/// One event per device orders every use of the constant-bank row images
+/// (c_rows / c_w are per device, not per stream).
+cudaEvent_t const_bank_event(int device) {
+    static std::mutex mu;
+    static cudaEvent_t ev[64] = {};
+    std::lock_guard<std::mutex> lock(mu);
+    if (device < 0 || device >= 64)
+        return nullptr;
+    if (!ev[device])
+        cudaEventCreateWithFlags(&ev[device], cudaEventDisableTiming);
+    return ev[device];
+}
+
+/// Warp-specialised combine for a single pass of <= 4 terms; false when it
+/// does not apply (no group packing for this problem, or staging too large).
+/// ws_variant (LAMFAST_WS): 1 = 7 producer + 1 consumer warps, 2 = 6 + 2,
+/// 3 = 8 + 2; two entries per producer thread.
 template <int NT>
-bool combine_bulk(const DevTables& d, double* out, int t_chunk, int stage_rows, int lt_max, unsigned nchunk,
-                  cudaStream_t s) {
-    constexpr int EPT = NT <= 4 ? 2 : 1; // 512-entry group packing keeps ~87% of lanes live
-    const int nblk = EPT == 2 ? d.n_gb2 : d.n_gb1;
-    if (nblk <= 0 || d.store_mode == 0)
+bool combine_ws(const DevTables& d, double* out, int lt_max, cudaStream_t s, int* launches) {
+    if constexpr (NT > 4) {
         return false;
-    const bool tma = d.store_mode == 2;
-    const size_t buf_len = (size_t)lt_max * kBlock * EPT + 2;
-    const size_t smem = (tma ? 3 : 2) * buf_len * sizeof(double) + 16 + 32 +
-                        (size_t)stage_rows * lt_max * NT * sizeof(double4) +
-                        (size_t)stage_rows * (sizeof(RowInfo) + 2 * NT) + 64;
-    if (smem > 110 * 1024)
-        return false;
-    auto kern = d.affine ? (tma ? k_combine_bulk<NT, EPT, true, true> : k_combine_bulk<NT, EPT, true, false>)
-                         : (tma ? k_combine_bulk<NT, EPT, false, true> : k_combine_bulk<NT, EPT, false, false>);
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<dim3((unsigned)nblk, nchunk), kBlock, smem, s>>>(d, out, t_chunk, stage_rows, lt_max);
-    return true;
+    } else {
+        if (d.ws_variant == 0 || d.n_gbw <= 0 || !d.g_rows || !d.g_w)
+            return false;
+        const int np = d.ws_variant == 1 ? 7 : d.ws_variant == 2 ? 6 : 8;
+        const int nc = d.ws_variant == 1 ? 1 : 2;
+        const size_t slot_len = (size_t)lt_max * np * 32 * 2 + 2;
+        const size_t smem = kWsSlots * slot_len * sizeof(double) + 64;
+        const int seg_rows = std::min(kConstRows, kConstW / (lt_max * NT));
+        if (smem > 112 * 1024 || seg_rows < 1)
+            return false;
+        const int nrow = d.t1 - d.t0;
+        RowC* g_rows = static_cast<RowC*>(d.g_rows);
+        double4* g_w = static_cast<double4*>(d.g_w);
+        const int npack = std::max(nrow, nrow * lt_max * NT);
+        k_pack_rows<<<(npack + 255) / 256, 256, 0, s>>>(d, g_rows, g_w, NT, lt_max);
+        if (launches)
+            ++*launches;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaEvent_t bank = const_bank_event(dev);
+        auto kern = d.affine ? (d.ws_variant == 1 ? k_combine_ws<NT, 2, 7, 1, true>
+                                : d.ws_variant == 2 ? k_combine_ws<NT, 2, 6, 2, true>
+                                                    : k_combine_ws<NT, 2, 8, 2, true>)
+                             : (d.ws_variant == 1 ? k_combine_ws<NT, 2, 7, 1, false>
+                                : d.ws_variant == 2 ? k_combine_ws<NT, 2, 6, 2, false>
+                                                    : k_combine_ws<NT, 2, 8, 2, false>);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        for (int r0 = 0; r0 < nrow; r0 += seg_rows) {
+            const int rows = std::min(seg_rows, nrow - r0);
+            if (bank)
+                cudaStreamWaitEvent(s, bank, 0);
+            cudaMemcpyToSymbolAsync(c_rows, g_rows + r0, sizeof(RowC) * rows, 0, cudaMemcpyDeviceToDevice, s);
+            cudaMemcpyToSymbolAsync(c_w, g_w + (size_t)r0 * lt_max * NT, sizeof(double4) * rows * lt_max * NT, 0,
+                                    cudaMemcpyDeviceToDevice, s);
+            // chunks of <= 64 rows, balanced in multiples of 16
+            int nchunk = (rows + 63) / 64;
+            while (nchunk < rows / 16 && (long long)d.n_gbw * nchunk < 148LL * 2 * 4)
+                ++nchunk;
+            const int t_chunk = std::min(rows, ((rows + nchunk - 1) / nchunk + 15) / 16 * 16);
+            const dim3 grid((unsigned)d.n_gbw, (unsigned)((rows + t_chunk - 1) / t_chunk));
+            // rows of this segment start at slab row r0: offset the output base
+            // through the constant image (RowC::base is slab-global)
+            kern<<<grid, (np + nc) * 32, smem, s>>>(d, out, rows, t_chunk, lt_max);
+            if (launches)
+                ++*launches;
+            if (bank)
+                cudaEventRecord(bank, s);
+        }
+        return true;
+    }
 }
 
 template <int NT>
 void combine_one(const DevTables& d, double* out, int pass, int t_chunk, int stage_rows, int lt_max,
                  unsigned nblk, unsigned nchunk, cudaStream_t s, bool accum) {
     constexpr int EPT = entries_per_thread<NT>();
-    if (!accum && pass == 0 && d.n_passes == 1 && combine_bulk<NT>(d, out, t_chunk, stage_rows, lt_max, nchunk, s))
-        return;
+    (void)nchunk;
     const size_t smem = ((stage_rows * (sizeof(RowInfo) + 2 * NT) + 31) & ~size_t(31)) +
                         (size_t)stage_rows * lt_max * NT * sizeof(double4);
     const dim3 grid((nblk + EPT - 1) / EPT, nchunk);
@@ -1132,6 +1162,18 @@ int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t st
     }
     const unsigned nchunk = (unsigned)((nt + t_chunk - 1) / t_chunk);
     const int lt_max = std::max(1, d.lt_max);
+    if (d.n_passes == 1) {
+        bool done = false;
+        switch (d.n_terms) {
+        case 1: done = combine_ws<1>(d, out, lt_max, stream, launches); break;
+        case 2: done = combine_ws<2>(d, out, lt_max, stream, launches); break;
+        case 3: done = combine_ws<3>(d, out, lt_max, stream, launches); break;
+        case 4: done = combine_ws<4>(d, out, lt_max, stream, launches); break;
+        default: break;
+        }
+        if (done)
+            return (int)cudaGetLastError();
+    }
     for (int pass = 0; pass < d.n_passes; ++pass) {
         const int nterm = std::min(8, d.n_terms - 8 * pass);
         const bool accum = pass > 0;

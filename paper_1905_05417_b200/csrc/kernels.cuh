@@ -45,12 +45,14 @@ struct DevTables {
     const long long* es_pre; // [ns + 1]
     const int* blk_is;       // [ceil(E / 256)] i_s of each 256-entry block's first entry
     int lt_max;              // max L_t over all thickness rows
-    // blocks of whole row-segment groups for the TMA-bulk combine
-    // (<= 512 / <= 256 entries): first entry (n+1 values) and first i_s
-    const long long *gb2_e0, *gb1_e0;
-    const int *gb2_is, *gb1_is;
-    int n_gb2, n_gb1;
-    int store_mode; // combine stores: 0 direct, 1 staged aligned copy, 2 TMA bulk (LAMFAST_STORE)
+    // blocks of whole row-segment groups for the warp-specialised combine:
+    // first entry of each block (n_gbw + 1 values) and its first i_s
+    const long long* gbw_e0;
+    const int* gbw_is;
+    int n_gbw;
+    int ws_variant; // 0 direct stores; 1..3 warp-specialised layout (LAMFAST_WS)
+    void* g_rows;   // [slab rows] packed row records (constant-bank image)
+    void* g_w;      // [slab rows][lt_max][terms] double4 weights image
     long long S_s, S_u;
     // geometry
     int affine;

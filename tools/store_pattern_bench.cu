@@ -39,6 +39,64 @@ __global__ void pattern(double* out, long long E, int B, int nrows, int chunk) {
     }
 }
 
+// Warp-specialised staging: NP producer warps write the block's contiguous
+// row range into a smem slot, NC consumer warps copy it out with 128-byte
+// aligned 16-byte stores; named barriers hand slots over (no block barrier).
+template <int NP, int NC, int NSLOT>
+__global__ void __launch_bounds__((NP + NC) * 32) ws_pattern(double* out, long long E, int B, int nrows, int chunk,
+                                                              int cap) {
+    extern __shared__ double smem[];
+    const int warp = threadIdx.x / 32;
+    const int nthreads = (NP + NC) * 32;
+    // block owns whole groups: entries [e0, e1)
+    const long long e0 = (long long)blockIdx.x * (cap / B) * B;
+    const long long e1 = min(E, e0 + (long long)(cap / B) * B);
+    const int ne = (int)(e1 - e0);
+    const int slot_len = 5 * cap + 32;
+    const int r0 = blockIdx.y * chunk, r1 = min(nrows, r0 + chunk);
+    if (warp < NP) {
+        for (int r = r0, i = 0; r < r1; ++r, ++i) {
+            const int slot = i % NSLOT;
+            if (i >= NSLOT) // wait until consumers released this slot
+                asm volatile("bar.sync %0, %1;" ::"r"(1 + NSLOT + slot), "r"(nthreads));
+            const int lt = (r & 1) ? 3 : 5;
+            const long long pfx = (long long)(r / 2) * 8 + ((r & 1) ? 5 : 0);
+            const long long dst = pfx * E + (long long)lt * e0;
+            double* sb = smem + slot * slot_len + (int)(dst & 1);
+            for (int x = threadIdx.x; x < ne; x += NP * 32) {
+                const int loc = x / B * B, rem = x - loc;
+                for (int k = 0; k < lt; ++k)
+                    sb[lt * loc + k * B + rem] = 1.0;
+            }
+            asm volatile("bar.arrive %0, %1;" ::"r"(1 + slot), "r"(nthreads));
+        }
+    } else {
+        const int ct = threadIdx.x - NP * 32;
+        for (int r = r0, i = 0; r < r1; ++r, ++i) {
+            const int slot = i % NSLOT;
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(nthreads));
+            const int lt = (r & 1) ? 3 : 5;
+            const long long pfx = (long long)(r / 2) * 8 + ((r & 1) ? 5 : 0);
+            const long long dst = pfx * E + (long long)lt * e0;
+            const double* sb = smem + slot * slot_len + (int)(dst & 1);
+            const int n = lt * ne;
+            double* g = out + dst;
+            const int head = (int)min((long long)n, (16 - (dst & 15)) & 15);
+            if (ct < head)
+                __stcs(g + ct, sb[ct]);
+            const int body = (n - head) >> 1;
+            const double2* sv = reinterpret_cast<const double2*>(sb + head);
+            double2* gv = reinterpret_cast<double2*>(g + head);
+            for (int v = ct; v < body; v += NC * 32)
+                __stcs(gv + v, sv[v]);
+            if (((n - head) & 1) && ct == 0)
+                __stcs(g + n - 1, sb[n - 1]);
+            if (r + NSLOT < r1) // release the slot for the producers' row i + NSLOT
+                asm volatile("bar.arrive %0, %1;" ::"r"(1 + NSLOT + slot), "r"(nthreads));
+        }
+    }
+}
+
 int main() {
     const int nrows = 257;
     long long E = 1884000; // ~C4 entry count
@@ -76,6 +134,21 @@ int main() {
         timeit(nm, [&] { pattern<false><<<grid, 256>>>(buf, EB, B, nrows, chunk); });
         snprintf(nm, sizeof nm, "pattern%d_cs", B);
         timeit(nm, [&] { pattern<true><<<grid, 256>>>(buf, EB, B, nrows, chunk); });
+    }
+    for (int B : {75, 147}) {
+        const int cap = 512;
+        const long long EB = E / B * B;
+        const long long per = cap / B * B;
+        const int chunk = 52;
+        dim3 grid((unsigned)((EB + per - 1) / per), (nrows + chunk - 1) / chunk);
+        const size_t smem = 3 * (5 * cap + 32) * sizeof(double);
+        char nm[32];
+        snprintf(nm, sizeof nm, "ws8+2_B%d", B);
+        cudaFuncSetAttribute(ws_pattern<8, 2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        timeit(nm, [&] { ws_pattern<8, 2, 3><<<grid, 320, smem>>>(buf, EB, B, nrows, chunk, cap); });
+        snprintf(nm, sizeof nm, "ws8+4_B%d", B);
+        cudaFuncSetAttribute(ws_pattern<8, 4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        timeit(nm, [&] { ws_pattern<8, 4, 3><<<grid, 384, smem>>>(buf, EB, B, nrows, chunk, cap); });
     }
     cudaFree(buf);
     return 0;
