@@ -658,8 +658,13 @@ __device__ __forceinline__ void element_tables(const DevTables& d, const ElemInf
 /// (pullbackContractionTable, voigt_free.cpp:125-140).
 __device__ __forceinline__ void pullback_tables(const DevTables& d, int e_index, int nq2,
                                                 const double* w2, const double* table, double* ctq) {
-    for (int idx = threadIdx.x; idx < nq2 * 81; idx += blockDim.x) {
-        const int q = idx / 81, xy = (idx % 81) / 9, ik = idx % 9;
+    // layout [q][xy][10]: ik padded to 10 so the consumers load 16-byte pairs
+    for (int idx = threadIdx.x; idx < nq2 * 90; idx += blockDim.x) {
+        const int q = idx / 90, xy = (idx % 90) / 10, ik = idx % 10;
+        if (ik == 9) {
+            ctq[idx] = 0.0;
+            continue;
+        }
         const int x = xy / 3, y = xy % 3;
         const double* G;
         double det;
@@ -697,10 +702,11 @@ __global__ void k_inplane_general(const DevTables d, int cu, int cv) {
     el.hv = 0.5 * (d.spv_hi[el.ev] - d.spv_lo[el.ev]);
     double* gh = sm;                    // nq2 * nl2 * 3
     double* w2 = gh + el.nq2 * el.nl2 * 3; // nq2
-    double* ctq = w2 + el.nq2;          // nq2 * 81
+    double* ctq = sm + ((el.nq2 * el.nl2 * 3 + el.nq2 + 1) & ~1); // nq2 * 90, 16-byte aligned
     element_tables(d, el, gh, w2);
     const int e_index = el.ev * d.nspu + el.eu;
-    for (int t = 0; t < d.n_terms; ++t) {
+    {
+        const int t = blockIdx.z; // one block per (element, term): 4x the blocks per colour
         __syncthreads();
         pullback_tables(d, e_index, el.nq2, w2, d.term_table + (long long)t * 81, ctq);
         __syncthreads();
@@ -721,13 +727,14 @@ __global__ void k_inplane_general(const DevTables d, int cu, int cv) {
 #pragma unroll
                     for (int y = 0; y < 3; ++y)
                         s[3 * x + y] = ga[x] * gb[y];
-                const double* C = ctq + q * 81;
+                // P11 <- C~00,01,10,11; P12 <- 02,12; P21 <- 20,21; P22 <- 22 (layout [q][xy][10])
+                const double* C = ctq + q * 90;
 #pragma unroll
                 for (int k = 0; k < 9; ++k) {
-                    acc[0][k] += C[0 * 9 + k] * s[0] + C[1 * 9 + k] * s[1] + C[3 * 9 + k] * s[3] + C[4 * 9 + k] * s[4];
-                    acc[1][k] += C[2 * 9 + k] * s[2] + C[5 * 9 + k] * s[5];
-                    acc[2][k] += C[6 * 9 + k] * s[6] + C[7 * 9 + k] * s[7];
-                    acc[3][k] += C[8 * 9 + k] * s[8];
+                    acc[0][k] += C[0 * 10 + k] * s[0] + C[1 * 10 + k] * s[1] + C[3 * 10 + k] * s[3] + C[4 * 10 + k] * s[4];
+                    acc[1][k] += C[2 * 10 + k] * s[2] + C[5 * 10 + k] * s[5];
+                    acc[2][k] += C[6 * 10 + k] * s[6] + C[7 * 10 + k] * s[7];
+                    acc[3][k] += C[8 * 10 + k] * s[8];
                 }
             }
             const int iu = el.fu + al % (d.pu + 1), iv = el.fv + al / (d.pu + 1);
@@ -777,8 +784,8 @@ __global__ void k_standard(const DevTables d, double* __restrict__ values, int c
     const int nl3 = el.nl2 * ntl;
     double* gh = sm;
     double* w2 = gh + el.nq2 * el.nl2 * 3;
-    double* ctq = w2 + el.nq2;
-    double* tv = ctq + el.nq2 * 81; // nqt * ntl values, then derivatives
+    double* ctq = sm + ((el.nq2 * el.nl2 * 3 + el.nq2 + 1) & ~1); // nq2 * 90, 16-byte aligned
+    double* tv = ctq + el.nq2 * 90; // nqt * ntl values, then derivatives
     double* td = tv + d.nqt * ntl;
     double* w3 = td + d.nqt * ntl;
     element_tables(d, el, gh, w2);
@@ -814,7 +821,12 @@ __global__ void k_standard(const DevTables d, double* __restrict__ values, int c
             for (int q2 = 0; q2 < el.nq2; ++q2) {
                 const double* ga = gh + (q2 * el.nl2 + as) * 3;
                 const double* gb = gh + (q2 * el.nl2 + bs) * 3;
-                const double* C = ctq + q2 * 81;
+                // the thickness points of the cell share the in-plane C~: sum the
+                // 9 gradient products over q3 first, then contract once with C~
+                double S[9];
+#pragma unroll
+                for (int xy = 0; xy < 9; ++xy)
+                    S[xy] = 0.0;
                 for (int q3 = 0; q3 < d.nqt; ++q3) {
                     const double Ta = tv[q3 * ntl + at], Tda = td[q3 * ntl + at];
                     const double Tb = tv[q3 * ntl + bt], Tdb = td[q3 * ntl + bt];
@@ -824,12 +836,19 @@ __global__ void k_standard(const DevTables d, double* __restrict__ values, int c
 #pragma unroll
                     for (int x = 0; x < 3; ++x)
 #pragma unroll
-                        for (int y = 0; y < 3; ++y) {
-                            const double s = xa[x] * xb[y];
+                        for (int y = 0; y < 3; ++y)
+                            S[3 * x + y] += xa[x] * xb[y];
+                }
+                const double2* C2 = reinterpret_cast<const double2*>(ctq + q2 * 90);
 #pragma unroll
-                            for (int k = 0; k < 9; ++k)
-                                acc[k] += C[(3 * x + y) * 9 + k] * s;
-                        }
+                for (int xy = 0; xy < 9; ++xy) {
+#pragma unroll
+                    for (int h = 0; h < 5; ++h) {
+                        const double2 c = C2[xy * 5 + h];
+                        acc[2 * h] += c.x * S[xy];
+                        if (2 * h + 1 < 9)
+                            acc[2 * h + 1] += c.y * S[xy];
+                    }
                 }
             }
             const int iu = el.fu + as % (d.pu + 1), iv = el.fv + as / (d.pu + 1);
@@ -1129,13 +1148,14 @@ int launch_affine_export(const DevTables& d, cudaStream_t stream) {
 
 int launch_inplane_general(const DevTables& d, cudaStream_t stream) {
     const int nl2 = (d.pu + 1) * (d.pv + 1), nq2 = d.nqu * d.nqv;
-    const size_t smem = sizeof(double) * ((size_t)nq2 * nl2 * 3 + nq2 + (size_t)nq2 * 81);
+    const size_t smem = sizeof(double) * ((size_t)nq2 * nl2 * 3 + nq2 + 1 + (size_t)nq2 * 90);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_inplane_general, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const dim3 grid((d.nspu + d.pu) / (d.pu + 1), (d.nspv + d.pv) / (d.pv + 1));
+    const dim3 grid((d.nspu + d.pu) / (d.pu + 1), (d.nspv + d.pv) / (d.pv + 1), d.n_terms);
+    const int threads = std::min(256, (nl2 * nl2 + 31) / 32 * 32); // one thread per local pair
     for (int cv = 0; cv <= d.pv; ++cv)
         for (int cu = 0; cu <= d.pu; ++cu)
-            k_inplane_general<<<grid, 128, smem, stream>>>(d, cu, cv);
+            k_inplane_general<<<grid, threads, smem, stream>>>(d, cu, cv);
     return (int)cudaGetLastError();
 }
 
@@ -1214,7 +1234,7 @@ int launch_pattern(const DevTables& d, long long* row_ptr, int* cols, cudaStream
 int launch_standard(const DevTables& d, double* values, long long nnz, cudaStream_t stream, int* launches) {
     cudaMemsetAsync(values, 0, sizeof(double) * (size_t)nnz, stream);
     const int nl2 = (d.pu + 1) * (d.pv + 1), nq2 = d.nqu * d.nqv, ntl = d.pt + 1;
-    const size_t smem = sizeof(double) * ((size_t)nq2 * nl2 * 3 + nq2 + (size_t)nq2 * 81 +
+    const size_t smem = sizeof(double) * ((size_t)nq2 * nl2 * 3 + nq2 + 1 + (size_t)nq2 * 90 +
                                           2 * (size_t)d.nqt * ntl + d.nqt);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_standard, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
