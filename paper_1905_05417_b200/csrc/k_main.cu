@@ -594,7 +594,15 @@ __global__ void __launch_bounds__((NP + NC) * 32) k_combine_ws(const DevTables d
             const int body = (n - head) >> 1;
             const double2* sv = reinterpret_cast<const double2*>(sbuf + head);
             double2* gv = reinterpret_cast<double2*>(g + head);
-            for (int v = ct; v < body; v += NC * 32)
+            int v = ct;
+            for (; v + 3 * NC * 32 < body; v += 4 * NC * 32) { // 4 loads in flight per lane
+                const double2 a0 = sv[v], a1 = sv[v + NC * 32], a2 = sv[v + 2 * NC * 32], a3 = sv[v + 3 * NC * 32];
+                __stcs(gv + v, a0);
+                __stcs(gv + v + NC * 32, a1);
+                __stcs(gv + v + 2 * NC * 32, a2);
+                __stcs(gv + v + 3 * NC * 32, a3);
+            }
+            for (; v < body; v += NC * 32)
                 __stcs(gv + v, sv[v]);
             if (((n - head) & 1) && ct == NC * 32 - 1)
                 __stcs(g + n - 1, sbuf[n - 1]);

@@ -39,6 +39,24 @@ __global__ void pattern(double* out, long long E, int B, int nrows, int chunk) {
     }
 }
 
+// Two adjacent entries per lane, one 16-byte store per (row, k): B even keeps
+// every piece 16-byte aligned (128-byte alignment still varies with k).
+__global__ void pattern_v2(double* out, long long E, int B, int nrows, int chunk) {
+    const long long e = ((long long)blockIdx.x * 256 + threadIdx.x) * 2;
+    if (e >= E)
+        return;
+    const long long A = e / B * B;
+    const int rem = (int)(e - A);
+    const int r0 = blockIdx.y * chunk, r1 = min(nrows, r0 + chunk);
+    for (int r = r0; r < r1; ++r) {
+        const int lt = (r & 1) ? 3 : 5;
+        const long long pfx = (long long)(r / 2) * 8 + ((r & 1) ? 5 : 0);
+        double* o = out + pfx * E + (long long)lt * A + rem;
+        for (int k = 0; k < lt; ++k)
+            __stcs(reinterpret_cast<double2*>(o + (long long)k * B), make_double2(1.0, 1.0));
+    }
+}
+
 // Warp-specialised staging: NP producer warps write the block's contiguous
 // row range into a smem slot, NC consumer warps copy it out with 128-byte
 // aligned 16-byte stores; named barriers hand slots over (no block barrier).
@@ -134,6 +152,17 @@ int main() {
         timeit(nm, [&] { pattern<false><<<grid, 256>>>(buf, EB, B, nrows, chunk); });
         snprintf(nm, sizeof nm, "pattern%d_cs", B);
         timeit(nm, [&] { pattern<true><<<grid, 256>>>(buf, EB, B, nrows, chunk); });
+    }
+    for (int B : {74, 146}) {
+        const long long EB = E / B * B;
+        dim3 grid((unsigned)((EB / 2 + 255) / 256), 5);
+        const int chunk = (nrows + 4) / 5;
+        char nm[32];
+        snprintf(nm, sizeof nm, "v2_B%d", B);
+        timeit(nm, [&] { pattern_v2<<<grid, 256>>>(buf, EB, B, nrows, chunk); });
+        dim3 grid1((unsigned)((EB + 255) / 256), 5);
+        snprintf(nm, sizeof nm, "scalar_B%d", B);
+        timeit(nm, [&] { pattern<true><<<grid1, 256>>>(buf, EB, B, nrows, chunk); });
     }
     for (int B : {75, 147}) {
         const int cap = 512;
