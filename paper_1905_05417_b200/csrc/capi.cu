@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -232,6 +233,76 @@ void upload_terms(DeviceArena& ar, lfb::DevTables& d, int n_terms, int n_layers,
     d.Ct = ar.alloc<double>(static_cast<std::size_t>(std::max(1, n_terms)) * 81);
 }
 
+
+/// Team layout of the bulk-store combine (k_combine_team): pick (team warps,
+/// entries per thread) so that an interior row-segment group fits, P stays
+/// in registers (EPT * terms * 4 <= 48 doubles) and the lanes are best used;
+/// then pack consecutive whole groups (i_s, a) greedily into team ranges.
+void upload_teams(const lfb::Setup& s, DeviceArena& ar, lfb::DevTables& d) {
+    d.n_team = 0;
+    d.tm_team = 0;
+    d.tm_ept = 0;
+    if (d.n_passes != 1 || d.n_terms > 4 || d.E == 0)
+        return;
+    long long bmax = 0;
+    for (int is = 0; is < s.n_s; ++is)
+        bmax = std::max<long long>(bmax, 3LL * s.au.len[static_cast<std::size_t>(is % s.n_u)] *
+                                             s.av.len[static_cast<std::size_t>(is / s.n_u)]);
+    // Opt-in (measured slower than the direct stores so far, profiles/r1_store_modes.md):
+    // LAMFAST_TEAM=<team>,<ept> selects a layout, LAMFAST_TEAM=auto the heuristic below.
+    const char* env = std::getenv("LAMFAST_TEAM");
+    if (!env)
+        return;
+    int team = 0, ept = 0;
+    if (std::strcmp(env, "auto") != 0) {
+        if (std::sscanf(env, "%d,%d", &team, &ept) != 2)
+            team = 0;
+        if (team <= 0 || team > 8 || ept < 1 || ept > 3)
+            return;
+    } else {
+        double best = -1.0;
+        for (int t = 1; t <= 8; ++t)
+            for (int e = 1; e <= 3; ++e) {
+                const long long cap = 32LL * t * e;
+                if (cap < bmax || e * d.n_terms * 4 > 48)
+                    continue;
+                const double util = static_cast<double>((cap / bmax) * bmax) / static_cast<double>(cap);
+                // prefer lane utilisation, then fewer warps per team barrier
+                const double score = util - 0.01 * t;
+                if (score > best) {
+                    best = score;
+                    team = t;
+                    ept = e;
+                }
+            }
+        if (team == 0)
+            return;
+    }
+    const long long cap = 32LL * team * ept;
+    if (cap < bmax)
+        return;
+    std::vector<long long> e0;
+    std::vector<int> is0;
+    long long cur = -1;
+    for (int is = 0; is < s.n_s; ++is) {
+        const long long B = 3LL * s.au.len[static_cast<std::size_t>(is % s.n_u)] *
+                            s.av.len[static_cast<std::size_t>(is / s.n_u)];
+        for (int a = 0; a < 3; ++a) {
+            const long long g0 = s.es_pre[static_cast<std::size_t>(is)] + a * B;
+            if (cur < 0 || g0 + B - cur > cap) {
+                e0.push_back(g0);
+                is0.push_back(is);
+                cur = g0;
+            }
+        }
+    }
+    e0.push_back(d.E);
+    d.n_team = static_cast<int>(e0.size()) - 1;
+    d.tm_team = team;
+    d.tm_ept = ept;
+    d.tm_e0 = reinterpret_cast<const long long*>(ar.upload(e0));
+    d.tm_is = ar.upload(is0);
+}
 } // namespace
 
 struct lf_plan {
@@ -300,6 +371,7 @@ void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void
     d.t1 = s.t1;
     d.n_pairs = s.n_pairs;
     if (backend != LF_BACKEND_STANDARD) {
+        upload_teams(s, ar, d);
         d.W = ar.alloc<double>(static_cast<std::size_t>(std::max<long long>(1, d.n_pairs)) * d.n_terms * 4);
         if (d.ws_variant > 0 && d.n_terms <= 4) {
             const std::size_t rows = static_cast<std::size_t>(std::max(1, d.t1 - d.t0));

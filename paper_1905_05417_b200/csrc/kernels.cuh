@@ -53,6 +53,12 @@ struct DevTables {
     int ws_variant; // 0 direct stores; 1..3 warp-specialised layout (LAMFAST_WS)
     void* g_rows;   // [slab rows] packed row records (constant-bank image)
     void* g_w;      // [slab rows][lt_max][terms] double4 weights image
+    // team/bulk combine: teams of tm_team warps own whole row-segment groups,
+    // at most 32 * tm_team * tm_ept entries; first entry of each team range
+    // (n_team + 1 values) and its first i_s.  n_team = 0 -> direct stores.
+    const long long* tm_e0;
+    const int* tm_is;
+    int n_team, tm_team, tm_ept;
     long long S_s, S_u;
     // geometry
     int affine;

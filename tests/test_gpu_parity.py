@@ -370,3 +370,42 @@ def test_c5_slab_fast_equals_standard_on_device(gpu):
     std = _device_csr(gpu, prob, "standard", t0, t0 + 4)
     assert torch.equal(fast[1], std[1]) and torch.equal(fast[2], std[2])
     assert _device_rel_diff(gpu, fast, std) <= RTOL
+
+
+@pytest.mark.parametrize("env", [
+    {"LAMFAST_TEAM": "auto"}, {"LAMFAST_TEAM": "1,3"}, {"LAMFAST_TEAM": "4,2"},
+    {"LAMFAST_TEAM": "3,1", "LAMFAST_TEAM_KR": "1"}, {"LAMFAST_WS": "1"},
+])
+def test_opt_in_store_variants_match_oracle(gpu, oracle, monkeypatch, env):
+    """The opt-in combine variants (team/bulk-copy stores, warp-specialised
+    stores; profiles/r1_store_modes.md) give the same CSR as the oracle:
+    boundary groups, mixed degrees / C0 thickness, skewed geometry (general
+    P), and slab plans whose output ranges start at odd 8-byte phases."""
+    import torch
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    mixed = P.LaminateProblem(
+        degree_u=2, degree_v=3, degree_t=2, knots_u=P.uniform_knots(2, 3),
+        knots_v=P.uniform_knots(3, 2), knots_t=P.c0_knots(2, 3),
+        interfaces=P.equal_interfaces(3),
+        layers=[(P.baseline_orthotropic(), 0.0), (P.isotropic(0.5, 0.3), 0.0),
+                (P.baseline_orthotropic(), 0.6)])
+    skew = P.cube_problem(2, 3, 2, [0.0, 0.9, 0.3], geometry="skewed")
+    for prob in (P.baseline_config("C1"), P.baseline_config("C2"), mixed, skew):
+        got = gpu.assemble_fast(prob)
+        assert_csr_match(got.astuple(), oracle.assemble(prob, "fast"), RTOL)
+    prob = P.baseline_config("C2")
+    for part in range(3):
+        b = gpu.slab_bounds(prob, 3, part)
+        plan = gpu.Plan(prob, "fast", 0, b["t_begin"], b["t_end"])
+        rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
+        cols = torch.empty(max(1, plan.nnz), dtype=torch.int32, device="cuda")
+        # values at an 8-byte (not 16-byte) aligned base: odd bulk-copy phase
+        raw = torch.empty(max(1, plan.nnz) + 1, dtype=torch.float64, device="cuda")
+        plan.build_pattern(rp.data_ptr(), cols.data_ptr())
+        plan.assemble(raw.data_ptr() + 8)
+        plan.synchronize()
+        want = oracle.assemble(prob, "fast", b["t_begin"], b["t_end"])
+        assert_csr_match((rp.cpu().numpy(), cols.cpu().numpy()[:plan.nnz],
+                          raw.cpu().numpy()[1:plan.nnz + 1]), want, RTOL)
+        plan.close()

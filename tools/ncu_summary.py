@@ -13,7 +13,7 @@ KEYS = [
     "sm__inst_executed.sum", "smsp__inst_executed.sum",
     "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
     "launch__grid_size", "launch__block_size", "launch__occupancy_limit_registers",
-    "launch__occupancy_limit_shared_mem", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "launch__occupancy_limit_shared_mem", "launch__occupancy_limit_barriers", "launch__occupancy_limit_warps", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
     "smsp__sass_inst_executed_op_global_st.sum", "lts__t_sectors_op_write.sum",
     "dram__sectors_write.sum", "sm__cycles_elapsed.avg.per_second",
 ]

@@ -115,6 +115,131 @@ __global__ void __launch_bounds__((NP + NC) * 32) ws_pattern(double* out, long l
     }
 }
 
+// Warp-private staging: warp w owns one whole row segment group (B entries,
+// lanes hold entries lane + 32x), writes its L_t*B values per row into its own
+// double-buffered smem slice, then copies the contiguous region out with
+// 16-byte stores whose warp footprint starts on a 128-byte line.  Only
+// __syncwarp, no block barriers.  MINB forces the blocks/SM of the real kernel.
+template <int EPT, int MINB, int GPW = 1, bool TMA = false>
+__global__ void __launch_bounds__(256, MINB) wp_pattern(double* out, long long E, int B, int nrows, int chunk) {
+    extern __shared__ double smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long g = (long long)blockIdx.x * 8 + warp;
+    const long long g0 = g * B * GPW;
+    if (g0 >= E)
+        return;
+    const int W = B * GPW; // entries of this warp
+    const int slot_len = (5 * W + 3) & ~1;
+    double* buf = smem + warp * 2 * slot_len;
+    const int r0 = blockIdx.y * chunk, r1 = min(nrows, r0 + chunk);
+    for (int r = r0, i = 0; r < r1; ++r, ++i) {
+        const int lt = (r & 1) ? 3 : 5;
+        const long long pfx = (long long)(r / 2) * 8 + ((r & 1) ? 5 : 0);
+        const long long G = pfx * E + (long long)lt * g0;
+        double* sb = buf + (i & 1) * slot_len + (int)(G & 1);
+#pragma unroll
+        for (int x = 0; x < EPT; ++x) {
+            const int ent = lane + 32 * x;
+            const int grp = ent / B, rem = ent - grp * B;
+            if (ent < W)
+                for (int k = 0; k < lt; ++k)
+                    sb[lt * B * grp + k * B + rem] = 1.0;
+        }
+        const int n = lt * W;
+        if constexpr (TMA) {
+            double* gp = out + G;
+            const int h = (int)(G & 1);
+            const int nb = (n - h) & ~1;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                if (h)
+                    __stcs(gp, sb[0]);
+                if (n - h - nb)
+                    __stcs(gp + n - 1, sb[n - 1]);
+                // the buffer written two rows ago must have been read
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gp + h),
+                             "r"((unsigned)__cvta_generic_to_shared(sb + h)), "r"(nb * 8)
+                             : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            }
+            __syncwarp();
+            continue;
+        }
+        __syncwarp();
+        double* gp = out + G;
+        const int head = (int)min((long long)n, (16 - (G & 15)) & 15);
+        if (lane < head)
+            __stcs(gp + lane, sb[lane]);
+        const int body = (n - head) >> 1;
+        const double2* sv = reinterpret_cast<const double2*>(sb + head);
+        double2* gv = reinterpret_cast<double2*>(gp + head);
+        for (int v = lane; v < body; v += 32)
+            __stcs(gv + v, sv[v]);
+        if (((n - head) & 1) && lane == 0)
+            __stcs(gp + n - 1, sb[n - 1]);
+    }
+    if (TMA && lane == 0)
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// Warp owns a contiguous sub-range of one group: `parts` warps split each group
+// (entries [part*B/parts, (part+1)*B/parts)); per row the warp stages its
+// L_t pieces and issues one bulk copy per piece (8-byte head/tail scalar).
+template <int EPT>
+__global__ void __launch_bounds__(256, 1) wp_part_pattern(double* out, long long E, int B, int nrows, int chunk,
+                                                         int parts) {
+    extern __shared__ double smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long gw = (long long)blockIdx.x * 8 + warp;
+    const long long g = gw / parts;
+    const int part = (int)(gw % parts);
+    const long long g0 = g * B;
+    if (g0 >= E)
+        return;
+    const int lo = part * B / parts, hi = (part + 1) * B / parts, W = hi - lo;
+    const int slot_len = (5 * (W + 2) + 3) & ~1;
+    double* buf = smem + warp * 2 * slot_len;
+    const int r0 = blockIdx.y * chunk, r1 = min(nrows, r0 + chunk);
+    for (int r = r0, i = 0; r < r1; ++r, ++i) {
+        const int lt = (r & 1) ? 3 : 5;
+        const long long pfx = (long long)(r / 2) * 8 + ((r & 1) ? 5 : 0);
+        const long long G = pfx * E + (long long)lt * g0 + lo;
+        double* sb = buf + (i & 1) * slot_len;
+        // piece k starts at G + k*B; staged at sb + k*(W+2) + ((G + k*B) & 1)
+#pragma unroll
+        for (int x = 0; x < EPT; ++x) {
+            const int ent = lane + 32 * x;
+            if (ent < W)
+                for (int k = 0; k < lt; ++k)
+                    sb[k * ((W + 3) & ~1) + (int)((G + (long long)k * B) & 1) + ent] = 1.0;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane < lt) {
+            const int k = lane;
+            const long long Gk = G + (long long)k * B;
+            double* gp = out + Gk;
+            const double* sk = sb + k * ((W + 3) & ~1) + (int)(Gk & 1);
+            const int h = (int)(Gk & 1);
+            const int nb = (W - h) & ~1;
+            if (h)
+                __stcs(gp, sk[0]);
+            if (W - h - nb)
+                __stcs(gp + W - 1, sk[W - 1]);
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gp + h),
+                         "r"((unsigned)__cvta_generic_to_shared(sk + h)), "r"(nb * 8)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        }
+        __syncwarp();
+    }
+    if (lane < 5)
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 int main() {
     const int nrows = 257;
     long long E = 1884000; // ~C4 entry count
@@ -178,6 +303,54 @@ int main() {
         snprintf(nm, sizeof nm, "ws8+4_B%d", B);
         cudaFuncSetAttribute(ws_pattern<8, 4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         timeit(nm, [&] { ws_pattern<8, 4, 3><<<grid, 384, smem>>>(buf, EB, B, nrows, chunk, cap); });
+    }
+    for (int B : {75, 147}) {
+        const long long EB = E / B * B;
+        const long long ng = EB / B;
+        const int chunk = 52;
+        dim3 grid((unsigned)((ng + 7) / 8), (nrows + chunk - 1) / chunk);
+        const size_t smem = 8 * 2 * ((5 * B * 2 + 3) & ~1) * sizeof(double);
+        char nm[32];
+        auto run = [&](auto kern, const char* tag) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            snprintf(nm, sizeof nm, "wp_%s_B%d", tag, B);
+            timeit(nm, [&] { kern<<<grid, 256, smem>>>(buf, EB, B, nrows, chunk); });
+        };
+        if (B == 75) {
+            run(wp_pattern<3, 1>, "m1");
+            run(wp_pattern<3, 1, 1, true>, "tma");
+        } else {
+            run(wp_pattern<5, 1>, "m1");
+            run(wp_pattern<5, 1, 1, true>, "tma");
+        }
+        dim3 grid2((unsigned)((ng / 2 + 7) / 8), (nrows + chunk - 1) / chunk);
+        auto run2 = [&](auto kern, const char* tag) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            snprintf(nm, sizeof nm, "wp2_%s_B%d", tag, B);
+            timeit(nm, [&] { kern<<<grid2, 256, smem>>>(buf, EB / (2 * B) * 2 * B, B, nrows, chunk); });
+        };
+        if (B == 75) {
+            run2(wp_pattern<5, 1, 2>, "m1");
+            run2(wp_pattern<5, 1, 2, true>, "tma");
+        } else {
+            run2(wp_pattern<10, 1, 2>, "m1");
+            run2(wp_pattern<10, 1, 2, true>, "tma");
+        }
+    }
+    for (int B : {75, 147}) {
+        const long long EB = E / B * B;
+        const long long ng = EB / B;
+        const int chunk = 52;
+        for (int parts : {1, 2, 3}) {
+            dim3 grid((unsigned)((ng * parts + 7) / 8), (nrows + chunk - 1) / chunk);
+            const int W = (B + parts - 1) / parts;
+            const size_t smem = 8 * 2 * ((5 * (W + 2) + 3) & ~1) * sizeof(double);
+            char nm[32];
+            snprintf(nm, sizeof nm, "part%d_B%d", parts, B);
+            auto kern = W <= 96 ? wp_part_pattern<3> : wp_part_pattern<5>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            timeit(nm, [&] { kern<<<grid, 256, smem>>>(buf, EB, B, nrows, chunk, parts); });
+        }
     }
     cudaFree(buf);
     return 0;
