@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -366,6 +367,22 @@ void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void
     upload_geometry(s, ar, d);
     upload_thickness(s, ar, d, s.at);
     upload_terms(ar, d, s.n_terms, p->n_layers, s.term_table, s.lam, s.lam_on);
+    {
+        // major symmetry of every term table (exact up to 1e-15 relative):
+        // lets K6 compute half the local pairs and mirror them
+        double amax = 0.0, dmax = 0.0;
+        for (std::size_t t = 0; t * 81 < s.term_table.size(); ++t)
+            for (int j = 0; j < 3; ++j)
+                for (int l = 0; l < 3; ++l)
+                    for (int a = 0; a < 3; ++a)
+                        for (int b = 0; b < 3; ++b) {
+                            const double x = s.term_table[t * 81 + (3 * j + l) * 9 + 3 * a + b];
+                            const double y = s.term_table[t * 81 + (3 * l + j) * 9 + 3 * b + a];
+                            amax = std::max(amax, std::fabs(x));
+                            dmax = std::max(dmax, std::fabs(x - y));
+                        }
+        d.sym = (dmax <= 1e-15 * amax && !std::getenv("LAMFAST_NO_SYM")) ? 1 : 0;
+    }
     d.layer_config = ar.upload(s.layup.layer_config);
     d.t0 = s.t0;
     d.t1 = s.t1;

@@ -1018,6 +1018,8 @@ __global__ void k_inplane_general(const DevTables d, int cu, int cv) {
         __syncthreads();
         pullback_tables(d, e_index, el.nq2, w2, d.term_table + (long long)t * 81, ctq);
         __syncthreads();
+        // all nl2^2 local pairs (halving them by symmetry was measured slower: this
+        // kernel is bound by the coloured read-modify-write of Pg, not by FP64)
         for (int pr = threadIdx.x; pr < el.nl2 * el.nl2; pr += blockDim.x) {
             const int al = pr / el.nl2, be = pr % el.nl2;
             double acc[4][9];
@@ -1115,12 +1117,27 @@ __global__ void k_standard(const DevTables d, double* __restrict__ values, int c
         for (int q = threadIdx.x; q < d.nqt; q += blockDim.x)
             w3[q] = d.cell_wts[(long long)c * d.nqt + q];
         __syncthreads();
-        for (int pr = threadIdx.x; pr < nl3 * nl3; pr += blockDim.x) {
-            const int al = pr / nl3, be = pr % nl3;
+        const int npair = d.sym ? nl3 * (nl3 + 1) / 2 : nl3 * nl3;
+        for (int pr = threadIdx.x; pr < npair; pr += blockDim.x) {
+            int al, be;
+            if (d.sym) { // triangular index: be >= al
+                al = 0;
+                int rest = pr;
+                while (rest >= nl3 - al) {
+                    rest -= nl3 - al;
+                    ++al;
+                }
+                be = al + rest;
+            } else {
+                al = pr / nl3;
+                be = pr % nl3;
+            }
             const int at = al / el.nl2, as = al % el.nl2;
             const int bt = be / el.nl2, bs = be % el.nl2;
             const int it = ft + at, jt = ft + bt;
-            if (it < d.t0 || it >= d.t1)
+            const bool row_i = it >= d.t0 && it < d.t1;
+            const bool row_j = d.sym && al != be && jt >= d.t0 && jt < d.t1;
+            if (!row_i && !row_j)
                 continue;
             double acc[9];
 #pragma unroll
@@ -1159,20 +1176,29 @@ __global__ void k_standard(const DevTables d, double* __restrict__ values, int c
                     }
                 }
             }
-            const int iu = el.fu + as % (d.pu + 1), iv = el.fv + as / (d.pu + 1);
-            const int ju = el.fu + bs % (d.pu + 1), jv = el.fv + bs / (d.pu + 1);
-            const int is = iv * d.nu + iu;
-            const int Lu = d.len_u[iu], Lv = d.len_v[iv];
-            const int B = 3 * Lu * Lv;
-            const int slot = (jv - d.lo_v[iv]) * Lu + (ju - d.lo_u[iu]);
-            const int Lt = d.len_t[it];
-            const long long pos = 9 * d.S_s * (d.pre_t[it] - pre0) + (long long)Lt * d.es_pre[is] +
-                                  (long long)(jt - d.lo_t[it]) * B + 3 * slot;
+            // K(i,j)[a][b] into row block i; with symmetric tables also
+            // K(j,i)[b][a] = K(i,j)[a][b] into row block j (same element, so the
+            // colouring still makes the += race-free)
+            for (int side = 0; side < 2; ++side) {
+                if (side == 0 ? !row_i : !row_j)
+                    continue;
+                const int ls = side ? bs : as, ms = side ? as : bs;
+                const int rt = side ? jt : it, ct_ = side ? it : jt;
+                const int iu = el.fu + ls % (d.pu + 1), iv = el.fv + ls / (d.pu + 1);
+                const int ju = el.fu + ms % (d.pu + 1), jv = el.fv + ms / (d.pu + 1);
+                const int is = iv * d.nu + iu;
+                const int Lu = d.len_u[iu], Lv = d.len_v[iv];
+                const int B = 3 * Lu * Lv;
+                const int slot = (jv - d.lo_v[iv]) * Lu + (ju - d.lo_u[iu]);
+                const int Lt = d.len_t[rt];
+                const long long pos = 9 * d.S_s * (d.pre_t[rt] - pre0) + (long long)Lt * d.es_pre[is] +
+                                      (long long)(ct_ - d.lo_t[rt]) * B + 3 * slot;
 #pragma unroll
-            for (int a = 0; a < 3; ++a)
+                for (int a = 0; a < 3; ++a)
 #pragma unroll
-                for (int b = 0; b < 3; ++b)
-                    values[pos + (long long)a * Lt * B + b] += acc[3 * a + b];
+                    for (int b = 0; b < 3; ++b)
+                        values[pos + (long long)a * Lt * B + b] += side ? acc[3 * b + a] : acc[3 * a + b];
+            }
         }
     }
 }

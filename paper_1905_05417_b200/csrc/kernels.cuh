@@ -59,6 +59,9 @@ struct DevTables {
     const long long* tm_e0;
     const int* tm_is;
     int n_team, tm_team, tm_ept;
+    // every term table has major symmetry C[(3j+l)9 + 3a+b] = C[(3l+j)9 + 3b+a]:
+    // the standard kernel (K6) then computes pairs al <= be and mirrors them
+    int sym;
     long long S_s, S_u;
     // geometry
     int affine;
