@@ -381,6 +381,8 @@ void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void
                             amax = std::max(amax, std::fabs(x));
                             dmax = std::max(dmax, std::fabs(x - y));
                         }
+        // warp-contiguous entry slots in k_combine (C4 2.79 -> 2.66 ms); LAMFAST_CONTIG=0 restores strided
+        d.contig = std::getenv("LAMFAST_CONTIG") ? std::atoi(std::getenv("LAMFAST_CONTIG")) : 1;
         d.sym = (dmax <= 1e-15 * amax && !std::getenv("LAMFAST_NO_SYM")) ? 1 : 0;
     }
     d.layer_config = ar.upload(s.layup.layer_config);

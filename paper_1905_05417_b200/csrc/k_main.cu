@@ -24,11 +24,6 @@ namespace lfb {
 namespace {
 
 constexpr int kBlock = 256;
-#ifdef LF_COMBINE_MIN_BLOCKS
-#define LF_COMBINE_BOUNDS __launch_bounds__(kBlock, LF_COMBINE_MIN_BLOCKS)
-#else
-#define LF_COMBINE_BOUNDS __launch_bounds__(kBlock)
-#endif
 
 /// Output store of the combine kernel: st.global.cs (evict-first), the
 /// values are written once and never re-read by this kernel (measured
@@ -290,9 +285,9 @@ __device__ __forceinline__ void stage_rows_block(const DevTables& d, int it0, in
     }
 }
 
-template <int NT, int EPT, bool AFFINE, bool ACCUM>
-__global__ void LF_COMBINE_BOUNDS k_combine(const DevTables d, double* __restrict__ out, int pass, int t_chunk,
-                                            int stage_rows, int lt_max) {
+template <int NT, int EPT, bool AFFINE, bool ACCUM, int BT>
+__device__ __forceinline__ void combine_body(const DevTables& d, double* __restrict__ out, int pass, int t_chunk,
+                                             int stage_rows, int lt_max) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     RowInfo* s_row = reinterpret_cast<RowInfo*>(smem_raw);
     unsigned char* s_kr = smem_raw + stage_rows * sizeof(RowInfo); // [row][NT][2]
@@ -307,11 +302,15 @@ __global__ void LF_COMBINE_BOUNDS k_combine(const DevTables d, double* __restric
     bool live[EPT];
 #pragma unroll
     for (int x = 0; x < EPT; ++x) {
-        const int sub = blockIdx.x * EPT + x; // 256-entry sub-block
-        const long long e = (long long)sub * kBlock + threadIdx.x;
+        // entry of slot x: 'strided' e = (blockIdx*EPT + x)*256 + tid, or
+        // 'contiguous' (d.contig) e = blockIdx*256*EPT + warp*32*EPT + x*32 + lane,
+        // where a warp's EPT stores per (row, k) are adjacent 256-byte runs
+        const long long e = d.contig ? (long long)blockIdx.x * BT * EPT + (threadIdx.x >> 5) * 32 * EPT + x * 32 +
+                                           (threadIdx.x & 31)
+                                     : (long long)(blockIdx.x * EPT + x) * BT + threadIdx.x;
         live[x] = e < d.E;
         const long long ec = live[x] ? e : d.E - 1;
-        int is = __ldg(d.blk_is + min((long long)sub, (d.E - 1) / kBlock));
+        int is = __ldg(d.blk_is + ec / kBlock);
         while (__ldg(d.es_pre + is + 1) <= ec)
             ++is;
         const long long ebase = __ldg(d.es_pre + is);
@@ -347,7 +346,7 @@ __global__ void LF_COMBINE_BOUNDS k_combine(const DevTables d, double* __restric
         const int nrow = min(stage_rows, it_end - it0);
         if (it0 != it_begin)
             __syncthreads();
-        stage_rows_block<NT>(d, it0, nrow, pass, lt_max, s_row, s_kr, s_w, threadIdx.x, kBlock);
+        stage_rows_block<NT>(d, it0, nrow, pass, lt_max, s_row, s_kr, s_w, threadIdx.x, BT);
         __syncthreads();
         if (!any_live)
             continue;
@@ -372,6 +371,22 @@ __global__ void LF_COMBINE_BOUNDS k_combine(const DevTables d, double* __restric
     }
 }
 
+
+
+// k_combine: 256-thread blocks and the compiler's own register choice (<= 128
+// here); k_combine_b: explicit bounds for the wide variant (4 terms, two
+// entries per thread: ~155 registers, 128-thread blocks, 3 per SM).
+template <int NT, int EPT, bool AFFINE, bool ACCUM>
+__global__ void __launch_bounds__(kBlock) k_combine(const DevTables d, double* __restrict__ out, int pass,
+                                                    int t_chunk, int stage_rows, int lt_max) {
+    combine_body<NT, EPT, AFFINE, ACCUM, kBlock>(d, out, pass, t_chunk, stage_rows, lt_max);
+}
+
+template <int NT, int EPT, bool AFFINE, bool ACCUM, int BT, int MINB>
+__global__ void __launch_bounds__(BT, MINB) k_combine_b(const DevTables d, double* __restrict__ out, int pass,
+                                                        int t_chunk, int stage_rows, int lt_max) {
+    combine_body<NT, EPT, AFFINE, ACCUM, BT>(d, out, pass, t_chunk, stage_rows, lt_max);
+}
 
 // ---------------------------------------------------------------------------
 // K4, team/bulk variant (opt-in: LAMFAST_TEAM, see upload_teams in capi.cu).  The direct kernel above
@@ -1361,8 +1376,12 @@ int reduce_launch(int blocks, double* partial, double* out, cudaStream_t stream)
 #define LF_COMBINE_EPT 2 // two entries per thread for <= 3 terms (C4: 3.04 -> 2.82 ms); 4 terms spill
 #endif
 
+#ifndef LF_COMBINE_EPT4
+#define LF_COMBINE_EPT4 1
+#endif
+
 template <int NT>
-constexpr int entries_per_thread() { return NT <= 3 ? LF_COMBINE_EPT : 1; }
+constexpr int entries_per_thread() { return NT <= 3 ? LF_COMBINE_EPT : NT == 4 ? LF_COMBINE_EPT4 : 1; }
 
 /// TMA-bulk variant for a first pass; false when it does not apply (group
 /// wider than a block, or staging buffers too large for two blocks per SM).
@@ -1502,27 +1521,32 @@ bool combine_team(const DevTables& d, double* out, int t_chunk_req, int lt_max, 
 
 template <int NT>
 void combine_one(const DevTables& d, double* out, int pass, int t_chunk, int stage_rows, int lt_max,
-                 unsigned nblk, unsigned nchunk, cudaStream_t s, bool accum) {
+                 unsigned nchunk, cudaStream_t s, bool accum) {
     constexpr int EPT = entries_per_thread<NT>();
-    (void)nchunk;
+    // two entries per thread with 4 terms need ~155 registers: 128-thread
+    // blocks, 3 per SM; everything else 256-thread blocks, <= 128 registers
+    constexpr int BT = (NT == 4 && EPT == 2) ? 128 : kBlock;
+    constexpr int MINB = (NT == 4 && EPT == 2) ? 3 : 2;
     const size_t smem = ((stage_rows * (sizeof(RowInfo) + 2 * NT) + 31) & ~size_t(31)) +
                         (size_t)stage_rows * lt_max * NT * sizeof(double4);
-    const dim3 grid((nblk + EPT - 1) / EPT, nchunk);
+    const dim3 grid((unsigned)((d.E + (long long)BT * EPT - 1) / ((long long)BT * EPT)), nchunk);
     auto launch = [&](auto kern) {
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<grid, kBlock, smem, s>>>(d, out, pass, t_chunk, stage_rows, lt_max);
+        kern<<<grid, BT, smem, s>>>(d, out, pass, t_chunk, stage_rows, lt_max);
     };
-    if (d.affine) {
-        if (accum)
-            launch(k_combine<NT, EPT, true, true>);
+    if constexpr (BT == kBlock) {
+        if (d.affine)
+            accum ? launch(k_combine<NT, EPT, true, true>) : launch(k_combine<NT, EPT, true, false>);
         else
-            launch(k_combine<NT, EPT, true, false>);
+            accum ? launch(k_combine<NT, EPT, false, true>) : launch(k_combine<NT, EPT, false, false>);
     } else {
-        if (accum)
-            launch(k_combine<NT, EPT, false, true>);
+        if (d.affine)
+            accum ? launch(k_combine_b<NT, EPT, true, true, BT, MINB>)
+                  : launch(k_combine_b<NT, EPT, true, false, BT, MINB>);
         else
-            launch(k_combine<NT, EPT, false, false>);
+            accum ? launch(k_combine_b<NT, EPT, false, true, BT, MINB>)
+                  : launch(k_combine_b<NT, EPT, false, false, BT, MINB>);
     }
 }
 
@@ -1605,16 +1629,15 @@ int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t st
         // rows per staged sub-chunk: ~24 KB of weights, at most the chunk
         int stage_rows = (int)((24 * 1024) / ((size_t)lt_max * nterm * sizeof(double4)));
         stage_rows = std::max(1, std::min(stage_rows, t_chunk));
-        const unsigned nb = (unsigned)nblk;
         switch (nterm) {
-        case 1: combine_one<1>(d, out, pass, t_chunk, stage_rows, lt_max, nb, nchunk, stream, accum); break;
-        case 2: combine_one<2>(d, out, pass, t_chunk, stage_rows, lt_max, nb, nchunk, stream, accum); break;
-        case 3: combine_one<3>(d, out, pass, t_chunk, stage_rows, lt_max, nb, nchunk, stream, accum); break;
-        case 4: combine_one<4>(d, out, pass, t_chunk, stage_rows, lt_max, nb, nchunk, stream, accum); break;
-        case 5: combine_one<5>(d, out, pass, t_chunk, stage_rows, lt_max, nb, nchunk, stream, accum); break;
-        case 6: combine_one<6>(d, out, pass, t_chunk, stage_rows, lt_max, nb, nchunk, stream, accum); break;
-        case 7: combine_one<7>(d, out, pass, t_chunk, stage_rows, lt_max, nb, nchunk, stream, accum); break;
-        default: combine_one<8>(d, out, pass, t_chunk, stage_rows, lt_max, nb, nchunk, stream, accum); break;
+        case 1: combine_one<1>(d, out, pass, t_chunk, stage_rows, lt_max, nchunk, stream, accum); break;
+        case 2: combine_one<2>(d, out, pass, t_chunk, stage_rows, lt_max, nchunk, stream, accum); break;
+        case 3: combine_one<3>(d, out, pass, t_chunk, stage_rows, lt_max, nchunk, stream, accum); break;
+        case 4: combine_one<4>(d, out, pass, t_chunk, stage_rows, lt_max, nchunk, stream, accum); break;
+        case 5: combine_one<5>(d, out, pass, t_chunk, stage_rows, lt_max, nchunk, stream, accum); break;
+        case 6: combine_one<6>(d, out, pass, t_chunk, stage_rows, lt_max, nchunk, stream, accum); break;
+        case 7: combine_one<7>(d, out, pass, t_chunk, stage_rows, lt_max, nchunk, stream, accum); break;
+        default: combine_one<8>(d, out, pass, t_chunk, stage_rows, lt_max, nchunk, stream, accum); break;
         }
         if (launches)
             ++*launches;

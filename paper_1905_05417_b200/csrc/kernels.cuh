@@ -62,6 +62,7 @@ struct DevTables {
     // every term table has major symmetry C[(3j+l)9 + 3a+b] = C[(3l+j)9 + 3b+a]:
     // the standard kernel (K6) then computes pairs al <= be and mirrors them
     int sym;
+    int contig; // k_combine entry mapping: warp-contiguous slots (LAMFAST_CONTIG)
     long long S_s, S_u;
     // geometry
     int affine;
