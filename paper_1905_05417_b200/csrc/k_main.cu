@@ -1523,10 +1523,11 @@ template <int NT>
 void combine_one(const DevTables& d, double* out, int pass, int t_chunk, int stage_rows, int lt_max,
                  unsigned nchunk, cudaStream_t s, bool accum) {
     constexpr int EPT = entries_per_thread<NT>();
-    // two entries per thread with 4 terms need ~155 registers: 128-thread
+    // P of >= 8 (entry, term) pairs per thread needs ~155+ registers: 128-thread
     // blocks, 3 per SM; everything else 256-thread blocks, <= 128 registers
-    constexpr int BT = (NT == 4 && EPT == 2) ? 128 : kBlock;
-    constexpr int MINB = (NT == 4 && EPT == 2) ? 3 : 2;
+    constexpr bool wide = EPT >= 2 && EPT * NT >= 8;
+    constexpr int BT = wide ? 128 : kBlock;
+    constexpr int MINB = wide ? 3 : 2;
     const size_t smem = ((stage_rows * (sizeof(RowInfo) + 2 * NT) + 31) & ~size_t(31)) +
                         (size_t)stage_rows * lt_max * NT * sizeof(double4);
     const dim3 grid((unsigned)((d.E + (long long)BT * EPT - 1) / ((long long)BT * EPT)), nchunk);
