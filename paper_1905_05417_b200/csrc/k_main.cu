@@ -193,6 +193,55 @@ __device__ __forceinline__ void combine_row(const double (&P)[EPT][NT][4], const
             }
 }
 
+/// k-outer form of combine_row: one neighbour at a time, all its terms, then
+/// the store -- EPT live accumulators instead of EPT * LT (register relief for
+/// the wide variants).
+template <int NT, int EPT, int LT, bool ACCUM>
+__device__ __forceinline__ void combine_row_k(const double (&P)[EPT][NT][4], const double4* __restrict__ w,
+                                              unsigned mask, const unsigned char* __restrict__ kr,
+                                              double* const (&o)[EPT], const int (&B)[EPT], const bool (&live)[EPT]) {
+    int klo[NT], khi[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        klo[t] = (mask & (1u << t)) ? kr[2 * t] : LT;
+        khi[t] = kr[2 * t + 1];
+    }
+#pragma unroll
+    for (int k = 0; k < LT; ++k) {
+        double acc[EPT];
+#pragma unroll
+        for (int x = 0; x < EPT; ++x)
+            acc[x] = (ACCUM && live[x]) ? o[x][(long long)k * B[x]] : 0.0;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            if (k >= klo[t] && k < khi[t]) {
+                const double4 ww = w[k * NT + t];
+#pragma unroll
+                for (int x = 0; x < EPT; ++x) {
+                    acc[x] = fma(P[x][t][0], ww.x, acc[x]);
+                    acc[x] = fma(P[x][t][1], ww.y, acc[x]);
+                    acc[x] = fma(P[x][t][2], ww.z, acc[x]);
+                    acc[x] = fma(P[x][t][3], ww.w, acc[x]);
+                }
+            }
+        }
+#pragma unroll
+        for (int x = 0; x < EPT; ++x)
+            if (live[x])
+                store_value(o[x] + (long long)k * B[x], acc[x]);
+    }
+}
+
+template <int NT, int EPT, int LT, bool ACCUM>
+__device__ __forceinline__ void row_dispatch(const double (&P)[EPT][NT][4], const double4* __restrict__ w,
+                                             unsigned mask, const unsigned char* __restrict__ kr,
+                                             double* const (&o)[EPT], const int (&B)[EPT], const bool (&live)[EPT]) {
+    if constexpr (EPT >= 2)
+        combine_row_k<NT, EPT, LT, ACCUM>(P, w, mask, kr, o, B, live);
+    else
+        combine_row<NT, EPT, LT, ACCUM>(P, w, mask, kr, o, B, live);
+}
+
 template <int NT, int EPT, bool ACCUM, bool SMEM = false>
 __device__ __forceinline__ void combine_row_dyn(const double (&P)[EPT][NT][4], const double4* __restrict__ w,
                                                 int lt, unsigned mask, double* const (&o)[EPT], const int (&B)[EPT],
@@ -358,13 +407,16 @@ __device__ __forceinline__ void combine_body(const DevTables& d, double* __restr
                 o[x] = o_thread[x] + ri.base + (long long)ri.lt * A[x];
             const double4* w = s_w + rr * lt_max * NT;
             const unsigned char* kr = s_kr + rr * NT * 2;
+            // EPT >= 2: k-outer rows (EPT live accumulators; C4 2.66 -> 2.53 ms,
+            // C3 1.39 -> 1.33 ms with two entries per thread); EPT = 1: the
+            // LT-unrolled form keeps more independent FMA chains in flight
             switch (ri.lt) {
-            case 1: combine_row<NT, EPT, 1, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
-            case 2: combine_row<NT, EPT, 2, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
-            case 3: combine_row<NT, EPT, 3, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
-            case 4: combine_row<NT, EPT, 4, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
-            case 5: combine_row<NT, EPT, 5, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
-            case 7: combine_row<NT, EPT, 7, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
+            case 1: row_dispatch<NT, EPT, 1, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
+            case 2: row_dispatch<NT, EPT, 2, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
+            case 3: row_dispatch<NT, EPT, 3, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
+            case 4: row_dispatch<NT, EPT, 4, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
+            case 5: row_dispatch<NT, EPT, 5, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
+            case 7: row_dispatch<NT, EPT, 7, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
             default: combine_row_dyn<NT, EPT, ACCUM>(P, w, ri.lt, ri.mask, o, B, live); break;
             }
         }
@@ -373,9 +425,9 @@ __device__ __forceinline__ void combine_body(const DevTables& d, double* __restr
 
 
 
-// k_combine: 256-thread blocks and the compiler's own register choice (<= 128
-// here); k_combine_b: explicit bounds for the wide variant (4 terms, two
-// entries per thread: ~155 registers, 128-thread blocks, 3 per SM).
+// k_combine: 256-thread blocks and the compiler's own register choice (one
+// entry per thread, 80-128 registers); k_combine_b: explicit bounds (two
+// entries per thread, <= 128 registers so that 2 blocks of 256 fit per SM).
 template <int NT, int EPT, bool AFFINE, bool ACCUM>
 __global__ void __launch_bounds__(kBlock) k_combine(const DevTables d, double* __restrict__ out, int pass,
                                                     int t_chunk, int stage_rows, int lt_max) {
@@ -1372,16 +1424,8 @@ int reduce_launch(int blocks, double* partial, double* out, cudaStream_t stream)
     return (int)cudaGetLastError();
 }
 
-#ifndef LF_COMBINE_EPT
-#define LF_COMBINE_EPT 2 // two entries per thread for <= 3 terms (C4: 3.04 -> 2.82 ms); 4 terms spill
-#endif
-
-#ifndef LF_COMBINE_EPT4
-#define LF_COMBINE_EPT4 1
-#endif
-
 template <int NT>
-constexpr int entries_per_thread() { return NT <= 3 ? LF_COMBINE_EPT : NT == 4 ? LF_COMBINE_EPT4 : 1; }
+constexpr int entries_per_thread() { return NT <= 4 ? 2 : 1; } // two entries: 64 P registers at 4 terms
 
 /// TMA-bulk variant for a first pass; false when it does not apply (group
 /// wider than a block, or staging buffers too large for two blocks per SM).
@@ -1523,11 +1567,11 @@ template <int NT>
 void combine_one(const DevTables& d, double* out, int pass, int t_chunk, int stage_rows, int lt_max,
                  unsigned nchunk, cudaStream_t s, bool accum) {
     constexpr int EPT = entries_per_thread<NT>();
-    // P of >= 8 (entry, term) pairs per thread needs ~155+ registers: 128-thread
-    // blocks, 3 per SM; everything else 256-thread blocks, <= 128 registers
-    constexpr bool wide = EPT >= 2 && EPT * NT >= 8;
-    constexpr int BT = wide ? 128 : kBlock;
-    constexpr int MINB = wide ? 3 : 2;
+    // two entries per thread: explicit bounds (<= 128 registers, 2 blocks of
+    // 256 per SM); one entry: the compiler's own choice (80-128 registers)
+    constexpr int BT = kBlock;
+    constexpr int MINB = 2;
+    constexpr bool bounded = EPT >= 2;
     const size_t smem = ((stage_rows * (sizeof(RowInfo) + 2 * NT) + 31) & ~size_t(31)) +
                         (size_t)stage_rows * lt_max * NT * sizeof(double4);
     const dim3 grid((unsigned)((d.E + (long long)BT * EPT - 1) / ((long long)BT * EPT)), nchunk);
@@ -1536,7 +1580,7 @@ void combine_one(const DevTables& d, double* out, int pass, int t_chunk, int sta
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<grid, BT, smem, s>>>(d, out, pass, t_chunk, stage_rows, lt_max);
     };
-    if constexpr (BT == kBlock) {
+    if constexpr (!bounded) {
         if (d.affine)
             accum ? launch(k_combine<NT, EPT, true, true>) : launch(k_combine<NT, EPT, true, false>);
         else
