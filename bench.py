@@ -8,8 +8,11 @@ thickness integrals, in-plane operators, combination into the FP64 CSR
 values) of the workload, inputs resident in HBM.  Workload at N=1: BASELINE
 config C4 (128x64 elements, p=2, 128 plies, 1.92e9 nnz, 23 GB CSR) -- the
 largest BASELINE config that fits one B200 (C5 is 203 GB).  With N ranks
-(torchrun) the matrix is split into N row slabs balanced by nnz, one per GPU,
-no collective on the data path ("strong" scaling).
+(torchrun) the path partitions into row slabs, one per GPU, no
+collective on the data path.  Default --scaling weak: the laminate of the
+config family grows with N (N x 128 plies for C4) and each rank assembles one
+nnz-balanced slab of it, i.e. one C4's worth of rows per GPU; --scaling strong
+splits the fixed config across the N GPUs instead.
 
 Reported beside the device number:
   e2e           the same metric through the C-ABI one-shot call lf_assemble
@@ -50,6 +53,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-plies", type=int, default=0)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: N x the config's plies, one slab per GPU; strong: the config split N ways")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the multi-rank path on fewer GPUs than ranks")
     return ap.parse_args()
@@ -143,7 +148,7 @@ def reference_arm(args, rank, world):
     line = {
         "impl": "reference", "metric": "assembled stiffness nnz/s (FP64 CSR)", "value": value,
         "unit": "nnz/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "backend": "fast", "sample_plies": plies,
                    "nnz_per_step": nnz},
@@ -218,7 +223,9 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", device))
         else:
             dist.init_process_group(args.dist_backend)
-    prob = P.baseline_config(args.config)
+    base_plies = len(P.baseline_config(args.config).layers)
+    plies = base_plies * world if args.scaling == "weak" else base_plies
+    prob = P.baseline_config(args.config, plies=plies)
     sz = P.sizes(prob)
     bounds = lf.slab_bounds(prob, world, rank) if world > 1 else {"t_begin": 0, "t_end": prob.n_t}
     stream = torch.cuda.Stream()
@@ -356,9 +363,11 @@ def main():
         line = {
             "metric": "assembled stiffness nnz/s (FP64 CSR)", "value": value, "unit": "nnz/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config, "backend": "fast", "nnz": total_nnz,
+            "config": {"workload": args.config if world == 1 or args.scaling == "strong"
+                       else f"{args.config} family, {plies} plies ({world} x {base_plies}), one slab per GPU",
+                       "backend": "fast", "nnz": total_nnz,
                        "dofs": sz["dim"], "plies": len(prob.layers),
                        "distinct_materials": prob.distinct_configs(),
                        "l2": "output > L2 (values %.1f GB vs 126 MB L2); no flush needed"
