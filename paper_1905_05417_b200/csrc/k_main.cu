@@ -1290,34 +1290,51 @@ __global__ void k_pattern_rows(const DevTables d, long long* __restrict__ row_pt
     row_ptr[r] = 9 * d.S_s * (d.pre_t[it] - d.pre_t[d.t0]) + (long long)Lt * (d.es_pre[is] + (long long)a * B);
 }
 
+constexpr int kColsEpt = 4; // entries per thread of k_pattern_cols
+
+/// Columns of the slab's CSR.  Thread slots are warp-contiguous (a warp owns
+/// 32 * kColsEpt consecutive entries, so its kColsEpt stores per (row, k) are
+/// adjacent 128-byte runs) and the stores stream (st.global.cs).
 __global__ void __launch_bounds__(kBlock) k_pattern_cols(const DevTables d, int* __restrict__ cols,
                                                          int t_chunk) {
-    const long long e = (long long)blockIdx.x * kBlock + threadIdx.x;
-    if (e >= d.E)
-        return;
-    int is = d.blk_is[blockIdx.x];
-    while (d.es_pre[is + 1] <= e)
-        ++is;
-    const long long ebase = d.es_pre[is];
-    const int r = (int)(e - ebase);
-    const int iu = is % d.nu, iv = is / d.nu;
-    const int Lu = d.len_u[iu], Lv = d.len_v[iv];
-    const int B = 3 * Lu * Lv;
-    const int a = r / B, rem = r - a * B;
-    const int s = rem / 3, b = rem % 3;
-    const int jv = d.lo_v[iv] + s / Lu, ju = d.lo_u[iu] + s % Lu;
-    const int col_s = 3 * (jv * d.nu + ju) + b;
-    const long long A = ebase + (long long)a * B;
+    int* o0[kColsEpt];
+    int B[kColsEpt], col_s[kColsEpt];
+    long long A[kColsEpt];
+    bool live[kColsEpt];
+#pragma unroll
+    for (int x = 0; x < kColsEpt; ++x) {
+        const long long e = (long long)blockIdx.x * kBlock * kColsEpt + (threadIdx.x >> 5) * 32 * kColsEpt +
+                            x * 32 + (threadIdx.x & 31);
+        live[x] = e < d.E;
+        const long long ec = live[x] ? e : d.E - 1;
+        int is = __ldg(d.blk_is + ec / kBlock);
+        while (__ldg(d.es_pre + is + 1) <= ec)
+            ++is;
+        const long long ebase = __ldg(d.es_pre + is);
+        const int r = (int)(ec - ebase);
+        const int iu = is % d.nu, iv = is / d.nu;
+        const int Lu = __ldg(d.len_u + iu), Lv = __ldg(d.len_v + iv);
+        B[x] = 3 * Lu * Lv;
+        const int a = r / B[x], rem = r - a * B[x];
+        const int s = rem / 3, b = rem % 3;
+        const int jv = __ldg(d.lo_v + iv) + s / Lu, ju = __ldg(d.lo_u + iu) + s % Lu;
+        col_s[x] = 3 * (jv * d.nu + ju) + b;
+        A[x] = ebase + (long long)a * B[x];
+        o0[x] = cols + rem;
+    }
     const int it_begin = d.t0 + blockIdx.y * t_chunk;
     const int it_end = min(d.t1, it_begin + t_chunk);
-    const long long pre0 = d.pre_t[d.t0];
+    const long long pre0 = __ldg(d.pre_t + d.t0);
     for (int it = it_begin; it < it_end; ++it) {
-        const int Lt = d.len_t[it];
-        const long long pfx = d.pre_t[it] - pre0;
-        int* o = cols + 9 * d.S_s * pfx + (long long)Lt * A + rem;
-        const int jt0 = d.lo_t[it];
-        for (int k = 0; k < Lt; ++k)
-            o[(long long)k * B] = 3 * d.ns * (jt0 + k) + col_s;
+        const int Lt = __ldg(d.len_t + it);
+        const long long base = 9 * d.S_s * (__ldg(d.pre_t + it) - pre0);
+        const int c0 = 3 * d.ns * __ldg(d.lo_t + it);
+        for (int k = 0; k < Lt; ++k) {
+#pragma unroll
+            for (int x = 0; x < kColsEpt; ++x)
+                if (live[x])
+                    __stcs(o0[x] + base + (long long)Lt * A[x] + (long long)k * B[x], c0 + 3 * d.ns * k + col_s[x]);
+        }
     }
 }
 
@@ -1694,9 +1711,9 @@ int launch_pattern(const DevTables& d, long long* row_ptr, int* cols, cudaStream
     const long long rows = 3LL * d.ns * (d.t1 - d.t0);
     k_pattern_rows<<<(unsigned)((rows + 1 + 255) / 256), 256, 0, stream>>>(d, row_ptr, rows);
     if (d.E > 0 && d.t1 > d.t0) {
-        const long long nblk = (d.E + kBlock - 1) / kBlock;
+        const long long nblk = (d.E + (long long)kBlock * kColsEpt - 1) / ((long long)kBlock * kColsEpt);
         const int nt = d.t1 - d.t0;
-        long long nchunks = std::max(1LL, std::min<long long>((148LL * 64 + nblk - 1) / nblk, nt));
+        long long nchunks = std::max(1LL, std::min<long long>((148LL * 16 + nblk - 1) / nblk, nt));
         const int t_chunk = (int)((nt + nchunks - 1) / nchunks);
         const dim3 grid((unsigned)nblk, (unsigned)((nt + t_chunk - 1) / t_chunk));
         k_pattern_cols<<<grid, kBlock, 0, stream>>>(d, cols, t_chunk);
