@@ -375,6 +375,7 @@ def test_c5_slab_fast_equals_standard_on_device(gpu):
 @pytest.mark.parametrize("env", [
     {"LAMFAST_TEAM": "auto"}, {"LAMFAST_TEAM": "1,3"}, {"LAMFAST_TEAM": "4,2"},
     {"LAMFAST_TEAM": "3,1", "LAMFAST_TEAM_KR": "1"}, {"LAMFAST_WS": "1"},
+    {"LAMFAST_CONTIG": "0"}, {"LAMFAST_TCHUNK": "7"},
 ])
 def test_opt_in_store_variants_match_oracle(gpu, oracle, monkeypatch, env):
     """The opt-in combine variants (team/bulk-copy stores, warp-specialised
@@ -409,3 +410,29 @@ def test_opt_in_store_variants_match_oracle(gpu, oracle, monkeypatch, env):
         assert_csr_match((rp.cpu().numpy(), cols.cpu().numpy()[:plan.nnz],
                           raw.cpu().numpy()[1:plan.nnz + 1]), want, RTOL)
         plan.close()
+
+
+@pytest.mark.parametrize("sym", ["1", "0"])
+def test_standard_symmetric_halving_matches_oracle(gpu, oracle, monkeypatch, sym):
+    """K6 computes local pairs al <= be and mirrors them when every term table
+    has major symmetry; LAMFAST_NO_SYM=1 forces all pairs.  Both match the
+    oracle, including a slab plan whose cut separates mirrored rows."""
+    import torch
+    if sym == "0":
+        monkeypatch.setenv("LAMFAST_NO_SYM", "1")
+    prob = P.cube_problem(2, 2, 2, [0.0, 0.9, 0.3], geometry="skewed")
+    got = gpu.assemble_standard(prob)
+    assert_csr_match(got.astuple(), oracle.assemble(prob, "standard"), RTOL)
+    prob = P.baseline_config("C1")
+    b = gpu.slab_bounds(prob, 2, 1)
+    plan = gpu.Plan(prob, "standard", 0, b["t_begin"], b["t_end"])
+    rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
+    cols = torch.empty(max(1, plan.nnz), dtype=torch.int32, device="cuda")
+    vals = torch.empty(max(1, plan.nnz), dtype=torch.float64, device="cuda")
+    plan.build_pattern(rp.data_ptr(), cols.data_ptr())
+    plan.assemble(vals.data_ptr())
+    plan.synchronize()
+    want = oracle.assemble(prob, "standard", b["t_begin"], b["t_end"])
+    assert_csr_match((rp.cpu().numpy(), cols.cpu().numpy()[:plan.nnz], vals.cpu().numpy()[:plan.nnz]),
+                     want, RTOL)
+    plan.close()
