@@ -405,10 +405,21 @@ def measure_e2e(args, prob, device, total_nnz):
     sec = (time.perf_counter() - t0) / n
     h2d = sum(a.nbytes for a in prob._keep if hasattr(a, "nbytes"))
     d2h = rp.numel() * 8 + total_nnz * 12
-    del rp, cols, vals
+    # the e2e roofline: plain pinned D2H bandwidth of this box, measured after
+    # the timed region into the same pinned buffer (4 GB, best of 3)
+    probe = torch.empty(min(total_nnz, 1 << 29), dtype=torch.float64, device=f"cuda:{device}")
+    best = 0.0
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        vals[:probe.numel()].copy_(probe)
+        torch.cuda.synchronize()
+        best = max(best, probe.numel() * 8 / (time.perf_counter() - t1) / 1e9)
+    del rp, cols, vals, probe
     return {"value": total_nnz / sec, "unit": "nnz/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": sec * 1e3, "steps": n,
-            "call": "lf_assemble(LF_BACKEND_FAST) -> host CSR (row_ptr, cols, values)"}
+            "call": "lf_assemble(LF_BACKEND_FAST) -> host CSR (row_ptr, cols, values)",
+            "d2h_gbs_measured": best, "pcie_frac": (d2h / sec / 1e9) / best if best else None}
 
 
 def measure_e2e_slab(args, prob, device, rank, world, bounds, total_nnz):
