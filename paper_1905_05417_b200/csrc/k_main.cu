@@ -1085,33 +1085,47 @@ __global__ void k_inplane_general(const DevTables d, int cu, int cv) {
         __syncthreads();
         pullback_tables(d, e_index, el.nq2, w2, d.term_table + (long long)t * 81, ctq);
         __syncthreads();
-        // all nl2^2 local pairs (halving them by symmetry was measured slower: this
-        // kernel is bound by the coloured read-modify-write of Pg, not by FP64)
-        for (int pr = threadIdx.x; pr < el.nl2 * el.nl2; pr += blockDim.x) {
+        // one thread per (local pair, family f): 9 accumulators and a 9-value
+        // read-modify-write each, so many more warps hide the latency of the
+        // coloured accumulation into Pg (the bound of this kernel).  Threads of
+        // a warp share f (warp-aligned quarters), so the C~ loads broadcast.
+        const int npair = el.nl2 * el.nl2;
+        const int qstride = (npair + 31) & ~31;
+        for (int idx = threadIdx.x; idx < 4 * qstride; idx += blockDim.x) {
+            const int f = idx / qstride;
+            const int pr = idx - f * qstride;
+            if (pr >= npair)
+                continue;
             const int al = pr / el.nl2, be = pr % el.nl2;
-            double acc[4][9];
+            // P11 <- C~00,01,10,11; P12 <- 02,12; P21 <- 20,21; P22 <- 22 (layout [q][xy][10])
+            const int nxy = f == 0 ? 4 : f == 3 ? 1 : 2;
+            int xys[4];
+            xys[0] = f == 0 ? 0 : f == 1 ? 2 : f == 2 ? 6 : 8;
+            xys[1] = f == 0 ? 1 : f == 1 ? 5 : 7;
+            xys[2] = 3;
+            xys[3] = 4;
+            double acc[9];
 #pragma unroll
-            for (int f = 0; f < 4; ++f)
-#pragma unroll
-                for (int k = 0; k < 9; ++k)
-                    acc[f][k] = 0.0;
+            for (int k = 0; k < 9; ++k)
+                acc[k] = 0.0;
             for (int q = 0; q < el.nq2; ++q) {
                 const double* ga = gh + (q * el.nl2 + al) * 3;
                 const double* gb = gh + (q * el.nl2 + be) * 3;
-                double s[9];
-#pragma unroll
-                for (int x = 0; x < 3; ++x)
-#pragma unroll
-                    for (int y = 0; y < 3; ++y)
-                        s[3 * x + y] = ga[x] * gb[y];
-                // P11 <- C~00,01,10,11; P12 <- 02,12; P21 <- 20,21; P22 <- 22 (layout [q][xy][10])
                 const double* C = ctq + q * 90;
 #pragma unroll
-                for (int k = 0; k < 9; ++k) {
-                    acc[0][k] += C[0 * 10 + k] * s[0] + C[1 * 10 + k] * s[1] + C[3 * 10 + k] * s[3] + C[4 * 10 + k] * s[4];
-                    acc[1][k] += C[2 * 10 + k] * s[2] + C[5 * 10 + k] * s[5];
-                    acc[2][k] += C[6 * 10 + k] * s[6] + C[7 * 10 + k] * s[7];
-                    acc[3][k] += C[8 * 10 + k] * s[8];
+                for (int u = 0; u < 4; ++u) {
+                    if (u < nxy) {
+                        const int xy = xys[u];
+                        const double sxy = ga[xy / 3] * gb[xy % 3];
+                        const double2* C2 = reinterpret_cast<const double2*>(C + xy * 10);
+#pragma unroll
+                        for (int h = 0; h < 5; ++h) {
+                            const double2 c = C2[h];
+                            acc[2 * h] += c.x * sxy;
+                            if (2 * h + 1 < 9)
+                                acc[2 * h + 1] += c.y * sxy;
+                        }
+                    }
                 }
             }
             const int iu = el.fu + al % (d.pu + 1), iv = el.fv + al / (d.pu + 1);
@@ -1121,14 +1135,12 @@ __global__ void k_inplane_general(const DevTables d, int cu, int cv) {
             const int slot = (jv - d.lo_v[iv]) * Lu + (ju - d.lo_u[iu]);
             const long long base = d.es_pre[is] + 3 * slot;
             const int B = 3 * Lu * Lv;
-            for (int f = 0; f < 4; ++f) {
-                double* dst = d.Pg + ((long long)t * 4 + f) * d.E + base;
+            double* dst = d.Pg + ((long long)t * 4 + f) * d.E + base;
 #pragma unroll
-                for (int a = 0; a < 3; ++a)
+            for (int a = 0; a < 3; ++a)
 #pragma unroll
-                    for (int b = 0; b < 3; ++b)
-                        dst[(long long)a * B + b] += acc[f][3 * a + b];
-            }
+                for (int b = 0; b < 3; ++b)
+                    dst[(long long)a * B + b] += acc[3 * a + b];
         }
     }
 }
@@ -1633,7 +1645,7 @@ int launch_inplane_general(const DevTables& d, cudaStream_t stream) {
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_inplane_general, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const dim3 grid((d.nspu + d.pu) / (d.pu + 1), (d.nspv + d.pv) / (d.pv + 1), d.n_terms);
-    const int threads = std::min(256, (nl2 * nl2 + 31) / 32 * 32); // one thread per local pair
+    const int threads = std::min(512, 4 * ((nl2 * nl2 + 31) / 32 * 32)); // one thread per (local pair, family)
     for (int cv = 0; cv <= d.pv; ++cv)
         for (int cu = 0; cu <= d.pu; ++cu)
             k_inplane_general<<<grid, threads, smem, stream>>>(d, cu, cv);
