@@ -389,6 +389,7 @@ void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void
     d.t0 = s.t0;
     d.t1 = s.t1;
     d.n_pairs = s.n_pairs;
+    d.nnz_slab = s.nnz;
     if (backend != LF_BACKEND_STANDARD) {
         upload_teams(s, ar, d);
         d.W = ar.alloc<double>(static_cast<std::size_t>(std::max<long long>(1, d.n_pairs)) * d.n_terms * 4);
@@ -721,7 +722,7 @@ static int inplane_common(const lf_problem* p, const double table[81], int devic
         CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         {
             DeviceArena ar;
-            lfb::DevTables d;
+            lfb::DevTables d{};
             upload_space(s, ar, d);
             upload_geometry(s, ar, d);
             std::vector<double> tab(table, table + 81), lam(1, 1.0);
@@ -797,7 +798,7 @@ int lf_thickness_operators(int32_t degree_t, int32_t n_knots_t, const double* kn
         CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         {
             DeviceArena ar;
-            lfb::DevTables d;
+            lfb::DevTables d{};
             std::memset(&d, 0, sizeof d);
             d.pt = s.kt.p;
             d.nt = s.n_t;
@@ -899,7 +900,7 @@ int lf_combine(const lf_problem* p, int32_t n_terms, const double* blocks, const
         CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         {
             DeviceArena ar;
-            lfb::DevTables d;
+            lfb::DevTables d{};
             upload_space(s, ar, d);
             d.lo_t = ar.upload(at.lo);
             d.len_t = ar.upload(at.len);
@@ -914,6 +915,8 @@ int lf_combine(const lf_problem* p, int32_t n_terms, const double* blocks, const
             d.t0 = 0;
             d.t1 = nt;
             d.n_pairs = at.total;
+            d.nnz_slab = nnz;
+            d.contig = 1;
             // P: banded -> entry layout
             const std::size_t per = static_cast<std::size_t>(s.n_s) * bv * bu;
             std::vector<double> pg(static_cast<std::size_t>(n_terms) * 4 * d.E);

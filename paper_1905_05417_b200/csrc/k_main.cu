@@ -405,6 +405,9 @@ __device__ __forceinline__ void combine_body(const DevTables& d, double* __restr
 #pragma unroll
             for (int x = 0; x < EPT; ++x)
                 o[x] = o_thread[x] + ri.base + (long long)ri.lt * A[x];
+#pragma unroll
+            for (int x = 0; x < EPT; ++x)
+                LF_CHECK(!live[x] || (o[x] >= out && o[x] + (long long)(ri.lt - 1) * B[x] < out + d.nnz_slab));
             const double4* w = s_w + rr * lt_max * NT;
             const unsigned char* kr = s_kr + rr * NT * 2;
             // EPT >= 2: k-outer rows (EPT live accumulators; C4 2.66 -> 2.53 ms,
@@ -1136,6 +1139,7 @@ __global__ void k_inplane_general(const DevTables d, int cu, int cv) {
             const long long base = d.es_pre[is] + 3 * slot;
             const int B = 3 * Lu * Lv;
             double* dst = d.Pg + ((long long)t * 4 + f) * d.E + base;
+            LF_CHECK(base >= 0 && base + 2LL * B + 2 < d.E && t < d.n_terms);
 #pragma unroll
             for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -1272,6 +1276,8 @@ __global__ void k_standard(const DevTables d, double* __restrict__ values, int c
                 const int Lt = d.len_t[rt];
                 const long long pos = 9 * d.S_s * (d.pre_t[rt] - pre0) + (long long)Lt * d.es_pre[is] +
                                       (long long)(ct_ - d.lo_t[rt]) * B + 3 * slot;
+                LF_CHECK(pos >= 0 && pos + 2LL * Lt * B + 2 < d.nnz_slab && ct_ >= d.lo_t[rt] &&
+                         ct_ < d.lo_t[rt] + Lt);
 #pragma unroll
                 for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -1341,6 +1347,11 @@ __global__ void __launch_bounds__(kBlock) k_pattern_cols(const DevTables d, int*
         const int Lt = __ldg(d.len_t + it);
         const long long base = 9 * d.S_s * (__ldg(d.pre_t + it) - pre0);
         const int c0 = 3 * d.ns * __ldg(d.lo_t + it);
+#pragma unroll
+        for (int x = 0; x < kColsEpt; ++x)
+            LF_CHECK(!live[x] || (base + (long long)Lt * A[x] + (o0[x] - cols) >= 0 &&
+                                  base + (long long)Lt * A[x] + (long long)(Lt - 1) * B[x] + (o0[x] - cols) <
+                                      d.nnz_slab));
         for (int k = 0; k < Lt; ++k) {
 #pragma unroll
             for (int x = 0; x < kColsEpt; ++x)

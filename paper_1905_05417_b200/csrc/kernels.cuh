@@ -13,8 +13,29 @@
 #pragma once
 
 #include <cstdint>
+#ifdef LF_DEBUG_CHECKS
+#include <cstdio>
+#endif
 
 namespace lfb {
+
+// Device-side bounds checks (debug builds: make EXTRA=-DLF_DEBUG_CHECKS).  The
+// pool's compute-sanitizer is unavailable, so every index a kernel writes
+// through is checked against its buffer and a violation traps the kernel.
+#ifdef LF_DEBUG_CHECKS
+#define LF_CHECK(cond)                                                                                         \
+    do {                                                                                                       \
+        if (!(cond)) {                                                                                         \
+            printf("LF_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, blockIdx.x, \
+                   threadIdx.x);                                                                               \
+            __trap();                                                                                          \
+        }                                                                                                      \
+    } while (0)
+#else
+#define LF_CHECK(cond) \
+    do {               \
+    } while (0)
+#endif
 
 struct DevTables {
     // degrees / sizes
@@ -81,6 +102,7 @@ struct DevTables {
     // slab
     int t0, t1;
     long long n_pairs, E;
+    long long nnz_slab; // values of this plan's slab (bounds checks in LF_DEBUG_CHECKS builds)
 };
 
 // Launchers (all asynchronous on `stream`).  Return cudaError_t as int.

@@ -1,0 +1,51 @@
+"""Small cases for compute-sanitizer (memcheck / racecheck / synccheck /
+initcheck) over every device kernel family: fast (affine, general), standard,
+Voigt-free, decompose_angles, multi-pass, slabs, operators, verification, and
+the opt-in store variants.  Usage:
+  compute-sanitizer --tool racecheck python tools/sanitize_cases.py"""
+import os
+import sys
+import numpy as np
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1905_05417_b200 as lf
+from paper_1905_05417_b200 import problem as P
+
+c1 = P.baseline_config("C1")
+skew = P.cube_problem(2, 2, 2, [0.0, 0.9, 0.3], geometry="skewed")
+mixed = P.LaminateProblem(
+    degree_u=2, degree_v=3, degree_t=2, knots_u=P.uniform_knots(2, 3), knots_v=P.uniform_knots(3, 2),
+    knots_t=P.c0_knots(2, 3), interfaces=P.equal_interfaces(3),
+    layers=[(P.baseline_orthotropic(), 0.0), (P.isotropic(0.5, 0.3), 0.0), (P.baseline_orthotropic(), 0.6)])
+many = P.cube_problem(1, 2, 1, [0.1 * k for k in range(10)])  # 10 terms -> 2 passes
+out = []
+for prob in (c1, skew, mixed):
+    for backend in ("fast", "standard", "voigt_free"):
+        out.append(lf.assemble_with(backend, prob).values.sum())
+out.append(lf.assemble_fast(c1.replace(decompose_angles=True)).values.sum())
+out.append(lf.assemble_fast(many).values.sum())
+for k, v in (("LAMFAST_WS", "1"), ("LAMFAST_TEAM", "auto"), ("LAMFAST_CONTIG", "0")):
+    os.environ[k] = v
+    out.append(lf.assemble_fast(c1).values.sum())
+    del os.environ[k]
+# operator-level entry points (affine + general P, thickness Q, long-form combine)
+d = np.diag([1, 1, 1, 0.5, 0.5, 0.5]).astype(float)
+for prob in (c1, skew):
+    blocks, flags, _ = lf.compute_inplane_operators(prob, d)
+    out.append(blocks.sum())
+q, occ = lf.compute_thickness_operators(2, skew.knots_t, skew.interfaces, 3)
+blocks, flags, _ = lf.compute_inplane_operators(skew, d)
+out.append(lf.combine_operators(skew, np.stack([blocks] * len(skew.layers)), flags, q, occ).values.sum())
+# slab plan + device verification kernels
+import torch
+b = lf.slab_bounds(c1, 2, 1)
+plan = lf.Plan(c1, "fast", 0, b["t_begin"], b["t_end"])
+rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
+cols = torch.empty(plan.nnz, dtype=torch.int32, device="cuda")
+vals = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
+plan.build_pattern(rp.data_ptr(), cols.data_ptr())
+plan.assemble(vals.data_ptr())
+plan.synchronize()
+st = lf.device_csr_stats(plan.rows, rp.data_ptr(), cols.data_ptr(), vals.data_ptr())
+out.append(st["fro_sq"])
+plan.close()
+print("ok", len(out), float(np.sum(out)))
