@@ -1153,12 +1153,16 @@ __global__ void k_inplane_general(const DevTables d, int cu, int cv) {
 // K6: standard full-3D quadrature (assembly.cpp:134-245), one block per
 // (element, thickness span) of one colour, accumulated straight into the
 // precomputed CSR (the duplicate summation of sparse.cpp:30-55).
-__global__ void k_standard(const DevTables d, double* __restrict__ values, int cu, int cv, int ct) {
+__global__ void k_standard(const DevTables d, double* __restrict__ values, int cu, int cv, int ct, int nchunk) {
     extern __shared__ double sm[];
     ElemInfo el;
     el.eu = cu + blockIdx.x * (d.pu + 1);
     el.ev = cv + blockIdx.y * (d.pv + 1);
-    const int ks = ct + blockIdx.z * (d.pt + 1);
+    // blockIdx.z = (span of this thickness colour, chunk of the local pairs):
+    // few elements per colour (small plates, many plies per span) still fill
+    // the GPU; chunks own disjoint pairs, so their writes never overlap
+    const int chunk = blockIdx.z % nchunk;
+    const int ks = ct + (blockIdx.z / nchunk) * (d.pt + 1);
     if (el.eu >= d.nspu || el.ev >= d.nspv || ks >= d.nspt)
         return;
     const int c0 = d.span_cell0[ks], c1 = d.span_cell0[ks + 1];
@@ -1201,7 +1205,9 @@ __global__ void k_standard(const DevTables d, double* __restrict__ values, int c
             w3[q] = d.cell_wts[(long long)c * d.nqt + q];
         __syncthreads();
         const int npair = d.sym ? nl3 * (nl3 + 1) / 2 : nl3 * nl3;
-        for (int pr = threadIdx.x; pr < npair; pr += blockDim.x) {
+        const int per = (npair + nchunk - 1) / nchunk;
+        const int p_end = min(npair, (chunk + 1) * per);
+        for (int pr = chunk * per + threadIdx.x; pr < p_end; pr += blockDim.x) {
             int al, be;
             if (d.sym) { // triangular index: be >= al
                 al = 0;
@@ -1756,11 +1762,19 @@ int launch_standard(const DevTables& d, double* values, long long nnz, cudaStrea
                                           2 * (size_t)d.nqt * ntl + d.nqt);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_standard, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const dim3 grid((d.nspu + d.pu) / (d.pu + 1), (d.nspv + d.pv) / (d.pv + 1), (d.nspt + d.pt) / (d.pt + 1));
+    const int gx = (d.nspu + d.pu) / (d.pu + 1), gy = (d.nspv + d.pv) / (d.pv + 1), gz = (d.nspt + d.pt) / (d.pt + 1);
+    // split the local pairs of each (element, span) over enough blocks for
+    // ~4 blocks per SM per colour launch (chunks of >= 256 pairs)
+    const int nl3 = nl2 * ntl;
+    const int npair = d.sym ? nl3 * (nl3 + 1) / 2 : nl3 * nl3;
+    const long long blocks = (long long)gx * gy * gz;
+    int nchunk = (int)std::min<long long>((148LL * 4 + blocks - 1) / blocks, (npair + 255) / 256);
+    nchunk = std::max(1, std::min(nchunk, 65535 / std::max(1, gz)));
+    const dim3 grid(gx, gy, gz * nchunk);
     for (int ct = 0; ct <= d.pt; ++ct)
         for (int cv = 0; cv <= d.pv; ++cv)
             for (int cu = 0; cu <= d.pu; ++cu) {
-                k_standard<<<grid, 256, smem, stream>>>(d, values, cu, cv, ct);
+                k_standard<<<grid, 256, smem, stream>>>(d, values, cu, cv, ct, nchunk);
                 if (launches)
                     ++*launches;
             }

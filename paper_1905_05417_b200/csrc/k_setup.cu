@@ -301,9 +301,15 @@ __device__ void integral_1d(const double* kn, const int* first, const double* sl
     }
 }
 
-/// Thickness integrals of one pair reduced per term (see k_thickness_pairs).
+/// Thickness integrals of one pair reduced per term (see k_thickness_pairs),
+/// one warp per pair: the lanes take the pair's cells round-robin, each cell's
+/// Q is added with its layer's term multiplier (q~ = sum_l w_l Q_l, with the
+/// layer sums distributed over cells), and the lanes' partial sums are combined
+/// by a fixed xor tree -- deterministic, and independent of the ply count in
+/// latency (a 64-ply single thickness element no longer walks 256 points in
+/// one thread).
 template <int P>
-__device__ void thickness_pair(const DevTables& d, long long pp) {
+__device__ void thickness_pair_warp(const DevTables& d, long long pp, int lane) {
     const long long target = pp + d.pre_t[d.t0];
     int lo = d.t0, hi = d.t1;
     while (hi - lo > 1) {
@@ -327,6 +333,7 @@ __device__ void thickness_pair(const DevTables& d, long long pp) {
     int s_end = s0;
     while (s_end < d.nspt && d.spt_first[s_end] <= mn)
         ++s_end;
+    const int c_begin = d.span_cell0[s0], c_end = d.span_cell0[s_end];
     constexpr int kChunk = 8;
     for (int t0 = 0; t0 < d.n_terms; t0 += kChunk) {
         const int tn = min(kChunk, d.n_terms - t0);
@@ -335,11 +342,24 @@ __device__ void thickness_pair(const DevTables& d, long long pp) {
 #pragma unroll
         for (int t = 0; t < kChunk; ++t)
             acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.0;
-        double ql[4] = {0.0, 0.0, 0.0, 0.0};
-        int cur = -1;
-        auto flush = [&](int layer) {
-            if (layer < 0)
-                return;
+        int s = s0;
+        for (int c = c_begin + lane; c < c_end; c += 32) {
+            while (d.span_cell0[s + 1] <= c)
+                ++s;
+            const int span = d.spt_first[s] + P;
+            double ql[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int q = 0; q < d.nqt; ++q) {
+                const long long hq = (long long)c * d.nqt + q;
+                double va, da, vb, db;
+                if (!eval_pair<P>(d.kt, span, d.cell_pts[hq], it, jt, va, da, vb, db))
+                    continue;
+                const double wq = d.cell_wts[hq];
+                ql[0] += wq * va * vb;
+                ql[1] += wq * va * db;
+                ql[2] += wq * da * vb;
+                ql[3] += wq * da * db;
+            }
+            const int layer = d.cell_layer[c];
 #pragma unroll
             for (int t = 0; t < kChunk; ++t) {
                 if (t >= tn)
@@ -348,40 +368,29 @@ __device__ void thickness_pair(const DevTables& d, long long pp) {
                 if (!d.lam_on[tl])
                     continue;
                 const double w = d.lam[tl];
+#pragma unroll
                 for (int f = 0; f < 4; ++f)
                     acc[t][f] += w * ql[f];
                 on |= 1u << t;
             }
-        };
-        for (int s = s0; s < s_end; ++s) {
-            const int span = d.spt_first[s] + P;
-            for (int c = d.span_cell0[s]; c < d.span_cell0[s + 1]; ++c) {
-                const int layer = d.cell_layer[c];
-                if (layer != cur) {
-                    flush(cur);
-                    cur = layer;
-                    ql[0] = ql[1] = ql[2] = ql[3] = 0.0;
-                }
-                for (int q = 0; q < d.nqt; ++q) {
-                    const long long hq = (long long)c * d.nqt + q;
-                    double va, da, vb, db;
-                    if (!eval_pair<P>(d.kt, span, d.cell_pts[hq], it, jt, va, da, vb, db))
-                        continue;
-                    const double wq = d.cell_wts[hq];
-                    ql[0] += wq * va * vb;
-                    ql[1] += wq * va * db;
-                    ql[2] += wq * da * vb;
-                    ql[3] += wq * da * db;
-                }
-            }
         }
-        flush(cur);
 #pragma unroll
-        for (int t = 0; t < kChunk; ++t)
-            if (t < tn)
+        for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+            for (int t = 0; t < kChunk; ++t)
+#pragma unroll
                 for (int f = 0; f < 4; ++f)
-                    d.W[(pp * d.n_terms + t0 + t) * 4 + f] = acc[t][f];
-        d.Wmask[(long long)(t0 / kChunk) * d.n_pairs + pp] = on;
+                    acc[t][f] += __shfl_xor_sync(0xffffffffu, acc[t][f], o);
+            on |= __shfl_xor_sync(0xffffffffu, on, o);
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int t = 0; t < kChunk; ++t)
+                if (t < tn)
+                    for (int f = 0; f < 4; ++f)
+                        d.W[(pp * d.n_terms + t0 + t) * 4 + f] = acc[t][f];
+            d.Wmask[(long long)(t0 / kChunk) * d.n_pairs + pp] = on;
+        }
     }
 }
 
@@ -395,11 +404,11 @@ __device__ void thickness_pair(const DevTables& d, long long pp) {
     default: { constexpr int PP = 6; CALL; } break;             \
     }
 
-/// Fused setup of the affine fast path: one launch computes, one thread per
-/// item,
-///   [0, nU)            U[i][slot][4]   1D in-plane integrals, u direction
+/// Fused setup of the affine fast path: one launch computes
+///   [0, nU)            U[i][slot][4]   1D in-plane integrals, u direction (thread per item)
 ///   [nU, nU+nV)        V[i][slot][4]   v direction
-///   [.., +n_pairs)     W / Wmask       thickness integrals reduced per term
+///   [uv, +32 n_pairs)  W / Wmask       thickness integrals reduced per term (warp per pair;
+///                                      uv = nU + nV rounded up to a warp)
 ///   [.., +T*81)        Ct              constant-frame pulled-back tables
 /// with the same arithmetic as k_integrals_1d / k_thickness_pairs / k_basis.
 __global__ void __launch_bounds__(64) k_prepare_affine(DevTables d) {
@@ -430,12 +439,16 @@ __global__ void __launch_bounds__(64) k_prepare_affine(DevTables d) {
         out[3] = acc[3];
         return;
     }
-    long long h = g - nU - nV;
-    if (h < d.n_pairs) {
-        LF_DISPATCH_P(d.pt, (thickness_pair<PP>(d, h)))
+    // thickness pairs: one warp per pair, region start aligned to a warp
+    const long long uv = (nU + nV + 31) / 32 * 32;
+    if (g < uv)
+        return;
+    long long h = g - uv;
+    if (h < d.n_pairs * 32) {
+        LF_DISPATCH_P(d.pt, (thickness_pair_warp<PP>(d, h >> 5, (int)(h & 31))))
         return;
     }
-    h -= d.n_pairs;
+    h -= d.n_pairs * 32;
     if (h < (long long)d.n_terms * 81) {
         const int t = (int)(h / 81), xy = (int)(h % 81) / 9, ik = (int)(h % 9);
         const int x = xy / 3, y = xy % 3;
@@ -451,7 +464,8 @@ __global__ void __launch_bounds__(64) k_prepare_affine(DevTables d) {
 } // namespace
 
 int launch_prepare_affine(const DevTables& d, cudaStream_t stream) {
-    const long long n = (long long)d.nu * d.bu + (long long)d.nv * d.bv + d.n_pairs + (long long)d.n_terms * 81;
+    const long long uv = ((long long)d.nu * d.bu + (long long)d.nv * d.bv + 31) / 32 * 32;
+    const long long n = uv + d.n_pairs * 32 + (long long)d.n_terms * 81;
     const int block = 64; // few items: spread them over more SMs
     k_prepare_affine<<<(unsigned)((n + block - 1) / block), block, 0, stream>>>(d);
     return (int)cudaGetLastError();
