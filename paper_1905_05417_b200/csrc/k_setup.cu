@@ -131,14 +131,18 @@ __global__ void k_basis(DevTables d, int with_ct) {
 }
 
 /// Thickness integrals per pair, reduced per term (fast.cpp:170-209 and the
-/// q~ pre-reduction fast.cpp:285-302 / 303-336).  One thread per thickness
-/// pair of the slab.  Cells are visited in the reference order (span-major;
-/// each layer's cells are consecutive), Q_l is completed per layer and then
-/// added with the term multiplier, as `term.thickness += w * Q_l` does.
+/// q~ pre-reduction fast.cpp:285-302 / 303-336), from the tabulated basis
+/// (general geometry path).  One warp per thickness pair of the slab; each
+/// lane takes cells round-robin and adds each cell's Q with its layer's term
+/// multiplier (term.thickness += w * Q_l, distributed over the layer's cells),
+/// then a fixed xor tree combines the lanes (deterministic).
 __global__ void k_thickness_pairs(DevTables d) {
-    const long long pp = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (pp >= d.n_pairs)
+    // one warp per pair (lanes over the pair's cells), as thickness_pair_warp
+    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (gw >= d.n_pairs)
         return;
+    const long long pp = gw;
     // locate (it, k): pre_t[it] - pre_t[t0] <= pp < pre_t[it+1] - pre_t[t0]
     const long long target = pp + d.pre_t[d.t0];
     int lo = d.t0, hi = d.t1; // it in [t0, t1)
@@ -159,32 +163,12 @@ __global__ void k_thickness_pairs(DevTables d) {
         unsigned on = 0;
         for (int t = 0; t < kChunk; ++t)
             acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.0;
-        double ql[4] = {0.0, 0.0, 0.0, 0.0};
-        int cur = -1;
-        auto flush = [&](int layer) {
-            if (layer < 0)
-                return;
-            for (int t = 0; t < tn; ++t) {
-                const long long tl = (long long)(t0 + t) * d.n_layers + layer;
-                if (!d.lam_on[tl])
-                    continue;
-                const double w = d.lam[tl];
-                for (int f = 0; f < 4; ++f)
-                    acc[t][f] += w * ql[f];
-                on |= 1u << t;
-            }
-        };
         for (int s = 0; s < d.nspt; ++s) {
             const int f0 = d.spt_first[s];
             if (f0 > mn || mx > f0 + d.pt)
                 continue;
-            for (int c = d.span_cell0[s]; c < d.span_cell0[s + 1]; ++c) {
-                const int layer = d.cell_layer[c];
-                if (layer != cur) {
-                    flush(cur);
-                    cur = layer;
-                    ql[0] = ql[1] = ql[2] = ql[3] = 0.0;
-                }
+            for (int c = d.span_cell0[s] + lane; c < d.span_cell0[s + 1]; c += 32) {
+                double ql[4] = {0.0, 0.0, 0.0, 0.0};
                 for (int q = 0; q < d.nqt; ++q) {
                     const long long h = (long long)c * d.nqt + q;
                     const int first = d.Bt_first[h];
@@ -199,14 +183,33 @@ __global__ void k_thickness_pairs(DevTables d) {
                     ql[2] += wq * da * vb;
                     ql[3] += wq * da * db;
                 }
+                const int layer = d.cell_layer[c];
+                for (int t = 0; t < tn; ++t) {
+                    const long long tl = (long long)(t0 + t) * d.n_layers + layer;
+                    if (!d.lam_on[tl])
+                        continue;
+                    const double w = d.lam[tl];
+                    for (int f = 0; f < 4; ++f)
+                        acc[t][f] += w * ql[f];
+                    on |= 1u << t;
+                }
             }
         }
-        flush(cur);
-        for (int t = 0; t < tn; ++t)
-            for (int f = 0; f < 4; ++f)
-                d.W[(pp * d.n_terms + t0 + t) * 4 + f] = acc[t][f];
-        // pass masks: pass = term / 8, bit = term % 8 (chunk == pass width)
-        d.Wmask[(long long)(t0 / kChunk) * d.n_pairs + pp] = on;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+            for (int t = 0; t < kChunk; ++t)
+#pragma unroll
+                for (int f = 0; f < 4; ++f)
+                    acc[t][f] += __shfl_xor_sync(0xffffffffu, acc[t][f], o);
+            on |= __shfl_xor_sync(0xffffffffu, on, o);
+        }
+        if (lane == 0) {
+            for (int t = 0; t < tn; ++t)
+                for (int f = 0; f < 4; ++f)
+                    d.W[(pp * d.n_terms + t0 + t) * 4 + f] = acc[t][f];
+            d.Wmask[(long long)(t0 / kChunk) * d.n_pairs + pp] = on;
+        }
     }
 }
 
@@ -484,8 +487,8 @@ int launch_basis(const DevTables& d, bool with_ct, cudaStream_t stream) {
 int launch_thickness_pairs(const DevTables& d, cudaStream_t stream) {
     if (d.n_pairs == 0)
         return 0;
-    const int block = 128;
-    k_thickness_pairs<<<(unsigned)((d.n_pairs + block - 1) / block), block, 0, stream>>>(d);
+    const int block = 128; // 4 pairs (warps) per block
+    k_thickness_pairs<<<(unsigned)((d.n_pairs * 32 + block - 1) / block), block, 0, stream>>>(d);
     return (int)cudaGetLastError();
 }
 
