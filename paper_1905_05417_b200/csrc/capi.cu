@@ -317,10 +317,18 @@ struct lf_plan {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> free_events, pending;
     double kernel_ms = 0.0;
     int64_t kernel_launches = 0;
+    // CUDA-graph replay of the per-step launch sequence (small, launch-bound
+    // plans): captured once per output pointer, replayed by one cudaGraphLaunch
+    bool use_graph = false;
+    cudaGraphExec_t graph = nullptr;
+    double* graph_values = nullptr;
+    int graph_launches = 0;
 
     ~lf_plan() {
         if (stream)
             cudaStreamSynchronize(stream);
+        if (graph)
+            cudaGraphExecDestroy(graph);
         for (auto& e : free_events) {
             cudaEventDestroy(e.first);
             cudaEventDestroy(e.second);
@@ -402,9 +410,15 @@ void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void
         if (!d.affine)
             d.Pg = ar.alloc<double>(static_cast<std::size_t>(d.n_terms) * 4 * static_cast<std::size_t>(d.E));
     }
+    // graph replay for launch-bound plans (<= 64M values, or any standard plan:
+    // its colour launches are many and short); not with the opt-in store
+    // variants, whose constant-bank hand-off orders launches through events
+    const char* ge = std::getenv("LAMFAST_GRAPH");
+    const bool small = s.nnz <= (64LL << 20) || backend == LF_BACKEND_STANDARD;
+    plan->use_graph = (ge ? std::atoi(ge) != 0 : small) && d.ws_variant == 0 && d.n_team == 0;
 }
 
-int plan_launch(lf_plan* plan, double* values) {
+int plan_launch(lf_plan* plan, double* values, bool timed = true) {
     const lfb::DevTables& d = plan->d;
     int launches = 0;
     cudaStream_t s = plan->stream;
@@ -422,6 +436,10 @@ int plan_launch(lf_plan* plan, double* values) {
     if (plan->setup.backend == LF_BACKEND_STANDARD) {
         CK(static_cast<cudaError_t>(lfb::launch_basis(d, false, s)));
         ++launches;
+        if (!timed) {
+            CK(static_cast<cudaError_t>(lfb::launch_standard(d, values, plan->setup.nnz, s, &launches)));
+            return launches;
+        }
         const auto ev = events(); // brackets the coloured standard kernels
         CK(cudaEventRecord(ev.first, s));
         CK(static_cast<cudaError_t>(lfb::launch_standard(d, values, plan->setup.nnz, s, &launches)));
@@ -444,6 +462,10 @@ int plan_launch(lf_plan* plan, double* values) {
         CK(static_cast<cudaError_t>(lfb::launch_inplane_general(d, s)));
         launches += (d.pu + 1) * (d.pv + 1);
     }
+    if (!timed) {
+        CK(static_cast<cudaError_t>(lfb::launch_combine(d, values, 0, s, &launches)));
+        return launches;
+    }
     const auto ev = events();
     CK(cudaEventRecord(ev.first, s));
     CK(static_cast<cudaError_t>(lfb::launch_combine(d, values, 0, s, &launches)));
@@ -452,6 +474,50 @@ int plan_launch(lf_plan* plan, double* values) {
     if (plan->pending.size() > 4096)
         plan->harvest();
     return launches;
+}
+
+/// One step through the captured graph: the events bracket the whole step
+/// (setup + combine), which is what a launch-bound plan's time is.
+int plan_launch_graph(lf_plan* plan, double* values) {
+    cudaStream_t s = plan->stream;
+    if (!plan->graph || plan->graph_values != values) {
+        if (plan->graph) {
+            CK(cudaGraphExecDestroy(plan->graph));
+            plan->graph = nullptr;
+        }
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        int n = 0;
+        try {
+            n = plan_launch(plan, values, false);
+        } catch (...) {
+            cudaStreamEndCapture(s, &g);
+            if (g)
+                cudaGraphDestroy(g);
+            throw;
+        }
+        CK(cudaStreamEndCapture(s, &g));
+        const cudaError_t e = cudaGraphInstantiate(&plan->graph, g, 0);
+        cudaGraphDestroy(g);
+        CK(e);
+        plan->graph_values = values;
+        plan->graph_launches = n;
+    }
+    std::pair<cudaEvent_t, cudaEvent_t> ev;
+    if (!plan->free_events.empty()) {
+        ev = plan->free_events.back();
+        plan->free_events.pop_back();
+    } else {
+        CK(cudaEventCreate(&ev.first));
+        CK(cudaEventCreate(&ev.second));
+    }
+    CK(cudaEventRecord(ev.first, s));
+    CK(cudaGraphLaunch(plan->graph, s));
+    CK(cudaEventRecord(ev.second, s));
+    plan->pending.push_back(ev);
+    if (plan->pending.size() > 4096)
+        plan->harvest();
+    return plan->graph_launches;
 }
 
 void copy_d2h(void* dst, const void* src, std::size_t bytes, cudaStream_t s) {
@@ -645,7 +711,7 @@ int lf_plan_build_pattern(lf_plan* plan, int64_t* d_row_ptr, int32_t* d_cols) {
 int lf_plan_assemble(lf_plan* plan, double* d_values) {
     return guarded([&] {
         CK(cudaSetDevice(plan->device));
-        plan->launches = plan_launch(plan, d_values);
+        plan->launches = plan->use_graph ? plan_launch_graph(plan, d_values) : plan_launch(plan, d_values);
     });
 }
 
