@@ -1,6 +1,6 @@
 // C ABI of the B200 assembler (include/lamfast_cuda.h).  Host orchestration
 // only: validation and setup tables come from setup.cpp, all O(nnz) and
-// O(elements) work runs in the kernels of k_setup.cu / k_main.cu.  No CPU
+// O(elements) work runs in the kernels of k_setup.cu / k_ops.cu / k_combine.cu.  No CPU
 // fallback exists: without a usable CUDA device every compute entry point
 // fails with LF_ERR_CUDA.
 #include <cuda_runtime.h>

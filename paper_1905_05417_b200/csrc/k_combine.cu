@@ -1,0 +1,219 @@
+// K4: the hot kernel -- P (x) q~ straight into the CSR value array
+// (fast.cpp:211-264 + sparse.cpp:30-55), and its launcher.  The opt-in store
+// variants (team/TMA bulk copy, warp-specialised) live in k_combine_variants.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "combine_common.cuh"
+
+namespace lfb {
+
+// k_combine_variants.cu: true when an opt-in store variant handled the launch
+bool launch_combine_variant(const DevTables& d, double* out, int t_chunk_req, int lt_max, cudaStream_t stream,
+                            int* launches);
+
+namespace {
+
+template <int NT, int EPT, bool AFFINE, bool ACCUM, int BT>
+__device__ __forceinline__ void combine_body(const DevTables& d, double* __restrict__ out, int pass, int t_chunk,
+                                             int stage_rows, int lt_max) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    RowInfo* s_row = reinterpret_cast<RowInfo*>(smem_raw);
+    unsigned char* s_kr = smem_raw + stage_rows * sizeof(RowInfo); // [row][NT][2]
+    double4* s_w = reinterpret_cast<double4*>(
+        smem_raw + ((stage_rows * (sizeof(RowInfo) + 2 * NT) + 31) & ~31));
+
+    const int t_first = pass * 8;
+    double P[EPT][NT][4];
+    double* o_thread[EPT];
+    long long A[EPT];
+    int B[EPT];
+    bool live[EPT];
+#pragma unroll
+    for (int x = 0; x < EPT; ++x) {
+        // entry of slot x: 'strided' e = (blockIdx*EPT + x)*256 + tid, or
+        // 'contiguous' (d.contig) e = blockIdx*256*EPT + warp*32*EPT + x*32 + lane,
+        // where a warp's EPT stores per (row, k) are adjacent 256-byte runs
+        const long long e = d.contig ? (long long)blockIdx.x * BT * EPT + (threadIdx.x >> 5) * 32 * EPT + x * 32 +
+                                           (threadIdx.x & 31)
+                                     : (long long)(blockIdx.x * EPT + x) * BT + threadIdx.x;
+        live[x] = e < d.E;
+        const long long ec = live[x] ? e : d.E - 1;
+        int is = __ldg(d.blk_is + ec / kBlock);
+        while (__ldg(d.es_pre + is + 1) <= ec)
+            ++is;
+        const long long ebase = __ldg(d.es_pre + is);
+        const int r = (int)(ec - ebase);
+        const int iu = is % d.nu, iv = is / d.nu;
+        const int Lu = __ldg(d.len_u + iu), Lv = __ldg(d.len_v + iv);
+        B[x] = 3 * Lu * Lv; // row segment length per thickness neighbour
+        const int a = r / B[x];
+        const int rem = r - a * B[x];
+        A[x] = ebase + (long long)a * B[x];
+        o_thread[x] = out + (long long)rem;
+        if constexpr (AFFINE) {
+            const int s = rem / 3, b = rem - 3 * (rem / 3);
+            const int sv = s / Lu, su = s - sv * Lu;
+            affine_p<NT>(d, iu, iv, su, sv, 3 * a + b, t_first, P[x]);
+        } else {
+#pragma unroll
+            for (int t = 0; t < NT; ++t)
+#pragma unroll
+                for (int f = 0; f < 4; ++f)
+                    P[x][t][f] = __ldg(d.Pg + ((long long)(t_first + t) * 4 + f) * d.E + ec);
+        }
+    }
+
+    const int it_begin = d.t0 + blockIdx.y * t_chunk;
+    const int it_end = min(d.t1, it_begin + t_chunk);
+    bool any_live = false;
+#pragma unroll
+    for (int x = 0; x < EPT; ++x)
+        any_live |= live[x];
+
+    for (int it0 = it_begin; it0 < it_end; it0 += stage_rows) {
+        const int nrow = min(stage_rows, it_end - it0);
+        if (it0 != it_begin)
+            __syncthreads();
+        stage_rows_block<NT>(d, it0, nrow, pass, lt_max, s_row, s_kr, s_w, threadIdx.x, BT);
+        __syncthreads();
+        if (!any_live)
+            continue;
+        for (int rr = 0; rr < nrow; ++rr) {
+            const RowInfo ri = s_row[rr];
+            double* o[EPT];
+#pragma unroll
+            for (int x = 0; x < EPT; ++x)
+                o[x] = o_thread[x] + ri.base + (long long)ri.lt * A[x];
+#pragma unroll
+            for (int x = 0; x < EPT; ++x)
+                LF_CHECK(!live[x] || (o[x] >= out && o[x] + (long long)(ri.lt - 1) * B[x] < out + d.nnz_slab));
+            const double4* w = s_w + rr * lt_max * NT;
+            const unsigned char* kr = s_kr + rr * NT * 2;
+            // EPT >= 2: k-outer rows (EPT live accumulators; C4 2.66 -> 2.53 ms,
+            // C3 1.39 -> 1.33 ms with two entries per thread); EPT = 1: the
+            // LT-unrolled form keeps more independent FMA chains in flight
+            switch (ri.lt) {
+            case 1: row_dispatch<NT, EPT, 1, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
+            case 2: row_dispatch<NT, EPT, 2, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
+            case 3: row_dispatch<NT, EPT, 3, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
+            case 4: row_dispatch<NT, EPT, 4, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
+            case 5: row_dispatch<NT, EPT, 5, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
+            case 7: row_dispatch<NT, EPT, 7, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
+            default: combine_row_dyn<NT, EPT, ACCUM>(P, w, ri.lt, ri.mask, o, B, live); break;
+            }
+        }
+    }
+}
+
+
+
+// k_combine: 256-thread blocks and the compiler's own register choice (one
+// entry per thread, 80-128 registers); k_combine_b: explicit bounds (two
+// entries per thread, <= 128 registers so that 2 blocks of 256 fit per SM).
+template <int NT, int EPT, bool AFFINE, bool ACCUM>
+__global__ void __launch_bounds__(kBlock) k_combine(const DevTables d, double* __restrict__ out, int pass,
+                                                    int t_chunk, int stage_rows, int lt_max) {
+    combine_body<NT, EPT, AFFINE, ACCUM, kBlock>(d, out, pass, t_chunk, stage_rows, lt_max);
+}
+
+template <int NT, int EPT, bool AFFINE, bool ACCUM, int BT, int MINB>
+__global__ void __launch_bounds__(BT, MINB) k_combine_b(const DevTables d, double* __restrict__ out, int pass,
+                                                        int t_chunk, int stage_rows, int lt_max) {
+    combine_body<NT, EPT, AFFINE, ACCUM, BT>(d, out, pass, t_chunk, stage_rows, lt_max);
+}
+
+template <int NT>
+constexpr int entries_per_thread() { return NT <= 4 ? 2 : 1; } // two entries: 64 P registers at 4 terms
+
+template <int NT>
+void combine_one(const DevTables& d, double* out, int pass, int t_chunk, int stage_rows, int lt_max,
+                 unsigned nchunk, cudaStream_t s, bool accum) {
+    constexpr int EPT = entries_per_thread<NT>();
+    // two entries per thread: explicit bounds (<= 128 registers, 2 blocks of
+    // 256 per SM); one entry: the compiler's own choice (80-128 registers)
+    constexpr int BT = kBlock;
+    constexpr int MINB = 2;
+    constexpr bool bounded = EPT >= 2;
+    const size_t smem = ((stage_rows * (sizeof(RowInfo) + 2 * NT) + 31) & ~size_t(31)) +
+                        (size_t)stage_rows * lt_max * NT * sizeof(double4);
+    const dim3 grid((unsigned)((d.E + (long long)BT * EPT - 1) / ((long long)BT * EPT)), nchunk);
+    auto launch = [&](auto kern) {
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, BT, smem, s>>>(d, out, pass, t_chunk, stage_rows, lt_max);
+    };
+    if constexpr (!bounded) {
+        if (d.affine)
+            accum ? launch(k_combine<NT, EPT, true, true>) : launch(k_combine<NT, EPT, true, false>);
+        else
+            accum ? launch(k_combine<NT, EPT, false, true>) : launch(k_combine<NT, EPT, false, false>);
+    } else {
+        if (d.affine)
+            accum ? launch(k_combine_b<NT, EPT, true, true, BT, MINB>)
+                  : launch(k_combine_b<NT, EPT, true, false, BT, MINB>);
+        else
+            accum ? launch(k_combine_b<NT, EPT, false, true, BT, MINB>)
+                  : launch(k_combine_b<NT, EPT, false, false, BT, MINB>);
+    }
+}
+
+} // namespace
+
+int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t stream, int* launches) {
+    if (d.E == 0 || d.t1 <= d.t0)
+        return 0;
+    const long long nblk = (d.E + kBlock - 1) / kBlock; // 256-entry sub-blocks
+    const int nt = d.t1 - d.t0;
+    if (t_chunk <= 0) {
+        if (const char* env = std::getenv("LAMFAST_TCHUNK"))
+            t_chunk = std::atoi(env);
+    }
+    const int t_chunk_req = t_chunk;
+    if (t_chunk <= 0) {
+        // 64 thickness rows per block amortise the per-block prologue (P in
+        // registers, entry decode, staging); shorter chunks (down to 32) only
+        // while the grid is under ~4 waves of 2 resident blocks on 148 SMs.
+        // Measured sweep: profiles/r1_tchunk_sweep.txt.
+        const long long blocks_x = (nblk + 1) / 2; // two entries per thread for <= 4 terms
+        // general geometry loads P from HBM once per block: whole-slab chunks
+        // (measured C3 bilinear 1.47 -> 1.38 ms); affine P is recomputed, so
+        // shorter chunks balance better (profiles/r1_tchunk_sweep.txt)
+        t_chunk = d.affine ? std::min(nt, 64) : nt;
+        while (!d.affine && t_chunk > 64 && blocks_x * ((nt + t_chunk - 1) / t_chunk) < 148LL * 2 * 4)
+            t_chunk = (t_chunk + 1) / 2;
+        while (t_chunk > 32 && blocks_x * ((nt + t_chunk - 1) / t_chunk) < 148LL * 2 * 4)
+            t_chunk /= 2;
+        const int nchunks = (nt + t_chunk - 1) / t_chunk; // balance, in multiples of 16 rows
+        t_chunk = std::min(nt, ((nt + nchunks - 1) / nchunks + 15) / 16 * 16);
+    }
+    const unsigned nchunk = (unsigned)((nt + t_chunk - 1) / t_chunk);
+    const int lt_max = std::max(1, d.lt_max);
+    if (d.n_passes == 1 && launch_combine_variant(d, out, t_chunk_req, lt_max, stream, launches))
+        return (int)cudaGetLastError();
+    for (int pass = 0; pass < d.n_passes; ++pass) {
+        const int nterm = std::min(8, d.n_terms - 8 * pass);
+        const bool accum = pass > 0;
+        // rows per staged sub-chunk: ~24 KB of weights, at most the chunk
+        int stage_rows = (int)((24 * 1024) / ((size_t)lt_max * nterm * sizeof(double4)));
+        stage_rows = std::max(1, std::min(stage_rows, t_chunk));
+        switch (nterm) {
+        case 1: combine_one<1>(d, out, pass, t_chunk, stage_rows, lt_max, nchunk, stream, accum); break;
+        case 2: combine_one<2>(d, out, pass, t_chunk, stage_rows, lt_max, nchunk, stream, accum); break;
+        case 3: combine_one<3>(d, out, pass, t_chunk, stage_rows, lt_max, nchunk, stream, accum); break;
+        case 4: combine_one<4>(d, out, pass, t_chunk, stage_rows, lt_max, nchunk, stream, accum); break;
+        case 5: combine_one<5>(d, out, pass, t_chunk, stage_rows, lt_max, nchunk, stream, accum); break;
+        case 6: combine_one<6>(d, out, pass, t_chunk, stage_rows, lt_max, nchunk, stream, accum); break;
+        case 7: combine_one<7>(d, out, pass, t_chunk, stage_rows, lt_max, nchunk, stream, accum); break;
+        default: combine_one<8>(d, out, pass, t_chunk, stage_rows, lt_max, nchunk, stream, accum); break;
+        }
+        if (launches)
+            ++*launches;
+    }
+    return (int)cudaGetLastError();
+}
+
+
+} // namespace lfb

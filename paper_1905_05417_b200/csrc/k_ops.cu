@@ -1,0 +1,673 @@
+// Operator, cross-check, pattern and verification kernels of the B200
+// laminate assembler (sm_100a).
+//
+//  K2a k_integrals_1d     1D basis-product integrals U, V (sum-factorised P
+//                         for affine geometry; fast.cpp:54-168 restated)
+//  K2b k_inplane_general  per-element P for non-affine geometry, coloured
+//                         (fast.cpp:54-168 / voigt_free.cpp:142-248)
+//  (K4 k_combine, the hot kernel, is in k_combine.cu)
+//  K5  k_pattern_*        closed-form CSR row offsets and columns
+//  K6  k_standard         full 3D quadrature cross-check, coloured
+//                         (assembly.cpp:134-245)
+//  K7  verification       ||K||_F, K x, ||A-B||_F, ||K-K^T||_F (sparse.cpp:66-139)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "combine_common.cuh"
+
+namespace lfb {
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// K2a: U[i][slot][2d+e] = sum over spans and Gauss points of
+//      (w h) N_i^{(d)} N_j^{(e)},  j = lo(i) + slot.
+// With a constant frame the 2D in-plane integrals factor exactly:
+//      I_xy(i_s, j_s) = U_{du_x du_y}(i_u, j_u) * V_{dv_x dv_y}(i_v, j_v).
+__global__ void k_integrals_1d(DevTables d) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nu_slots = d.nu * d.bu, nv_slots = d.nv * d.bv;
+    if (g >= nu_slots + nv_slots)
+        return;
+    const bool is_u = g < nu_slots;
+    const int h = is_u ? g : g - nu_slots;
+    const int b = is_u ? d.bu : d.bv;
+    const int i = h / b, slot = h % b;
+    const int p = is_u ? d.pu : d.pv;
+    const int* lo = is_u ? d.lo_u : d.lo_v;
+    const int* len = is_u ? d.len_u : d.len_v;
+    const int* first = is_u ? d.spu_first : d.spv_first;
+    const double* slo = is_u ? d.spu_lo : d.spv_lo;
+    const double* shi = is_u ? d.spu_hi : d.spv_hi;
+    const double* wref = is_u ? d.wu : d.wv;
+    const double* bval = is_u ? d.Bu_val : d.Bv_val;
+    const double* bder = is_u ? d.Bu_der : d.Bv_der;
+    const int nsp = is_u ? d.nspu : d.nspv, nq = is_u ? d.nqu : d.nqv;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    if (slot < len[i]) {
+        const int j = lo[i] + slot;
+        const int mn = min(i, j), mx = max(i, j);
+        for (int s = 0; s < nsp; ++s) {
+            const int f = first[s];
+            if (f > mn || mx > f + p)
+                continue;
+            const double half = 0.5 * (shi[s] - slo[s]);
+            for (int q = 0; q < nq; ++q) {
+                const long long row = ((long long)s * nq + q) * (p + 1);
+                const double w = wref[q] * half;
+                const double vi = bval[row + i - f], di = bder[row + i - f];
+                const double vj = bval[row + j - f], dj = bder[row + j - f];
+                acc[0] += w * vi * vj;
+                acc[1] += w * vi * dj;
+                acc[2] += w * di * vj;
+                acc[3] += w * di * dj;
+            }
+        }
+    }
+    double* out = (is_u ? d.U : d.V) + (long long)h * 4;
+    out[0] = acc[0];
+    out[1] = acc[1];
+    out[2] = acc[2];
+    out[3] = acc[3];
+}
+
+/// Exports P of every term in the entry layout Pg[t][f][e] (affine path),
+/// for the operator-level entry point.
+__global__ void k_affine_export(const DevTables d) {
+    const long long e = (long long)blockIdx.x * kBlock + threadIdx.x;
+    if (e >= d.E)
+        return;
+    const int is = find_is(d.es_pre, d.ns, e);
+    const int r = (int)(e - d.es_pre[is]);
+    const int iu = is % d.nu, iv = is / d.nu;
+    const int Lu = d.len_u[iu], Lv = d.len_v[iv];
+    const int B = 3 * Lu * Lv;
+    const int a = r / B, rem = r - a * B;
+    const int s = rem / 3, b = rem % 3;
+    const int sv = s / Lu, su = s - sv * Lu;
+    for (int t = 0; t < d.n_terms; ++t) {
+        double P[1][4];
+        affine_p<1>(d, iu, iv, su, sv, 3 * a + b, t, P);
+        for (int f = 0; f < 4; ++f)
+            d.Pg[((long long)t * 4 + f) * d.E + e] = P[0][f];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Shared per-element prologue: gradient tables and quadrature weights.
+struct ElemInfo {
+    int eu, ev, fu, fv, nl2, nq2;
+    double hu, hv;
+};
+
+__device__ __forceinline__ void element_tables(const DevTables& d, const ElemInfo& el, double* gh,
+                                               double* w2) {
+    // gh[(q*nl2 + a)*3 + {0,1,2}] = (du, dv, val) of local function a at in-plane point q
+    for (int idx = threadIdx.x; idx < el.nq2 * el.nl2; idx += blockDim.x) {
+        const int q = idx / el.nl2, a = idx % el.nl2;
+        const int qv = q / d.nqu, qu = q % d.nqu;
+        const int jv = a / (d.pu + 1), ju = a % (d.pu + 1);
+        const long long ru = ((long long)el.eu * d.nqu + qu) * (d.pu + 1) + ju;
+        const long long rv = ((long long)el.ev * d.nqv + qv) * (d.pv + 1) + jv;
+        const double bu = d.Bu_val[ru], bud = d.Bu_der[ru];
+        const double bv = d.Bv_val[rv], bvd = d.Bv_der[rv];
+        gh[idx * 3 + 0] = bud * bv;
+        gh[idx * 3 + 1] = bu * bvd;
+        gh[idx * 3 + 2] = bu * bv;
+    }
+    for (int q = threadIdx.x; q < el.nq2; q += blockDim.x) {
+        const int qv = q / d.nqu, qu = q % d.nqu;
+        w2[q] = d.wu[qu] * el.hu * d.wv[qv] * el.hv; // assembly.cpp:44-45
+    }
+}
+
+/// Ctq[q][3x+y][3i+k] = scale_q * sum_{j,l} G_q(j,x) G_q(l,y) C{e_j,e_l}(i,k)
+/// (pullbackContractionTable, voigt_free.cpp:125-140).
+__device__ __forceinline__ void pullback_tables(const DevTables& d, int e_index, int nq2,
+                                                const double* w2, const double* table, double* ctq) {
+    // layout [q][xy][10]: ik padded to 10 so the consumers load 16-byte pairs
+    for (int idx = threadIdx.x; idx < nq2 * 90; idx += blockDim.x) {
+        const int q = idx / 90, xy = (idx % 90) / 10, ik = idx % 10;
+        if (ik == 9) {
+            ctq[idx] = 0.0;
+            continue;
+        }
+        const int x = xy / 3, y = xy % 3;
+        const double* G;
+        double det;
+        if (d.affine) {
+            G = d.G;
+            det = d.det;
+        } else {
+            const double* f = d.frames + ((long long)e_index * nq2 + q) * 19;
+            G = f + 9;
+            det = f[18];
+        }
+        double s = 0.0;
+        for (int j = 0; j < 3; ++j)
+            for (int l = 0; l < 3; ++l)
+                s += G[3 * x + j] * G[3 * y + l] * table[(3 * j + l) * 9 + ik];
+        ctq[idx] = w2[q] * det * s;
+    }
+}
+
+// K2b: in-plane operators of every term for one element colour.  Elements of
+// one colour share no basis function, so plain += is race-free and the
+// result is deterministic.
+__global__ void k_inplane_general(const DevTables d, int cu, int cv) {
+    extern __shared__ double sm[];
+    ElemInfo el;
+    el.eu = cu + blockIdx.x * (d.pu + 1);
+    el.ev = cv + blockIdx.y * (d.pv + 1);
+    if (el.eu >= d.nspu || el.ev >= d.nspv)
+        return;
+    el.fu = d.spu_first[el.eu];
+    el.fv = d.spv_first[el.ev];
+    el.nl2 = (d.pu + 1) * (d.pv + 1);
+    el.nq2 = d.nqu * d.nqv;
+    el.hu = 0.5 * (d.spu_hi[el.eu] - d.spu_lo[el.eu]);
+    el.hv = 0.5 * (d.spv_hi[el.ev] - d.spv_lo[el.ev]);
+    double* gh = sm;                    // nq2 * nl2 * 3
+    double* w2 = gh + el.nq2 * el.nl2 * 3; // nq2
+    double* ctq = sm + ((el.nq2 * el.nl2 * 3 + el.nq2 + 1) & ~1); // nq2 * 90, 16-byte aligned
+    element_tables(d, el, gh, w2);
+    const int e_index = el.ev * d.nspu + el.eu;
+    {
+        const int t = blockIdx.z; // one block per (element, term): 4x the blocks per colour
+        __syncthreads();
+        pullback_tables(d, e_index, el.nq2, w2, d.term_table + (long long)t * 81, ctq);
+        __syncthreads();
+        // one thread per (local pair, family f): 9 accumulators and a 9-value
+        // read-modify-write each, so many more warps hide the latency of the
+        // coloured accumulation into Pg (the bound of this kernel).  Threads of
+        // a warp share f (warp-aligned quarters), so the C~ loads broadcast.
+        const int npair = el.nl2 * el.nl2;
+        const int qstride = (npair + 31) & ~31;
+        for (int idx = threadIdx.x; idx < 4 * qstride; idx += blockDim.x) {
+            const int f = idx / qstride;
+            const int pr = idx - f * qstride;
+            if (pr >= npair)
+                continue;
+            const int al = pr / el.nl2, be = pr % el.nl2;
+            // P11 <- C~00,01,10,11; P12 <- 02,12; P21 <- 20,21; P22 <- 22 (layout [q][xy][10])
+            const int nxy = f == 0 ? 4 : f == 3 ? 1 : 2;
+            int xys[4];
+            xys[0] = f == 0 ? 0 : f == 1 ? 2 : f == 2 ? 6 : 8;
+            xys[1] = f == 0 ? 1 : f == 1 ? 5 : 7;
+            xys[2] = 3;
+            xys[3] = 4;
+            double acc[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k)
+                acc[k] = 0.0;
+            for (int q = 0; q < el.nq2; ++q) {
+                const double* ga = gh + (q * el.nl2 + al) * 3;
+                const double* gb = gh + (q * el.nl2 + be) * 3;
+                const double* C = ctq + q * 90;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (u < nxy) {
+                        const int xy = xys[u];
+                        const double sxy = ga[xy / 3] * gb[xy % 3];
+                        const double2* C2 = reinterpret_cast<const double2*>(C + xy * 10);
+#pragma unroll
+                        for (int h = 0; h < 5; ++h) {
+                            const double2 c = C2[h];
+                            acc[2 * h] += c.x * sxy;
+                            if (2 * h + 1 < 9)
+                                acc[2 * h + 1] += c.y * sxy;
+                        }
+                    }
+                }
+            }
+            const int iu = el.fu + al % (d.pu + 1), iv = el.fv + al / (d.pu + 1);
+            const int ju = el.fu + be % (d.pu + 1), jv = el.fv + be / (d.pu + 1);
+            const int is = iv * d.nu + iu;
+            const int Lu = d.len_u[iu], Lv = d.len_v[iv];
+            const int slot = (jv - d.lo_v[iv]) * Lu + (ju - d.lo_u[iu]);
+            const long long base = d.es_pre[is] + 3 * slot;
+            const int B = 3 * Lu * Lv;
+            double* dst = d.Pg + ((long long)t * 4 + f) * d.E + base;
+            LF_CHECK(base >= 0 && base + 2LL * B + 2 < d.E && t < d.n_terms);
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b)
+                    dst[(long long)a * B + b] += acc[3 * a + b];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K6: standard full-3D quadrature (assembly.cpp:134-245), one block per
+// (element, thickness span) of one colour, accumulated straight into the
+// precomputed CSR (the duplicate summation of sparse.cpp:30-55).
+__global__ void k_standard(const DevTables d, double* __restrict__ values, int cu, int cv, int ct, int nchunk) {
+    extern __shared__ double sm[];
+    ElemInfo el;
+    el.eu = cu + blockIdx.x * (d.pu + 1);
+    el.ev = cv + blockIdx.y * (d.pv + 1);
+    // blockIdx.z = (span of this thickness colour, chunk of the local pairs):
+    // few elements per colour (small plates, many plies per span) still fill
+    // the GPU; chunks own disjoint pairs, so their writes never overlap
+    const int chunk = blockIdx.z % nchunk;
+    const int ks = ct + (blockIdx.z / nchunk) * (d.pt + 1);
+    if (el.eu >= d.nspu || el.ev >= d.nspv || ks >= d.nspt)
+        return;
+    const int c0 = d.span_cell0[ks], c1 = d.span_cell0[ks + 1];
+    if (c0 == c1)
+        return; // span with no unmasked cell (assembly.cpp:185-186)
+    if (d.spt_first[ks] + d.pt < d.t0 || d.spt_first[ks] >= d.t1)
+        return; // no row of this span lies in the slab
+    el.fu = d.spu_first[el.eu];
+    el.fv = d.spv_first[el.ev];
+    el.nl2 = (d.pu + 1) * (d.pv + 1);
+    el.nq2 = d.nqu * d.nqv;
+    el.hu = 0.5 * (d.spu_hi[el.eu] - d.spu_lo[el.eu]);
+    el.hv = 0.5 * (d.spv_hi[el.ev] - d.spv_lo[el.ev]);
+    const int ft = d.spt_first[ks];
+    const int ntl = d.pt + 1;
+    const int nl3 = el.nl2 * ntl;
+    double* gh = sm;
+    double* w2 = gh + el.nq2 * el.nl2 * 3;
+    double* ctq = sm + ((el.nq2 * el.nl2 * 3 + el.nq2 + 1) & ~1); // nq2 * 90, 16-byte aligned
+    double* tv = ctq + el.nq2 * 90; // nqt * ntl values, then derivatives
+    double* td = tv + d.nqt * ntl;
+    double* w3 = td + d.nqt * ntl;
+    element_tables(d, el, gh, w2);
+    const int e_index = el.ev * d.nspu + el.eu;
+    const long long pre0 = d.pre_t[d.t0];
+    for (int c = c0; c < c1; ++c) {
+        __syncthreads();
+        const int cfg = d.layer_config[d.cell_layer[c]];
+        pullback_tables(d, e_index, el.nq2, w2, d.term_table + (long long)cfg * 81, ctq);
+        for (int idx = threadIdx.x; idx < d.nqt * ntl; idx += blockDim.x) {
+            const int q = idx / ntl, a = idx % ntl;
+            const long long h = (long long)c * d.nqt + q;
+            const int sh = ft - d.Bt_first[h]; // 0 unless a point rounds onto a knot
+            const int aa = a + sh;
+            const bool ok = aa >= 0 && aa <= d.pt;
+            tv[idx] = ok ? d.Bt_val[h * ntl + aa] : 0.0;
+            td[idx] = ok ? d.Bt_der[h * ntl + aa] : 0.0;
+        }
+        for (int q = threadIdx.x; q < d.nqt; q += blockDim.x)
+            w3[q] = d.cell_wts[(long long)c * d.nqt + q];
+        __syncthreads();
+        const int npair = d.sym ? nl3 * (nl3 + 1) / 2 : nl3 * nl3;
+        const int per = (npair + nchunk - 1) / nchunk;
+        const int p_end = min(npair, (chunk + 1) * per);
+        for (int pr = chunk * per + threadIdx.x; pr < p_end; pr += blockDim.x) {
+            int al, be;
+            if (d.sym) { // triangular index: be >= al
+                al = 0;
+                int rest = pr;
+                while (rest >= nl3 - al) {
+                    rest -= nl3 - al;
+                    ++al;
+                }
+                be = al + rest;
+            } else {
+                al = pr / nl3;
+                be = pr % nl3;
+            }
+            const int at = al / el.nl2, as = al % el.nl2;
+            const int bt = be / el.nl2, bs = be % el.nl2;
+            const int it = ft + at, jt = ft + bt;
+            const bool row_i = it >= d.t0 && it < d.t1;
+            const bool row_j = d.sym && al != be && jt >= d.t0 && jt < d.t1;
+            if (!row_i && !row_j)
+                continue;
+            double acc[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k)
+                acc[k] = 0.0;
+            for (int q2 = 0; q2 < el.nq2; ++q2) {
+                const double* ga = gh + (q2 * el.nl2 + as) * 3;
+                const double* gb = gh + (q2 * el.nl2 + bs) * 3;
+                // the thickness points of the cell share the in-plane C~: sum the
+                // 9 gradient products over q3 first, then contract once with C~
+                double S[9];
+#pragma unroll
+                for (int xy = 0; xy < 9; ++xy)
+                    S[xy] = 0.0;
+                for (int q3 = 0; q3 < d.nqt; ++q3) {
+                    const double Ta = tv[q3 * ntl + at], Tda = td[q3 * ntl + at];
+                    const double Tb = tv[q3 * ntl + bt], Tdb = td[q3 * ntl + bt];
+                    // grad_hat = (du T, dv T, val T') (assembly.cpp:203-206)
+                    const double xa[3] = {ga[0] * Ta, ga[1] * Ta, ga[2] * Tda};
+                    const double xb[3] = {gb[0] * Tb * w3[q3], gb[1] * Tb * w3[q3], gb[2] * Tdb * w3[q3]};
+#pragma unroll
+                    for (int x = 0; x < 3; ++x)
+#pragma unroll
+                        for (int y = 0; y < 3; ++y)
+                            S[3 * x + y] += xa[x] * xb[y];
+                }
+                const double2* C2 = reinterpret_cast<const double2*>(ctq + q2 * 90);
+#pragma unroll
+                for (int xy = 0; xy < 9; ++xy) {
+#pragma unroll
+                    for (int h = 0; h < 5; ++h) {
+                        const double2 c = C2[xy * 5 + h];
+                        acc[2 * h] += c.x * S[xy];
+                        if (2 * h + 1 < 9)
+                            acc[2 * h + 1] += c.y * S[xy];
+                    }
+                }
+            }
+            // K(i,j)[a][b] into row block i; with symmetric tables also
+            // K(j,i)[b][a] = K(i,j)[a][b] into row block j (same element, so the
+            // colouring still makes the += race-free)
+            for (int side = 0; side < 2; ++side) {
+                if (side == 0 ? !row_i : !row_j)
+                    continue;
+                const int ls = side ? bs : as, ms = side ? as : bs;
+                const int rt = side ? jt : it, ct_ = side ? it : jt;
+                const int iu = el.fu + ls % (d.pu + 1), iv = el.fv + ls / (d.pu + 1);
+                const int ju = el.fu + ms % (d.pu + 1), jv = el.fv + ms / (d.pu + 1);
+                const int is = iv * d.nu + iu;
+                const int Lu = d.len_u[iu], Lv = d.len_v[iv];
+                const int B = 3 * Lu * Lv;
+                const int slot = (jv - d.lo_v[iv]) * Lu + (ju - d.lo_u[iu]);
+                const int Lt = d.len_t[rt];
+                const long long pos = 9 * d.S_s * (d.pre_t[rt] - pre0) + (long long)Lt * d.es_pre[is] +
+                                      (long long)(ct_ - d.lo_t[rt]) * B + 3 * slot;
+                LF_CHECK(pos >= 0 && pos + 2LL * Lt * B + 2 < d.nnz_slab && ct_ >= d.lo_t[rt] &&
+                         ct_ < d.lo_t[rt] + Lt);
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int b = 0; b < 3; ++b)
+                        values[pos + (long long)a * Lt * B + b] += side ? acc[3 * b + a] : acc[3 * a + b];
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K5: closed-form CSR pattern, slab-local row offsets.
+__global__ void k_pattern_rows(const DevTables d, long long* __restrict__ row_ptr, long long rows) {
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r > rows)
+        return;
+    if (r == rows) {
+        row_ptr[rows] = 9 * d.S_s * (d.pre_t[d.t1] - d.pre_t[d.t0]);
+        return;
+    }
+    const long long per_t = 3LL * d.ns;
+    const int it = d.t0 + (int)(r / per_t);
+    const long long rr = r % per_t;
+    const int is = (int)(rr / 3), a = (int)(rr % 3);
+    const int iu = is % d.nu, iv = is / d.nu;
+    const int B = 3 * d.len_u[iu] * d.len_v[iv];
+    const int Lt = d.len_t[it];
+    row_ptr[r] = 9 * d.S_s * (d.pre_t[it] - d.pre_t[d.t0]) + (long long)Lt * (d.es_pre[is] + (long long)a * B);
+}
+
+constexpr int kColsEpt = 4; // entries per thread of k_pattern_cols
+
+/// Columns of the slab's CSR.  Thread slots are warp-contiguous (a warp owns
+/// 32 * kColsEpt consecutive entries, so its kColsEpt stores per (row, k) are
+/// adjacent 128-byte runs) and the stores stream (st.global.cs).
+__global__ void __launch_bounds__(kBlock) k_pattern_cols(const DevTables d, int* __restrict__ cols,
+                                                         int t_chunk) {
+    int* o0[kColsEpt];
+    int B[kColsEpt], col_s[kColsEpt];
+    long long A[kColsEpt];
+    bool live[kColsEpt];
+#pragma unroll
+    for (int x = 0; x < kColsEpt; ++x) {
+        const long long e = (long long)blockIdx.x * kBlock * kColsEpt + (threadIdx.x >> 5) * 32 * kColsEpt +
+                            x * 32 + (threadIdx.x & 31);
+        live[x] = e < d.E;
+        const long long ec = live[x] ? e : d.E - 1;
+        int is = __ldg(d.blk_is + ec / kBlock);
+        while (__ldg(d.es_pre + is + 1) <= ec)
+            ++is;
+        const long long ebase = __ldg(d.es_pre + is);
+        const int r = (int)(ec - ebase);
+        const int iu = is % d.nu, iv = is / d.nu;
+        const int Lu = __ldg(d.len_u + iu), Lv = __ldg(d.len_v + iv);
+        B[x] = 3 * Lu * Lv;
+        const int a = r / B[x], rem = r - a * B[x];
+        const int s = rem / 3, b = rem % 3;
+        const int jv = __ldg(d.lo_v + iv) + s / Lu, ju = __ldg(d.lo_u + iu) + s % Lu;
+        col_s[x] = 3 * (jv * d.nu + ju) + b;
+        A[x] = ebase + (long long)a * B[x];
+        o0[x] = cols + rem;
+    }
+    const int it_begin = d.t0 + blockIdx.y * t_chunk;
+    const int it_end = min(d.t1, it_begin + t_chunk);
+    const long long pre0 = __ldg(d.pre_t + d.t0);
+    for (int it = it_begin; it < it_end; ++it) {
+        const int Lt = __ldg(d.len_t + it);
+        const long long base = 9 * d.S_s * (__ldg(d.pre_t + it) - pre0);
+        const int c0 = 3 * d.ns * __ldg(d.lo_t + it);
+#pragma unroll
+        for (int x = 0; x < kColsEpt; ++x)
+            LF_CHECK(!live[x] || (base + (long long)Lt * A[x] + (o0[x] - cols) >= 0 &&
+                                  base + (long long)Lt * A[x] + (long long)(Lt - 1) * B[x] + (o0[x] - cols) <
+                                      d.nnz_slab));
+        for (int k = 0; k < Lt; ++k) {
+#pragma unroll
+            for (int x = 0; x < kColsEpt; ++x)
+                if (live[x])
+                    __stcs(o0[x] + base + (long long)Lt * A[x] + (long long)k * B[x], c0 + 3 * d.ns * k + col_s[x]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K7: verification reductions (deterministic two-pass).
+__device__ __forceinline__ double block_sum(double v) {
+    __shared__ double red[32];
+    for (int o = 16; o > 0; o >>= 1)
+        v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0)
+        red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    if (threadIdx.x < 32)
+        for (int o = 16; o > 0; o >>= 1)
+            v += __shfl_down_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__global__ void k_sumsq(const double* v, long long n, double* partial) {
+    double s = 0.0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        s += v[i] * v[i];
+    s = block_sum(s);
+    if (threadIdx.x == 0)
+        partial[blockIdx.x] = s;
+}
+
+__global__ void k_final_sum(const double* partial, int n, double* out) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        s += partial[i];
+    s = block_sum(s);
+    if (threadIdx.x == 0)
+        *out = s;
+}
+
+__global__ void k_spmv(long long rows, const long long* rp, const int* c, const double* v, const double* x,
+                       double* y) {
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows)
+        return;
+    double s = 0.0;
+    for (long long k = rp[r]; k < rp[r + 1]; ++k)
+        s += v[k] * x[c[k]];
+    y[r] = s;
+}
+
+__global__ void k_diff_rows(long long rows, const long long* ra, const int* ca, const double* va,
+                            const long long* rb, const int* cb, const double* vb, double* partial) {
+    double s = 0.0;
+    for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+         r += (long long)gridDim.x * blockDim.x) {
+        long long ka = ra[r], kb = rb[r];
+        const long long ea = ra[r + 1], eb = rb[r + 1];
+        while (ka < ea || kb < eb) {
+            const long long xa = ka < ea ? ca[ka] : (1LL << 40);
+            const long long xb = kb < eb ? cb[kb] : (1LL << 40);
+            double dd;
+            if (xa == xb) {
+                dd = va[ka++] - vb[kb++];
+            } else if (xa < xb) {
+                dd = va[ka++];
+            } else {
+                dd = -vb[kb++];
+            }
+            s += dd * dd;
+        }
+    }
+    s = block_sum(s);
+    if (threadIdx.x == 0)
+        partial[blockIdx.x] = s;
+}
+
+__global__ void k_symmetry_rows(long long rows, const long long* rp, const int* c, const double* v,
+                                double* partial) {
+    double s = 0.0;
+    for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+         r += (long long)gridDim.x * blockDim.x) {
+        for (long long k = rp[r]; k < rp[r + 1]; ++k) {
+            const int col = c[k];
+            long long lo = rp[col], hi = rp[col + 1];
+            while (lo < hi) {
+                const long long mid = (lo + hi) >> 1;
+                if (c[mid] < r)
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+            const bool mirrored = lo < rp[col + 1] && c[lo] == r;
+            const double dd = v[k] - (mirrored ? v[lo] : 0.0);
+            s += dd * dd;
+            if (!mirrored)
+                s += dd * dd; // symmetryRelError counts the absent mirror slot (sparse.cpp:87-90)
+        }
+    }
+    s = block_sum(s);
+    if (threadIdx.x == 0)
+        partial[blockIdx.x] = s;
+}
+
+int reduce_launch(int blocks, double* partial, double* out, cudaStream_t stream) {
+    k_final_sum<<<1, 1024, 0, stream>>>(partial, blocks, out);
+    return (int)cudaGetLastError();
+}
+
+} // namespace
+
+int launch_integrals_1d(const DevTables& d, cudaStream_t stream) {
+    const int n = d.nu * d.bu + d.nv * d.bv;
+    k_integrals_1d<<<(n + 127) / 128, 128, 0, stream>>>(d);
+    return (int)cudaGetLastError();
+}
+
+int launch_affine_export(const DevTables& d, cudaStream_t stream) {
+    if (d.E == 0)
+        return 0;
+    k_affine_export<<<(unsigned)((d.E + kBlock - 1) / kBlock), kBlock, 0, stream>>>(d);
+    return (int)cudaGetLastError();
+}
+
+int launch_inplane_general(const DevTables& d, cudaStream_t stream) {
+    const int nl2 = (d.pu + 1) * (d.pv + 1), nq2 = d.nqu * d.nqv;
+    const size_t smem = sizeof(double) * ((size_t)nq2 * nl2 * 3 + nq2 + 1 + (size_t)nq2 * 90);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_inplane_general, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const dim3 grid((d.nspu + d.pu) / (d.pu + 1), (d.nspv + d.pv) / (d.pv + 1), d.n_terms);
+    const int threads = std::min(512, 4 * ((nl2 * nl2 + 31) / 32 * 32)); // one thread per (local pair, family)
+    for (int cv = 0; cv <= d.pv; ++cv)
+        for (int cu = 0; cu <= d.pu; ++cu)
+            k_inplane_general<<<grid, threads, smem, stream>>>(d, cu, cv);
+    return (int)cudaGetLastError();
+}
+
+int launch_pattern(const DevTables& d, long long* row_ptr, int* cols, cudaStream_t stream) {
+    const long long rows = 3LL * d.ns * (d.t1 - d.t0);
+    k_pattern_rows<<<(unsigned)((rows + 1 + 255) / 256), 256, 0, stream>>>(d, row_ptr, rows);
+    if (d.E > 0 && d.t1 > d.t0) {
+        const long long nblk = (d.E + (long long)kBlock * kColsEpt - 1) / ((long long)kBlock * kColsEpt);
+        const int nt = d.t1 - d.t0;
+        long long nchunks = std::max(1LL, std::min<long long>((148LL * 16 + nblk - 1) / nblk, nt));
+        const int t_chunk = (int)((nt + nchunks - 1) / nchunks);
+        const dim3 grid((unsigned)nblk, (unsigned)((nt + t_chunk - 1) / t_chunk));
+        k_pattern_cols<<<grid, kBlock, 0, stream>>>(d, cols, t_chunk);
+    }
+    return (int)cudaGetLastError();
+}
+
+int launch_standard(const DevTables& d, double* values, long long nnz, cudaStream_t stream, int* launches) {
+    cudaMemsetAsync(values, 0, sizeof(double) * (size_t)nnz, stream);
+    const int nl2 = (d.pu + 1) * (d.pv + 1), nq2 = d.nqu * d.nqv, ntl = d.pt + 1;
+    const size_t smem = sizeof(double) * ((size_t)nq2 * nl2 * 3 + nq2 + 1 + (size_t)nq2 * 90 +
+                                          2 * (size_t)d.nqt * ntl + d.nqt);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_standard, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int gx = (d.nspu + d.pu) / (d.pu + 1), gy = (d.nspv + d.pv) / (d.pv + 1), gz = (d.nspt + d.pt) / (d.pt + 1);
+    // split the local pairs of each (element, span) over enough blocks for
+    // ~4 blocks per SM per colour launch (chunks of >= 256 pairs)
+    const int nl3 = nl2 * ntl;
+    const int npair = d.sym ? nl3 * (nl3 + 1) / 2 : nl3 * nl3;
+    const long long blocks = (long long)gx * gy * gz;
+    int nchunk = (int)std::min<long long>((148LL * 4 + blocks - 1) / blocks, (npair + 255) / 256);
+    nchunk = std::max(1, std::min(nchunk, 65535 / std::max(1, gz)));
+    const dim3 grid(gx, gy, gz * nchunk);
+    for (int ct = 0; ct <= d.pt; ++ct)
+        for (int cv = 0; cv <= d.pv; ++cv)
+            for (int cu = 0; cu <= d.pu; ++cu) {
+                k_standard<<<grid, 256, smem, stream>>>(d, values, cu, cv, ct, nchunk);
+                if (launches)
+                    ++*launches;
+            }
+    return (int)cudaGetLastError();
+}
+
+int launch_frobenius_sq(long long rows, const long long* rp, const double* v, double* out, cudaStream_t stream) {
+    long long nnz = 0;
+    cudaMemcpyAsync(&nnz, rp + rows, sizeof nnz, cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    const int blocks = 1024;
+    double* partial = nullptr;
+    cudaMallocAsync(&partial, sizeof(double) * blocks, stream);
+    k_sumsq<<<blocks, 256, 0, stream>>>(v, nnz, partial);
+    reduce_launch(blocks, partial, out, stream);
+    cudaFreeAsync(partial, stream);
+    return (int)cudaGetLastError();
+}
+
+int launch_spmv(long long rows, const long long* rp, const int* c, const double* v, const double* x, double* y,
+                cudaStream_t stream) {
+    k_spmv<<<(unsigned)((rows + 255) / 256), 256, 0, stream>>>(rows, rp, c, v, x, y);
+    return (int)cudaGetLastError();
+}
+
+int launch_diff_sq(long long rows, const long long* ra, const int* ca, const double* va, const long long* rb,
+                   const int* cb, const double* vb, double* out, cudaStream_t stream) {
+    const int blocks = 1024;
+    double* partial = nullptr;
+    cudaMallocAsync(&partial, sizeof(double) * blocks, stream);
+    k_diff_rows<<<blocks, 256, 0, stream>>>(rows, ra, ca, va, rb, cb, vb, partial);
+    reduce_launch(blocks, partial, out, stream);
+    cudaFreeAsync(partial, stream);
+    return (int)cudaGetLastError();
+}
+
+int launch_symmetry_sq(long long rows, const long long* rp, const int* c, const double* v, double* out,
+                       cudaStream_t stream) {
+    const int blocks = 1024;
+    double* partial = nullptr;
+    cudaMallocAsync(&partial, sizeof(double) * blocks, stream);
+    k_symmetry_rows<<<blocks, 256, 0, stream>>>(rows, rp, c, v, partial);
+    reduce_launch(blocks, partial, out, stream);
+    cudaFreeAsync(partial, stream);
+    return (int)cudaGetLastError();
+}
+
+} // namespace lfb
