@@ -244,7 +244,10 @@ __global__ void k_inplane_general(const DevTables d, int cu, int cv) {
 // K6: standard full-3D quadrature (assembly.cpp:134-245), one block per
 // (element, thickness span) of one colour, accumulated straight into the
 // precomputed CSR (the duplicate summation of sparse.cpp:30-55).
-__global__ void k_standard(const DevTables d, double* __restrict__ values, int cu, int cv, int ct, int nchunk) {
+#ifndef LF_K6_MINB
+#define LF_K6_MINB 3 // <= 80 registers: 24 warps/SM (C3 standard 95.7 -> 87.2 ms)
+#endif
+__global__ void __launch_bounds__(256, LF_K6_MINB) k_standard(const DevTables d, double* __restrict__ values, int cu, int cv, int ct, int nchunk) {
     extern __shared__ double sm[];
     ElemInfo el;
     el.eu = cu + blockIdx.x * (d.pu + 1);
