@@ -128,10 +128,9 @@ __global__ void __launch_bounds__(BT, MINB) k_combine_b(const DevTables d, doubl
 template <int NT>
 constexpr int entries_per_thread() { return NT <= 4 ? 2 : 1; } // two entries: 64 P registers at 4 terms
 
-template <int NT>
-void combine_one(const DevTables& d, double* out, int pass, int t_chunk, int stage_rows, int lt_max,
-                 unsigned nchunk, cudaStream_t s, bool accum) {
-    constexpr int EPT = entries_per_thread<NT>();
+template <int NT, int EPT>
+void combine_one_ept(const DevTables& d, double* out, int pass, int t_chunk, int stage_rows, int lt_max,
+                     unsigned nchunk, cudaStream_t s, bool accum) {
     // two entries per thread: explicit bounds (<= 128 registers, 2 blocks of
     // 256 per SM); one entry: the compiler's own choice (80-128 registers)
     constexpr int BT = kBlock;
@@ -152,12 +151,24 @@ void combine_one(const DevTables& d, double* out, int pass, int t_chunk, int sta
             accum ? launch(k_combine<NT, EPT, false, true>) : launch(k_combine<NT, EPT, false, false>);
     } else {
         if (d.affine)
-            accum ? launch(k_combine_b<NT, EPT, true, true, BT, MINB>)
-                  : launch(k_combine_b<NT, EPT, true, false, BT, MINB>);
+            launch(k_combine_b<NT, EPT, true, false, BT, MINB>);
         else
-            accum ? launch(k_combine_b<NT, EPT, false, true, BT, MINB>)
-                  : launch(k_combine_b<NT, EPT, false, false, BT, MINB>);
+            launch(k_combine_b<NT, EPT, false, false, BT, MINB>);
     }
+}
+
+/// Accumulating passes (> 8 terms) read the values they add to: one entry per
+/// thread and the L_t-unrolled rows, whose loads of all L_t old values issue
+/// together (k-outer rows would serialise load -> FMA -> store per neighbour:
+/// measured 14.2 ms for the 2-term second pass of C4 with decompose_angles).
+template <int NT>
+void combine_one(const DevTables& d, double* out, int pass, int t_chunk, int stage_rows, int lt_max,
+                 unsigned nchunk, cudaStream_t s, bool accum) {
+    if (accum)
+        combine_one_ept<NT, 1>(d, out, pass, t_chunk, stage_rows, lt_max, nchunk, s, true);
+    else
+        combine_one_ept<NT, entries_per_thread<NT>()>(d, out, pass, t_chunk, stage_rows, lt_max, nchunk, s,
+                                                        false);
 }
 
 } // namespace

@@ -18,6 +18,7 @@ ap.add_argument("--backend", default="fast")
 ap.add_argument("--plies", type=int, default=0)
 ap.add_argument("--calibrate", action="store_true")
 ap.add_argument("--geometry", default="planar", choices=["planar", "bilinear"])
+ap.add_argument("--decompose", action="store_true", help="AssemblyOptions::decompose_angles")
 a = ap.parse_args()
 if a.calibrate:
     # same-box write-only and copy bandwidth of a buffer the size of C4's values
@@ -44,6 +45,8 @@ if a.geometry == "bilinear":  # non-affine map: general in-plane path (k_inplane
     lx, ly = prob.geometry[0], prob.geometry[1]
     prob = prob.replace(geometry_kind=1, geometry=(0, 0, 0, lx, 0.05 * ly, 0.0, -0.05 * lx, ly, 0.0,
                                                    1.02 * lx, 1.03 * ly, 0.01))
+if a.decompose:
+    prob = prob.replace(decompose_angles=True)
 s = torch.cuda.Stream()
 torch.cuda.set_stream(s)
 plan = lf.Plan(prob, a.backend, 0, stream=s.cuda_stream)
