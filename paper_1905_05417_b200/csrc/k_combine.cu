@@ -134,7 +134,10 @@ void combine_one_ept(const DevTables& d, double* out, int pass, int t_chunk, int
     // two entries per thread: explicit bounds (<= 128 registers, 2 blocks of
     // 256 per SM); one entry: the compiler's own choice (80-128 registers)
     constexpr int BT = kBlock;
-    constexpr int MINB = 2;
+#ifndef LF_COMBINE_MINB
+#define LF_COMBINE_MINB 2
+#endif
+    constexpr int MINB = LF_COMBINE_MINB;
     constexpr bool bounded = EPT >= 2;
     const size_t smem = ((stage_rows * (sizeof(RowInfo) + 2 * NT) + 31) & ~size_t(31)) +
                         (size_t)stage_rows * lt_max * NT * sizeof(double4);
