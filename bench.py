@@ -23,7 +23,11 @@ Reported beside the device number:
                 the measured HBM copy bandwidth (MEASURED_PEAKS.json);
   cpu_baseline  the reference's own fast assembler (compiled from its
                 unmodified sources, oracle/_ref) on a bounded sample of the
-                same workload family, all host threads.
+                same workload family, all host threads;
+  standard      side measurement: the standard full-3D quadrature assembly
+                (assembleStandard, the path the fast one replaces) on the
+                same workload on this GPU, and the reference's own
+                assembleStandard on a 1-ply sample on the host cores.
 """
 from __future__ import annotations
 
@@ -53,6 +57,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-plies", type=int, default=0)
+    ap.add_argument("--no-standard", action="store_true",
+                    help="skip the standard-assembly (cross-check path) side measurement")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: N x the config's plies, one slab per GPU; strong: the config split N ways")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -361,6 +367,14 @@ def main():
         except Exception as exc:  # reported, not fatal
             cpu = {"error": str(exc)}
 
+    standard = None
+    if world == 1 and with_pattern and not args.no_standard:
+        try:
+            standard = measure_standard(args, prob, device, stream)
+            standard["gpu_fast_over_standard"] = standard["gpu"]["ms_per_step"] / ms_per_step
+        except Exception as exc:  # reported, not fatal
+            standard = {"error": str(exc)}
+
     if rank == 0:
         line = {
             "metric": "assembled stiffness nnz/s (FP64 CSR)", "value": value, "unit": "nnz/s",
@@ -376,11 +390,55 @@ def main():
                              % (total_nnz * 8 / 1e9),
                        "parallelism": f"row-slab x{world}", "slab_passes_per_gpu": passes},
             "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
-            "clocks": clocks, "verify": verify,
+            "clocks": clocks, "verify": verify, "standard": standard,
         }
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def measure_standard(args, prob, device, stream):
+    """Side measurement (not the headline): the standard full-3D quadrature
+    assembly (assembleStandard, the path the fast one replaces) on the same
+    workload -- device nnz/s on this GPU (k_standard, event-timed, values in
+    the same precomputed CSR) and the reference's own assembleStandard
+    (oracle/_ref, all host threads) on a bounded sample of the family."""
+    import torch
+    import paper_1905_05417_b200 as lf
+    from paper_1905_05417_b200 import problem as P
+    out = {}
+    plan = lf.Plan(prob, "standard", device, stream=stream.cuda_stream)
+    vals = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
+    plan.assemble(vals.data_ptr())  # warm-up
+    torch.cuda.synchronize()
+    steps = 2
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(steps):
+        plan.assemble(vals.data_ptr())
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / steps
+    out["gpu"] = {"value": plan.nnz / (ms / 1e3), "unit": "nnz/s", "ms_per_step": ms, "steps": steps,
+                  "launches_per_step": plan.launch_count, "workload": args.config}
+    plan.close()
+    del vals
+    torch.cuda.empty_cache()
+    if not args.no_cpu_baseline:
+        from oracle.checkers import Reference
+        if Reference.available():
+            ref = Reference()
+            threads = os.cpu_count() or 1
+            sample = P.baseline_config(args.config, plies=1)
+            nnz = P.sizes(sample)["nnz"]
+            t0 = time.perf_counter()
+            ref.assemble(sample, "standard", threads)
+            dt = time.perf_counter() - t0
+            out["cpu_baseline"] = {
+                "value": nnz / dt, "unit": "nnz/s", "cores": threads, "kind": "reference",
+                "sample": f"{args.config} family with 1 ply ({nnz} nnz), one assembleStandard, "
+                          f"reference sources compiled with the Eigen subset, threads={threads}"}
+    return out
 
 
 def measure_e2e(args, prob, device, total_nnz):
