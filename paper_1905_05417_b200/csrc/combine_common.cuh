@@ -80,8 +80,8 @@ struct RowInfo {
     unsigned mask;  // union of term masks over the row's pairs (this pass)
 };
 
-template <int NT, int EPT, int LT, bool ACCUM, bool SMEM = false>
-__device__ __forceinline__ void combine_row(const double (&P)[EPT][NT][4], const double4* __restrict__ w,
+template <int NT, int EPT, int LT, bool ACCUM, bool SMEM = false, typename WP = const double4*>
+__device__ __forceinline__ void combine_row(const double (&P)[EPT][NT][4], WP w,
                                             unsigned mask, const unsigned char* __restrict__ kr,
                                             double* const (&o)[EPT], const int (&B)[EPT], const bool (&live)[EPT]) {
     double acc[EPT][LT];
@@ -132,8 +132,8 @@ __device__ __forceinline__ void combine_row(const double (&P)[EPT][NT][4], const
 /// k-outer form of combine_row: one neighbour at a time, all its terms, then
 /// the store -- EPT live accumulators instead of EPT * LT (register relief for
 /// the wide variants).
-template <int NT, int EPT, int LT, bool ACCUM>
-__device__ __forceinline__ void combine_row_k(const double (&P)[EPT][NT][4], const double4* __restrict__ w,
+template <int NT, int EPT, int LT, bool ACCUM, typename WP = const double4*>
+__device__ __forceinline__ void combine_row_k(const double (&P)[EPT][NT][4], WP w,
                                               unsigned mask, const unsigned char* __restrict__ kr,
                                               double* const (&o)[EPT], const int (&B)[EPT], const bool (&live)[EPT]) {
     int klo[NT], khi[NT];
@@ -168,8 +168,74 @@ __device__ __forceinline__ void combine_row_k(const double (&P)[EPT][NT][4], con
     }
 }
 
-template <int NT, int EPT, int LT, bool ACCUM>
-__device__ __forceinline__ void row_dispatch(const double (&P)[EPT][NT][4], const double4* __restrict__ w,
+/// Rows whose active terms are the compile-time set M: straight-line FMAs
+/// over all LT neighbours, no per-(neighbour, term) range tests.  A pair a
+/// term of M does not reach has exactly zero weights (W accumulates only
+/// contributing cells, k_prepare_affine / k_thickness_pairs), so the extra
+/// products add zeros.  The range tests and their branches were ~29% of the
+/// instructions of the k-outer rows (ncu source page, C3: ISETP 19%, BRA 9%,
+/// DFMA 17%); fully unrolled, the LT neighbours' chains are independent.
+template <int NT, int EPT, int LT, unsigned M, typename WP = const double4*>
+__device__ __forceinline__ void combine_row_m(const double (&P)[EPT][NT][4], WP w,
+                                              double* const (&o)[EPT], const int (&B)[EPT], const bool (&live)[EPT]) {
+    static_assert(M != 0u && ((M & (M - 1u)) & ((M & (M - 1u)) - 1u)) == 0u, "at most two terms");
+    constexpr int t_first = __builtin_ctz(M), t_last = 31 - __builtin_clz(M); // M has <= 2 bits
+#pragma unroll
+    for (int k = 0; k < LT; ++k) {
+        double acc[EPT];
+        {
+            const double4 ww = w[k * NT + t_first];
+#pragma unroll
+            for (int x = 0; x < EPT; ++x) {
+                acc[x] = P[x][t_first][0] * ww.x;
+                acc[x] = fma(P[x][t_first][1], ww.y, acc[x]);
+                acc[x] = fma(P[x][t_first][2], ww.z, acc[x]);
+                acc[x] = fma(P[x][t_first][3], ww.w, acc[x]);
+            }
+        }
+        if constexpr (t_last != t_first) {
+            const double4 ww = w[k * NT + t_last];
+#pragma unroll
+            for (int x = 0; x < EPT; ++x) {
+                acc[x] = fma(P[x][t_last][0], ww.x, acc[x]);
+                acc[x] = fma(P[x][t_last][1], ww.y, acc[x]);
+                acc[x] = fma(P[x][t_last][2], ww.z, acc[x]);
+                acc[x] = fma(P[x][t_last][3], ww.w, acc[x]);
+            }
+        }
+#pragma unroll
+        for (int x = 0; x < EPT; ++x)
+            if (live[x])
+                store_value(o[x] + (long long)k * B[x], acc[x]);
+    }
+}
+
+/// Selects combine_row_m for a row whose union term mask has at most two
+/// terms (every row of a C0 thickness space with one element per ply: a
+/// vertex function spans two plies, a bubble one); false -> generic rows.
+template <int NT, int EPT, int LT, typename WP = const double4*>
+__device__ __forceinline__ bool row_masked(unsigned mask, const double (&P)[EPT][NT][4],
+                                           WP w, double* const (&o)[EPT],
+                                           const int (&B)[EPT], const bool (&live)[EPT]) {
+    switch (mask) {
+#define LF_ROW_M(m)                                                  \
+    case m:                                                          \
+        if constexpr ((m >> NT) == 0u) {                             \
+            combine_row_m<NT, EPT, LT, m>(P, w, o, B, live);         \
+            return true;                                             \
+        }                                                            \
+        break;
+        LF_ROW_M(1u) LF_ROW_M(2u) LF_ROW_M(3u) LF_ROW_M(4u) LF_ROW_M(5u)
+        LF_ROW_M(6u) LF_ROW_M(8u) LF_ROW_M(9u) LF_ROW_M(10u) LF_ROW_M(12u)
+#undef LF_ROW_M
+    default:
+        break;
+    }
+    return false;
+}
+
+template <int NT, int EPT, int LT, bool ACCUM, typename WP = const double4*>
+__device__ __forceinline__ void row_dispatch(const double (&P)[EPT][NT][4], WP w,
                                              unsigned mask, const unsigned char* __restrict__ kr,
                                              double* const (&o)[EPT], const int (&B)[EPT], const bool (&live)[EPT]) {
     if constexpr (EPT >= 2)
@@ -178,8 +244,8 @@ __device__ __forceinline__ void row_dispatch(const double (&P)[EPT][NT][4], cons
         combine_row<NT, EPT, LT, ACCUM>(P, w, mask, kr, o, B, live);
 }
 
-template <int NT, int EPT, bool ACCUM, bool SMEM = false>
-__device__ __forceinline__ void combine_row_dyn(const double (&P)[EPT][NT][4], const double4* __restrict__ w,
+template <int NT, int EPT, bool ACCUM, bool SMEM = false, typename WP = const double4*>
+__device__ __forceinline__ void combine_row_dyn(const double (&P)[EPT][NT][4], WP w,
                                                 int lt, unsigned mask, double* const (&o)[EPT], const int (&B)[EPT],
                                                 const bool (&live)[EPT]) {
     for (int k = 0; k < lt; ++k) {

@@ -92,6 +92,25 @@ __device__ __forceinline__ void combine_body(const DevTables& d, double* __restr
                 LF_CHECK(!live[x] || (o[x] >= out && o[x] + (long long)(ri.lt - 1) * B[x] < out + d.nnz_slab));
             const double4* w = s_w + rr * lt_max * NT;
             const unsigned char* kr = s_kr + rr * NT * 2;
+#ifndef LF_NO_MASKED_ROWS
+            // rows with <= 2 terms and L_t = 3 (bubble) or 5 (vertex) -- every
+            // row of a C0 thickness space with one element per ply -- take the
+            // branch-free bodies (combine_row_m).  Measured A/B
+            // (profiles/r1_masked_rows.txt): 4 terms C3 1.341 -> 1.301 ms, C5
+            // family 6.08 -> 5.88 ms; 3 terms (C4) 2.52 -> 2.65 ms, so 4 only.
+#ifndef LF_MASKED_LTS
+#define LF_MASKED_LTS 40 // bit L set: rows with L_t = L take the branch-free bodies
+#endif
+#ifndef LF_MASKED_MIN_NT
+#define LF_MASKED_MIN_NT 4
+#endif
+            if constexpr (EPT >= 2 && NT <= 4 && NT >= LF_MASKED_MIN_NT && !ACCUM) {
+                if (((LF_MASKED_LTS >> 5) & 1) && ri.lt == 5 && row_masked<NT, EPT, 5>(ri.mask, P, w, o, B, live))
+                    continue;
+                if (((LF_MASKED_LTS >> 3) & 1) && ri.lt == 3 && row_masked<NT, EPT, 3>(ri.mask, P, w, o, B, live))
+                    continue;
+            }
+#endif
             // EPT >= 2: k-outer rows (EPT live accumulators; C4 2.66 -> 2.53 ms,
             // C3 1.39 -> 1.33 ms with two entries per thread); EPT = 1: the
             // LT-unrolled form keeps more independent FMA chains in flight
