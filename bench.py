@@ -320,11 +320,11 @@ def main():
     elif world > 1 and with_pattern:
         # gather of slab summaries (verification only, never timed)
         from paper_1905_05417_b200 import distributed as D
-        s = D.slab_summary(rp, cols, vals[:plans[0].nnz])
+        s = D.slab_summary(rp, cols, vals[:plans[0].nnz], bounds["row_begin"], bounds["nnz_begin"])
         parts = D.gather_summaries(s.cuda() if args.dist_backend == "nccl" else s)
         tot = D.combine_summaries(parts)
         verify = {"fro_norm": tot["fro_sq"] ** 0.5, "nnz_gathered": int(tot["nnz"]),
-                  "rows_gathered": int(tot["rows"])}
+                  "rows_gathered": int(tot["rows"]), "pattern_hash": tot["pattern_hash"]}
 
     hbm, peak_src = peaks()
     achieved = k_bytes / (k_avg_ms / 1e3) / 1e9

@@ -15,7 +15,8 @@ from typing import Dict, List
 from .assembler import slab_bounds
 from .problem import LaminateProblem
 
-SUMMARY_FIELDS = ("rows", "nnz", "fro_sq", "checksum", "max_abs")
+SUMMARY_FIELDS = ("rows", "nnz", "fro_sq", "checksum", "max_abs", "pattern_hash")
+HASH_P = (1 << 31) - 1  # pattern hashes are sums mod this prime: exact in float64 across ranks
 
 
 def env_rank():
@@ -28,11 +29,50 @@ def slab_for_rank(prob: LaminateProblem, rank: int, world: int, backend: str = "
     return slab_bounds(prob, world, rank, backend)
 
 
-def slab_summary(row_ptr, cols, values):
+def _mix(x):
+    """splitmix64 finaliser on int64 tensors (wrapping arithmetic, logical
+    shifts), reduced to [0, HASH_P)."""
+    import torch
+
+    def shr(v, s):
+        return (v >> s) & ((1 << (64 - s)) - 1)
+    x = x ^ shr(x, 30)
+    x = x * -4658895280553007687  # 0xbf58476d1ce4e5b9 as int64
+    x = x ^ shr(x, 27)
+    x = x * -7723592293110705685  # 0x94d049bb133111eb as int64
+    x = x ^ shr(x, 31)
+    return torch.remainder(shr(x, 1), HASH_P)
+
+
+def pattern_hash(row_ptr, cols, row_begin: int = 0, nnz_begin: int = 0, chunk: int = 1 << 27) -> int:
+    """Additive hash of a slab's CSR pattern in global coordinates: every
+    (global entry position, column) and every (global row, global row
+    offset) contributes mix(.) mod HASH_P, so the slabs' hashes sum (mod
+    HASH_P) to the full matrix's.  Runs on the tensors' device, in chunks."""
+    import torch
+    rp = torch.as_tensor(row_ptr).to(torch.int64)
+    c = torch.as_tensor(cols)
+    nnz = int(rp[-1] - rp[0])
+    dev = c.device
+    h = 0
+    for lo in range(0, nnz, chunk):
+        hi = min(nnz, lo + chunk)
+        pos = torch.arange(lo + nnz_begin, hi + nnz_begin, dtype=torch.int64, device=dev)
+        h += int(_mix((pos << 32) | c[lo:hi].to(torch.int64)).sum())
+    rows = len(rp) - 1
+    for lo in range(0, rows, chunk):
+        hi = min(rows, lo + chunk)
+        r = torch.arange(lo + row_begin, hi + row_begin, dtype=torch.int64, device=rp.device)
+        h += int(_mix((r << 40) ^ (rp[lo:hi] - rp[0] + nnz_begin) ^ (1 << 62)).sum())
+    return h % HASH_P
+
+
+def slab_summary(row_ptr, cols, values, row_begin: int = 0, nnz_begin: int = 0):
     """Summary of one slab CSR (torch tensors on any device, or numpy):
-    rows, nnz, sum of squares, a position-weighted checksum, max |v|.
-    The checksum weights each value by its global column, so a value stored
-    in the wrong column changes it."""
+    rows, nnz, sum of squares, a position-weighted checksum, max |v|, and
+    the additive pattern hash (global coordinates: pass the slab's first
+    global row and nnz offset).  The checksum weights each value by its
+    global column, so a value stored in the wrong column changes it."""
     import torch
     rp = torch.as_tensor(row_ptr)
     c = torch.as_tensor(cols)
@@ -41,8 +81,9 @@ def slab_summary(row_ptr, cols, values):
     v = v[:nnz]
     c = c[:nnz]
     w = (c.to(torch.int64) % 97 + 1).to(torch.float64)
+    ph = pattern_hash(rp, c, row_begin, nnz_begin)
     return torch.tensor([float(len(rp) - 1), float(nnz), float((v * v).sum()),
-                         float((v * w).sum()), float(v.abs().max()) if nnz else 0.0],
+                         float((v * w).sum()), float(v.abs().max()) if nnz else 0.0, float(ph)],
                         dtype=torch.float64)
 
 
@@ -64,4 +105,5 @@ def combine_summaries(parts) -> Dict[str, float]:
     for p in parts:
         for i, k in enumerate(SUMMARY_FIELDS):
             tot[k] = max(tot[k], float(p[i])) if k == "max_abs" else tot[k] + float(p[i])
+    tot["pattern_hash"] = int(tot["pattern_hash"]) % HASH_P
     return tot

@@ -34,7 +34,8 @@ def _worker(rank, world, port, config, q):
     b = D.slab_for_rank(prob, r, w)
     rp, cols, vals = Oracle().assemble(prob, "fast", b["t_begin"], b["t_end"])
     assert rp[0] == 0 and int(rp[-1]) == b["nnz_end"] - b["nnz_begin"]
-    s = D.slab_summary(torch.from_numpy(rp), torch.from_numpy(cols), torch.from_numpy(vals))
+    s = D.slab_summary(torch.from_numpy(rp), torch.from_numpy(cols), torch.from_numpy(vals),
+                       b["row_begin"], b["nnz_begin"])
     parts = D.gather_summaries(s)
     if rank == 0:
         q.put(D.combine_summaries(parts))
@@ -65,3 +66,30 @@ def test_two_rank_slabs_reproduce_full_matrix(config, oracle):
     assert got["fro_sq"] == pytest.approx(full["fro_sq"], rel=1e-13)
     assert got["checksum"] == pytest.approx(full["checksum"], rel=1e-12)
     assert got["max_abs"] == full["max_abs"]
+    assert got["pattern_hash"] == full["pattern_hash"]
+
+
+def test_pattern_hash_is_additive_and_sensitive(oracle):
+    """The slab pattern hashes sum (mod p) to the full matrix's for any cut,
+    and a single moved column or shifted row offset changes the hash."""
+    from paper_1905_05417_b200 import distributed as D
+    from paper_1905_05417_b200 import problem as P
+    import paper_1905_05417_b200 as lf
+    prob = P.baseline_config("C1")
+    rp, cols, _ = oracle.assemble(prob, "fast")
+    rp_t, c_t = torch.from_numpy(rp), torch.from_numpy(cols)
+    full = D.pattern_hash(rp_t, c_t)
+    for parts in (2, 3):
+        tot = 0
+        for k in range(parts):
+            b = lf.slab_bounds(prob, parts, k)
+            r0, r1 = b["row_begin"], b["row_end"]
+            z0, z1 = int(rp[r0]), int(rp[r1])
+            tot += D.pattern_hash(torch.from_numpy(rp[r0:r1 + 1] - z0), c_t[z0:z1], r0, z0, chunk=1000)
+        assert tot % D.HASH_P == full
+    bad = c_t.clone()
+    bad[12345] += 1
+    assert D.pattern_hash(rp_t, bad) != full
+    bad_rp = rp_t.clone()
+    bad_rp[77] += 1
+    assert D.pattern_hash(bad_rp, c_t) != full
