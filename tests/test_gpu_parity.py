@@ -436,3 +436,36 @@ def test_standard_symmetric_halving_matches_oracle(gpu, oracle, monkeypatch, sym
     assert_csr_match((rp.cpu().numpy(), cols.cpu().numpy()[:plan.nnz], vals.cpu().numpy()[:plan.nnz]),
                      want, RTOL)
     plan.close()
+
+
+def test_concurrent_calls_are_reentrant(gpu):
+    """The reference's assembly functions are pure and reentrant and may be
+    called concurrently: eight host threads calling the
+    C ABI at once (ctypes drops the GIL) get the bitwise results of the
+    sequential calls -- every call owns its stream and device buffers."""
+    import threading
+    cases = [("fast", P.baseline_config("C1")), ("standard", P.baseline_config("C1")),
+             ("fast", P.cube_problem(3, 2, 2, [0.0, 0.5 * P.PI, 0.25 * P.PI])),
+             ("voigt_free", P.cube_problem(2, 2, 1, [0.0, 0.25 * P.PI], geometry="skewed")),
+             ("fast", P.baseline_config("C2"))]
+    want = [gpu.assemble_with(b, p).astuple() for b, p in cases]
+    got = [None] * (2 * len(cases))
+    errors = []
+
+    def run(i):
+        try:
+            b, p = cases[i % len(cases)]
+            got[i] = gpu.assemble_with(b, p).astuple()
+        except Exception as exc:  # surfaced below
+            errors.append(exc)
+
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(len(got))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for i, g in enumerate(got):
+        w = want[i % len(cases)]
+        for a, b in zip(g, w):
+            assert np.array_equal(a, b)
