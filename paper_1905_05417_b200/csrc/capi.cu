@@ -356,6 +356,23 @@ struct lf_plan {
 
 namespace {
 
+/// Element-local scratch of the two-phase general in-plane kernel (K2b):
+/// as many terms per batch as fit in ~2 GB (one at least).  LAMFAST_K2B=coloured
+/// keeps the coloured in-place form, LAMFAST_K2B=mma the DMMA element kernel (A/B).
+void alloc_element_scratch(DeviceArena& ar, lfb::DevTables& d, int n_terms) {
+    const char* env = std::getenv("LAMFAST_K2B");
+    if (env && std::string(env) == "coloured") {
+        d.Pe = nullptr;
+        d.pe_terms = 0;
+        return;
+    }
+    const std::size_t nl2 = static_cast<std::size_t>(d.pu + 1) * (d.pv + 1);
+    const std::size_t per_term = static_cast<std::size_t>(d.nspu) * d.nspv * 36 * nl2 * nl2;
+    const std::size_t budget = (std::size_t(2) << 30) / sizeof(double);
+    d.pe_terms = static_cast<int>(std::max<std::size_t>(1, std::min<std::size_t>(n_terms, budget / std::max<std::size_t>(1, per_term))));
+    d.Pe = ar.alloc<double>(per_term * static_cast<std::size_t>(d.pe_terms));
+}
+
 void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void* stream, int t0, int t1) {
     if (!p)
         raise(LF_ERR_INVALID_ARGUMENT, "null problem");
@@ -407,8 +424,10 @@ void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void
             d.g_w = ar.alloc<double>(rows * static_cast<std::size_t>(std::max(1, d.lt_max)) * d.n_terms * 4);
         }
         d.Wmask = ar.alloc<unsigned>(static_cast<std::size_t>(std::max<long long>(1, d.n_pairs)) * d.n_passes);
-        if (!d.affine)
+        if (!d.affine) {
             d.Pg = ar.alloc<double>(static_cast<std::size_t>(d.n_terms) * 4 * static_cast<std::size_t>(d.E));
+            alloc_element_scratch(ar, d, d.n_terms);
+        }
     }
     // graph replay for launch-bound plans (<= 64M values, or any standard plan:
     // its colour launches are many and short); not with the opt-in store
@@ -458,9 +477,10 @@ int plan_launch(lf_plan* plan, double* values, bool timed = true) {
             CK(static_cast<cudaError_t>(lfb::launch_thickness_pairs(d, s)));
             ++launches;
         }
-        CK(cudaMemsetAsync(d.Pg, 0, sizeof(double) * static_cast<std::size_t>(d.n_terms) * 4 * d.E, s));
+        if (!d.Pe) // the coloured form accumulates in place
+            CK(cudaMemsetAsync(d.Pg, 0, sizeof(double) * static_cast<std::size_t>(d.n_terms) * 4 * d.E, s));
         CK(static_cast<cudaError_t>(lfb::launch_inplane_general(d, s)));
-        launches += (d.pu + 1) * (d.pv + 1);
+        launches += lfb::inplane_general_launches(d);
     }
     if (!timed) {
         CK(static_cast<cudaError_t>(lfb::launch_combine(d, values, 0, s, &launches)));
@@ -796,6 +816,8 @@ static int inplane_common(const lf_problem* p, const double table[81], int devic
             upload_terms(ar, d, 1, 1, tab, lam, on);
             d.Pg = ar.alloc<double>(4 * static_cast<std::size_t>(d.E));
             CK(cudaMemsetAsync(d.Pg, 0, sizeof(double) * 4 * d.E, st));
+            if (!d.affine)
+                alloc_element_scratch(ar, d, 1);
             CK(static_cast<cudaError_t>(lfb::launch_basis(d, d.affine != 0, st)));
             if (d.affine) {
                 CK(static_cast<cudaError_t>(lfb::launch_integrals_1d(d, st)));

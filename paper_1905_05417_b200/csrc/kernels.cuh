@@ -99,6 +99,8 @@ struct DevTables {
     double* W;                                 // [n_pairs][T][4]
     unsigned* Wmask;                           // [n_passes][n_pairs]
     double* Pg;                                // [T][4][E] (general geometry)
+    double* Pe;     // element-local P of a batch of pe_terms terms: [term][el][4][nl2][3][nl2][3]
+    int pe_terms;   // terms per batch (0: the coloured in-place K2b)
     // slab
     int t0, t1;
     long long n_pairs, E;
@@ -111,7 +113,10 @@ int launch_thickness_pairs(const DevTables& d, cudaStream_t stream);
 /// Affine fast path: U, V, thickness pairs and Ct in one launch.
 int launch_prepare_affine(const DevTables& d, cudaStream_t stream);
 int launch_integrals_1d(const DevTables& d, cudaStream_t stream);
+/// General-geometry in-plane operators into Pg: two-phase (Pe set) or coloured in place
+/// (Pg zeroed by the caller).
 int launch_inplane_general(const DevTables& d, cudaStream_t stream);
+int inplane_general_launches(const DevTables& d);
 int launch_affine_export(const DevTables& d, cudaStream_t stream);
 /// Combine: one launch per pass of <= 8 terms.  `t_chunk` thickness rows per
 /// block row; returns the number of kernels launched via *launches.
