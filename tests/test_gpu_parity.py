@@ -469,3 +469,25 @@ def test_concurrent_calls_are_reentrant(gpu):
         w = want[i % len(cases)]
         for a, b in zip(g, w):
             assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("k2b", ["default", "mma", "coloured"])
+def test_general_inplane_forms_match_oracle(gpu, oracle, monkeypatch, k2b):
+    """Non-affine maps take the general in-plane path (K2b): the two-phase
+    default (element-local P + gather), its DMMA element kernel and the
+    coloured in-place form all match the oracle -- degrees 1..4, mixed
+    in-plane degrees (the runtime-degree gather), several terms, slabs."""
+    if k2b != "default":
+        monkeypatch.setenv("LAMFAST_K2B", k2b)
+    cases = [P.cube_problem(p, 3, 1, [0.0, 0.9, 0.3, 1.2][:p + 1], geometry="skewed") for p in (1, 2, 3, 4)]
+    cases.append(P.LaminateProblem(
+        degree_u=2, degree_v=3, degree_t=2, knots_u=P.uniform_knots(2, 4),
+        knots_v=P.uniform_knots(3, 3), knots_t=P.c0_knots(2, 3),
+        interfaces=P.equal_interfaces(3),
+        layers=[(P.baseline_orthotropic(), 0.0), (P.isotropic(0.5, 0.3), 0.0),
+                (P.baseline_orthotropic(), 0.6)],
+        geometry_kind=1, geometry=(0, 0, 0, 1.2, 0.1, 0.05, -0.1, 0.9, -0.02, 1.0, 1.1, 0.08),
+        direction=(0.03, -0.02, 0.2)))
+    for prob in cases:
+        got = gpu.assemble_fast(prob)
+        assert_csr_match(got.astuple(), oracle.assemble(prob, "fast"), RTOL)

@@ -27,6 +27,14 @@ for k, v in (("LAMFAST_WS", "1"), ("LAMFAST_TEAM", "auto"), ("LAMFAST_CONTIG", "
     os.environ[k] = v
     out.append(lf.assemble_fast(c1).values.sum())
     del os.environ[k]
+# general in-plane operator forms (two-phase default, DMMA element kernel, coloured)
+skew3 = P.cube_problem(3, 3, 1, [0.0, 0.9, 0.3, 1.2], geometry="skewed")
+for v in ("mma", "coloured"):
+    os.environ["LAMFAST_K2B"] = v
+    out.append(lf.assemble_fast(skew).values.sum())
+    out.append(lf.assemble_fast(skew3).values.sum())
+    del os.environ["LAMFAST_K2B"]
+out.append(lf.assemble_fast(skew3).values.sum())
 # operator-level entry points (affine + general P, thickness Q, long-form combine)
 d = np.diag([1, 1, 1, 0.5, 0.5, 0.5]).astype(float)
 for prob in (c1, skew):
