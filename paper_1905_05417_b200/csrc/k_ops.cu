@@ -476,135 +476,6 @@ __global__ void __launch_bounds__(256) k_inplane_elem_mma(const DevTables d, int
     }
 }
 
-/// Shared-memory layout of the register-blocked element kernel (doubles).
-struct ElemGemmLayout {
-    int nl2, nq2, npad;
-    long long gh, w2, ctq, g3, h, total;
-    __host__ __device__ ElemGemmLayout(int pu, int pv, int nqu, int nqv) {
-        nl2 = (pu + 1) * (pv + 1);
-        nq2 = nqu * nqv;
-        npad = (nl2 + 1) & ~1;
-        gh = 0;
-        w2 = gh + (long long)nq2 * nl2 * 3;
-        ctq = (w2 + nq2 + 1) & ~1LL;
-        g3 = ctq + (long long)nq2 * 90;
-        h = g3 + (long long)nq2 * 3 * npad;
-        total = h + 2LL * (2 * nq2) * nl2 * 10; // two families of K = 2 nq2 at a time
-    }
-};
-
-/// K2b phase 1, register-blocked on the CUDA cores (default).  Per family f
-/// the element's P is the contraction
-///   P_f[(al, ab), be] = sum_{(q, y) in K_f} H_f[(q, y), al, ab] * g_y(be, q),
-///   H_f[(q, y), al, ab] = sum_{x in X_f} Ct_q[xy][ab] g_x(al, q)
-/// (P11: x, y in {0,1}; P12: x in {0,1}, y = 2; P21: x = 2, y in {0,1}; P22:
-/// x = y = 2), so the sum over x is paid once per (q, y, al) in the staged H_f
-/// instead of once per pair.  Two families at a time ({P11, P21}: K = 2 nq2,
-/// then {P12, P22}: K = nq2); one thread per (family, al, pair of be) keeps
-/// 18 accumulators and reads per k five 16-byte H words (broadcast across the
-/// be pairs) and one 16-byte g word.
-__global__ void __launch_bounds__(256) k_inplane_elem_gemm(const DevTables d, int t0) {
-    extern __shared__ double sm[];
-    const int e_index = blockIdx.x;
-    const int t = t0 + blockIdx.y;
-    if (t >= d.n_terms)
-        return;
-    const ElemGemmLayout L(d.pu, d.pv, d.nqu, d.nqv);
-    ElemInfo el;
-    el.eu = e_index % d.nspu;
-    el.ev = e_index / d.nspu;
-    el.fu = d.spu_first[el.eu];
-    el.fv = d.spv_first[el.ev];
-    el.nl2 = L.nl2;
-    el.nq2 = L.nq2;
-    el.hu = 0.5 * (d.spu_hi[el.eu] - d.spu_lo[el.eu]);
-    el.hv = 0.5 * (d.spv_hi[el.ev] - d.spv_lo[el.ev]);
-    double* gh = sm + L.gh;
-    double* w2 = sm + L.w2;
-    double* ctq = sm + L.ctq;
-    double* g3 = sm + L.g3;
-    double* H = sm + L.h;
-    element_tables(d, el, gh, w2);
-    __syncthreads();
-    pullback_tables(d, e_index, el.nq2, w2, d.term_table + (long long)t * 81, ctq);
-    const int nl2 = L.nl2, nq2 = L.nq2, npad = L.npad;
-    // g3[q][y][be] (be padded with zeros to an even count)
-    for (int idx = threadIdx.x; idx < nq2 * 3 * npad; idx += blockDim.x) {
-        const int be = idx % npad, qy = idx / npad;
-        const int q = qy / 3, y = qy - 3 * q;
-        g3[idx] = be < nl2 ? gh[(q * nl2 + be) * 3 + y] : 0.0;
-    }
-    const int nel = d.nspu * d.nspv;
-    const long long per_el = 36LL * nl2 * nl2;
-    double* pe = d.Pe + ((long long)blockIdx.y * nel + e_index) * per_el;
-    const int nbg = npad >> 1;
-    for (int phase = 0; phase < 2; ++phase) {
-        // phase 0: f = 0 (P11, x in {0,1}) and f = 2 (P21, x = 2), y in {0,1};
-        // phase 1: f = 1 (P12, x in {0,1}) and f = 3 (P22, x = 2), y = 2
-        const int ny = phase == 0 ? 2 : 1, y0 = phase == 0 ? 0 : 2;
-        const int K = nq2 * ny;
-        __syncthreads(); // ctq / g3 ready, previous phase's H consumed
-        for (int idx = threadIdx.x; idx < 2 * K * nl2; idx += blockDim.x) {
-            const int s = idx / (K * nl2), rem = idx - s * (K * nl2);
-            const int k = rem / nl2, al = rem - k * nl2;
-            const int q = ny == 2 ? k >> 1 : k, y = y0 + (ny == 2 ? (k & 1) : 0);
-            const double* g = gh + (q * nl2 + al) * 3;
-            const double* c = ctq + q * 90;
-            double* h = H + ((long long)s * K * nl2 + k * nl2 + al) * 10;
-            if (s == 0) { // x in {0, 1}
-                const double ga = g[0], gb = g[1];
-#pragma unroll
-                for (int ab = 0; ab < 9; ++ab)
-                    h[ab] = c[y * 10 + ab] * ga + c[(3 + y) * 10 + ab] * gb;
-            } else {      // x = 2
-                const double gc = g[2];
-#pragma unroll
-                for (int ab = 0; ab < 9; ++ab)
-                    h[ab] = c[(6 + y) * 10 + ab] * gc;
-            }
-            h[9] = 0.0;
-        }
-        __syncthreads();
-        for (int idx = threadIdx.x; idx < 2 * nl2 * nbg; idx += blockDim.x) {
-            const int s = idx / (nl2 * nbg), rem = idx - s * (nl2 * nbg);
-            const int al = rem / nbg, bg = rem - al * nbg;
-            const int f = phase == 0 ? (s == 0 ? 0 : 2) : (s == 0 ? 1 : 3);
-            double acc[9][2];
-#pragma unroll
-            for (int ab = 0; ab < 9; ++ab)
-                acc[ab][0] = acc[ab][1] = 0.0;
-            const double2* hp = reinterpret_cast<const double2*>(H + ((long long)s * K * nl2 + al) * 10);
-            for (int k = 0; k < K; ++k) {
-                const int q = ny == 2 ? k >> 1 : k, y = y0 + (ny == 2 ? (k & 1) : 0);
-                const double2 gg = *reinterpret_cast<const double2*>(g3 + (q * 3 + y) * npad + 2 * bg);
-                const double2* hk = hp + (long long)k * nl2 * 5;
-#pragma unroll
-                for (int w = 0; w < 5; ++w) {
-                    const double2 hv = hk[w];
-                    acc[2 * w][0] = fma(hv.x, gg.x, acc[2 * w][0]);
-                    acc[2 * w][1] = fma(hv.x, gg.y, acc[2 * w][1]);
-                    if (w < 4) {
-                        acc[2 * w + 1][0] = fma(hv.y, gg.x, acc[2 * w + 1][0]);
-                        acc[2 * w + 1][1] = fma(hv.y, gg.y, acc[2 * w + 1][1]);
-                    }
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const int be = 2 * bg + j;
-                if (be >= nl2)
-                    continue;
-                LF_CHECK(pe_local(f, al, 2, be, 2, nl2) < per_el);
-#pragma unroll
-                for (int a = 0; a < 3; ++a)
-#pragma unroll
-                    for (int b = 0; b < 3; ++b)
-                        pe[pe_local(f, al, a, be, b, nl2)] = acc[3 * a + b][j];
-            }
-        }
-    }
-}
-
 /// First span index s with first[s] >= lo (first[] strictly increasing).
 __device__ __forceinline__ int span_lower(const int* first, int nsp, int lo) {
     int a = 0, b = nsp;
@@ -1057,22 +928,15 @@ int launch_inplane_general(const DevTables& d, cudaStream_t stream) {
         // DMMA element kernel opt-in (LAMFAST_K2B=mma): measured no faster than
         // the scalar one at p <= 3 and slower at p = 2 (profiles/r1_k2b.txt)
         const bool mma = smem_mma <= 200 * 1024 && k2b && std::string(k2b) == "mma";
-        const ElemGemmLayout LG(d.pu, d.pv, d.nqu, d.nqv);
-        const size_t smem_gemm = sizeof(double) * (size_t)LG.total;
-        const bool gemm = !mma && smem_gemm <= 110 * 1024 && !(k2b && std::string(k2b) == "scalar");
-        if (gemm && smem_gemm > 48 * 1024)
-            cudaFuncSetAttribute(k_inplane_elem_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_gemm);
         if (mma && smem_mma > 48 * 1024)
             cudaFuncSetAttribute(k_inplane_elem_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mma);
-        if (!mma && !gemm && smem > 48 * 1024)
+        if (!mma && smem > 48 * 1024)
             cudaFuncSetAttribute(k_inplane_elem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         const unsigned nel = (unsigned)(d.nspu * d.nspv);
         for (int t0 = 0; t0 < d.n_terms; t0 += d.pe_terms) {
             const int tb = std::min(d.pe_terms, d.n_terms - t0);
             if (mma)
                 k_inplane_elem_mma<<<dim3(nel, (unsigned)tb), 256, smem_mma, stream>>>(d, t0);
-            else if (gemm)
-                k_inplane_elem_gemm<<<dim3(nel, (unsigned)tb), 256, smem_gemm, stream>>>(d, t0);
             else
                 k_inplane_elem<<<dim3(nel, (unsigned)tb), threads, smem, stream>>>(d, t0);
             const dim3 grid((unsigned)((d.E + kBlock - 1) / kBlock), (unsigned)tb);

@@ -471,7 +471,7 @@ def test_concurrent_calls_are_reentrant(gpu):
             assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("k2b", ["default", "scalar", "mma", "coloured"])
+@pytest.mark.parametrize("k2b", ["default", "mma", "coloured"])
 def test_general_inplane_forms_match_oracle(gpu, oracle, monkeypatch, k2b):
     """Non-affine maps take the general in-plane path (K2b): the two-phase
     default (element-local P + gather), its DMMA element kernel and the

@@ -1,8 +1,7 @@
-# A/B of the general-geometry in-plane operators (K2b), all two-phase except the last:
-# register-blocked element kernel (default), scalar element kernel, DMMA element kernel,
-# coloured in-place form.
+# A/B of the general-geometry in-plane operators (K2b): two-phase with the scalar element
+# kernel (default), two-phase with the DMMA element kernel, coloured in-place form.
 for c in C3 C4 C2; do
-  for v in default scalar mma coloured; do
+  for v in default mma coloured; do
     echo -n "$v "; LAMFAST_K2B=$v python tools/run_steps.py --config $c --geometry bilinear --steps 10
   done
 done

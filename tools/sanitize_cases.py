@@ -29,7 +29,7 @@ for k, v in (("LAMFAST_WS", "1"), ("LAMFAST_TEAM", "auto"), ("LAMFAST_CONTIG", "
     del os.environ[k]
 # general in-plane operator forms (two-phase default, DMMA element kernel, coloured)
 skew3 = P.cube_problem(3, 3, 1, [0.0, 0.9, 0.3, 1.2], geometry="skewed")
-for v in ("scalar", "mma", "coloured"):
+for v in ("mma", "coloured"):
     os.environ["LAMFAST_K2B"] = v
     out.append(lf.assemble_fast(skew).values.sum())
     out.append(lf.assemble_fast(skew3).values.sum())
