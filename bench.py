@@ -497,12 +497,23 @@ def measure_e2e_slab(args, prob, device, rank, world, bounds, total_nnz):
     probe = lf.Plan(prob, "fast", device, bounds["t_begin"], bounds["t_end"])
     rows, nnz = probe.rows, probe.nnz
     probe.close()
-    h_rp = torch.empty(rows + 1, dtype=torch.int64, pin_memory=True)
-    h_cols = torch.empty(nnz, dtype=torch.int32, pin_memory=True)
-    h_vals = torch.empty(nnz, dtype=torch.float64, pin_memory=True)
-    d_rp = torch.empty(rows + 1, dtype=torch.int64, device="cuda")
-    d_cols = torch.empty(nnz, dtype=torch.int32, device="cuda")
-    d_vals = torch.empty(nnz, dtype=torch.float64, device="cuda")
+    # every rank must get its buffers before any enters a collective
+    err = ""
+    try:
+        h_rp = torch.empty(rows + 1, dtype=torch.int64, pin_memory=True)
+        h_cols = torch.empty(nnz, dtype=torch.int32, pin_memory=True)
+        h_vals = torch.empty(nnz, dtype=torch.float64, pin_memory=True)
+        d_rp = torch.empty(rows + 1, dtype=torch.int64, device="cuda")
+        d_cols = torch.empty(nnz, dtype=torch.int32, device="cuda")
+        d_vals = torch.empty(nnz, dtype=torch.float64, device="cuda")
+    except Exception as exc:
+        err = f"rank {rank}: {type(exc).__name__}: {exc}"[:300]
+    ok = torch.tensor([0.0 if err else 1.0], dtype=torch.float64)
+    if args.dist_backend == "nccl":
+        ok = ok.cuda()
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if float(ok[0]) < 1.0:
+        return {"value": None, "unit": "nnz/s", "error": err or "buffer allocation failed on another rank"}
 
     def once():
         plan = lf.Plan(prob, "fast", device, bounds["t_begin"], bounds["t_end"])
