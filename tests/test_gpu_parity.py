@@ -491,3 +491,44 @@ def test_general_inplane_forms_match_oracle(gpu, oracle, monkeypatch, k2b):
     for prob in cases:
         got = gpu.assemble_fast(prob)
         assert_csr_match(got.astuple(), oracle.assemble(prob, "fast"), RTOL)
+
+
+@pytest.mark.parametrize("p", [5, 6])
+def test_maximum_supported_degrees_match_oracle(gpu, oracle, p):
+    """The device tables are sized for degree <= 6 (kMaxP; degree 7 maps to
+    LF_ERR_UNSUPPORTED, test_host.py): the largest degrees, in-plane and
+    through the thickness, on flat and skewed maps, fast and standard."""
+    for geom in ("flat", "skewed"):
+        prob = P.cube_problem(p, 1, 1, [0.0, 0.7], geometry=geom)
+        for backend in ("fast", "standard"):
+            got = gpu.assemble_with(backend, prob)
+            assert_csr_match(got.astuple(), oracle.assemble(prob, backend), RTOL)
+
+
+def test_empty_and_single_row_slabs(gpu, oracle):
+    """Degenerate slab plans: an empty thickness range has no rows and no
+    values (row_ptr = [0]); a single thickness function's slab equals the
+    oracle's rows; assembling an empty slab is a no-op."""
+    import torch
+    prob = P.baseline_config("C1")
+    plan = gpu.Plan(prob, "fast", 0, 2, 2)
+    assert plan.rows == 0 and plan.nnz == 0
+    rp = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    cols = torch.empty(1, dtype=torch.int32, device="cuda")
+    vals = torch.full((1,), 7.0, dtype=torch.float64, device="cuda")
+    plan.build_pattern(rp.data_ptr(), cols.data_ptr())
+    plan.assemble(vals.data_ptr())
+    plan.synchronize()
+    assert int(rp[0]) == 0 and float(vals[0]) == 7.0
+    plan.close()
+    for t in (0, prob.n_t - 1):
+        plan = gpu.Plan(prob, "fast", 0, t, t + 1)
+        rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
+        cols = torch.empty(plan.nnz, dtype=torch.int32, device="cuda")
+        vals = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
+        plan.build_pattern(rp.data_ptr(), cols.data_ptr())
+        plan.assemble(vals.data_ptr())
+        plan.synchronize()
+        assert_csr_match((rp.cpu().numpy(), cols.cpu().numpy(), vals.cpu().numpy()),
+                         oracle.assemble(prob, "fast", t, t + 1), RTOL)
+        plan.close()
