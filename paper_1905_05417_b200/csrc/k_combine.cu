@@ -206,15 +206,16 @@ int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t st
     }
     const int t_chunk_req = t_chunk;
     if (t_chunk <= 0) {
-        // 64 thickness rows per block amortise the per-block prologue (P in
+        // 48 thickness rows per block amortise the per-block prologue (P in
         // registers, entry decode, staging); shorter chunks (down to 32) only
         // while the grid is under ~4 waves of 2 resident blocks on 148 SMs.
-        // Measured sweep: profiles/r1_tchunk_sweep.txt.
+        // Measured sweeps: profiles/r1_tchunk_sweep.txt (k-outer rows: C4 48
+        // rows 2.488 ms vs 64 rows 2.520 ms; C3 48 rows already the balanced choice).
         const long long blocks_x = (nblk + 1) / 2; // two entries per thread for <= 4 terms
         // general geometry loads P from HBM once per block: whole-slab chunks
         // (measured C3 bilinear 1.47 -> 1.38 ms); affine P is recomputed, so
         // shorter chunks balance better (profiles/r1_tchunk_sweep.txt)
-        t_chunk = d.affine ? std::min(nt, 64) : nt;
+        t_chunk = d.affine ? std::min(nt, 48) : nt;
         while (!d.affine && t_chunk > 64 && blocks_x * ((nt + t_chunk - 1) / t_chunk) < 148LL * 2 * 4)
             t_chunk = (t_chunk + 1) / 2;
         while (t_chunk > 32 && blocks_x * ((nt + t_chunk - 1) / t_chunk) < 148LL * 2 * 4)
