@@ -781,12 +781,31 @@ int lf_assemble(const lf_problem* p, int backend, int device, int64_t* row_ptr, 
         DeviceBuffer drp(sizeof(int64_t) * (rows + 1), plan.stream);
         DeviceBuffer dcols(sizeof(int32_t) * nnz, plan.stream);
         DeviceBuffer dvals(sizeof(double) * nnz, plan.stream);
+        // the pattern and its read-back run on a side stream, so the values are
+        // computed while the row offsets and columns cross PCIe
+        struct Side {
+            cudaStream_t s = nullptr;
+            cudaEvent_t e = nullptr;
+            ~Side() {
+                if (s) {
+                    cudaStreamSynchronize(s);
+                    cudaStreamDestroy(s);
+                }
+                if (e)
+                    cudaEventDestroy(e);
+            }
+        } side;
+        CK(cudaStreamCreateWithFlags(&side.s, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&side.e, cudaEventDisableTiming));
+        CK(cudaEventRecord(side.e, plan.stream)); // buffers allocated (stream-ordered)
+        CK(cudaStreamWaitEvent(side.s, side.e, 0));
         CK(static_cast<cudaError_t>(lfb::launch_pattern(plan.d, static_cast<long long*>(drp.p),
-                                                        static_cast<int*>(dcols.p), plan.stream)));
+                                                        static_cast<int*>(dcols.p), side.s)));
+        copy_d2h(row_ptr, drp.p, sizeof(int64_t) * (rows + 1), side.s);
+        copy_d2h(cols, dcols.p, sizeof(int32_t) * nnz, side.s);
         plan_launch(&plan, static_cast<double*>(dvals.p));
-        copy_d2h(row_ptr, drp.p, sizeof(int64_t) * (rows + 1), plan.stream);
-        copy_d2h(cols, dcols.p, sizeof(int32_t) * nnz, plan.stream);
         copy_d2h(values, dvals.p, sizeof(double) * nnz, plan.stream);
+        CK(cudaStreamSynchronize(side.s));
         CK(cudaStreamSynchronize(plan.stream));
         CK(cudaGetLastError());
         if (stats) {
