@@ -532,3 +532,34 @@ def test_empty_and_single_row_slabs(gpu, oracle):
         assert_csr_match((rp.cpu().numpy(), cols.cpu().numpy(), vals.cpu().numpy()),
                          oracle.assemble(prob, "fast", t, t + 1), RTOL)
         plan.close()
+
+
+@pytest.mark.parametrize("p", [1, 3])
+def test_uniform_stretch_stores_the_axial_stiffness(gpu, p):
+    """test_assembly.cpp:156-174 on the device: u(x) = x e_1 on a flat box of
+    isotropic material (E = 2.3, nu = 0.28) is a uniform stretch, so
+    u^T K u = (lambda + 2 mu) * volume for every backend.  p = 1 is the
+    reference's unit cube (coefficients = node x-coordinates); p = 3 uses
+    the Greville abscissae (linear fields are reproduced exactly) on a
+    2x2-element, 3-ply box of 1.5 x 0.8 x 0.4."""
+    e, nu = 2.3, 0.28
+    lam = e * nu / ((1 + nu) * (1 - 2 * nu))
+    mu = e / (2 * (1 + nu))
+    mat = P.isotropic(e, nu)
+    if p == 1:
+        prob = P.cube_problem(1, 1, 1, [(mat, 0.0)], thickness=1.0)
+        lx, vol = 1.0, 1.0
+    else:
+        lx, ly, h = 1.5, 0.8, 0.4
+        prob = P.cube_problem(3, 2, 1, [(mat, 0.0), (mat, 0.7), (mat, -0.3)], lx=lx, ly=ly, thickness=h)
+        vol = lx * ly * h
+    ku = prob.knots_u
+    greville = np.array([ku[i + 1:i + 1 + p].mean() for i in range(prob.n_u)])
+    u = np.zeros(prob.dim)
+    for f in range(prob.n_u * prob.n_v * prob.n_t):
+        u[3 * f] = lx * greville[f % prob.n_u]
+    for backend in ("fast", "standard", "voigt_free"):
+        k = gpu.assemble_with(backend, prob)
+        rows = np.repeat(np.arange(prob.dim), np.diff(k.row_ptr))
+        ku_vec = np.bincount(rows, weights=k.values * u[k.cols], minlength=prob.dim)
+        assert u @ ku_vec == pytest.approx((lam + 2 * mu) * vol, rel=1e-13)
