@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--cpu-sample-plies", type=int, default=0)
     ap.add_argument("--no-standard", action="store_true",
                     help="skip the standard-assembly (cross-check path) side measurement")
+    ap.add_argument("--verify-gather", action="store_true",
+                    help="N>1 over NCCL: also gather the full CSR to rank 0 when it fits and check it there")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: N x the config's plies, one slab per GPU; strong: the config split N ways")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -325,6 +327,22 @@ def main():
         tot = D.combine_summaries(parts)
         verify = {"fro_norm": tot["fro_sq"] ** 0.5, "nnz_gathered": int(tot["nnz"]),
                   "rows_gathered": int(tot["rows"]), "pattern_hash": tot["pattern_hash"]}
+        # full-slab gather to rank 0 over NCCL where the whole K fits there
+        fits = torch.tensor([1.0 if (sz["nnz"] * 12 + sz["dim"] * 8) * 2 <= 0.8 * torch.cuda.mem_get_info()[0]
+                             else 0.0], dtype=torch.float64, device="cuda")
+        if args.dist_backend == "nccl" and args.verify_gather:
+            dist.all_reduce(fits, op=dist.ReduceOp.MIN)
+            if float(fits[0]) > 0:
+                full_csr = D.gather_csr(rp, cols, vals[:plans[0].nnz], dst=0)
+                if rank == 0:
+                    g_rp, g_cols, g_vals = full_csr
+                    st = lf.device_csr_stats(sz["dim"], g_rp.data_ptr(), g_cols.data_ptr(), g_vals.data_ptr(),
+                                             stream.cuda_stream)
+                    verify["full_gather"] = {"fro_norm": st["fro_sq"] ** 0.5,
+                                             "symmetry_rel": (st["sym_sq"] / st["fro_sq"]) ** 0.5,
+                                             "rows": int(g_rp.numel() - 1), "nnz": int(g_cols.numel())}
+                del full_csr
+                torch.cuda.empty_cache()
 
     hbm, peak_src = peaks()
     achieved = k_bytes / (k_avg_ms / 1e3) / 1e9

@@ -107,3 +107,53 @@ def combine_summaries(parts) -> Dict[str, float]:
             tot[k] = max(tot[k], float(p[i])) if k == "max_abs" else tot[k] + float(p[i])
     tot["pattern_hash"] = int(tot["pattern_hash"]) % HASH_P
     return tot
+
+
+def gather_csr(row_ptr, cols, values, dst: int = 0, group=None):
+    """Full-slab gather for verification (only where the whole
+    K fits one device -- C1..C4, up to 23 GB): every rank sends its slab CSR
+    (row offsets rebased to 0, global columns) to rank `dst` with
+    point-to-point send/recv (NCCL over NVLink on GPUs, gloo on CPU); `dst`
+    returns the whole matrix (row_ptr, cols, values) in rank order, the
+    others None.  Never on the timed path."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    rp = torch.as_tensor(row_ptr)
+    c = torch.as_tensor(cols)
+    v = torch.as_tensor(values)
+    nnz = int(rp[-1] - rp[0])
+    dev = c.device
+    nccl = dist.get_backend(group) == "nccl"
+    comm_dev = torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
+    sizes = torch.tensor([len(rp) - 1, nnz], dtype=torch.int64, device=comm_dev)
+    all_sizes = [torch.empty_like(sizes) for _ in range(world)]
+    dist.all_gather(all_sizes, sizes, group=group)
+    all_sizes = [(int(s[0]), int(s[1])) for s in all_sizes]
+    rp_local = (rp[:-1] - rp[0]).to(comm_dev)
+    c_local = c[:nnz].to(comm_dev)
+    v_local = v[:nnz].to(comm_dev)
+    if rank != dst:
+        for t in (rp_local, c_local, v_local):
+            dist.send(t.contiguous(), dst, group=group)
+        return None
+    parts = []
+    for r in range(world):
+        rows_r, nnz_r = all_sizes[r]
+        if r == dst:
+            parts.append((rp_local, c_local, v_local))
+            continue
+        bufs = (torch.empty(rows_r, dtype=rp_local.dtype, device=comm_dev),
+                torch.empty(nnz_r, dtype=c_local.dtype, device=comm_dev),
+                torch.empty(nnz_r, dtype=v_local.dtype, device=comm_dev))
+        for t in bufs:
+            dist.recv(t, r, group=group)
+        parts.append(bufs)
+    offs, rps = 0, []
+    for (prp, pc, _), (_, nnz_r) in zip(parts, all_sizes):
+        rps.append(prp + offs)
+        offs += nnz_r
+    rps.append(torch.tensor([offs], dtype=rp_local.dtype, device=comm_dev))
+    return (torch.cat(rps).to(dev), torch.cat([p[1] for p in parts]).to(dev),
+            torch.cat([p[2] for p in parts]).to(dev))

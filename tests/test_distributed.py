@@ -37,8 +37,11 @@ def _worker(rank, world, port, config, q):
     s = D.slab_summary(torch.from_numpy(rp), torch.from_numpy(cols), torch.from_numpy(vals),
                        b["row_begin"], b["nnz_begin"])
     parts = D.gather_summaries(s)
+    full = D.gather_csr(torch.from_numpy(rp), torch.from_numpy(cols), torch.from_numpy(vals), dst=0)
     if rank == 0:
-        q.put(D.combine_summaries(parts))
+        q.put((D.combine_summaries(parts), tuple(t.numpy() for t in full)))
+    else:
+        assert full is None
     dist.barrier()
     dist.destroy_process_group()
 
@@ -53,7 +56,7 @@ def test_two_rank_slabs_reproduce_full_matrix(config, oracle):
     procs = [ctx.Process(target=_worker, args=(r, 2, port, config, q)) for r in range(2)]
     for p in procs:
         p.start()
-    got = q.get(timeout=600)
+    got, gathered = q.get(timeout=600)
     for p in procs:
         p.join(timeout=600)
         assert p.exitcode == 0
@@ -67,6 +70,9 @@ def test_two_rank_slabs_reproduce_full_matrix(config, oracle):
     assert got["checksum"] == pytest.approx(full["checksum"], rel=1e-12)
     assert got["max_abs"] == full["max_abs"]
     assert got["pattern_hash"] == full["pattern_hash"]
+    # the full-slab gather reassembles the single-rank matrix exactly
+    assert np.array_equal(gathered[0], rp) and np.array_equal(gathered[1], cols)
+    assert np.array_equal(gathered[2], vals)
 
 
 def test_pattern_hash_is_additive_and_sensitive(oracle):
