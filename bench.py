@@ -510,10 +510,10 @@ def measure_e2e(args, prob, device, total_nnz):
 
 
 def measure_e2e_slab(args, prob, device, rank, world, bounds, total_nnz):
-    """Per-rank e2e of the slab path: every step creates the rank's plan
-    (host setup + H2D of the problem tables), builds the slab pattern,
-    assembles the values and reads the slab CSR back into pinned host
-    buffers; max over ranks."""
+    """Per-rank e2e of the slab path through the C-ABI one-shot call
+    lf_assemble_slab (setup + table H2D, pattern, values, D2H of the slab
+    CSR into pinned host buffers, the pattern read back while the values are
+    computed); max over ranks."""
     import torch
     import torch.distributed as dist
     import paper_1905_05417_b200 as lf
@@ -523,12 +523,9 @@ def measure_e2e_slab(args, prob, device, rank, world, bounds, total_nnz):
     # every rank must get its buffers before any enters a collective
     err = ""
     try:
-        h_rp = torch.empty(rows + 1, dtype=torch.int64, pin_memory=True)
-        h_cols = torch.empty(nnz, dtype=torch.int32, pin_memory=True)
-        h_vals = torch.empty(nnz, dtype=torch.float64, pin_memory=True)
-        d_rp = torch.empty(rows + 1, dtype=torch.int64, device="cuda")
-        d_cols = torch.empty(nnz, dtype=torch.int32, device="cuda")
-        d_vals = torch.empty(nnz, dtype=torch.float64, device="cuda")
+        out = (torch.empty(rows + 1, dtype=torch.int64, pin_memory=True),
+               torch.empty(nnz, dtype=torch.int32, pin_memory=True),
+               torch.empty(nnz, dtype=torch.float64, pin_memory=True))
     except Exception as exc:
         err = f"rank {rank}: {type(exc).__name__}: {exc}"[:300]
     ok = torch.tensor([0.0 if err else 1.0], dtype=torch.float64)
@@ -539,15 +536,7 @@ def measure_e2e_slab(args, prob, device, rank, world, bounds, total_nnz):
         return {"value": None, "unit": "nnz/s", "error": err or "buffer allocation failed on another rank"}
 
     def once():
-        plan = lf.Plan(prob, "fast", device, bounds["t_begin"], bounds["t_end"])
-        plan.build_pattern(d_rp.data_ptr(), d_cols.data_ptr())
-        plan.assemble(d_vals.data_ptr())
-        plan.synchronize()
-        h_rp.copy_(d_rp)
-        h_cols.copy_(d_cols)
-        h_vals.copy_(d_vals)
-        torch.cuda.synchronize()
-        plan.close()
+        lf.assemble_slab(prob, bounds["t_begin"], bounds["t_end"], "fast", device, out=out)
 
     once()
     dist.barrier()
@@ -567,7 +556,7 @@ def measure_e2e_slab(args, prob, device, rank, world, bounds, total_nnz):
     dist.all_reduce(d2h)
     return {"value": total_nnz / sec, "unit": "nnz/s", "h2d_bytes_per_step": int(h2d) * world,
             "d2h_bytes_per_step": int(d2h[0]), "ms_per_step": sec * 1e3, "steps": n,
-            "call": "per rank: Plan (setup + table H2D) + slab pattern + values + D2H of the slab CSR"}
+            "call": "per rank: lf_assemble_slab (setup + table H2D, pattern, values, slab CSR D2H)"}
 
 
 if __name__ == "__main__":

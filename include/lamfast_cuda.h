@@ -199,6 +199,13 @@ int lf_plan_synchronize(lf_plan* plan);
  * PCIe speed; pageable memory is staged. */
 int lf_assemble(const lf_problem* p, int backend, int device, int64_t* row_ptr, int32_t* cols,
                 double* values, lf_stats* stats);
+/* The row slab of thickness functions [t_begin, t_end) (lf_slab_bounds) of
+ * the same matrix, one-shot into host arrays of rows+1 / nnz / nnz entries
+ * (lf_plan_create + lf_plan_rows/nnz give the sizes): row offsets rebased to
+ * 0, global columns -- what one rank of a multi-GPU assembly returns.  No
+ * reference counterpart (the reference is single-process). */
+int lf_assemble_slab(const lf_problem* p, int backend, int device, int32_t t_begin, int32_t t_end,
+                     int64_t* row_ptr, int32_t* cols, double* values, lf_stats* stats);
 
 /* ---- operator-level entry points -------------------------------------- */
 /* InPlaneOperatorSet in the reference's banded layout (fast.cpp:13-32):

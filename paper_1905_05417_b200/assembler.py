@@ -90,6 +90,29 @@ def assemble_with(backend: str, prob: LaminateProblem, device: int = 0,
     return CSR(rp, cols[:nnz], vals[:nnz], st)
 
 
+def assemble_slab(prob: LaminateProblem, t_begin: int, t_end: int, backend: str = "fast", device: int = 0,
+                  out: Optional[Tuple] = None) -> CSR:
+    """One-shot assembly of the row slab of thickness functions [t_begin,
+    t_end) into host buffers (lf_assemble_slab): row offsets rebased to 0,
+    global columns -- one rank's part of a multi-GPU assembly.  ``out`` may
+    hold (row_ptr, cols, values) numpy arrays or pinned torch tensors."""
+    lib = abi.library()
+    c = prob.to_c()
+    rows = 3 * prob.n_s * (t_end - t_begin)
+    if out is None:
+        plan = Plan(prob, backend, device, t_begin, t_end) # exact slab sizes for any backend
+        nnz = plan.nnz
+        plan.close()
+        out = (np.empty(rows + 1, dtype=np.int64), np.empty(max(nnz, 1), dtype=np.int32),
+               np.empty(max(nnz, 1), dtype=np.float64))
+    ptrs = [a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data for a in out]
+    st = abi.Stats()
+    abi.check(lib.lf_assemble_slab(byref(c), abi.BACKENDS[backend], device, t_begin, t_end, *ptrs, byref(st)))
+    rp, cols, vals = out
+    nnz = int(rp[rows])
+    return CSR(rp[:rows + 1], cols[:nnz], vals[:nnz], st)
+
+
 def assemble_fast(prob: LaminateProblem, device: int = 0) -> CSR:
     return assemble_with("fast", prob, device)
 

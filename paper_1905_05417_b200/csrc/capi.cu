@@ -767,15 +767,19 @@ int lf_plan_synchronize(lf_plan* plan) {
     });
 }
 
-int lf_assemble(const lf_problem* p, int backend, int device, int64_t* row_ptr, int32_t* cols, double* values,
-                lf_stats* stats) {
+static int assemble_one_shot(const lf_problem* p, int backend, int device, int t0, int t1, int64_t* row_ptr,
+                             int32_t* cols, double* values, lf_stats* stats) {
     return guarded([&] {
         lf_plan plan;
-        plan_init(&plan, p, backend, device, nullptr, 0, -1);
+        plan_init(&plan, p, backend, device, nullptr, t0, t1);
         keep_pool_memory(device);
         const lfb::Setup& s = plan.setup;
-        if (s.nnz == 0)
-            raise(LF_ERR_LOGIC, "SparseMatrixBuilder: nothing accumulated");
+        if (s.nnz == 0) {
+            if (t0 == 0 && t1 < 0) // the whole matrix: SparseMatrixBuilder::finalize (sparse.cpp:15-18)
+                raise(LF_ERR_LOGIC, "SparseMatrixBuilder: nothing accumulated");
+            row_ptr[0] = 0; // an empty slab
+            return;
+        }
         const std::size_t rows = static_cast<std::size_t>(s.rows);
         const std::size_t nnz = static_cast<std::size_t>(s.nnz);
         DeviceBuffer drp(sizeof(int64_t) * (rows + 1), plan.stream);
@@ -814,6 +818,16 @@ int lf_assemble(const lf_problem* p, int backend, int device, int64_t* row_ptr, 
             stats->operator_builds += s.stats.operator_builds;
         }
     });
+}
+
+int lf_assemble(const lf_problem* p, int backend, int device, int64_t* row_ptr, int32_t* cols, double* values,
+                lf_stats* stats) {
+    return assemble_one_shot(p, backend, device, 0, -1, row_ptr, cols, values, stats);
+}
+
+int lf_assemble_slab(const lf_problem* p, int backend, int device, int32_t t_begin, int32_t t_end, int64_t* row_ptr,
+                     int32_t* cols, double* values, lf_stats* stats) {
+    return assemble_one_shot(p, backend, device, t_begin, t_end, row_ptr, cols, values, stats);
 }
 
 static int inplane_common(const lf_problem* p, const double table[81], int device, double* blocks, char* flags,

@@ -563,3 +563,28 @@ def test_uniform_stretch_stores_the_axial_stiffness(gpu, p):
         rows = np.repeat(np.arange(prob.dim), np.diff(k.row_ptr))
         ku_vec = np.bincount(rows, weights=k.values * u[k.cols], minlength=prob.dim)
         assert u @ ku_vec == pytest.approx((lam + 2 * mu) * vol, rel=1e-13)
+
+
+def test_one_shot_slabs_match_oracle(gpu, oracle):
+    """lf_assemble_slab (one rank's one-shot call, host buffers) returns the
+    oracle's rows for every part of a 3-way split, for fast and standard;
+    the parts concatenate to the whole matrix; an empty slab is row_ptr [0]."""
+    import torch
+    for backend in ("fast", "standard"):
+        prob = P.baseline_config("C2")
+        full = gpu.assemble_with(backend, prob)
+        vals = []
+        for part in range(3):
+            b = gpu.slab_bounds(prob, 3, part, backend)
+            got = gpu.assemble_slab(prob, b["t_begin"], b["t_end"], backend)
+            assert_csr_match(got.astuple(), oracle.assemble(prob, backend, b["t_begin"], b["t_end"]), RTOL)
+            vals.append(got.values)
+        cat = np.concatenate(vals)
+        if backend == "fast": # same arithmetic per value (test_slabs_are_bitwise_rows_of_the_full_matrix)
+            assert np.array_equal(cat, full.values)
+        else:
+            assert np.abs(cat - full.values).max() <= RTOL * np.abs(full.values).max()
+    pinned = (torch.empty(1, dtype=torch.int64, pin_memory=True), torch.empty(1, dtype=torch.int32, pin_memory=True),
+              torch.empty(1, dtype=torch.float64, pin_memory=True))
+    empty = gpu.assemble_slab(P.baseline_config("C1"), 3, 3, out=pinned)
+    assert int(empty.row_ptr[0]) == 0 and empty.nnz == 0

@@ -41,6 +41,11 @@ def test_compute_entry_points_fail_loudly_without_gpu():
     with pytest.raises(lf.LamfastError) as e:
         lf.assemble_fast(P.baseline_config("C1"))
     assert "no CUDA device" in str(e.value) and e.value.status == abi.LF_ERR_CUDA
+    import numpy as np
+    out = (np.empty(8, np.int64), np.empty(8, np.int32), np.empty(8))
+    with pytest.raises(lf.LamfastError) as e:
+        lf.assemble_slab(P.baseline_config("C1"), 0, 1, out=out)
+    assert e.value.status == abi.LF_ERR_CUDA
 
 
 def test_voigt_and_rotation_match_reference_known_answers(oracle):
