@@ -434,4 +434,27 @@ Backend backendFromName(const std::string& name);
 StiffnessMatrix assembleWith(Backend backend, const ProblemSetup& setup, const AssemblyOptions& options = {},
                              AssemblyStats* stats = nullptr);
 
+// Problem builders of the reference's benchmark header (bench.hpp:22-46): the
+// callers' side of the path.  The sweep harness itself (BenchConfig, runBench,
+// the JSON config parser) is not part of this edition; its CSV/JSON report
+// format is reproduced by paper_1905_05417_b200/report.py.
+enum class LayupFamily { CrossPly, QuadPly, Custom };
+std::string layupFamilyName(LayupFamily family);
+LayupFamily layupFamilyFromName(const std::string& name);
+/// Cross-ply alternates {0, 90} deg, quad-ply cycles {0, 45, -45, 90} deg;
+/// throws std::invalid_argument for the custom family or m < 1.
+std::vector<double> familyAngles(LayupFamily family, int m);
+
+struct PlateDimensions {
+    double lx = 1.0, ly = 1.0, thickness = 0.1;
+};
+
+/// Pagano's material: E1 = 25, E2 = E3 = 1, G12 = G13 = 0.2, G23 = 0.5, nu = 0.25.
+OrthotropicConstants paganoConstants();
+/// Equal Pagano layers at `angles`, an lx x ly plate extruded along
+/// (0, 0, thickness), uniform maximum-continuity knots of `degree` everywhere.
+ProblemSetup paganoSetup(const std::vector<double>& angles, int degree, int elements_x, int elements_y,
+                         int thickness_elements = 1, const PlateDimensions& plate = {});
+ProblemSetup paganoSetup(int m, LayupFamily family, int degree, int elements);
+
 } // namespace lamfast

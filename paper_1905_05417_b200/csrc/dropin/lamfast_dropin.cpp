@@ -913,4 +913,65 @@ StiffnessMatrix assembleWith(Backend backend, const ProblemSetup& setup, const A
     throw std::logic_error("assembleWith: unknown backend");
 }
 
+std::string layupFamilyName(LayupFamily family) {
+    switch (family) {
+    case LayupFamily::CrossPly: return "cross_ply_0_90";
+    case LayupFamily::QuadPly: return "quad_ply_0_p45_m45_90";
+    case LayupFamily::Custom: return "custom";
+    }
+    throw std::logic_error("layupFamilyName: unknown family");
+}
+
+LayupFamily layupFamilyFromName(const std::string& name) {
+    static const std::pair<const char*, LayupFamily> names[] = {
+        {"cross_ply_0_90", LayupFamily::CrossPly}, {"cross_ply", LayupFamily::CrossPly},
+        {"quad_ply_0_p45_m45_90", LayupFamily::QuadPly}, {"quad_ply", LayupFamily::QuadPly},
+        {"custom", LayupFamily::Custom}};
+    for (const auto& [n, f] : names)
+        if (name == n)
+            return f;
+    throw std::invalid_argument("unknown layup family '" + name + "'");
+}
+
+std::vector<double> familyAngles(LayupFamily family, int m) {
+    if (m < 1)
+        throw std::invalid_argument("familyAngles: need at least one layer");
+    if (family == LayupFamily::Custom)
+        throw std::invalid_argument("familyAngles: the custom family has no fixed angles");
+    constexpr double pi = 3.14159265358979323846;
+    const std::vector<double> cycle = family == LayupFamily::CrossPly
+                                          ? std::vector<double>{0.0, 0.5 * pi}
+                                          : std::vector<double>{0.0, 0.25 * pi, -0.25 * pi, 0.5 * pi};
+    std::vector<double> angles(static_cast<std::size_t>(m));
+    for (int l = 0; l < m; ++l)
+        angles[static_cast<std::size_t>(l)] = cycle[static_cast<std::size_t>(l) % cycle.size()];
+    return angles;
+}
+
+OrthotropicConstants paganoConstants() {
+    OrthotropicConstants c;
+    c.E1 = 25.0;
+    c.E2 = c.E3 = 1.0;
+    c.G12 = c.G13 = 0.2;
+    c.G23 = 0.5;
+    c.nu12 = c.nu13 = c.nu23 = 0.25;
+    return c;
+}
+
+ProblemSetup paganoSetup(const std::vector<double>& angles, int degree, int elements_x, int elements_y,
+                         int thickness_elements, const PlateDimensions& plate) {
+    std::vector<LayerSpec> layers;
+    for (const double a : angles)
+        layers.push_back(LayerSpec{paganoConstants(), a});
+    TensorProductSpace space(KnotVector::uniform(degree, elements_x), KnotVector::uniform(degree, elements_y),
+                             KnotVector::uniform(degree, thickness_elements));
+    ExtrudedGeometry geometry(std::make_shared<PlanarRectangle>(plate.lx, plate.ly),
+                              Eigen::Vector3d(0.0, 0.0, plate.thickness));
+    return ProblemSetup{std::move(space), std::move(geometry), Layup::equalLayers(layers)};
+}
+
+ProblemSetup paganoSetup(int m, LayupFamily family, int degree, int elements) {
+    return paganoSetup(familyAngles(family, m), degree, elements, elements);
+}
+
 } // namespace lamfast

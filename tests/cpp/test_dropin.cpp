@@ -151,6 +151,18 @@ static void hostOnly() {
     CHECK(mm.str().rfind("%%MatrixMarket", 0) == 0);
     CHECK(throws<std::logic_error>([] { SparseMatrixBuilder(3).finalize(); }));
     CHECK(backendFromName("voigt-free") == Backend::VoigtFree && backendName(Backend::Fast) == "fast");
+    // problem builders (bench.hpp:22-46)
+    const auto quad = familyAngles(LayupFamily::QuadPly, 5);
+    CHECK(quad.size() == 5 && quad[1] == 0.25 * 3.14159265358979323846 && quad[2] == -quad[1] && quad[4] == 0.0);
+    CHECK(familyAngles(LayupFamily::CrossPly, 3)[1] == 0.5 * 3.14159265358979323846);
+    CHECK(throws<std::invalid_argument>([] { familyAngles(LayupFamily::Custom, 2); }));
+    CHECK(throws<std::invalid_argument>([] { familyAngles(LayupFamily::CrossPly, 0); }));
+    CHECK(layupFamilyFromName(layupFamilyName(LayupFamily::QuadPly)) == LayupFamily::QuadPly &&
+          layupFamilyFromName("cross_ply") == LayupFamily::CrossPly);
+    CHECK(throws<std::invalid_argument>([] { layupFamilyFromName("angle_ply"); }));
+    CHECK(paganoConstants().E1 == 25.0 && paganoConstants().G23 == 0.5 && paganoConstants().G12 == 0.2);
+    const ProblemSetup ps = paganoSetup(4, LayupFamily::CrossPly, 2, 3);
+    CHECK(ps.space.numU() == 5 && ps.space.numV() == 5 && ps.layup.numDistinctConfigs() == 2);
 }
 
 static StiffnessMatrix hexOracle(double E, double nu) {
@@ -316,6 +328,11 @@ static void gpuCases() {
         }
         const double a = referenceBilinear(s, v, u), b2 = v.dot(k.apply(u));
         CHECK(std::abs(a - b2) <= 1e-11 * std::abs(b2));
+    }
+    // a benchmark-family problem through the drop-in builders, fast vs standard
+    {
+        const ProblemSetup ps = paganoSetup(8, LayupFamily::QuadPly, 3, 2);
+        CHECK(frobeniusRelDiff(assembleFast(ps), assembleStandard(ps)) <= 1e-12);
     }
     // exceptions (test_assembly.cpp:256-262)
     {
