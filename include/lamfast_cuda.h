@@ -207,6 +207,11 @@ int lf_assemble(const lf_problem* p, int backend, int device, int64_t* row_ptr, 
 int lf_assemble_slab(const lf_problem* p, int backend, int device, int32_t t_begin, int32_t t_end,
                      int64_t* row_ptr, int32_t* cols, double* values, lf_stats* stats);
 
+/* v^T K u by full 3D quadrature without forming K (referenceBilinear,
+ * include/lamfast/assembly.hpp; assembly.cpp:247-318): host coefficient
+ * arrays of 3 * (number of functions) doubles, result in *out. */
+int lf_reference_bilinear(const lf_problem* p, const double* v, const double* u, int device, double* out);
+
 /* ---- operator-level entry points -------------------------------------- */
 /* InPlaneOperatorSet in the reference's banded layout (fast.cpp:13-32):
  * blocks[4][n_s][2p_v+1][2p_u+1][9] (3x3 row-major), flags[n_s][2p_v+1][2p_u+1]. */

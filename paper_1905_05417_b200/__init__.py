@@ -7,7 +7,7 @@ runs as hand-written sm_100a CUDA kernels behind a C ABI
 Python host layer over that ABI; see DESIGN.md.
 """
 from .abi import LamfastError, library
-from .assembler import (CSR, Plan, assemble_fast, assemble_slab, assemble_standard, assemble_voigt_free,
+from .assembler import (CSR, Plan, assemble_fast, assemble_slab, reference_bilinear, assemble_standard, assemble_voigt_free,
                         assemble_with, combine_operators, compute_inplane_operators,
                         compute_thickness_operators, device_csr_stats, pattern_size, slab_bounds)
 from .problem import (LaminateProblem, baseline_config, baseline_orthotropic, c0_knots,
@@ -15,6 +15,7 @@ from .problem import (LaminateProblem, baseline_config, baseline_orthotropic, c0
                       uniform_knots)
 
 __all__ = [
+    "reference_bilinear",
     "assemble_slab",
     "LamfastError", "library", "CSR", "Plan", "assemble_fast", "assemble_standard",
     "assemble_voigt_free", "assemble_with", "combine_operators", "compute_inplane_operators",

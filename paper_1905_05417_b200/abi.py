@@ -115,6 +115,7 @@ SIGNATURES = [
     ("lf_plan_synchronize", c_int, [c_void_p]),
     ("lf_assemble", c_int, [_P(Problem), c_int, c_int, c_void_p, c_void_p, c_void_p,
                             _P(Stats)]),
+    ("lf_reference_bilinear", c_int, [_P(Problem), _P(c_double), _P(c_double), c_int, _P(c_double)]),
     ("lf_assemble_slab", c_int, [_P(Problem), c_int, c_int, c_int32, c_int32, c_void_p, c_void_p,
                                  c_void_p, _P(Stats)]),
     ("lf_inplane_operators", c_int, [_P(Problem), _P(c_double), c_int, _P(c_double),

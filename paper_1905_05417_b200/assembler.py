@@ -113,6 +113,21 @@ def assemble_slab(prob: LaminateProblem, t_begin: int, t_end: int, backend: str 
     return CSR(rp[:rows + 1], cols[:nnz], vals[:nnz], st)
 
 
+def reference_bilinear(prob: LaminateProblem, v: np.ndarray, u: np.ndarray, device: int = 0) -> float:
+    """v^T K u by full 3D quadrature on the device without forming K
+    (referenceBilinear, assembly.cpp:247-318; lf_reference_bilinear)."""
+    lib = abi.library()
+    c = prob.to_c()
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    if v.size != prob.dim or u.size != prob.dim:
+        raise ValueError("referenceBilinear: coefficient length mismatch")
+    out = c_double()
+    abi.check(lib.lf_reference_bilinear(byref(c), v.ctypes.data_as(POINTER(c_double)),
+                                        u.ctypes.data_as(POINTER(c_double)), device, byref(out)))
+    return out.value
+
+
 def assemble_fast(prob: LaminateProblem, device: int = 0) -> CSR:
     return assemble_with("fast", prob, device)
 

@@ -830,6 +830,29 @@ int lf_assemble_slab(const lf_problem* p, int backend, int device, int32_t t_beg
     return assemble_one_shot(p, backend, device, t_begin, t_end, row_ptr, cols, values, stats);
 }
 
+int lf_reference_bilinear(const lf_problem* p, const double* v, const double* u, int device, double* out) {
+    return guarded([&] {
+        if (!p || !v || !u || !out)
+            raise(LF_ERR_INVALID_ARGUMENT, "referenceBilinear: null argument");
+        lf_plan plan;
+        plan_init(&plan, p, LF_BACKEND_STANDARD, device, nullptr, 0, -1);
+        const lfb::DevTables& d = plan.d;
+        const std::size_t n = 3 * static_cast<std::size_t>(plan.setup.n_s) * static_cast<std::size_t>(d.nt);
+        const std::size_t nblk = static_cast<std::size_t>(d.nspu) * d.nspv * d.nspt;
+        DeviceBuffer du(sizeof(double) * n, plan.stream), dv(sizeof(double) * n, plan.stream),
+            dpart(sizeof(double) * std::max<std::size_t>(1, nblk), plan.stream), dout(sizeof(double), plan.stream);
+        CK(cudaMemcpyAsync(du.p, u, sizeof(double) * n, cudaMemcpyHostToDevice, plan.stream));
+        CK(cudaMemcpyAsync(dv.p, v, sizeof(double) * n, cudaMemcpyHostToDevice, plan.stream));
+        CK(static_cast<cudaError_t>(lfb::launch_basis(d, false, plan.stream)));
+        CK(static_cast<cudaError_t>(lfb::launch_bilinear(d, static_cast<const double*>(du.p),
+                                                         static_cast<const double*>(dv.p),
+                                                         static_cast<double*>(dpart.p),
+                                                         static_cast<double*>(dout.p), plan.stream)));
+        CK(cudaMemcpyAsync(out, dout.p, sizeof(double), cudaMemcpyDeviceToHost, plan.stream));
+        CK(cudaStreamSynchronize(plan.stream));
+    });
+}
+
 static int inplane_common(const lf_problem* p, const double table[81], int device, double* blocks, char* flags,
                           lf_stats* stats) {
     return guarded([&] {

@@ -732,12 +732,21 @@ StiffnessMatrix assembleVoigtFree(const ProblemSetup& setup, const AssemblyOptio
 
 double referenceBilinear(const ProblemSetup& setup, const Eigen::VectorXd& v, const Eigen::VectorXd& u,
                          const AssemblyOptions& options) {
-    // v' K u with K from the device standard (full 3D quadrature) assembly.
+    // v' K u by full 3D quadrature on the device, without forming K (K8)
     const int n = 3 * setup.space.numFunctions();
     if (v.size() != n || u.size() != n)
         throw std::invalid_argument("referenceBilinear: coefficient length mismatch");
-    const StiffnessMatrix k = assembleStandard(setup, options);
-    return v.dot(k.apply(u));
+    if (setup.layup.numLayers() < 1)
+        throw std::invalid_argument("referenceBilinear: empty layup");
+    CProblem cp;
+    fillSpace(cp, setup.space);
+    fillGeometry(cp, setup.space, setup.geom, options);
+    fillLayup(cp, setup.layup);
+    fillOptions(cp, options);
+    const std::vector<double> hv(v.data(), v.data() + n), hu(u.data(), u.data() + n);
+    double out = 0.0;
+    ok(lf_reference_bilinear(&cp.p, hv.data(), hu.data(), device(), &out));
+    return out;
 }
 
 InPlaneOperatorSet computeInplaneOperators(const TensorProductSpace& space, const ExtrudedGeometry& geom,

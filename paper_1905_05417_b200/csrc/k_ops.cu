@@ -726,6 +726,137 @@ __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard(const DevTables d,
 }
 
 // ---------------------------------------------------------------------------
+// K8: matrix-free v^T K u by full 3D quadrature (referenceBilinear,
+// assembly.cpp:247-318): no matrix is formed.  One block per (element,
+// thickness span); the element's local coefficients of u and v sit in shared
+// memory, each thread takes quadrature points, forms the reference-space
+// gradients G(a, x) = sum_al c[al][a] dN_al/dx and adds
+// sum_{a,b,x,y} Gv(a,x) Ct_q[xy][ab] Gu(b,y) w3 (Ct_q = pulled-back C with
+// the in-plane weight and |det|: the same tables as K6).  Block partials go to
+// partial[block]; k_bilinear_final sums them in block order (deterministic).
+__global__ void __launch_bounds__(128) k_bilinear(const DevTables d, const double* __restrict__ u,
+                                                  const double* __restrict__ v, double* __restrict__ partial) {
+    extern __shared__ double sm[];
+    const long long bid = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    ElemInfo el;
+    el.eu = blockIdx.x;
+    el.ev = blockIdx.y;
+    const int ks = blockIdx.z;
+    el.fu = d.spu_first[el.eu];
+    el.fv = d.spv_first[el.ev];
+    el.nl2 = (d.pu + 1) * (d.pv + 1);
+    el.nq2 = d.nqu * d.nqv;
+    el.hu = 0.5 * (d.spu_hi[el.eu] - d.spu_lo[el.eu]);
+    el.hv = 0.5 * (d.spv_hi[el.ev] - d.spv_lo[el.ev]);
+    const int ft = d.spt_first[ks];
+    const int ntl = d.pt + 1;
+    const int nl3 = el.nl2 * ntl;
+    double* gh = sm;
+    double* w2 = gh + el.nq2 * el.nl2 * 3;
+    double* ctq = sm + ((el.nq2 * el.nl2 * 3 + el.nq2 + 1) & ~1); // nq2 * 90
+    double* tv = ctq + el.nq2 * 90;                                 // nqt * ntl values, then derivatives
+    double* td = tv + d.nqt * ntl;
+    double* w3 = td + d.nqt * ntl;
+    double* cu = w3 + d.nqt; // [nl3][3] local coefficients of u, then v
+    double* cv = cu + 3 * nl3;
+    double* red = cv + 3 * nl3; // [warps]
+    const int c0 = d.span_cell0[ks], c1 = d.span_cell0[ks + 1];
+    double acc = 0.0;
+    if (c0 < c1) {
+        element_tables(d, el, gh, w2);
+        for (int idx = threadIdx.x; idx < 3 * nl3; idx += blockDim.x) {
+            const int l = idx / 3, comp = idx - 3 * l;
+            const int at = l / el.nl2, as = l - at * el.nl2;
+            const int iu = el.fu + as % (d.pu + 1), iv = el.fv + as / (d.pu + 1);
+            const long long gi = (long long)(ft + at) * d.ns + (long long)iv * d.nu + iu;
+            cu[idx] = u[3 * gi + comp];
+            cv[idx] = v[3 * gi + comp];
+        }
+        const int e_index = el.ev * d.nspu + el.eu;
+        for (int c = c0; c < c1; ++c) {
+            __syncthreads();
+            const int cfg = d.layer_config[d.cell_layer[c]];
+            pullback_tables(d, e_index, el.nq2, w2, d.term_table + (long long)cfg * 81, ctq);
+            for (int idx = threadIdx.x; idx < d.nqt * ntl; idx += blockDim.x) {
+                const int q = idx / ntl, a = idx % ntl;
+                const long long h = (long long)c * d.nqt + q;
+                const int sh = ft - d.Bt_first[h]; // 0 unless a point rounds onto a knot
+                const int aa = a + sh;
+                const bool ok = aa >= 0 && aa <= d.pt;
+                tv[idx] = ok ? d.Bt_val[h * ntl + aa] : 0.0;
+                td[idx] = ok ? d.Bt_der[h * ntl + aa] : 0.0;
+            }
+            for (int q = threadIdx.x; q < d.nqt; q += blockDim.x)
+                w3[q] = d.cell_wts[(long long)c * d.nqt + q];
+            __syncthreads();
+            for (int ip = threadIdx.x; ip < el.nq2 * d.nqt; ip += blockDim.x) {
+                const int q2 = ip / d.nqt, q3 = ip - q2 * d.nqt;
+                double Gu[3][3] = {}, Gv[3][3] = {}; // [component][reference direction]
+                for (int l = 0; l < nl3; ++l) {
+                    const int at = l / el.nl2, as = l - at * el.nl2;
+                    const double* g = gh + (q2 * el.nl2 + as) * 3;
+                    const double T = tv[q3 * ntl + at], Td = td[q3 * ntl + at];
+                    const double gx[3] = {g[0] * T, g[1] * T, g[2] * Td}; // (du T, dv T, val T')
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        const double ua = cu[3 * l + a], va = cv[3 * l + a];
+#pragma unroll
+                        for (int x = 0; x < 3; ++x) {
+                            Gu[a][x] += ua * gx[x];
+                            Gv[a][x] += va * gx[x];
+                        }
+                    }
+                }
+                const double* C = ctq + q2 * 90;
+                double form = 0.0;
+#pragma unroll
+                for (int x = 0; x < 3; ++x)
+#pragma unroll
+                    for (int y = 0; y < 3; ++y)
+#pragma unroll
+                        for (int a = 0; a < 3; ++a)
+#pragma unroll
+                            for (int b = 0; b < 3; ++b)
+                                form += Gv[a][x] * C[(3 * x + y) * 10 + 3 * a + b] * Gu[b][y];
+                acc += form * w3[q3];
+            }
+        }
+    }
+    // block reduction in a fixed order
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0)
+        red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+            s += red[w];
+        partial[bid] = s;
+    }
+}
+
+__global__ void k_bilinear_final(const double* __restrict__ partial, long long n, double* __restrict__ out) {
+    __shared__ double red[32];
+    double s = 0.0;
+    for (long long i = threadIdx.x; i < n; i += blockDim.x)
+        s += partial[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0)
+        red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+            t += red[w];
+        *out = t;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K5: closed-form CSR pattern, slab-local row offsets.
 __global__ void k_pattern_rows(const DevTables d, long long* __restrict__ row_ptr, long long rows) {
     const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1005,6 +1136,19 @@ int launch_standard(const DevTables& d, double* values, long long nnz, cudaStrea
                 if (launches)
                     ++*launches;
             }
+    return (int)cudaGetLastError();
+}
+
+int launch_bilinear(const DevTables& d, const double* u, const double* v, double* partial, double* out,
+                    cudaStream_t stream) {
+    const int nl2 = (d.pu + 1) * (d.pv + 1), nq2 = d.nqu * d.nqv, ntl = d.pt + 1, nl3 = nl2 * ntl;
+    const size_t smem = sizeof(double) * ((size_t)nq2 * nl2 * 3 + nq2 + 1 + (size_t)nq2 * 90 +
+                                          2 * (size_t)d.nqt * ntl + d.nqt + 6 * (size_t)nl3 + 4 + 1);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_bilinear, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const dim3 grid(d.nspu, d.nspv, d.nspt);
+    k_bilinear<<<grid, 128, smem, stream>>>(d, u, v, partial);
+    k_bilinear_final<<<1, 1024, 0, stream>>>(partial, (long long)d.nspu * d.nspv * d.nspt, out);
     return (int)cudaGetLastError();
 }
 

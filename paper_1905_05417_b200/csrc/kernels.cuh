@@ -126,6 +126,11 @@ int launch_pattern(const DevTables& d, long long* row_ptr, int* cols, cudaStream
 int launch_standard(const DevTables& d, double* values, long long nnz, cudaStream_t stream,
                     int* launches);
 
+/// Matrix-free v^T K u (referenceBilinear, assembly.cpp:247-318); partial holds
+/// nspu * nspv * nspt doubles, *out (device) the result.
+int launch_bilinear(const DevTables& d, const double* u, const double* v, double* partial, double* out,
+                    cudaStream_t stream);
+
 // Verification (sparse.cpp:66-139)
 int launch_frobenius_sq(long long rows, const long long* rp, const double* v, double* out,
                         cudaStream_t stream);

@@ -46,6 +46,10 @@ def test_compute_entry_points_fail_loudly_without_gpu():
     with pytest.raises(lf.LamfastError) as e:
         lf.assemble_slab(P.baseline_config("C1"), 0, 1, out=out)
     assert e.value.status == abi.LF_ERR_CUDA
+    prob = P.baseline_config("C1")
+    with pytest.raises(lf.LamfastError) as e:
+        lf.reference_bilinear(prob, np.zeros(prob.dim), np.zeros(prob.dim))
+    assert e.value.status == abi.LF_ERR_CUDA
 
 
 def test_voigt_and_rotation_match_reference_known_answers(oracle):

@@ -35,6 +35,9 @@ for v in ("mma", "coloured"):
     out.append(lf.assemble_fast(skew3).values.sum())
     del os.environ["LAMFAST_K2B"]
 out.append(lf.assemble_fast(skew3).values.sum())
+# matrix-free bilinear form (K8)
+for prob in (c1, skew, mixed):
+    out.append(lf.reference_bilinear(prob, np.ones(prob.dim), np.linspace(0, 1, prob.dim)))
 # operator-level entry points (affine + general P, thickness Q, long-form combine)
 d = np.diag([1, 1, 1, 0.5, 0.5, 0.5]).astype(float)
 for prob in (c1, skew):
