@@ -152,7 +152,10 @@ void combine_one_ept(const DevTables& d, double* out, int pass, int t_chunk, int
                      unsigned nchunk, cudaStream_t s, bool accum) {
     // two entries per thread: explicit bounds (<= 128 registers, 2 blocks of
     // 256 per SM); one entry: the compiler's own choice (80-128 registers)
-    constexpr int BT = kBlock;
+#ifndef LF_COMBINE_BT
+#define LF_COMBINE_BT 256 // threads per block (A/B knob)
+#endif
+    constexpr int BT = EPT >= 2 ? LF_COMBINE_BT : kBlock;
 #ifndef LF_COMBINE_MINB
 #define LF_COMBINE_MINB 2
 #endif
