@@ -365,6 +365,25 @@ def main():
     for p in plans:
         p.close()
     torch.cuda.empty_cache()
+    # context for the write-only kernel: a plain write-only fill of a buffer of
+    # the same size on this GPU (torch fill_, best of 3, CUDA events)
+    try:
+        fbuf = torch.empty(int(k_bytes // 8), dtype=torch.float64, device="cuda")
+        fbuf.fill_(0.0)
+        best = 0.0
+        for _ in range(3):
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record()
+            fbuf.fill_(1.0)
+            f1.record()
+            torch.cuda.synchronize()
+            best = max(best, fbuf.numel() * 8 / (f0.elapsed_time(f1) / 1e3) / 1e9)
+        roofline["write_fill_gbs"] = best
+        roofline["frac_of_write_fill"] = achieved / best
+        del fbuf
+        torch.cuda.empty_cache()
+    except Exception:
+        pass
 
     e2e = None
     if args.no_e2e:
