@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C4")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-plies", type=int, default=0)
@@ -500,9 +500,12 @@ def measure_e2e(args, prob, device, total_nnz):
 
     once()  # warm-up (allocator pool, module load)
     n = max(1, args.e2e_steps)
+    per = []
     t0 = time.perf_counter()
     for _ in range(n):
+        t1 = time.perf_counter()
         once()
+        per.append(time.perf_counter() - t1)
     sec = (time.perf_counter() - t0) / n
     h2d = sum(a.nbytes for a in prob._keep if hasattr(a, "nbytes"))
     d2h = rp.numel() * 8 + total_nnz * 12
@@ -524,6 +527,7 @@ def measure_e2e(args, prob, device, total_nnz):
     return {"value": total_nnz / sec, "unit": "nnz/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": sec * 1e3, "steps": n,
             "call": "lf_assemble(LF_BACKEND_FAST) -> host CSR (row_ptr, cols, values)",
+            "ms_median": statistics.median(per) * 1e3,
             "d2h_gbs_measured": best, "d2h_probe": "plain pinned D2H of the same arrays, best of 2",
             "pcie_frac": (d2h / sec / 1e9) / best if best else None}
 

@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <string>
 #include <utility>
@@ -545,15 +546,85 @@ void copy_d2h(void* dst, const void* src, std::size_t bytes, cudaStream_t s) {
         CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
 }
 
+/// Large one-shot buffers (the CSR arrays of lf_assemble: 23 GB for C4) are
+/// kept between calls: the stream-ordered pool sometimes maps fresh memory
+/// for them, which measured as 0.4 -> 0.8-1.1 s outliers of a C4 call
+/// (tools/e2e_ab.py).  Blocks are reused by size (up to 2x) per device; at
+/// most kMaxCached stay cached.
+struct BufferCache {
+    static constexpr std::size_t kLarge = std::size_t(64) << 20;
+    static constexpr std::size_t kMaxCached = 8;
+    std::mutex mu;
+    struct Block {
+        int device;
+        std::size_t bytes;
+        void* p;
+    };
+    std::vector<Block> free;
+
+    void* acquire(int device, std::size_t bytes) {
+        {
+            std::lock_guard<std::mutex> lock(mu);
+            std::size_t best = free.size();
+            for (std::size_t i = 0; i < free.size(); ++i)
+                if (free[i].device == device && free[i].bytes >= bytes && free[i].bytes <= 2 * bytes &&
+                    (best == free.size() || free[i].bytes < free[best].bytes))
+                    best = i;
+            if (best < free.size()) {
+                void* p = free[best].p;
+                free.erase(free.begin() + static_cast<std::ptrdiff_t>(best));
+                return p;
+            }
+        }
+        void* p = nullptr;
+        if (cudaMalloc(&p, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            trim(device, 0); // give the cached blocks back and retry once
+            CK(cudaMalloc(&p, bytes));
+        }
+        return p;
+    }
+    void release(int device, std::size_t bytes, void* p) {
+        std::lock_guard<std::mutex> lock(mu);
+        free.push_back({device, bytes, p});
+        while (free.size() > kMaxCached) {
+            cudaFree(free.front().p);
+            free.erase(free.begin());
+        }
+    }
+    void trim(int device, std::size_t keep) {
+        std::lock_guard<std::mutex> lock(mu);
+        for (std::size_t i = free.size(); i-- > 0;)
+            if (free[i].device == device && free.size() > keep) {
+                cudaFree(free[i].p);
+                free.erase(free.begin() + static_cast<std::ptrdiff_t>(i));
+            }
+    }
+};
+BufferCache g_buffers;
+
 struct DeviceBuffer {
     void* p = nullptr;
     cudaStream_t s = nullptr;
-    DeviceBuffer(std::size_t bytes, cudaStream_t st) : s(st) {
-        CK(cudaMallocAsync(&p, std::max<std::size_t>(bytes, 8), st));
+    std::size_t bytes = 0;
+    int device = -1;
+    DeviceBuffer(std::size_t n, cudaStream_t st) : s(st), bytes(std::max<std::size_t>(n, 8)) {
+        if (bytes >= BufferCache::kLarge) {
+            CK(cudaGetDevice(&device));
+            p = g_buffers.acquire(device, bytes);
+        } else {
+            CK(cudaMallocAsync(&p, bytes, st));
+        }
     }
     ~DeviceBuffer() {
-        if (p)
+        if (!p)
+            return;
+        if (device >= 0) {
+            cudaStreamSynchronize(s); // no pending work may touch a block going back to the cache
+            g_buffers.release(device, bytes, p);
+        } else {
             cudaFreeAsync(p, s);
+        }
     }
 };
 
@@ -803,13 +874,14 @@ static int assemble_one_shot(const lf_problem* p, int backend, int device, int t
         CK(cudaEventCreateWithFlags(&side.e, cudaEventDisableTiming));
         CK(cudaEventRecord(side.e, plan.stream)); // buffers allocated (stream-ordered)
         CK(cudaStreamWaitEvent(side.s, side.e, 0));
+        cudaStream_t ps = side.s;
         CK(static_cast<cudaError_t>(lfb::launch_pattern(plan.d, static_cast<long long*>(drp.p),
-                                                        static_cast<int*>(dcols.p), side.s)));
-        copy_d2h(row_ptr, drp.p, sizeof(int64_t) * (rows + 1), side.s);
-        copy_d2h(cols, dcols.p, sizeof(int32_t) * nnz, side.s);
+                                                        static_cast<int*>(dcols.p), ps)));
+        copy_d2h(row_ptr, drp.p, sizeof(int64_t) * (rows + 1), ps);
+        copy_d2h(cols, dcols.p, sizeof(int32_t) * nnz, ps);
         plan_launch(&plan, static_cast<double*>(dvals.p));
         copy_d2h(values, dvals.p, sizeof(double) * nnz, plan.stream);
-        CK(cudaStreamSynchronize(side.s));
+        CK(cudaStreamSynchronize(ps));
         CK(cudaStreamSynchronize(plan.stream));
         CK(cudaGetLastError());
         if (stats) {
