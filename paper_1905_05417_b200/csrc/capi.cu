@@ -66,25 +66,38 @@ void use_device(int device) {
     CK(cudaSetDevice(device));
 }
 
-/// Device allocations owned by a plan.
+/// Device allocations owned by a plan.  With a stream set (plans), they come
+/// from the stream-ordered pool and go back to it without a device-wide
+/// synchronisation: per-call cudaMalloc/cudaFree of the ~50 table buffers
+/// measured as 40-370 ms outliers of plan creation / destruction on the box
+/// (tools/e2e_phases.py).  Without a stream: plain cudaMalloc/cudaFree.
 struct DeviceArena {
     std::vector<void*> ptrs;
-    ~DeviceArena() {
+    cudaStream_t s = nullptr;
+    ~DeviceArena() { clear(); }
+    void clear() {
         for (void* p : ptrs)
-            cudaFree(p);
+            s ? cudaFreeAsync(p, s) : cudaFree(p);
+        ptrs.clear();
     }
     template <typename T>
     T* alloc(std::size_t n) {
         void* p = nullptr;
-        CK(cudaMalloc(&p, std::max<std::size_t>(1, n) * sizeof(T)));
+        const std::size_t bytes = std::max<std::size_t>(1, n) * sizeof(T);
+        CK(s ? cudaMallocAsync(&p, bytes, s) : cudaMalloc(&p, bytes));
         ptrs.push_back(p);
         return static_cast<T*>(p);
     }
     template <typename T>
     T* upload(const T* src, std::size_t n) {
         T* d = alloc<T>(n);
-        if (n)
-            CK(cudaMemcpy(d, src, n * sizeof(T), cudaMemcpyHostToDevice));
+        if (n) {
+            if (s) { // stream-ordered; the caller synchronises before the host data dies
+                CK(cudaMemcpyAsync(d, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
+            } else {
+                CK(cudaMemcpy(d, src, n * sizeof(T), cudaMemcpyHostToDevice));
+            }
+        }
         return d;
     }
     template <typename T>
@@ -338,6 +351,7 @@ struct lf_plan {
             cudaEventDestroy(e.first);
             cudaEventDestroy(e.second);
         }
+        arena.clear(); // stream-ordered frees, before the stream goes away
         if (own_stream && stream)
             cudaStreamDestroy(stream);
     }
@@ -374,6 +388,14 @@ void alloc_element_scratch(DeviceArena& ar, lfb::DevTables& d, int n_terms) {
     d.Pe = ar.alloc<double>(per_term * static_cast<std::size_t>(d.pe_terms));
 }
 
+void keep_pool_memory(int device) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t threshold = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+    }
+}
+
 void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void* stream, int t0, int t1) {
     if (!p)
         raise(LF_ERR_INVALID_ARGUMENT, "null problem");
@@ -386,9 +408,11 @@ void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void
         CK(cudaStreamCreateWithFlags(&plan->stream, cudaStreamNonBlocking));
         plan->own_stream = true;
     }
+    keep_pool_memory(device);
     const lfb::Setup& s = plan->setup;
     lfb::DevTables& d = plan->d;
     DeviceArena& ar = plan->arena;
+    ar.s = plan->stream;
     upload_space(s, ar, d);
     upload_geometry(s, ar, d);
     upload_thickness(s, ar, d, s.at);
@@ -436,6 +460,7 @@ void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void
     const char* ge = std::getenv("LAMFAST_GRAPH");
     const bool small = s.nnz <= (64LL << 20) || backend == LF_BACKEND_STANDARD;
     plan->use_graph = (ge ? std::atoi(ge) != 0 : small) && d.ws_variant == 0 && d.n_team == 0;
+    CK(cudaStreamSynchronize(plan->stream)); // the uploads' host sources are temporaries
 }
 
 int plan_launch(lf_plan* plan, double* values, bool timed = true) {
@@ -585,11 +610,26 @@ struct BufferCache {
         return p;
     }
     void release(int device, std::size_t bytes, void* p) {
+        std::size_t avail = 0, total = 0;
+        cudaMemGetInfo(&avail, &total);
         std::lock_guard<std::mutex> lock(mu);
         free.push_back({device, bytes, p});
-        while (free.size() > kMaxCached) {
-            cudaFree(free.front().p);
-            free.erase(free.begin());
+        // at most kMaxCached blocks and a quarter of the device's memory stay cached
+        auto cached = [&] {
+            std::size_t b = 0;
+            for (const Block& f : free)
+                if (f.device == device)
+                    b += f.bytes;
+            return b;
+        };
+        while (free.size() > kMaxCached || (total && cached() > total / 4)) {
+            std::size_t i = 0;
+            while (i < free.size() && free[i].device != device && free.size() <= kMaxCached)
+                ++i;
+            if (i == free.size())
+                break;
+            cudaFree(free[i].p);
+            free.erase(free.begin() + static_cast<std::ptrdiff_t>(i));
         }
     }
     void trim(int device, std::size_t keep) {
@@ -628,13 +668,6 @@ struct DeviceBuffer {
     }
 };
 
-void keep_pool_memory(int device) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-        uint64_t threshold = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
-    }
-}
 
 /// Entry-layout P (Pg[t][f][e]) -> banded InPlaneOperator blocks (fast.cpp:13-32).
 void export_banded(const lfb::Setup& s, const std::vector<double>& pg, int n_terms, double* blocks, char* flags) {
