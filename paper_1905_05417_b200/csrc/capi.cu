@@ -571,103 +571,17 @@ void copy_d2h(void* dst, const void* src, std::size_t bytes, cudaStream_t s) {
         CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
 }
 
-/// Large one-shot buffers (the CSR arrays of lf_assemble: 23 GB for C4) are
-/// kept between calls: the stream-ordered pool sometimes maps fresh memory
-/// for them, which measured as 0.4 -> 0.8-1.1 s outliers of a C4 call
-/// (tools/e2e_ab.py).  Blocks are reused by size (up to 2x) per device; at
-/// most kMaxCached stay cached.
-struct BufferCache {
-    static constexpr std::size_t kLarge = std::size_t(64) << 20;
-    static constexpr std::size_t kMaxCached = 8;
-    std::mutex mu;
-    struct Block {
-        int device;
-        std::size_t bytes;
-        void* p;
-    };
-    std::vector<Block> free;
-
-    void* acquire(int device, std::size_t bytes) {
-        {
-            std::lock_guard<std::mutex> lock(mu);
-            std::size_t best = free.size();
-            for (std::size_t i = 0; i < free.size(); ++i)
-                if (free[i].device == device && free[i].bytes >= bytes && free[i].bytes <= 2 * bytes &&
-                    (best == free.size() || free[i].bytes < free[best].bytes))
-                    best = i;
-            if (best < free.size()) {
-                void* p = free[best].p;
-                free.erase(free.begin() + static_cast<std::ptrdiff_t>(best));
-                return p;
-            }
-        }
-        void* p = nullptr;
-        if (cudaMalloc(&p, bytes) != cudaSuccess) {
-            cudaGetLastError();
-            trim(device, 0); // give the cached blocks back and retry once
-            CK(cudaMalloc(&p, bytes));
-        }
-        return p;
-    }
-    void release(int device, std::size_t bytes, void* p) {
-        std::size_t avail = 0, total = 0;
-        cudaMemGetInfo(&avail, &total);
-        std::lock_guard<std::mutex> lock(mu);
-        free.push_back({device, bytes, p});
-        // at most kMaxCached blocks and a quarter of the device's memory stay cached
-        auto cached = [&] {
-            std::size_t b = 0;
-            for (const Block& f : free)
-                if (f.device == device)
-                    b += f.bytes;
-            return b;
-        };
-        while (free.size() > kMaxCached || (total && cached() > total / 4)) {
-            std::size_t i = 0;
-            while (i < free.size() && free[i].device != device && free.size() <= kMaxCached)
-                ++i;
-            if (i == free.size())
-                break;
-            cudaFree(free[i].p);
-            free.erase(free.begin() + static_cast<std::ptrdiff_t>(i));
-        }
-    }
-    void trim(int device, std::size_t keep) {
-        std::lock_guard<std::mutex> lock(mu);
-        for (std::size_t i = free.size(); i-- > 0;)
-            if (free[i].device == device && free.size() > keep) {
-                cudaFree(free[i].p);
-                free.erase(free.begin() + static_cast<std::ptrdiff_t>(i));
-            }
-    }
-};
-BufferCache g_buffers;
-
 struct DeviceBuffer {
     void* p = nullptr;
     cudaStream_t s = nullptr;
-    std::size_t bytes = 0;
-    int device = -1;
-    DeviceBuffer(std::size_t n, cudaStream_t st) : s(st), bytes(std::max<std::size_t>(n, 8)) {
-        if (bytes >= BufferCache::kLarge) {
-            CK(cudaGetDevice(&device));
-            p = g_buffers.acquire(device, bytes);
-        } else {
-            CK(cudaMallocAsync(&p, bytes, st));
-        }
+    DeviceBuffer(std::size_t bytes, cudaStream_t st) : s(st) {
+        CK(cudaMallocAsync(&p, std::max<std::size_t>(bytes, 8), st));
     }
     ~DeviceBuffer() {
-        if (!p)
-            return;
-        if (device >= 0) {
-            cudaStreamSynchronize(s); // no pending work may touch a block going back to the cache
-            g_buffers.release(device, bytes, p);
-        } else {
+        if (p)
             cudaFreeAsync(p, s);
-        }
     }
 };
-
 
 /// Entry-layout P (Pg[t][f][e]) -> banded InPlaneOperator blocks (fast.cpp:13-32).
 void export_banded(const lfb::Setup& s, const std::vector<double>& pg, int n_terms, double* blocks, char* flags) {
