@@ -876,11 +876,12 @@ __global__ void k_pattern_rows(const DevTables d, long long* __restrict__ row_pt
     row_ptr[r] = 9 * d.S_s * (d.pre_t[it] - d.pre_t[d.t0]) + (long long)Lt * (d.es_pre[is] + (long long)a * B);
 }
 
-constexpr int kColsEpt = 4; // entries per thread of k_pattern_cols
-
 /// Columns of the slab's CSR.  Thread slots are warp-contiguous (a warp owns
 /// 32 * kColsEpt consecutive entries, so its kColsEpt stores per (row, k) are
-/// adjacent 128-byte runs) and the stores stream (st.global.cs).
+/// adjacent 128-byte runs) and the stores stream (st.global.cs).  16 entries
+/// per thread on large slabs (C4 1.63 -> 1.45 ms), 8 on small ones (C2: 16
+/// leaves too few blocks); profiles/r1_pattern_ept.txt.
+template <int kColsEpt>
 __global__ void __launch_bounds__(kBlock) k_pattern_cols(const DevTables d, int* __restrict__ cols,
                                                          int t_chunk) {
     int* o0[kColsEpt];
@@ -1103,12 +1104,19 @@ int launch_pattern(const DevTables& d, long long* row_ptr, int* cols, cudaStream
     const long long rows = 3LL * d.ns * (d.t1 - d.t0);
     k_pattern_rows<<<(unsigned)((rows + 1 + 255) / 256), 256, 0, stream>>>(d, row_ptr, rows);
     if (d.E > 0 && d.t1 > d.t0) {
-        const long long nblk = (d.E + (long long)kBlock * kColsEpt - 1) / ((long long)kBlock * kColsEpt);
         const int nt = d.t1 - d.t0;
-        long long nchunks = std::max(1LL, std::min<long long>((148LL * 16 + nblk - 1) / nblk, nt));
-        const int t_chunk = (int)((nt + nchunks - 1) / nchunks);
-        const dim3 grid((unsigned)nblk, (unsigned)((nt + t_chunk - 1) / t_chunk));
-        k_pattern_cols<<<grid, kBlock, 0, stream>>>(d, cols, t_chunk);
+        auto launch = [&](auto kern, int ept) {
+            const long long nblk = (d.E + (long long)kBlock * ept - 1) / ((long long)kBlock * ept);
+            long long nchunks = std::max(1LL, std::min<long long>((148LL * 16 + nblk - 1) / nblk, nt));
+            const int t_chunk = (int)((nt + nchunks - 1) / nchunks);
+            const dim3 grid((unsigned)nblk, (unsigned)((nt + t_chunk - 1) / t_chunk));
+            kern<<<grid, kBlock, 0, stream>>>(d, cols, t_chunk);
+        };
+        const long long blocks16 = (d.E + kBlock * 16LL - 1) / (kBlock * 16LL) * nt;
+        if (blocks16 >= 148LL * 32)
+            launch(k_pattern_cols<16>, 16);
+        else
+            launch(k_pattern_cols<8>, 8);
     }
     return (int)cudaGetLastError();
 }
