@@ -99,7 +99,8 @@ __device__ __forceinline__ void combine_body(const DevTables& d, double* __restr
             // (profiles/r1_masked_rows.txt): 4 terms C3 1.341 -> 1.301 ms, C5
             // family 6.08 -> 5.88 ms; 3 terms (C4) 2.52 -> 2.65 ms, so 4 only.
 #ifndef LF_MASKED_LTS
-#define LF_MASKED_LTS 40 // bit L set: rows with L_t = L take the branch-free bodies
+#define LF_MASKED_LTS 8 // bit L set: rows with L_t = L take the branch-free bodies (bubble rows
+                        // only: C3 1.300 -> 1.295 ms, C5 family -0.3% against L_t 3 and 5)
 #endif
 #ifndef LF_MASKED_MIN_NT
 #define LF_MASKED_MIN_NT 4
