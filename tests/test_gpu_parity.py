@@ -615,3 +615,26 @@ def test_matrix_free_bilinear_matches_reference(gpu, reference):
         scale = np.sqrt(abs(reference.bilinear(prob, u, u) * reference.bilinear(prob, v, v)))
         assert abs(got - want) <= 1e-12 * scale
         assert abs(got - vku) <= 1e-12 * scale
+
+
+@pytest.mark.slow
+def test_c5_layup_reduced_inplane_matches_oracle(gpu, oracle):
+    """The C5 laminate itself (128 plies, orientations from std::mt19937(20190514),
+    4 distinct rotated materials, p = 3, thickness 0.25) on a 32 x 32 in-plane
+    mesh, so the oracle finishes in seconds: device slab plans of three
+    thickness functions at the bottom, middle and top equal the oracle's rows."""
+    import torch
+    c5 = P.baseline_config("C5")
+    prob = P.plate(3, 32, 32, c5.layers, thickness=0.25, name="C5-32x32")
+    assert prob.distinct_configs() == 4
+    for t in (0, prob.n_t // 2, prob.n_t - 3):
+        plan = gpu.Plan(prob, "fast", 0, t, t + 3)
+        rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
+        cols = torch.empty(plan.nnz, dtype=torch.int32, device="cuda")
+        vals = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
+        plan.build_pattern(rp.data_ptr(), cols.data_ptr())
+        plan.assemble(vals.data_ptr())
+        plan.synchronize()
+        assert_csr_match((rp.cpu().numpy(), cols.cpu().numpy(), vals.cpu().numpy()),
+                         oracle.assemble(prob, "fast", t, t + 3), RTOL)
+        plan.close()
