@@ -355,7 +355,13 @@ def test_full_size_fast_equals_standard_on_device(gpu, name):
     std = _device_csr(gpu, prob, "standard")
     assert torch.equal(fast[1], std[1]) and torch.equal(fast[2], std[2])
     assert _device_rel_diff(gpu, fast, std) <= RTOL
-    del fast, std
+    del std
+    torch.cuda.empty_cache()
+    # the Voigt-free formulation (contraction tables from the bracket fit) too
+    vf = _device_csr(gpu, prob, "voigt_free")
+    assert torch.equal(fast[1], vf[1]) and torch.equal(fast[2], vf[2])
+    assert _device_rel_diff(gpu, fast, vf) <= RTOL
+    del fast, vf
     torch.cuda.empty_cache()
 
 
