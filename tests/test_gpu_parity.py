@@ -644,3 +644,18 @@ def test_c5_layup_reduced_inplane_matches_oracle(gpu, oracle):
         assert_csr_match((rp.cpu().numpy(), cols.cpu().numpy(), vals.cpu().numpy()),
                          oracle.assemble(prob, "fast", t, t + 3), RTOL)
         plan.close()
+
+
+@pytest.mark.slow
+def test_full_size_decompose_angles_equals_direct_on_device(gpu):
+    """AssemblyOptions::decompose_angles at BASELINE C3 size (4 angles of one
+    material -> 5 trigonometric terms, one multi-term pass) equals the direct
+    per-angle fast assembly: same pattern, frobeniusRelDiff <= 1e-12."""
+    import torch
+    prob = P.baseline_config("C3")
+    direct = _device_csr(gpu, prob, "fast")
+    dec = _device_csr(gpu, prob.replace(decompose_angles=True), "fast")
+    assert torch.equal(direct[1], dec[1]) and torch.equal(direct[2], dec[2])
+    assert _device_rel_diff(gpu, direct, dec) <= RTOL
+    del direct, dec
+    torch.cuda.empty_cache()
