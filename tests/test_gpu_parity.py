@@ -659,3 +659,19 @@ def test_full_size_decompose_angles_equals_direct_on_device(gpu):
     assert _device_rel_diff(gpu, direct, dec) <= RTOL
     del direct, dec
     torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+def test_full_size_general_geometry_fast_equals_standard_on_device(gpu):
+    """C3's mesh and layup on a bilinear (non-affine) map: the general in-plane
+    path (two-phase K2b, per-point frames) against the standard assembly on
+    the device, at full size."""
+    import torch
+    prob = P.baseline_config("C3")
+    prob = prob.replace(geometry_kind=1, geometry=(0, 0, 0, 1.0, 0.05, 0.0, -0.05, 1.0, 0.0, 1.02, 1.03, 0.01))
+    fast = _device_csr(gpu, prob, "fast")
+    std = _device_csr(gpu, prob, "standard")
+    assert torch.equal(fast[1], std[1]) and torch.equal(fast[2], std[2])
+    assert _device_rel_diff(gpu, fast, std) <= RTOL
+    del fast, std
+    torch.cuda.empty_cache()
