@@ -1008,6 +1008,10 @@ __global__ void k_symmetry_rows(long long rows, const long long* rp, const int* 
          r += (long long)gridDim.x * blockDim.x) {
         for (long long k = rp[r]; k < rp[r + 1]; ++k) {
             const int col = c[k];
+            if (col < 0 || col >= rows) { // no mirror row in this matrix (e.g. a row slab): absent
+                s += 2.0 * v[k] * v[k];
+                continue;
+            }
             long long lo = rp[col], hi = rp[col + 1];
             while (lo < hi) {
                 const long long mid = (lo + hi) >> 1;
