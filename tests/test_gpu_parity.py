@@ -682,7 +682,8 @@ def test_c5_full_size_rows_annihilate_translations(gpu):
     """C5 at full size (1.69e10 nnz, 203 GB as CSR -- never resident at once):
     every one of its rows, assembled slab by slab (8 row slabs, pattern and
     values each), annihilates the three rigid translations (acceptance.cpp:
-    95-104) within 1e-12 of ||K||_F, and the slabs' nnz add up to the closed form."""
+    95-104) within 1e-12 of ||K||_F, the slabs' nnz add up to the closed form,
+    and K is symmetric in the bilinear sense v.(K u) = u.(K v) for random u, v."""
     import ctypes
     import torch
     prob = P.baseline_config("C5")
@@ -693,6 +694,12 @@ def test_c5_full_size_rows_annihilate_translations(gpu):
         x = torch.zeros(prob.dim, dtype=torch.float64, device="cuda")
         x[d::3] = 1.0
         xs.append(x)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    u = torch.randn(prob.dim, dtype=torch.float64, device="cuda", generator=gen)
+    v = torch.randn(prob.dim, dtype=torch.float64, device="cuda", generator=gen)
+    ku = torch.empty_like(u)
+    kv = torch.empty_like(v)
+    xs += [u, v]
     for part in range(parts):
         b = gpu.slab_bounds(prob, parts, part)
         plan = gpu.Plan(prob, "fast", 0, b["t_begin"], b["t_end"])
@@ -708,14 +715,20 @@ def test_c5_full_size_rows_annihilate_translations(gpu):
                                        None, ctypes.byref(f)) == 0
         fro_sq += f.value
         y = torch.empty(plan.rows, dtype=torch.float64, device="cuda")
-        for x in xs:
+        r0, r1 = b["row_begin"], b["row_end"]
+        for i, x in enumerate(xs):
             assert lib.lf_csr_spmv(plan.rows, ctypes.c_void_p(rp.data_ptr()), ctypes.c_void_p(cols.data_ptr()),
                                    ctypes.c_void_p(vals.data_ptr()), ctypes.c_void_p(x.data_ptr()),
                                    ctypes.c_void_p(y.data_ptr()), None) == 0
             torch.cuda.synchronize()
-            worst = max(worst, float(y.abs().max()))
+            if i < 3:
+                worst = max(worst, float(y.abs().max()))
+            else:
+                (ku if i == 3 else kv)[r0:r1] = y
         plan.close()
         del rp, cols, vals, y
         torch.cuda.empty_cache()
     assert total_nnz == P.sizes(prob)["nnz"]
     assert worst / np.sqrt(fro_sq) <= 1e-12
+    asym = abs(float(v @ ku) - float(u @ kv))
+    assert asym <= 1e-12 * np.sqrt(fro_sq) * float(u.norm()) * float(v.norm())
