@@ -784,11 +784,33 @@ int lf_plan_synchronize(lf_plan* plan) {
     });
 }
 
+/// One-shot calls run on a per-(thread, device) pair of streams kept for the
+/// thread's lifetime, so the device buffers a call frees are reused by the
+/// next call's stream-ordered allocations on the same stream (no fresh
+/// mappings of the 23 GB of a C4 CSR).
+struct OneShotStreams {
+    cudaStream_t main = nullptr, side = nullptr;
+};
+
+static OneShotStreams& one_shot_streams(int device) {
+    thread_local std::vector<OneShotStreams> per_device;
+    if (static_cast<int>(per_device.size()) <= device)
+        per_device.resize(static_cast<std::size_t>(device) + 1);
+    OneShotStreams& st = per_device[static_cast<std::size_t>(device)];
+    if (!st.main) {
+        CK(cudaStreamCreateWithFlags(&st.main, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&st.side, cudaStreamNonBlocking));
+    }
+    return st;
+}
+
 static int assemble_one_shot(const lf_problem* p, int backend, int device, int t0, int t1, int64_t* row_ptr,
                              int32_t* cols, double* values, lf_stats* stats) {
     return guarded([&] {
+        use_device(device);
+        OneShotStreams& streams = one_shot_streams(device);
         lf_plan plan;
-        plan_init(&plan, p, backend, device, nullptr, t0, t1);
+        plan_init(&plan, p, backend, device, streams.main, t0, t1);
         keep_pool_memory(device);
         const lfb::Setup& s = plan.setup;
         if (s.nnz == 0) {
@@ -808,15 +830,13 @@ static int assemble_one_shot(const lf_problem* p, int backend, int device, int t
             cudaStream_t s = nullptr;
             cudaEvent_t e = nullptr;
             ~Side() {
-                if (s) {
+                if (s)
                     cudaStreamSynchronize(s);
-                    cudaStreamDestroy(s);
-                }
                 if (e)
                     cudaEventDestroy(e);
             }
         } side;
-        CK(cudaStreamCreateWithFlags(&side.s, cudaStreamNonBlocking));
+        side.s = streams.side;
         CK(cudaEventCreateWithFlags(&side.e, cudaEventDisableTiming));
         CK(cudaEventRecord(side.e, plan.stream)); // buffers allocated (stream-ordered)
         CK(cudaStreamWaitEvent(side.s, side.e, 0));
