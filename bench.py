@@ -266,6 +266,20 @@ def main():
         cols = torch.empty(plan.nnz, dtype=torch.int32, device="cuda")
         plan.build_pattern(rp.data_ptr(), cols.data_ptr())
     torch.cuda.synchronize()
+    # the precomputed CSR pattern (K5), reported separately (outside the timed
+    # region): 4 B per column + 8 B per row offset
+    pattern = None
+    if with_pattern:
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        for _ in range(3):
+            plan.build_pattern(rp.data_ptr(), cols.data_ptr())
+        p1.record(stream)
+        torch.cuda.synchronize()
+        pms = p0.elapsed_time(p1) / 3
+        pbytes = plan.nnz * 4 + (plan.rows + 1) * 8
+        pattern = {"ms": pms, "bytes": pbytes, "gbs": pbytes / (pms / 1e3) / 1e9,
+                   "kernels": "k_pattern_rows + k_pattern_cols"}
 
     def step():
         for p in plans:
@@ -345,6 +359,8 @@ def main():
                 torch.cuda.empty_cache()
 
     hbm, peak_src = peaks()
+    if pattern:
+        pattern["frac"] = pattern["gbs"] / hbm
     achieved = k_bytes / (k_avg_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": None,
@@ -431,7 +447,7 @@ def main():
                              % (total_nnz * 8 / 1e9),
                        "parallelism": f"row-slab x{world}", "slab_passes_per_gpu": passes},
             "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
-            "clocks": clocks, "verify": verify, "standard": standard,
+            "clocks": clocks, "verify": verify, "standard": standard, "pattern": pattern,
         }
         print(json.dumps(line))
     if world > 1:
