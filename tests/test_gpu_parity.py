@@ -746,3 +746,25 @@ def test_c5_full_size_rows_annihilate_translations(gpu):
     assert worst / np.sqrt(fro_sq) <= 1e-12
     asym = abs(float(v @ ku) - float(u @ kv))
     assert asym <= 1e-12 * np.sqrt(fro_sq) * float(u.norm()) * float(v.norm())
+
+
+def test_symmetry_check_accepts_row_slabs(gpu):
+    """lf_csr_symmetry_sq on a row slab (global columns beyond the slab's rows)
+    counts those entries as missing mirrors instead of reading out of bounds;
+    on the whole matrix it stays at roundoff."""
+    import ctypes
+    import torch
+    prob = P.baseline_config("C2")
+    lib = gpu.library()
+    ptr = lambda t: ctypes.c_void_p(t.data_ptr())
+    full = _device_csr(gpu, prob, "fast")
+    out = ctypes.c_double()
+    assert lib.lf_csr_symmetry_sq(full[0], ptr(full[1]), ptr(full[2]), ptr(full[3]), None, ctypes.byref(out)) == 0
+    fro = ctypes.c_double()
+    assert lib.lf_csr_frobenius_sq(full[0], ptr(full[1]), ptr(full[3]), None, ctypes.byref(fro)) == 0
+    assert out.value ** 0.5 <= 1e-13 * fro.value ** 0.5
+    b = gpu.slab_bounds(prob, 3, 1)
+    slab = _device_csr(gpu, prob, "fast", b["t_begin"], b["t_end"])
+    assert lib.lf_csr_symmetry_sq(slab[0], ptr(slab[1]), ptr(slab[2]), ptr(slab[3]), None, ctypes.byref(out)) == 0
+    torch.cuda.synchronize()
+    assert out.value > 0.0 and np.isfinite(out.value)
