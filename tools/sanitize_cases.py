@@ -59,4 +59,16 @@ plan.synchronize()
 st = lf.device_csr_stats(plan.rows, rp.data_ptr(), cols.data_ptr(), vals.data_ptr())
 out.append(st["fro_sq"])
 plan.close()
+# a BASELINE-size plan (C3): the large-slab pattern kernel (16 entries per thread) and the
+# 4-term combine with the branch-free bodies
+c3 = P.baseline_config("C3")
+plan = lf.Plan(c3, "fast", 0)
+rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
+cols = torch.empty(plan.nnz, dtype=torch.int32, device="cuda")
+vals = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
+plan.build_pattern(rp.data_ptr(), cols.data_ptr())
+plan.assemble(vals.data_ptr())
+plan.synchronize()
+out.append(float(vals[:1000].sum()))
+plan.close()
 print("ok", len(out), float(np.sum(out)))
