@@ -243,9 +243,27 @@ int lf_csr_spmv(int64_t rows, const int64_t* d_row_ptr, const int32_t* d_cols,
 int lf_csr_diff_sq(int64_t rows, const int64_t* d_ra, const int32_t* d_ca, const double* d_va,
                    const int64_t* d_rb, const int32_t* d_cb, const double* d_vb,
                    void* cuda_stream, double* out);
-/* ||K - K^T||_F^2 numerator of symmetryRelError for a full (non-slab) CSR. */
+/* ||K - K^T||_F^2 numerator of symmetryRelError (sparse.cpp:73-95) for a
+ * full CSR of `rows` rows; LF_ERR_INVALID_ARGUMENT if a column lies outside
+ * the matrix (a row slab: use lf_csr_symmetry_sq_slab). */
 int lf_csr_symmetry_sq(int64_t rows, const int64_t* d_row_ptr, const int32_t* d_cols,
                        const double* d_values, void* cuda_stream, double* out);
+/* The same numerator restricted to a row slab holding global rows
+ * [row_begin, row_begin + rows) (row offsets rebased to 0, global columns):
+ * sum over the slab's entries (r, c) whose mirror row c is also in the slab.
+ * *n_skipped (may be NULL) receives the number of entries whose mirror row
+ * lies outside.  For row_begin = 0 and the whole matrix it equals
+ * lf_csr_symmetry_sq. */
+int lf_csr_symmetry_sq_slab(int64_t rows, int64_t row_begin, const int64_t* d_row_ptr,
+                            const int32_t* d_cols, const double* d_values, void* cuda_stream,
+                            double* out, int64_t* n_skipped);
+/* Symmetry numerator of a plan's slab values (pattern order, as written by
+ * lf_plan_assemble) from the closed-form pattern: no binary searches, every
+ * value read once.  Same slab convention as lf_csr_symmetry_sq_slab. */
+int lf_plan_symmetry_sq(lf_plan* plan, const double* d_values, double* out);
+/* Returns the library's cached device memory (its private stream-ordered
+ * pool, kept across one-shot calls) to the driver. */
+int lf_release_memory(int device);
 
 #ifdef __cplusplus
 }

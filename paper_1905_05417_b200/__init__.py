@@ -9,7 +9,8 @@ Python host layer over that ABI; see DESIGN.md.
 from .abi import LamfastError, library
 from .assembler import (CSR, Plan, assemble_fast, assemble_slab, reference_bilinear, assemble_standard, assemble_voigt_free,
                         assemble_with, combine_operators, compute_inplane_operators,
-                        compute_thickness_operators, device_csr_stats, pattern_size, slab_bounds)
+                        compute_thickness_operators, device_csr_stats, pattern_size, release_memory,
+                        slab_bounds)
 from .problem import (LaminateProblem, baseline_config, baseline_orthotropic, c0_knots,
                       cube_problem, equal_interfaces, isotropic, pagano, plate, sizes,
                       uniform_knots)
@@ -19,7 +20,7 @@ __all__ = [
     "assemble_slab",
     "LamfastError", "library", "CSR", "Plan", "assemble_fast", "assemble_standard",
     "assemble_voigt_free", "assemble_with", "combine_operators", "compute_inplane_operators",
-    "compute_thickness_operators", "device_csr_stats", "pattern_size", "slab_bounds",
+    "compute_thickness_operators", "device_csr_stats", "pattern_size", "release_memory", "slab_bounds",
     "LaminateProblem", "baseline_config", "baseline_orthotropic", "c0_knots", "cube_problem",
     "equal_interfaces", "isotropic", "pagano", "plate", "sizes", "uniform_knots",
 ]

@@ -134,6 +134,10 @@ SIGNATURES = [
                                c_void_p, c_void_p, _P(c_double)]),
     ("lf_csr_symmetry_sq", c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
                                    _P(c_double)]),
+    ("lf_csr_symmetry_sq_slab", c_int, [c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
+                                        _P(c_double), _P(c_int64)]),
+    ("lf_plan_symmetry_sq", c_int, [c_void_p, c_void_p, _P(c_double)]),
+    ("lf_release_memory", c_int, [c_int]),
 ]
 
 _lib = None

@@ -235,6 +235,14 @@ class Plan:
         abi.check(self.lib.lf_plan_kernel_time(self.handle, 1 if reset else 0, byref(ms), byref(n)))
         return ms.value, n.value
 
+    def symmetry_sq(self, values_ptr: int) -> float:
+        """||K - K^T||_F^2 numerator of symmetryRelError over this plan's slab
+        (entries whose mirror row is in the slab), from the closed-form pattern
+        (lf_plan_symmetry_sq)."""
+        out = c_double()
+        abi.check(self.lib.lf_plan_symmetry_sq(self.handle, c_void_p(values_ptr), byref(out)))
+        return out.value
+
     def stats(self) -> abi.Stats:
         st = abi.Stats()
         abi.check(self.lib.lf_plan_stats(self.handle, byref(st)))
@@ -258,12 +266,21 @@ class Plan:
         self.close()
 
 
-def device_csr_stats(rows: int, row_ptr_ptr: int, cols_ptr: int, values_ptr: int, stream: int = 0) -> dict:
-    """||K||_F^2 and ||K - K^T||_F^2 on the device (sparse.cpp:66-95)."""
+def device_csr_stats(rows: int, row_ptr_ptr: int, cols_ptr: int, values_ptr: int, stream: int = 0,
+                     row_begin: int = 0) -> dict:
+    """||K||_F^2 and ||K - K^T||_F^2 on the device (sparse.cpp:66-95) of a
+    CSR holding the global rows [row_begin, row_begin + rows); for a slab the
+    symmetry sum covers the entries whose mirror row is in the slab."""
     lib = abi.library()
-    fro, sym = c_double(), c_double()
+    fro, sym, skipped = c_double(), c_double(), c_int64()
     abi.check(lib.lf_csr_frobenius_sq(rows, c_void_p(row_ptr_ptr), c_void_p(values_ptr),
                                       c_void_p(stream), byref(fro)))
-    abi.check(lib.lf_csr_symmetry_sq(rows, c_void_p(row_ptr_ptr), c_void_p(cols_ptr),
-                                     c_void_p(values_ptr), c_void_p(stream), byref(sym)))
-    return {"fro_sq": fro.value, "sym_sq": sym.value}
+    abi.check(lib.lf_csr_symmetry_sq_slab(rows, row_begin, c_void_p(row_ptr_ptr), c_void_p(cols_ptr),
+                                          c_void_p(values_ptr), c_void_p(stream), byref(sym),
+                                          byref(skipped)))
+    return {"fro_sq": fro.value, "sym_sq": sym.value, "sym_skipped": skipped.value}
+
+
+def release_memory(device: int = 0) -> None:
+    """Returns the library's cached device memory to the driver (lf_release_memory)."""
+    abi.check(abi.library().lf_release_memory(device))

@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <string>
 #include <utility>
@@ -65,6 +66,43 @@ void use_device(int device) {
     CK(cudaSetDevice(device));
 }
 
+/// The library's own stream-ordered memory pool per device.  Its release
+/// threshold is unlimited, so one-shot calls reuse the buffers the previous
+/// call freed (no fresh mappings of a 23 GB CSR per call), but it is private:
+/// torch's caching allocator and other users of the device's default pool
+/// never see it, and lf_release_memory() returns it to the driver.
+cudaMemPool_t lib_pool(int device) {
+    static std::mutex mu;
+    static std::vector<cudaMemPool_t> pools;
+    std::lock_guard<std::mutex> lock(mu);
+    if (static_cast<int>(pools.size()) <= device)
+        pools.resize(static_cast<std::size_t>(device) + 1, nullptr);
+    cudaMemPool_t& pool = pools[static_cast<std::size_t>(device)];
+    if (!pool) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        CK(cudaMemPoolCreate(&pool, &props));
+        uint64_t threshold = UINT64_MAX;
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+    }
+    return pool;
+}
+
+int current_device() {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    return dev;
+}
+
+void* pool_alloc(std::size_t bytes, cudaStream_t s) {
+    void* p = nullptr;
+    CK(cudaMallocFromPoolAsync(&p, std::max<std::size_t>(bytes, 8), lib_pool(current_device()), s));
+    return p;
+}
+
 /// Device allocations owned by a plan.  With a stream set (plans), they come
 /// from the stream-ordered pool and go back to it without a device-wide
 /// synchronisation: per-call cudaMalloc/cudaFree of the ~50 table buffers
@@ -83,7 +121,10 @@ struct DeviceArena {
     T* alloc(std::size_t n) {
         void* p = nullptr;
         const std::size_t bytes = std::max<std::size_t>(1, n) * sizeof(T);
-        CK(s ? cudaMallocAsync(&p, bytes, s) : cudaMalloc(&p, bytes));
+        if (s)
+            p = pool_alloc(bytes, s);
+        else
+            CK(cudaMalloc(&p, bytes));
         ptrs.push_back(p);
         return static_cast<T*>(p);
     }
@@ -387,14 +428,6 @@ void alloc_element_scratch(DeviceArena& ar, lfb::DevTables& d, int n_terms) {
     d.Pe = ar.alloc<double>(per_term * static_cast<std::size_t>(d.pe_terms));
 }
 
-void keep_pool_memory(int device) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-        uint64_t threshold = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
-    }
-}
-
 void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void* stream, int t0, int t1) {
     if (!p)
         raise(LF_ERR_INVALID_ARGUMENT, "null problem");
@@ -407,7 +440,6 @@ void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void
         CK(cudaStreamCreateWithFlags(&plan->stream, cudaStreamNonBlocking));
         plan->own_stream = true;
     }
-    keep_pool_memory(device);
     const lfb::Setup& s = plan->setup;
     lfb::DevTables& d = plan->d;
     DeviceArena& ar = plan->arena;
@@ -573,9 +605,7 @@ void copy_d2h(void* dst, const void* src, std::size_t bytes, cudaStream_t s) {
 struct DeviceBuffer {
     void* p = nullptr;
     cudaStream_t s = nullptr;
-    DeviceBuffer(std::size_t bytes, cudaStream_t st) : s(st) {
-        CK(cudaMallocAsync(&p, std::max<std::size_t>(bytes, 8), st));
-    }
+    DeviceBuffer(std::size_t bytes, cudaStream_t st) : s(st) { p = pool_alloc(bytes, st); }
     ~DeviceBuffer() {
         if (p)
             cudaFreeAsync(p, s);
@@ -811,12 +841,11 @@ static int assemble_one_shot(const lf_problem* p, int backend, int device, int t
         OneShotStreams& streams = one_shot_streams(device);
         lf_plan plan;
         plan_init(&plan, p, backend, device, streams.main, t0, t1);
-        keep_pool_memory(device);
-        const lfb::Setup& s = plan.setup;
+            const lfb::Setup& s = plan.setup;
         if (s.nnz == 0) {
             if (t0 == 0 && t1 < 0) // the whole matrix: SparseMatrixBuilder::finalize (sparse.cpp:15-18)
                 raise(LF_ERR_LOGIC, "SparseMatrixBuilder: nothing accumulated");
-            row_ptr[0] = 0; // an empty slab
+            std::fill(row_ptr, row_ptr + s.rows + 1, int64_t(0)); // an empty slab: every row empty
             return;
         }
         const std::size_t rows = static_cast<std::size_t>(s.rows);
@@ -902,6 +931,7 @@ static int inplane_common(const lf_problem* p, const double table[81], int devic
         CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         {
             DeviceArena ar;
+            ar.s = st; // uploads ordered on the kernels' stream (a non-blocking stream does not wait for legacy copies)
             lfb::DevTables d{};
             upload_space(s, ar, d);
             upload_geometry(s, ar, d);
@@ -980,6 +1010,7 @@ int lf_thickness_operators(int32_t degree_t, int32_t n_knots_t, const double* kn
         CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         {
             DeviceArena ar;
+            ar.s = st; // uploads ordered on the kernels' stream
             lfb::DevTables d{};
             std::memset(&d, 0, sizeof d);
             d.pt = s.kt.p;
@@ -1077,11 +1108,11 @@ int lf_combine(const lf_problem* p, int32_t n_terms, const double* blocks, const
         if (nnz == 0)
             raise(LF_ERR_LOGIC, "SparseMatrixBuilder: nothing accumulated");
         use_device(device);
-        keep_pool_memory(device);
-        cudaStream_t st;
+            cudaStream_t st;
         CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         {
             DeviceArena ar;
+            ar.s = st; // uploads ordered on the kernels' stream
             lfb::DevTables d{};
             upload_space(s, ar, d);
             d.lo_t = ar.upload(at.lo);
@@ -1164,12 +1195,10 @@ int lf_csr_frobenius_sq(int64_t rows, const int64_t* d_row_ptr, const double* d_
                         double* out) {
     return guarded([&] {
         cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-        double* d_out = nullptr;
-        CK(cudaMallocAsync(&d_out, sizeof(double), st));
+        DeviceBuffer d_out(sizeof(double), st);
         CK(static_cast<cudaError_t>(lfb::launch_frobenius_sq(rows, reinterpret_cast<const long long*>(d_row_ptr),
-                                                             d_values, d_out, st)));
-        *out = fetch_scalar(d_out, st);
-        cudaFreeAsync(d_out, st);
+                                                             d_values, static_cast<double*>(d_out.p), st)));
+        *out = fetch_scalar(static_cast<double*>(d_out.p), st);
     });
 }
 
@@ -1186,27 +1215,66 @@ int lf_csr_diff_sq(int64_t rows, const int64_t* d_ra, const int32_t* d_ca, const
                    const int32_t* d_cb, const double* d_vb, void* cuda_stream, double* out) {
     return guarded([&] {
         cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-        double* d_out = nullptr;
-        CK(cudaMallocAsync(&d_out, sizeof(double), st));
+        DeviceBuffer d_out(sizeof(double), st);
         CK(static_cast<cudaError_t>(lfb::launch_diff_sq(
             rows, reinterpret_cast<const long long*>(d_ra), reinterpret_cast<const int*>(d_ca), d_va,
-            reinterpret_cast<const long long*>(d_rb), reinterpret_cast<const int*>(d_cb), d_vb, d_out, st)));
-        *out = fetch_scalar(d_out, st);
-        cudaFreeAsync(d_out, st);
+            reinterpret_cast<const long long*>(d_rb), reinterpret_cast<const int*>(d_cb), d_vb,
+            static_cast<double*>(d_out.p), st)));
+        *out = fetch_scalar(static_cast<double*>(d_out.p), st);
     });
+}
+
+static double symmetry_sq(int64_t rows, int64_t row_begin, const int64_t* d_row_ptr, const int32_t* d_cols,
+                          const double* d_values, cudaStream_t st, unsigned long long* n_outside) {
+    DeviceBuffer d_out(sizeof(double), st), d_cnt(sizeof(unsigned long long), st);
+    CK(static_cast<cudaError_t>(lfb::launch_symmetry_sq(
+        rows, row_begin, reinterpret_cast<const long long*>(d_row_ptr), reinterpret_cast<const int*>(d_cols),
+        d_values, static_cast<double*>(d_out.p), static_cast<unsigned long long*>(d_cnt.p), st)));
+    CK(cudaMemcpyAsync(n_outside, d_cnt.p, sizeof *n_outside, cudaMemcpyDeviceToHost, st));
+    return fetch_scalar(static_cast<double*>(d_out.p), st);
 }
 
 int lf_csr_symmetry_sq(int64_t rows, const int64_t* d_row_ptr, const int32_t* d_cols, const double* d_values,
                        void* cuda_stream, double* out) {
     return guarded([&] {
-        cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-        double* d_out = nullptr;
-        CK(cudaMallocAsync(&d_out, sizeof(double), st));
-        CK(static_cast<cudaError_t>(lfb::launch_symmetry_sq(rows, reinterpret_cast<const long long*>(d_row_ptr),
-                                                            reinterpret_cast<const int*>(d_cols), d_values, d_out,
-                                                            st)));
-        *out = fetch_scalar(d_out, st);
-        cudaFreeAsync(d_out, st);
+        unsigned long long outside = 0;
+        const double v = symmetry_sq(rows, 0, d_row_ptr, d_cols, d_values, static_cast<cudaStream_t>(cuda_stream),
+                                     &outside);
+        if (outside)
+            raise(LF_ERR_INVALID_ARGUMENT, "symmetryRelError: column index outside the matrix (a row slab? use "
+                                           "lf_csr_symmetry_sq_slab)");
+        *out = v;
+    });
+}
+
+int lf_csr_symmetry_sq_slab(int64_t rows, int64_t row_begin, const int64_t* d_row_ptr, const int32_t* d_cols,
+                            const double* d_values, void* cuda_stream, double* out, int64_t* n_skipped) {
+    return guarded([&] {
+        if (row_begin < 0)
+            raise(LF_ERR_INVALID_ARGUMENT, "symmetry: negative row_begin");
+        unsigned long long outside = 0;
+        *out = symmetry_sq(rows, row_begin, d_row_ptr, d_cols, d_values, static_cast<cudaStream_t>(cuda_stream),
+                           &outside);
+        if (n_skipped)
+            *n_skipped = static_cast<int64_t>(outside);
+    });
+}
+
+int lf_plan_symmetry_sq(lf_plan* plan, const double* d_values, double* out) {
+    return guarded([&] {
+        CK(cudaSetDevice(plan->device));
+        DeviceBuffer d_out(sizeof(double), plan->stream);
+        CK(static_cast<cudaError_t>(lfb::launch_plan_symmetry(plan->d, d_values, static_cast<double*>(d_out.p),
+                                                              plan->stream)));
+        *out = fetch_scalar(static_cast<double*>(d_out.p), plan->stream);
+    });
+}
+
+int lf_release_memory(int device) {
+    return guarded([&] {
+        use_device(device);
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemPoolTrimTo(lib_pool(device), 0));
     });
 }
 

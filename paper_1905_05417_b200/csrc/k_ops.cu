@@ -1001,35 +1001,113 @@ __global__ void k_diff_rows(long long rows, const long long* ra, const int* ca, 
         partial[blockIdx.x] = s;
 }
 
-__global__ void k_symmetry_rows(long long rows, const long long* rp, const int* c, const double* v,
-                                double* partial) {
+/// symmetryRelError numerator (sparse.cpp:73-95) of a CSR holding the rows
+/// [row_begin, row_begin + rows) of a matrix: one warp per row, the row's
+/// entries loaded coalesced, each lane's mirror found by a binary search of
+/// its column's row.  Entries whose mirror row lies outside the rows held are
+/// not counted (a row slab cannot see them); *outside counts them, so the
+/// full-matrix entry point can reject a slab passed as a whole matrix.
+__global__ void __launch_bounds__(256) k_symmetry_rows(long long rows, long long row_begin, const long long* rp,
+                                                       const int* c, const double* v, double* partial,
+                                                       unsigned long long* outside) {
     double s = 0.0;
-    for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
-         r += (long long)gridDim.x * blockDim.x) {
-        for (long long k = rp[r]; k < rp[r + 1]; ++k) {
-            const int col = c[k];
-            if (col < 0 || col >= rows) { // no mirror row in this matrix (e.g. a row slab): absent
-                s += 2.0 * v[k] * v[k];
+    unsigned long long n_out = 0;
+    const int lane = threadIdx.x & 31;
+    const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long r = w0; r < rows; r += nw) {
+        const long long gr = r + row_begin;
+        const long long k1 = __ldg(rp + r + 1);
+        for (long long k = __ldg(rp + r) + lane; k < k1; k += 32) {
+            const long long lr = (long long)__ldg(c + k) - row_begin;
+            if (lr < 0 || lr >= rows) {
+                ++n_out;
                 continue;
             }
-            long long lo = rp[col], hi = rp[col + 1];
+            long long lo = __ldg(rp + lr), hi = __ldg(rp + lr + 1);
+            const long long end = hi;
             while (lo < hi) {
                 const long long mid = (lo + hi) >> 1;
-                if (c[mid] < r)
+                if ((long long)__ldg(c + mid) < gr)
                     lo = mid + 1;
                 else
                     hi = mid;
             }
-            const bool mirrored = lo < rp[col + 1] && c[lo] == r;
-            const double dd = v[k] - (mirrored ? v[lo] : 0.0);
+            const bool mirrored = lo < end && (long long)__ldg(c + lo) == gr;
+            const double dd = __ldg(v + k) - (mirrored ? __ldg(v + lo) : 0.0);
             s += dd * dd;
             if (!mirrored)
-                s += dd * dd; // symmetryRelError counts the absent mirror slot (sparse.cpp:87-90)
+                s += dd * dd; // the structurally absent mirror slot counts too (sparse.cpp:87-90)
         }
     }
     s = block_sum(s);
     if (threadIdx.x == 0)
         partial[blockIdx.x] = s;
+    if (n_out)
+        atomicAdd(outside, n_out);
+}
+
+/// Closed-form symmetry numerator of a plan's slab: one
+/// thread per in-plane pair (i_s, slot) and thickness chunk.  For every
+/// coupled block (i, j) with i <= j whose mirror row block j lies in the slab,
+/// the 9 values of K_ij and the 9 of K_ji are read at their closed-form
+/// positions and sum_ab (K_ij[a][b] - K_ji[b][a])^2 is added once for i = j
+/// and twice for i < j (the reference visits both blocks).  The pattern is
+/// structurally symmetric, so no mirror slot is absent.  Reads each value
+/// once: consecutive threads take consecutive slots, so the K_ij rows load as
+/// contiguous 768-byte runs per warp.
+__global__ void __launch_bounds__(256) k_plan_symmetry(const DevTables d, const double* __restrict__ v,
+                                                       int t_chunk, double* partial) {
+    double s = 0.0;
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; // in-plane pair
+    if (q < d.S_s) {
+        const long long e = 9 * q;
+        int is = __ldg(d.blk_is + e / kBlock);
+        while (__ldg(d.es_pre + is + 1) <= e)
+            ++is;
+        const int slot = (int)((e - __ldg(d.es_pre + is)) / 9);
+        const int iu = is % d.nu, iv = is / d.nu;
+        const int Lu = __ldg(d.len_u + iu), Lv = __ldg(d.len_v + iv);
+        const int sv = slot / Lu, su = slot - sv * Lu;
+        const int ju = __ldg(d.lo_u + iu) + su, jv = __ldg(d.lo_v + iv) + sv;
+        const int js = jv * d.nu + ju;
+        const int Luj = __ldg(d.len_u + ju), Lvj = __ldg(d.len_v + jv);
+        const int slot_m = (iv - __ldg(d.lo_v + jv)) * Luj + (iu - __ldg(d.lo_u + ju));
+        const long long Bi = 3LL * Lu * Lv, Bj = 3LL * Luj * Lvj;
+        const long long esi = __ldg(d.es_pre + is), esj = __ldg(d.es_pre + js);
+        const long long pre0 = __ldg(d.pre_t + d.t0), nine_S = 9 * d.S_s;
+        const int it0 = d.t0 + blockIdx.y * t_chunk, it1 = min(d.t1, it0 + t_chunk);
+        for (int it = it0; it < it1; ++it) {
+            const int Lt = __ldg(d.len_t + it), lot = __ldg(d.lo_t + it);
+            const long long base_i = nine_S * (__ldg(d.pre_t + it) - pre0);
+            for (int k = 0; k < Lt; ++k) {
+                const int jt = lot + k;
+                if (jt < d.t0 || jt >= d.t1)
+                    continue; // mirror row block outside the slab
+                const long long gi = (long long)it * d.ns + is, gj = (long long)jt * d.ns + js;
+                if (gi > gj)
+                    continue;
+                const int Ltj = __ldg(d.len_t + jt);
+                const long long base_j = nine_S * (__ldg(d.pre_t + jt) - pre0);
+                const double* own = v + base_i + (long long)Lt * esi + (long long)k * Bi + 3 * slot;
+                const double* mir = v + base_j + (long long)Ltj * esj + (long long)(it - __ldg(d.lo_t + jt)) * Bj +
+                                    3 * slot_m;
+                double blk = 0.0;
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int b = 0; b < 3; ++b) {
+                        const double x = __ldg(own + (long long)a * Lt * Bi + b);
+                        const double y = __ldg(mir + (long long)b * Ltj * Bj + a);
+                        blk += (x - y) * (x - y);
+                    }
+                s += gi == gj ? blk : 2.0 * blk;
+            }
+        }
+    }
+    s = block_sum(s);
+    if (threadIdx.x == 0)
+        partial[(long long)blockIdx.y * gridDim.x + blockIdx.x] = s;
 }
 
 int reduce_launch(int blocks, double* partial, double* out, cudaStream_t stream) {
@@ -1194,12 +1272,33 @@ int launch_diff_sq(long long rows, const long long* ra, const int* ca, const dou
     return (int)cudaGetLastError();
 }
 
-int launch_symmetry_sq(long long rows, const long long* rp, const int* c, const double* v, double* out,
-                       cudaStream_t stream) {
-    const int blocks = 1024;
+int launch_symmetry_sq(long long rows, long long row_begin, const long long* rp, const int* c, const double* v,
+                       double* out, unsigned long long* outside, cudaStream_t stream) {
+    const int blocks = 148 * 8;
     double* partial = nullptr;
     cudaMallocAsync(&partial, sizeof(double) * blocks, stream);
-    k_symmetry_rows<<<blocks, 256, 0, stream>>>(rows, rp, c, v, partial);
+    cudaMemsetAsync(outside, 0, sizeof(unsigned long long), stream);
+    k_symmetry_rows<<<blocks, 256, 0, stream>>>(rows, row_begin, rp, c, v, partial, outside);
+    reduce_launch(blocks, partial, out, stream);
+    cudaFreeAsync(partial, stream);
+    return (int)cudaGetLastError();
+}
+
+int launch_plan_symmetry(const DevTables& d, const double* v, double* out, cudaStream_t stream) {
+    const int nt = d.t1 - d.t0;
+    if (d.S_s == 0 || nt <= 0) {
+        cudaMemsetAsync(out, 0, sizeof(double), stream);
+        return (int)cudaGetLastError();
+    }
+    const unsigned gx = (unsigned)((d.S_s + 255) / 256);
+    // ~16 blocks per SM in total, chunks of whole thickness rows
+    const int nchunk = (int)std::max(1LL, std::min<long long>(nt, (148LL * 16 + gx - 1) / gx));
+    const int t_chunk = (nt + nchunk - 1) / nchunk;
+    const unsigned gy = (unsigned)((nt + t_chunk - 1) / t_chunk);
+    const int blocks = (int)(gx * gy);
+    double* partial = nullptr;
+    cudaMallocAsync(&partial, sizeof(double) * blocks, stream);
+    k_plan_symmetry<<<dim3(gx, gy), 256, 0, stream>>>(d, v, t_chunk, partial);
     reduce_launch(blocks, partial, out, stream);
     cudaFreeAsync(partial, stream);
     return (int)cudaGetLastError();

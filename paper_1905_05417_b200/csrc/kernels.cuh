@@ -139,7 +139,11 @@ int launch_spmv(long long rows, const long long* rp, const int* c, const double*
 int launch_diff_sq(long long rows, const long long* ra, const int* ca, const double* va,
                    const long long* rb, const int* cb, const double* vb, double* out,
                    cudaStream_t stream);
-int launch_symmetry_sq(long long rows, const long long* rp, const int* c, const double* v,
-                       double* out, cudaStream_t stream);
+/// rows [row_begin, row_begin + rows) of a CSR; mirrors outside are skipped
+/// and counted into *outside (device)
+int launch_symmetry_sq(long long rows, long long row_begin, const long long* rp, const int* c,
+                       const double* v, double* out, unsigned long long* outside, cudaStream_t stream);
+/// closed-form symmetry numerator of a plan's slab values (pattern order)
+int launch_plan_symmetry(const DevTables& d, const double* v, double* out, cudaStream_t stream);
 
 } // namespace lfb

@@ -261,6 +261,7 @@ def test_full_size_config_slab_and_properties(gpu, oracle, name):
     st = gpu.device_csr_stats(plan.rows, rp.data_ptr(), cols.data_ptr(), vals.data_ptr())
     norm = np.sqrt(st["fro_sq"])
     assert np.sqrt(st["sym_sq"]) / norm <= 1e-13
+    assert np.sqrt(plan.symmetry_sq(vals.data_ptr())) / norm <= 1e-13
     import ctypes
     for d in range(3):
         x = torch.zeros(plan.rows, dtype=torch.float64, device="cuda")
@@ -748,23 +749,66 @@ def test_c5_full_size_rows_annihilate_translations(gpu):
     assert asym <= 1e-12 * np.sqrt(fro_sq) * float(u.norm()) * float(v.norm())
 
 
-def test_symmetry_check_accepts_row_slabs(gpu):
-    """lf_csr_symmetry_sq on a row slab (global columns beyond the slab's rows)
-    counts those entries as missing mirrors instead of reading out of bounds;
-    on the whole matrix it stays at roundoff."""
+def _host_symmetry_sq(rp, cols, vals, row_begin, dim):
+    """Reference numerator (sparse.cpp:73-95) restricted to the entries of the
+    slab whose mirror row lies in the slab: ||S - S^T||_F^2 of the slab's
+    square in-slab block (an absent mirror contributes v^2 twice either way)."""
+    import scipy.sparse as sp
+    rows = len(rp) - 1
+    S = sp.csr_matrix((vals, cols, rp), shape=(rows, dim))[:, row_begin:row_begin + rows].tocsr()
+    D = (S - S.T).tocsr()
+    return float(D.data @ D.data), int(len(vals) - S.nnz)
+
+
+@pytest.mark.parametrize("parts,part", [(1, 0), (3, 0), (3, 1), (3, 2)])
+def test_symmetry_sums_match_host_on_slabs(gpu, parts, part):
+    """Device symmetry numerators -- the generic CSR kernel with a global row
+    offset (lf_csr_symmetry_sq_slab) and the plan's closed-form kernel
+    (lf_plan_symmetry_sq) -- equal the host's on a C2 row slab whose values
+    carry a seeded asymmetric perturbation (a symmetric K would only compare
+    roundoff); the full-matrix entry point rejects a slab."""
     import ctypes
     import torch
     prob = P.baseline_config("C2")
     lib = gpu.library()
-    ptr = lambda t: ctypes.c_void_p(t.data_ptr())
-    full = _device_csr(gpu, prob, "fast")
+    b = gpu.slab_bounds(prob, parts, part)
+    plan = gpu.Plan(prob, "fast", 0, b["t_begin"], b["t_end"])
+    rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
+    cols = torch.empty(plan.nnz, dtype=torch.int32, device="cuda")
+    vals = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
+    plan.build_pattern(rp.data_ptr(), cols.data_ptr())
+    plan.assemble(vals.data_ptr())
+    plan.synchronize()
+    gen = torch.Generator(device="cuda").manual_seed(17 + part)
+    vals += 1e-3 * vals.abs().max() * torch.rand(plan.nnz, dtype=torch.float64, device="cuda", generator=gen)
+    want, skipped = _host_symmetry_sq(rp.cpu().numpy(), cols.cpu().numpy(), vals.cpu().numpy(),
+                                      b["row_begin"], prob.dim)
+    st = gpu.device_csr_stats(plan.rows, rp.data_ptr(), cols.data_ptr(), vals.data_ptr(), row_begin=b["row_begin"])
+    assert st["sym_sq"] == pytest.approx(want, rel=1e-12)
+    assert st["sym_skipped"] == skipped
+    assert plan.symmetry_sq(vals.data_ptr()) == pytest.approx(want, rel=1e-12)
     out = ctypes.c_double()
-    assert lib.lf_csr_symmetry_sq(full[0], ptr(full[1]), ptr(full[2]), ptr(full[3]), None, ctypes.byref(out)) == 0
-    fro = ctypes.c_double()
-    assert lib.lf_csr_frobenius_sq(full[0], ptr(full[1]), ptr(full[3]), None, ctypes.byref(fro)) == 0
-    assert out.value ** 0.5 <= 1e-13 * fro.value ** 0.5
-    b = gpu.slab_bounds(prob, 3, 1)
-    slab = _device_csr(gpu, prob, "fast", b["t_begin"], b["t_end"])
-    assert lib.lf_csr_symmetry_sq(slab[0], ptr(slab[1]), ptr(slab[2]), ptr(slab[3]), None, ctypes.byref(out)) == 0
-    torch.cuda.synchronize()
-    assert out.value > 0.0 and np.isfinite(out.value)
+    ptr = lambda t: ctypes.c_void_p(t.data_ptr())
+    status = lib.lf_csr_symmetry_sq(plan.rows, ptr(rp), ptr(cols), ptr(vals), None, ctypes.byref(out))
+    assert (status == 0) == (parts == 1)
+    if parts == 1:
+        assert out.value == pytest.approx(want, rel=1e-12)
+    plan.close()
+
+
+def test_symmetry_of_unperturbed_matrix_is_roundoff(gpu):
+    """Both symmetry kernels on the unperturbed C2 matrix: at roundoff."""
+    prob = P.baseline_config("C2")
+    import torch
+    plan = gpu.Plan(prob, "fast", 0)
+    rows, rp, cols, vals = plan.rows, None, None, None
+    rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
+    cols = torch.empty(plan.nnz, dtype=torch.int32, device="cuda")
+    vals = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
+    plan.build_pattern(rp.data_ptr(), cols.data_ptr())
+    plan.assemble(vals.data_ptr())
+    plan.synchronize()
+    st = gpu.device_csr_stats(rows, rp.data_ptr(), cols.data_ptr(), vals.data_ptr())
+    assert st["sym_sq"] ** 0.5 <= 1e-13 * st["fro_sq"] ** 0.5
+    assert plan.symmetry_sq(vals.data_ptr()) ** 0.5 <= 1e-13 * st["fro_sq"] ** 0.5
+    plan.close()
