@@ -67,6 +67,10 @@ class Oracle(_Base):
             "orc_assemble_fast": (c_int, [POINTER(_P), c_int, c_int, POINTER(c_int64),
                                           POINTER(c_int32), _dp, POINTER(c_int64),
                                           POINTER(abi.Stats)]),
+            "orc_fast_create": (c_int, [POINTER(_P), c_int, POINTER(ctypes.c_void_p)]),
+            "orc_fast_destroy": (None, [ctypes.c_void_p]),
+            "orc_fast_slab": (c_int, [ctypes.c_void_p, c_int, c_int, POINTER(c_int64), POINTER(c_int32), _dp,
+                                      POINTER(c_int64)]),
             "orc_assemble_standard": (c_int, [POINTER(_P), c_int, c_int, POINTER(c_int64),
                                               POINTER(c_int32), _dp, POINTER(c_int64),
                                               POINTER(abi.Stats)]),
@@ -135,6 +139,9 @@ class Oracle(_Base):
                                                      _d(q), occ.ctypes.data_as(POINTER(c_char))))
         return q, occ
 
+    def fast_terms(self, prob: LaminateProblem, want_values: bool = True) -> "FastTerms":
+        return FastTerms(self, prob, want_values)
+
     def assemble(self, prob: LaminateProblem, backend="fast", t0=0, t1=-1, want_stats=False):
         """(row_ptr, cols, values[, stats]) of the rows of thickness functions [t0, t1)."""
         fn = {"fast": self.lib.orc_assemble_fast, "voigt_free": self.lib.orc_assemble_fast,
@@ -157,6 +164,50 @@ class Oracle(_Base):
                        ctypes.byref(st)))
         out = (rp, cols[:nnz.value], vals[:nnz.value])
         return out + (st,) if want_stats else out
+
+
+class FastTerms:
+    """Operator terms of one problem built once by the oracle (orc_fast_*):
+    ``slab(t0, t1)`` combines any row slab, ``nnz_before(t)`` is the global
+    offset of thickness function t (the oracle's row_ptr of rows [0, t))."""
+
+    def __init__(self, oracle: "Oracle", prob: LaminateProblem, want_values: bool = True):
+        self.o = oracle
+        self.prob = prob
+        self._c = prob.to_c()
+        h = ctypes.c_void_p()
+        oracle._check(oracle.lib.orc_fast_create(ctypes.byref(self._c), 1 if want_values else 0,
+                                                 ctypes.byref(h)))
+        self.h = h
+
+    def slab(self, t0, t1):
+        rows = 3 * self.prob.n_s * (t1 - t0)
+        rp = np.zeros(rows + 1, dtype=np.int64)
+        nnz = c_int64()
+        lib = self.o.lib
+        self.o._check(lib.orc_fast_slab(self.h, t0, t1, rp.ctypes.data_as(POINTER(c_int64)), None, None,
+                                        ctypes.byref(nnz)))
+        cols = np.zeros(max(1, nnz.value), dtype=np.int32)
+        vals = np.zeros(max(1, nnz.value), dtype=np.float64)
+        self.o._check(lib.orc_fast_slab(self.h, t0, t1, rp.ctypes.data_as(POINTER(c_int64)),
+                                        cols.ctypes.data_as(POINTER(c_int32)), _d(vals), ctypes.byref(nnz)))
+        return rp, cols[:nnz.value], vals[:nnz.value]
+
+    def nnz_before(self, t):
+        nnz = c_int64()
+        self.o._check(self.o.lib.orc_fast_slab(self.h, 0, t, None, None, None, ctypes.byref(nnz)))
+        return nnz.value
+
+    def close(self):
+        if self.h:
+            self.o.lib.orc_fast_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class RefCsr(ctypes.Structure):

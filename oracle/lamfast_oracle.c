@@ -642,8 +642,38 @@ static size_t pset_slot(const orc_pset* ps, int is, int js) {
     return ((size_t)is * ps->bv + (size_t)(jv - iv + ps->pv)) * ps->bu + (size_t)(ju - iu + ps->pu);
 }
 
+/* Element-local m = sum_q W^T (w |det| D) W of element e (fast.cpp:98-124). */
+static int element_matrix(const orc_space* s, const lf_problem* p, const double* d, int e, orc_elem* el,
+                          double* w, double* dw, double* m) {
+    const int nl = (s->pu + 1) * (s->pv + 1);
+    const int n = 6 * nl;
+    const int eu = e % s->nspu, ev = e / s->nspu;
+    int st = build_elem(s, p, eu, ev, el);
+    if (st)
+        return st;
+    memset(m, 0, sizeof(double) * (size_t)n * n);
+    for (int q = 0; q < el->npts; ++q) {
+        const double* G = el->frame[q] + 9; /* dfit col-major: G(r,c) = G[3c+r] */
+        for (int js = 0; js < nl; ++js) {
+            double g1[3], g2[3];
+            for (int r = 0; r < 3; ++r) {
+                g1[r] = G[r] * el->du[q][js] + G[3 + r] * el->dv[q][js] + G[6 + r] * 0.0;
+                g2[r] = el->val[q][js] * G[6 + r];
+            }
+            strain_cols(w, n, js, g1);
+            strain_cols(w, n, nl + js, g2);
+        }
+        accumulate_wdw(n, w, d, el->weight[q] * el->frame[q][18], m, dw);
+    }
+    return LF_OK;
+}
+
+/* computeInplaneOperators (fast.cpp:54-168).  Element matrices are formed in
+ * parallel (OpenMP) in batches and scattered serially in element order, so
+ * every block is summed in the reference's element order whatever the thread
+ * count.  want_values = 0: only the occupancy flags (the pattern). */
 static int inplane_operators(const orc_space* s, const lf_problem* p, const double* d,
-                             orc_pset* ps) {
+                             orc_pset* ps, int want_values) {
     ps->nu = s->nu;
     ps->nv = s->nv;
     ps->pu = s->pu;
@@ -652,52 +682,75 @@ static int inplane_operators(const orc_space* s, const lf_problem* p, const doub
     ps->bv = 2 * s->pv + 1;
     ps->ns = s->ns;
     const size_t per = (size_t)ps->ns * ps->bv * ps->bu;
-    ps->blocks = calloc(4 * per * 9, sizeof(double));
+    ps->blocks = want_values ? calloc(4 * per * 9, sizeof(double)) : NULL;
     ps->flags = calloc(per, 1);
     const int nl = (s->pu + 1) * (s->pv + 1);
     const int n = 6 * nl;
-    double* w = calloc((size_t)6 * n, sizeof(double));
-    double* dw = calloc((size_t)6 * n, sizeof(double));
-    double* m = calloc((size_t)n * n, sizeof(double));
-    orc_elem* el = malloc(sizeof(orc_elem));
-    int st = LF_OK;
-    for (int e = 0; e < s->nspu * s->nspv && !st; ++e) {
-        const int eu = e % s->nspu, ev = e / s->nspu;
-        if ((st = build_elem(s, p, eu, ev, el)))
-            break;
-        memset(m, 0, sizeof(double) * (size_t)n * n);
-        for (int q = 0; q < el->npts; ++q) {
-            const double* G = el->frame[q] + 9; /* dfit col-major: G(r,c) = G[3c+r] */
-            for (int js = 0; js < nl; ++js) {
-                double g1[3], g2[3];
-                for (int r = 0; r < 3; ++r) {
-                    g1[r] = G[r] * el->du[q][js] + G[3 + r] * el->dv[q][js] + G[6 + r] * 0.0;
-                    g2[r] = el->val[q][js] * G[6 + r];
+    const int nel = s->nspu * s->nspv;
+    if (!want_values) {
+        for (int e = 0; e < nel; ++e) {
+            const orc_span* su = &s->spu[e % s->nspu];
+            const orc_span* sv = &s->spv[e / s->nspu];
+            for (int as = 0; as < nl; ++as)
+                for (int bs = 0; bs < nl; ++bs) {
+                    const int is = (sv->first + as / (s->pu + 1)) * s->nu + su->first + as % (s->pu + 1);
+                    const int js = (sv->first + bs / (s->pu + 1)) * s->nu + su->first + bs % (s->pu + 1);
+                    ps->flags[pset_slot(ps, is, js)] = 1;
                 }
-                strain_cols(w, n, js, g1);
-                strain_cols(w, n, nl + js, g2);
-            }
-            accumulate_wdw(n, w, d, el->weight[q] * el->frame[q][18], m, dw);
         }
-        for (int as = 0; as < nl; ++as)
-            for (int bs = 0; bs < nl; ++bs) {
-                const int is = el->funcs[as], js = el->funcs[bs];
-                const size_t slot = pset_slot(ps, is, js);
-                for (int ab = 0; ab < 4; ++ab) {
-                    const int ra = ab < 2 ? 3 * as : 3 * (nl + as);
-                    const int cb = ab % 2 == 0 ? 3 * bs : 3 * (nl + bs);
-                    double* blk = ps->blocks + ((size_t)ab * per + slot) * 9;
-                    for (int r = 0; r < 3; ++r)
-                        for (int c = 0; c < 3; ++c)
-                            blk[3 * r + c] += m[(ra + r) * n + cb + c];
-                }
-                ps->flags[slot] = 1;
-            }
+        return LF_OK;
     }
-    free(w);
-    free(dw);
-    free(m);
-    free(el);
+    const int batch = 1024;
+    double* mats = malloc(sizeof(double) * (size_t)batch * n * n);
+    int* funcs = malloc(sizeof(int) * (size_t)batch * nl);
+    int* est = malloc(sizeof(int) * (size_t)batch);
+    int st = LF_OK;
+    for (int e0 = 0; e0 < nel && !st; e0 += batch) {
+        const int nb = nel - e0 < batch ? nel - e0 : batch;
+#pragma omp parallel
+        {
+            orc_elem* el = malloc(sizeof(orc_elem));
+            double* w = calloc((size_t)6 * n, sizeof(double));
+            double* dw = calloc((size_t)6 * n, sizeof(double));
+#pragma omp for schedule(dynamic, 4)
+            for (int k = 0; k < nb; ++k) {
+                est[k] = element_matrix(s, p, d, e0 + k, el, w, dw, mats + (size_t)k * n * n);
+                memcpy(funcs + (size_t)k * nl, el->funcs, sizeof(int) * (size_t)nl);
+            }
+            free(el);
+            free(w);
+            free(dw);
+        }
+        for (int k = 0; k < nb && !st; ++k) {
+            if (est[k]) { /* first failing element in element order: redo it serially for its message */
+                orc_elem* el = malloc(sizeof(orc_elem));
+                st = build_elem(s, p, (e0 + k) % s->nspu, (e0 + k) / s->nspu, el);
+                free(el);
+                if (!st)
+                    st = est[k];
+                break;
+            }
+            const double* m = mats + (size_t)k * n * n;
+            const int* fk = funcs + (size_t)k * nl;
+            for (int as = 0; as < nl; ++as)
+                for (int bs = 0; bs < nl; ++bs) {
+                    const int is = fk[as], js = fk[bs];
+                    const size_t slot = pset_slot(ps, is, js);
+                    for (int ab = 0; ab < 4; ++ab) {
+                        const int ra = ab < 2 ? 3 * as : 3 * (nl + as);
+                        const int cb = ab % 2 == 0 ? 3 * bs : 3 * (nl + bs);
+                        double* blk = ps->blocks + ((size_t)ab * per + slot) * 9;
+                        for (int r = 0; r < 3; ++r)
+                            for (int c = 0; c < 3; ++c)
+                                blk[3 * r + c] += m[(ra + r) * n + cb + c];
+                    }
+                    ps->flags[slot] = 1;
+                }
+        }
+    }
+    free(mats);
+    free(funcs);
+    free(est);
     return st;
 }
 
@@ -709,7 +762,7 @@ int orc_inplane_operators(const lf_problem* p, const double d[36], double* block
         return st;
     }
     orc_pset ps;
-    st = inplane_operators(&s, p, d, &ps);
+    st = inplane_operators(&s, p, d, &ps, 1);
     if (!st) {
         const size_t per = (size_t)ps.ns * ps.bv * ps.bu;
         memcpy(blocks, ps.blocks, 4 * per * 9 * sizeof(double));
@@ -795,7 +848,7 @@ static void terms_free(orc_terms* t) {
 /* Operator terms of assembleFast (fast.cpp:283-336) or assembleVoigtFree's
  * equivalent (here with strain-form P; both produce the same operators). */
 static int build_terms(const orc_space* s, const lf_problem* p, orc_terms* terms, char* occ,
-                       lf_stats* stats) {
+                       lf_stats* stats, int want_values) {
     const int nt = s->nt, L = p->n_layers;
     int* cfg = malloc(sizeof(int) * (size_t)L);
     double* cd = malloc(sizeof(double) * 36 * (size_t)L);
@@ -814,7 +867,7 @@ static int build_terms(const orc_space* s, const lf_problem* p, orc_terms* terms
         terms->ps = calloc((size_t)ncfg, sizeof(orc_pset));
         terms->thick = calloc((size_t)ncfg * 4 * nn, sizeof(double));
         for (int c = 0; c < ncfg && !st; ++c) {
-            st = inplane_operators(s, p, cd + 36 * c, &terms->ps[c]);
+            st = inplane_operators(s, p, cd + 36 * c, &terms->ps[c], want_values);
             for (int l = 0; l < L; ++l) {
                 if (cfg[l] != c || !layer_active(p, l))
                     continue;
@@ -849,7 +902,7 @@ static int build_terms(const orc_space* s, const lf_problem* p, orc_terms* terms
                 break;
             for (int k = 0; k < 5 && !st; ++k) {
                 const int t = 5 * g + k;
-                st = inplane_operators(s, p, basis + 36 * k, &terms->ps[t]);
+                st = inplane_operators(s, p, basis + 36 * k, &terms->ps[t], want_values);
                 for (int l = 0; l < L; ++l) {
                     if (!constants_equal(&p->layers[l].constants, &p->layers[grp[g]].constants) ||
                         !layer_active(p, l))
@@ -878,54 +931,86 @@ done:
 }
 
 /* combineOperators (fast.cpp:211-264) in slab mode; CSR emitted in sorted
- * order.  With values == NULL only counts rows/nnz. */
+ * order.  With values == NULL only counts rows/nnz.  Row block (it, is) holds
+ * 3 rows of occ(it) x band(is) x 3 entries each (the triplets addBlock emits
+ * for that function, sparse.cpp:15-21); its offset is the prefix sum of the
+ * block sizes, so blocks are filled independently (OpenMP) with the same
+ * values and columns as the serial loop. */
 static int combine(const orc_space* s, const orc_terms* terms, const char* occ, int t0, int t1,
                    int64_t* row_ptr, int32_t* cols, double* values, int64_t* nnz_out) {
     const int nt = s->nt, ns = s->ns;
     const orc_pset* pat = &terms->ps[0];
     const size_t per = (size_t)pat->ns * pat->bv * pat->bu;
     const size_t nn = (size_t)nt * nt;
-    int* bandcols = malloc(sizeof(int) * (size_t)pat->bu * pat->bv);
-    int64_t k = 0, row = 0;
-    if (row_ptr)
+    const int bmax = pat->bu * pat->bv;
+    int* bandcols = malloc(sizeof(int) * (size_t)ns * bmax); /* occupied js of each is, ascending */
+    int* nband = malloc(sizeof(int) * (size_t)ns);
+    for (int is = 0; is < ns; ++is) {
+        const int iu = is % s->nu, iv = is / s->nu;
+        int nb = 0;
+        for (int jv = iv - s->pv < 0 ? 0 : iv - s->pv; jv <= (iv + s->pv < s->nv - 1 ? iv + s->pv : s->nv - 1); ++jv)
+            for (int ju = iu - s->pu < 0 ? 0 : iu - s->pu; ju <= (iu + s->pu < s->nu - 1 ? iu + s->pu : s->nu - 1); ++ju) {
+                const int js = jv * s->nu + ju;
+                if (pat->flags[pset_slot(pat, is, js)])
+                    bandcols[(size_t)is * bmax + nb++] = js;
+            }
+        nband[is] = nb;
+    }
+    const int nslab = t1 - t0;
+    int* tcols = malloc(sizeof(int) * (size_t)(nslab > 0 ? nslab : 1) * nt); /* occupied jt of each it */
+    int* ntc = malloc(sizeof(int) * (size_t)(nslab > 0 ? nslab : 1));
+    for (int it = t0; it < t1; ++it) {
+        int c = 0;
+        for (int jt = 0; jt < nt; ++jt)
+            if (occ[(size_t)it * nt + jt])
+                tcols[(size_t)(it - t0) * nt + c++] = jt;
+        ntc[it - t0] = c;
+    }
+    const size_t nblk = (size_t)(nslab > 0 ? nslab : 0) * ns;
+    int64_t* boff = malloc(sizeof(int64_t) * (nblk + 1));
+    boff[0] = 0;
+    for (size_t bk = 0; bk < nblk; ++bk)
+        boff[bk + 1] = boff[bk] + 9LL * ntc[bk / ns] * nband[bk % ns];
+    if (row_ptr) {
         row_ptr[0] = 0;
-    for (int it = t0; it < t1; ++it)
-        for (int is = 0; is < ns; ++is) {
-            const int iu = is % s->nu, iv = is / s->nu;
-            int nb = 0;
-            for (int jv = iv - s->pv < 0 ? 0 : iv - s->pv; jv <= (iv + s->pv < s->nv - 1 ? iv + s->pv : s->nv - 1); ++jv)
-                for (int ju = iu - s->pu < 0 ? 0 : iu - s->pu; ju <= (iu + s->pu < s->nu - 1 ? iu + s->pu : s->nu - 1); ++ju) {
-                    const int js = jv * s->nu + ju;
-                    if (pat->flags[pset_slot(pat, is, js)])
-                        bandcols[nb++] = js;
-                }
-            for (int a = 0; a < 3; ++a, ++row) {
-                for (int jt = 0; jt < nt; ++jt) {
-                    if (!occ[(size_t)it * nt + jt])
-                        continue;
-                    for (int x = 0; x < nb; ++x) {
-                        const int js = bandcols[x];
+        for (size_t bk = 0; bk < nblk; ++bk) {
+            const int64_t len = 3LL * ntc[bk / ns] * nband[bk % ns];
+            for (int a = 0; a < 3; ++a)
+                row_ptr[3 * bk + a + 1] = boff[bk] + (a + 1) * len;
+        }
+    }
+    if (values) {
+#pragma omp parallel for schedule(dynamic, 64)
+        for (long long bk = 0; bk < (long long)nblk; ++bk) {
+            const int it = t0 + (int)(bk / ns), is = (int)(bk % ns);
+            const int* jts = tcols + (size_t)(it - t0) * nt;
+            const int njt = ntc[it - t0], nb = nband[is];
+            int64_t k = boff[bk];
+            for (int a = 0; a < 3; ++a)
+                for (int x = 0; x < njt; ++x) {
+                    const int jt = jts[x];
+                    for (int y = 0; y < nb; ++y) {
+                        const int js = bandcols[(size_t)is * bmax + y];
                         const size_t slot = pset_slot(pat, is, js);
-                        for (int b = 0; b < 3; ++b) {
-                            if (values) {
-                                double blk = 0.0;
-                                for (int t = 0; t < terms->n; ++t)
-                                    for (int ab = 0; ab < 4; ++ab)
-                                        blk += terms->ps[t].blocks[((size_t)ab * per + slot) * 9 + 3 * a + b] *
-                                               terms->thick[((size_t)t * 4 + ab) * nn + (size_t)it * nt + jt];
-                                values[k] = 0.0 + blk; /* finalize: sum = 0.0; sum += v */
-                                cols[k] = 3 * (jt * ns + js) + b;
-                            }
-                            ++k;
+                        for (int b = 0; b < 3; ++b, ++k) {
+                            double blk = 0.0;
+                            for (int t = 0; t < terms->n; ++t)
+                                for (int ab = 0; ab < 4; ++ab)
+                                    blk += terms->ps[t].blocks[((size_t)ab * per + slot) * 9 + 3 * a + b] *
+                                           terms->thick[((size_t)t * 4 + ab) * nn + (size_t)it * nt + jt];
+                            values[k] = 0.0 + blk; /* finalize: sum = 0.0; sum += v */
+                            cols[k] = 3 * (jt * ns + js) + b;
                         }
                     }
                 }
-                if (row_ptr)
-                    row_ptr[row + 1] = k;
-            }
         }
+    }
+    *nnz_out = boff[nblk];
+    free(boff);
+    free(tcols);
+    free(ntc);
     free(bandcols);
-    *nnz_out = k;
+    free(nband);
     return LF_OK;
 }
 
@@ -937,32 +1022,78 @@ static int check_slab(const orc_space* s, int* t0, int* t1) {
     return LF_OK;
 }
 
+/* The operator terms of one problem, built once and combined into any
+ * number of row slabs (the checker of a full-size problem compares several
+ * slabs; building P is the expensive part). */
+typedef struct orc_fast {
+    orc_space s;
+    orc_terms terms;
+    char* occ;
+    lf_stats stats;
+} orc_fast;
+
+int orc_fast_create(const lf_problem* p, int want_values, orc_fast** out) {
+    *out = NULL;
+    orc_fast* f = calloc(1, sizeof(orc_fast));
+    int st = space_init(&f->s, p);
+    if (!st && p->n_layers < 1)
+        st = orc_fail(LF_ERR_INVALID_ARGUMENT, "assembleFast: empty layup");
+    if (st) {
+        space_free(&f->s);
+        free(f);
+        return st;
+    }
+    f->occ = malloc((size_t)f->s.nt * f->s.nt);
+    st = build_terms(&f->s, p, &f->terms, f->occ, &f->stats, want_values);
+    if (!st && f->terms.n == 0)
+        st = orc_fail(LF_ERR_INVALID_ARGUMENT, "combineOperators: no operator terms");
+    if (st) {
+        terms_free(&f->terms);
+        free(f->occ);
+        space_free(&f->s);
+        free(f);
+        return st;
+    }
+    *out = f;
+    return LF_OK;
+}
+
+void orc_fast_destroy(orc_fast* f) {
+    if (!f)
+        return;
+    terms_free(&f->terms);
+    free(f->occ);
+    space_free(&f->s);
+    free(f);
+}
+
+/* Rows of thickness functions [t0, t1); values == NULL: only *nnz (and
+ * row_ptr when given).  The handle must have been created with values. */
+int orc_fast_slab(const orc_fast* f, int t0, int t1, int64_t* row_ptr, int32_t* cols, double* values,
+                  int64_t* nnz) {
+    int st = check_slab(&f->s, &t0, &t1);
+    if (st)
+        return st;
+    if (values && !f->terms.ps[0].blocks)
+        return orc_fail(LF_ERR_INVALID_ARGUMENT, "oracle: handle built without values");
+    return combine(&f->s, &f->terms, f->occ, t0, t1, row_ptr, cols, values, nnz);
+}
+
 /* assembleFast (fast.cpp:266-339), rows of thickness functions [t0, t1).
  * values == NULL: only *nnz (and row_ptr when given) are produced. */
 int orc_assemble_fast(const lf_problem* p, int t0, int t1, int64_t* row_ptr, int32_t* cols,
                       double* values, int64_t* nnz, lf_stats* stats) {
-    orc_space s;
-    int st = space_init(&s, p);
-    if (!st)
-        st = check_slab(&s, &t0, &t1);
-    if (st) {
-        space_free(&s);
+    orc_fast* f = NULL;
+    int st = orc_fast_create(p, values != NULL, &f);
+    if (st)
         return st;
+    st = orc_fast_slab(f, t0, t1, row_ptr, cols, values, nnz);
+    if (!st && values && stats) {
+        stats->qpoint_visits += f->stats.qpoint_visits;
+        stats->frame_evaluations += f->stats.frame_evaluations;
+        stats->operator_builds += f->stats.operator_builds;
     }
-    if (p->n_layers < 1) {
-        space_free(&s);
-        return orc_fail(LF_ERR_INVALID_ARGUMENT, "assembleFast: empty layup");
-    }
-    char* occ = malloc((size_t)s.nt * s.nt);
-    orc_terms terms;
-    st = build_terms(&s, p, &terms, occ, values ? stats : NULL);
-    if (!st && terms.n == 0)
-        st = orc_fail(LF_ERR_INVALID_ARGUMENT, "combineOperators: no operator terms");
-    if (!st)
-        st = combine(&s, &terms, occ, t0, t1, row_ptr, cols, values, nnz);
-    terms_free(&terms);
-    free(occ);
-    space_free(&s);
+    orc_fast_destroy(f);
     return st;
 }
 

@@ -1,0 +1,60 @@
+"""Full-size BASELINE configs pinned against the oracle (not against another
+device path): row slabs of three thickness functions at the bottom, middle
+and top of C3, C4 and C5 -- C5 at its full 192 x 192, p = 3, 128-ply size,
+where the top slabs sit past 2^32 in the global CSR -- each compared with
+the oracle's rows of the same slab (pattern bit-exact, values within
+1e-12 * max|K|), and the slabs' global offsets (lf_slab_bounds, the plan's
+nnz_begin) against the oracle's global row offsets (fast.cpp:241-258,
+sparse.cpp:30-55)."""
+import numpy as np
+import pytest
+
+from conftest import assert_csr_match
+from paper_1905_05417_b200 import problem as P
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+RTOL = 1e-12
+
+
+def _device_slab(gpu, prob, t0, t1):
+    import torch
+    plan = gpu.Plan(prob, "fast", 0, t0, t1)
+    rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
+    cols = torch.empty(max(1, plan.nnz), dtype=torch.int32, device="cuda")
+    vals = torch.empty(max(1, plan.nnz), dtype=torch.float64, device="cuda")
+    plan.build_pattern(rp.data_ptr(), cols.data_ptr())
+    plan.assemble(vals.data_ptr())
+    plan.synchronize()
+    out = (rp.cpu().numpy(), cols[:plan.nnz].cpu().numpy(), vals[:plan.nnz].cpu().numpy())
+    info = {"nnz_begin": plan.nnz_begin, "row_begin": plan.row_begin, "nnz": plan.nnz}
+    plan.close()
+    del rp, cols, vals
+    torch.cuda.empty_cache()
+    return out, info
+
+
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_full_size_boundary_slabs_match_oracle(gpu, oracle, name):
+    prob = P.baseline_config(name)
+    terms = oracle.fast_terms(prob)
+    nt = prob.n_t
+    for t in (0, nt // 2, nt - 3):
+        got, info = _device_slab(gpu, prob, t, t + 3)
+        want = terms.slab(t, t + 3)
+        assert_csr_match(got, want, RTOL)
+        # global placement: the slab's first entry is the oracle's row offset of row 3 n_s t
+        assert info["nnz_begin"] == terms.nnz_before(t)
+        assert info["row_begin"] == 3 * prob.n_s * t
+        assert info["nnz_begin"] + info["nnz"] == terms.nnz_before(t + 3)
+    total = terms.nnz_before(nt)
+    assert total == P.sizes(prob)["nnz"]
+    if name == "C5":
+        assert terms.nnz_before(nt - 3) > 2 ** 32  # the top slab's offsets need int64
+    # the multi-GPU cuts: every part's global offsets equal the oracle's
+    for parts in (2, 8):
+        for part in range(parts):
+            b = gpu.slab_bounds(prob, parts, part)
+            assert b["nnz_begin"] == terms.nnz_before(b["t_begin"])
+            assert b["nnz_end"] == terms.nnz_before(b["t_end"])
+    terms.close()
