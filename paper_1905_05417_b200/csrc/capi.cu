@@ -208,35 +208,6 @@ void upload_space(const lfb::Setup& s, DeviceArena& ar, lfb::DevTables& d) {
             blk[b] = is;
         }
         d.blk_is = ar.upload(blk);
-        // warp-specialised combine: blocks of whole row segments (a, slot, b)
-        // of one i_s, packed greedily up to the producers' capacity
-        // (profiles/r1_store_modes.md)
-        d.ws_variant = 0; // direct stores by default; warp-specialised is opt-in (slower so far)
-        if (const char* m = std::getenv("LAMFAST_WS"))
-            d.ws_variant = std::atoi(m);
-        const long long cap = d.ws_variant == 1 ? 448 : d.ws_variant == 2 ? 384 : 512;
-        std::vector<long long> e0;
-        std::vector<int> is0;
-        long long cur = -1;
-        bool ok = d.ws_variant > 0;
-        for (int is = 0; is < s.n_s && ok; ++is) {
-            const long long B = 3LL * s.au.len[static_cast<std::size_t>(is % s.n_u)] *
-                                s.av.len[static_cast<std::size_t>(is / s.n_u)];
-            if (B > cap)
-                ok = false;
-            for (int a = 0; a < 3 && ok; ++a) {
-                const long long g0 = s.es_pre[static_cast<std::size_t>(is)] + a * B;
-                if (cur < 0 || g0 + B - cur > cap) {
-                    e0.push_back(g0);
-                    is0.push_back(is);
-                    cur = g0;
-                }
-            }
-        }
-        e0.push_back(E);
-        d.n_gbw = ok ? static_cast<int>(e0.size()) - 1 : 0;
-        d.gbw_e0 = reinterpret_cast<const long long*>(ar.upload(e0));
-        d.gbw_is = ar.upload(is0);
     }
     d.S_s = s.S_s;
     d.S_u = s.au.total;
@@ -289,75 +260,6 @@ void upload_terms(DeviceArena& ar, lfb::DevTables& d, int n_terms, int n_layers,
 }
 
 
-/// Team layout of the bulk-store combine (k_combine_team): pick (team warps,
-/// entries per thread) so that an interior row-segment group fits, P stays
-/// in registers (EPT * terms * 4 <= 48 doubles) and the lanes are best used;
-/// then pack consecutive whole groups (i_s, a) greedily into team ranges.
-void upload_teams(const lfb::Setup& s, DeviceArena& ar, lfb::DevTables& d) {
-    d.n_team = 0;
-    d.tm_team = 0;
-    d.tm_ept = 0;
-    if (d.n_passes != 1 || d.n_terms > 4 || d.E == 0)
-        return;
-    long long bmax = 0;
-    for (int is = 0; is < s.n_s; ++is)
-        bmax = std::max<long long>(bmax, 3LL * s.au.len[static_cast<std::size_t>(is % s.n_u)] *
-                                             s.av.len[static_cast<std::size_t>(is / s.n_u)]);
-    // Opt-in (measured slower than the direct stores so far, profiles/r1_store_modes.md):
-    // LAMFAST_TEAM=<team>,<ept> selects a layout, LAMFAST_TEAM=auto the heuristic below.
-    const char* env = std::getenv("LAMFAST_TEAM");
-    if (!env)
-        return;
-    int team = 0, ept = 0;
-    if (std::strcmp(env, "auto") != 0) {
-        if (std::sscanf(env, "%d,%d", &team, &ept) != 2)
-            team = 0;
-        if (team <= 0 || team > 8 || ept < 1 || ept > 3)
-            return;
-    } else {
-        double best = -1.0;
-        for (int t = 1; t <= 8; ++t)
-            for (int e = 1; e <= 3; ++e) {
-                const long long cap = 32LL * t * e;
-                if (cap < bmax || e * d.n_terms * 4 > 48)
-                    continue;
-                const double util = static_cast<double>((cap / bmax) * bmax) / static_cast<double>(cap);
-                // prefer lane utilisation, then fewer warps per team barrier
-                const double score = util - 0.01 * t;
-                if (score > best) {
-                    best = score;
-                    team = t;
-                    ept = e;
-                }
-            }
-        if (team == 0)
-            return;
-    }
-    const long long cap = 32LL * team * ept;
-    if (cap < bmax)
-        return;
-    std::vector<long long> e0;
-    std::vector<int> is0;
-    long long cur = -1;
-    for (int is = 0; is < s.n_s; ++is) {
-        const long long B = 3LL * s.au.len[static_cast<std::size_t>(is % s.n_u)] *
-                            s.av.len[static_cast<std::size_t>(is / s.n_u)];
-        for (int a = 0; a < 3; ++a) {
-            const long long g0 = s.es_pre[static_cast<std::size_t>(is)] + a * B;
-            if (cur < 0 || g0 + B - cur > cap) {
-                e0.push_back(g0);
-                is0.push_back(is);
-                cur = g0;
-            }
-        }
-    }
-    e0.push_back(d.E);
-    d.n_team = static_cast<int>(e0.size()) - 1;
-    d.tm_team = team;
-    d.tm_ept = ept;
-    d.tm_e0 = reinterpret_cast<const long long*>(ar.upload(e0));
-    d.tm_is = ar.upload(is0);
-}
 } // namespace
 
 struct lf_plan {
@@ -412,15 +314,8 @@ struct lf_plan {
 namespace {
 
 /// Element-local scratch of the two-phase general in-plane kernel (K2b):
-/// as many terms per batch as fit in ~2 GB (one at least).  LAMFAST_K2B=coloured
-/// keeps the coloured in-place form, LAMFAST_K2B=mma the DMMA element kernel (A/B).
+/// as many terms per batch as fit in ~2 GB (one at least).
 void alloc_element_scratch(DeviceArena& ar, lfb::DevTables& d, int n_terms) {
-    const char* env = std::getenv("LAMFAST_K2B");
-    if (env && std::string(env) == "coloured") {
-        d.Pe = nullptr;
-        d.pe_terms = 0;
-        return;
-    }
     const std::size_t nl2 = static_cast<std::size_t>(d.pu + 1) * (d.pv + 1);
     const std::size_t per_term = static_cast<std::size_t>(d.nspu) * d.nspv * 36 * nl2 * nl2;
     const std::size_t budget = (std::size_t(2) << 30) / sizeof(double);
@@ -462,8 +357,6 @@ void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void
                             amax = std::max(amax, std::fabs(x));
                             dmax = std::max(dmax, std::fabs(x - y));
                         }
-        // warp-contiguous entry slots in k_combine (C4 2.79 -> 2.66 ms); LAMFAST_CONTIG=0 restores strided
-        d.contig = std::getenv("LAMFAST_CONTIG") ? std::atoi(std::getenv("LAMFAST_CONTIG")) : 1;
         d.sym = (dmax <= 1e-15 * amax && !std::getenv("LAMFAST_NO_SYM")) ? 1 : 0;
     }
     d.layer_config = ar.upload(s.layup.layer_config);
@@ -472,13 +365,7 @@ void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void
     d.n_pairs = s.n_pairs;
     d.nnz_slab = s.nnz;
     if (backend != LF_BACKEND_STANDARD) {
-        upload_teams(s, ar, d);
         d.W = ar.alloc<double>(static_cast<std::size_t>(std::max<long long>(1, d.n_pairs)) * d.n_terms * 4);
-        if (d.ws_variant > 0 && d.n_terms <= 4) {
-            const std::size_t rows = static_cast<std::size_t>(std::max(1, d.t1 - d.t0));
-            d.g_rows = ar.alloc<unsigned char>(rows * 32);
-            d.g_w = ar.alloc<double>(rows * static_cast<std::size_t>(std::max(1, d.lt_max)) * d.n_terms * 4);
-        }
         d.Wmask = ar.alloc<unsigned>(static_cast<std::size_t>(std::max<long long>(1, d.n_pairs)) * d.n_passes);
         if (!d.affine) {
             d.Pg = ar.alloc<double>(static_cast<std::size_t>(d.n_terms) * 4 * static_cast<std::size_t>(d.E));
@@ -486,11 +373,10 @@ void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void
         }
     }
     // graph replay for launch-bound plans (<= 64M values, or any standard plan:
-    // its colour launches are many and short); not with the opt-in store
-    // variants, whose constant-bank hand-off orders launches through events
+    // its colour launches are many and short)
     const char* ge = std::getenv("LAMFAST_GRAPH");
     const bool small = s.nnz <= (64LL << 20) || backend == LF_BACKEND_STANDARD;
-    plan->use_graph = (ge ? std::atoi(ge) != 0 : small) && d.ws_variant == 0 && d.n_team == 0;
+    plan->use_graph = ge ? std::atoi(ge) != 0 : small;
     CK(cudaStreamSynchronize(plan->stream)); // the uploads' host sources are temporaries
 }
 
@@ -534,8 +420,6 @@ int plan_launch(lf_plan* plan, double* values, bool timed = true) {
             CK(static_cast<cudaError_t>(lfb::launch_thickness_pairs(d, s)));
             ++launches;
         }
-        if (!d.Pe) // the coloured form accumulates in place
-            CK(cudaMemsetAsync(d.Pg, 0, sizeof(double) * static_cast<std::size_t>(d.n_terms) * 4 * d.E, s));
         CK(static_cast<cudaError_t>(lfb::launch_inplane_general(d, s)));
         launches += lfb::inplane_general_launches(d);
     }
@@ -1129,7 +1013,6 @@ int lf_combine(const lf_problem* p, int32_t n_terms, const double* blocks, const
             d.t1 = nt;
             d.n_pairs = at.total;
             d.nnz_slab = nnz;
-            d.contig = 1;
             // P: banded -> entry layout
             const std::size_t per = static_cast<std::size_t>(s.n_s) * bv * bu;
             std::vector<double> pg(static_cast<std::size_t>(n_terms) * 4 * d.E);

@@ -1,6 +1,7 @@
 // K4: the hot kernel -- P (x) q~ straight into the CSR value array
-// (fast.cpp:211-264 + sparse.cpp:30-55), and its launcher.  The opt-in store
-// variants (team/TMA bulk copy, warp-specialised) live in k_combine_variants.cu.
+// (fast.cpp:211-264 + sparse.cpp:30-55), and its launcher.  The store
+// variants measured slower in round 1 (team/TMA bulk copy, warp-specialised)
+// are kept out of the product in tools/experiments/k_combine_variants.cu.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -9,10 +10,6 @@
 #include "combine_common.cuh"
 
 namespace lfb {
-
-// k_combine_variants.cu: true when an opt-in store variant handled the launch
-bool launch_combine_variant(const DevTables& d, double* out, int t_chunk_req, int lt_max, cudaStream_t stream,
-                            int* launches);
 
 namespace {
 
@@ -33,12 +30,11 @@ __device__ __forceinline__ void combine_body(const DevTables& d, double* __restr
     bool live[EPT];
 #pragma unroll
     for (int x = 0; x < EPT; ++x) {
-        // entry of slot x: 'strided' e = (blockIdx*EPT + x)*256 + tid, or
-        // 'contiguous' (d.contig) e = blockIdx*256*EPT + warp*32*EPT + x*32 + lane,
-        // where a warp's EPT stores per (row, k) are adjacent 256-byte runs
-        const long long e = d.contig ? (long long)blockIdx.x * BT * EPT + (threadIdx.x >> 5) * 32 * EPT + x * 32 +
-                                           (threadIdx.x & 31)
-                                     : (long long)(blockIdx.x * EPT + x) * BT + threadIdx.x;
+        // entry of slot x: e = blockIdx*256*EPT + warp*32*EPT + x*32 + lane, so
+        // a warp's EPT stores per (row, k) are adjacent 256-byte runs (these
+        // warp-contiguous slots measured C4 2.79 -> 2.66 ms against strided ones)
+        const long long e = (long long)blockIdx.x * BT * EPT + (threadIdx.x >> 5) * 32 * EPT + x * 32 +
+                            (threadIdx.x & 31);
         live[x] = e < d.E;
         const long long ec = live[x] ? e : d.E - 1;
         int is = __ldg(d.blk_is + ec / kBlock);
@@ -208,7 +204,6 @@ int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t st
         if (const char* env = std::getenv("LAMFAST_TCHUNK"))
             t_chunk = std::atoi(env);
     }
-    const int t_chunk_req = t_chunk;
     if (t_chunk <= 0) {
         // 48 thickness rows per block amortise the per-block prologue (P in
         // registers, entry decode, staging); shorter chunks (down to 32) only
@@ -229,8 +224,6 @@ int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t st
     }
     const unsigned nchunk = (unsigned)((nt + t_chunk - 1) / t_chunk);
     const int lt_max = std::max(1, d.lt_max);
-    if (d.n_passes == 1 && launch_combine_variant(d, out, t_chunk_req, lt_max, stream, launches))
-        return (int)cudaGetLastError();
     for (int pass = 0; pass < d.n_passes; ++pass) {
         const int nterm = std::min(8, d.n_terms - 8 * pass);
         const bool accum = pass > 0;

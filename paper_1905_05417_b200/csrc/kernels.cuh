@@ -66,24 +66,9 @@ struct DevTables {
     const long long* es_pre; // [ns + 1]
     const int* blk_is;       // [ceil(E / 256)] i_s of each 256-entry block's first entry
     int lt_max;              // max L_t over all thickness rows
-    // blocks of whole row-segment groups for the warp-specialised combine:
-    // first entry of each block (n_gbw + 1 values) and its first i_s
-    const long long* gbw_e0;
-    const int* gbw_is;
-    int n_gbw;
-    int ws_variant; // 0 direct stores; 1..3 warp-specialised layout (LAMFAST_WS)
-    void* g_rows;   // [slab rows] packed row records (constant-bank image)
-    void* g_w;      // [slab rows][lt_max][terms] double4 weights image
-    // team/bulk combine: teams of tm_team warps own whole row-segment groups,
-    // at most 32 * tm_team * tm_ept entries; first entry of each team range
-    // (n_team + 1 values) and its first i_s.  n_team = 0 -> direct stores.
-    const long long* tm_e0;
-    const int* tm_is;
-    int n_team, tm_team, tm_ept;
     // every term table has major symmetry C[(3j+l)9 + 3a+b] = C[(3l+j)9 + 3b+a]:
     // the standard kernel (K6) then computes pairs al <= be and mirrors them
     int sym;
-    int contig; // k_combine entry mapping: warp-contiguous slots (LAMFAST_CONTIG)
     long long S_s, S_u;
     // geometry
     int affine;
@@ -100,7 +85,7 @@ struct DevTables {
     unsigned* Wmask;                           // [n_passes][n_pairs]
     double* Pg;                                // [T][4][E] (general geometry)
     double* Pe;     // element-local P of a batch of pe_terms terms: [term][el][4][nl2][3][nl2][3]
-    int pe_terms;   // terms per batch (0: the coloured in-place K2b)
+    int pe_terms;   // terms per batch
     // slab
     int t0, t1;
     long long n_pairs, E;
@@ -113,8 +98,7 @@ int launch_thickness_pairs(const DevTables& d, cudaStream_t stream);
 /// Affine fast path: U, V, thickness pairs and Ct in one launch.
 int launch_prepare_affine(const DevTables& d, cudaStream_t stream);
 int launch_integrals_1d(const DevTables& d, cudaStream_t stream);
-/// General-geometry in-plane operators into Pg: two-phase (Pe set) or coloured in place
-/// (Pg zeroed by the caller).
+/// General-geometry in-plane operators into Pg (two-phase: Pe, then the gather).
 int launch_inplane_general(const DevTables& d, cudaStream_t stream);
 int inplane_general_launches(const DevTables& d);
 int launch_affine_export(const DevTables& d, cudaStream_t stream);

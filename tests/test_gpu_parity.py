@@ -393,16 +393,12 @@ def test_c5_slab_fast_equals_standard_on_device(gpu):
     assert (d2 / max(fa, fb)) ** 0.5 <= RTOL
 
 
-@pytest.mark.parametrize("env", [
-    {"LAMFAST_TEAM": "auto"}, {"LAMFAST_TEAM": "1,3"}, {"LAMFAST_TEAM": "4,2"},
-    {"LAMFAST_TEAM": "3,1", "LAMFAST_TEAM_KR": "1"}, {"LAMFAST_WS": "1"},
-    {"LAMFAST_CONTIG": "0"}, {"LAMFAST_TCHUNK": "7"},
-])
-def test_opt_in_store_variants_match_oracle(gpu, oracle, monkeypatch, env):
-    """The opt-in combine variants (team/bulk-copy stores, warp-specialised
-    stores; profiles/r1_store_modes.md) give the same CSR as the oracle:
-    boundary groups, mixed degrees / C0 thickness, skewed geometry (general
-    P), and slab plans whose output ranges start at odd 8-byte phases."""
+@pytest.mark.parametrize("env", [{}, {"LAMFAST_TCHUNK": "7"}])
+def test_combine_chunking_and_odd_phases_match_oracle(gpu, oracle, monkeypatch, env):
+    """The combine with its default and an odd thickness chunk (7 rows) gives
+    the oracle's CSR: boundary groups, mixed degrees / C0 thickness, skewed
+    geometry (general P), and slab plans whose output ranges start at odd
+    8-byte phases."""
     import torch
     for k, v in env.items():
         monkeypatch.setenv(k, v)
@@ -492,14 +488,10 @@ def test_concurrent_calls_are_reentrant(gpu):
             assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("k2b", ["default", "mma", "coloured"])
-def test_general_inplane_forms_match_oracle(gpu, oracle, monkeypatch, k2b):
-    """Non-affine maps take the general in-plane path (K2b): the two-phase
-    default (element-local P + gather), its DMMA element kernel and the
-    coloured in-place form all match the oracle -- degrees 1..4, mixed
-    in-plane degrees (the runtime-degree gather), several terms, slabs."""
-    if k2b != "default":
-        monkeypatch.setenv("LAMFAST_K2B", k2b)
+def test_general_inplane_forms_match_oracle(gpu, oracle):
+    """Non-affine maps take the general in-plane path (K2b, element-local P +
+    gather), which matches the oracle -- degrees 1..4, mixed in-plane degrees
+    (the runtime-degree gather), several terms."""
     cases = [P.cube_problem(p, 3, 1, [0.0, 0.9, 0.3, 1.2][:p + 1], geometry="skewed") for p in (1, 2, 3, 4)]
     cases.append(P.LaminateProblem(
         degree_u=2, degree_v=3, degree_t=2, knots_u=P.uniform_knots(2, 4),

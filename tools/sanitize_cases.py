@@ -1,7 +1,6 @@
 """Small cases for compute-sanitizer (memcheck / racecheck / synccheck /
 initcheck) over every device kernel family: fast (affine, general), standard,
-Voigt-free, decompose_angles, multi-pass, slabs, operators, verification, and
-the opt-in store variants.  Usage:
+Voigt-free, decompose_angles, many terms, slabs, operators, verification.  Usage:
   compute-sanitizer --tool racecheck python tools/sanitize_cases.py"""
 import os
 import sys
@@ -23,17 +22,8 @@ for prob in (c1, skew, mixed):
         out.append(lf.assemble_with(backend, prob).values.sum())
 out.append(lf.assemble_fast(c1.replace(decompose_angles=True)).values.sum())
 out.append(lf.assemble_fast(many).values.sum())
-for k, v in (("LAMFAST_WS", "1"), ("LAMFAST_TEAM", "auto"), ("LAMFAST_CONTIG", "0")):
-    os.environ[k] = v
-    out.append(lf.assemble_fast(c1).values.sum())
-    del os.environ[k]
-# general in-plane operator forms (two-phase default, DMMA element kernel, coloured)
+# general in-plane operators (two-phase)
 skew3 = P.cube_problem(3, 3, 1, [0.0, 0.9, 0.3, 1.2], geometry="skewed")
-for v in ("mma", "coloured"):
-    os.environ["LAMFAST_K2B"] = v
-    out.append(lf.assemble_fast(skew).values.sum())
-    out.append(lf.assemble_fast(skew3).values.sum())
-    del os.environ["LAMFAST_K2B"]
 out.append(lf.assemble_fast(skew3).values.sum())
 # matrix-free bilinear form (K8)
 for prob in (c1, skew, mixed):
