@@ -167,6 +167,15 @@ int lf_slab_bounds(const lf_problem* p, int backend, int n_parts, int part, int3
                    int32_t* t_end, int64_t* row_begin, int64_t* row_end, int64_t* nnz_begin,
                    int64_t* nnz_end);
 
+/* Row slab `part` of `n_parts` cut at FUNCTION boundaries (a function is
+ * f = i_t * n_s + i_s, rows 3f .. 3f+2), balanced by nnz to within one
+ * function's row block: slabs may start and end inside a thickness row.
+ * Functions [f_begin, f_end) = rows [row_begin, row_end) hold entries
+ * [nnz_begin, nnz_end) of the global CSR. */
+int lf_slab_bounds_functions(const lf_problem* p, int backend, int n_parts, int part,
+                             int64_t* f_begin, int64_t* f_end, int64_t* row_begin,
+                             int64_t* row_end, int64_t* nnz_begin, int64_t* nnz_end);
+
 /* ---- device-resident plan (bench / multi-GPU slab path) --------------- */
 typedef struct lf_plan lf_plan;
 /* Uploads the problem tables to `device` and sizes the workspace for the
@@ -174,6 +183,10 @@ typedef struct lf_plan lf_plan;
  * `cuda_stream` is a cudaStream_t (NULL = a private stream). */
 int lf_plan_create(const lf_problem* p, int backend, int device, void* cuda_stream,
                    int32_t t_begin, int32_t t_end, lf_plan** out);
+/* The same for the functions [f_begin, f_end) (f_end < 0: all), i.e. rows
+ * [3 f_begin, 3 f_end): a slab cut inside thickness rows. */
+int lf_plan_create_range(const lf_problem* p, int backend, int device, void* cuda_stream,
+                         int64_t f_begin, int64_t f_end, lf_plan** out);
 int lf_plan_destroy(lf_plan* plan);
 /* Local slab sizes: rows, nnz, and their global offsets. */
 int lf_plan_info(const lf_plan* plan, int64_t* rows, int64_t* nnz, int64_t* row_begin,
@@ -195,8 +208,12 @@ int lf_plan_synchronize(lf_plan* plan);
 
 /* ---- one-shot, host buffers (what the drop-in C++ entry points call) -- */
 /* Assembles the full matrix; host arrays must hold dim+1 / nnz / nnz
- * entries (query lf_pattern_size).  Pinned host memory is used at full
- * PCIe speed; pageable memory is staged. */
+ * entries (query lf_pattern_size).  The CSR is produced in chunks of at
+ * most ~2 GiB (or half the free device memory): each chunk's pattern and
+ * values are computed on the device while the previous chunk is copied out,
+ * so the matrix only has to fit in host memory, not in HBM.  Pinned host
+ * arrays receive the copies directly at full PCIe speed; pageable ones are
+ * filled from pinned staging buffers by host threads. */
 int lf_assemble(const lf_problem* p, int backend, int device, int64_t* row_ptr, int32_t* cols,
                 double* values, lf_stats* stats);
 /* The row slab of thickness functions [t_begin, t_end) (lf_slab_bounds) of
@@ -206,6 +223,24 @@ int lf_assemble(const lf_problem* p, int backend, int device, int64_t* row_ptr, 
  * reference counterpart (the reference is single-process). */
 int lf_assemble_slab(const lf_problem* p, int backend, int device, int32_t t_begin, int32_t t_end,
                      int64_t* row_ptr, int32_t* cols, double* values, lf_stats* stats);
+/* The same for the functions [f_begin, f_end) (lf_slab_bounds_functions). */
+int lf_assemble_range(const lf_problem* p, int backend, int device, int64_t f_begin, int64_t f_end,
+                      int64_t* row_ptr, int32_t* cols, double* values, lf_stats* stats);
+/* Receives one chunk of rows of a streamed assembly: global rows
+ * [row_begin, row_begin + rows) holding global entries [nnz_begin, nnz_begin
+ * + nnz); row_ptr (rows + 1 entries) is chunk-local (starts at 0), columns
+ * are global.  The arrays are pinned staging memory valid only during the
+ * call; while it runs the device computes and copies the next chunk.
+ * Return 0 to continue, non-zero to abort (the assembly then fails with
+ * LF_ERR_RUNTIME). */
+typedef int (*lf_chunk_sink)(void* user, int64_t row_begin, int64_t rows, int64_t nnz_begin, int64_t nnz,
+                             const int64_t* row_ptr, const int32_t* cols, const double* values);
+/* The whole matrix streamed through `sink` in row order, in chunks of at most
+ * max_chunk_nnz values (0: the library's default): a CSR larger than both
+ * HBM and host memory can be written out, reduced or verified chunk by chunk.
+ * No reference counterpart (the reference returns one StiffnessMatrix). */
+int lf_assemble_stream(const lf_problem* p, int backend, int device, int64_t max_chunk_nnz,
+                       lf_chunk_sink sink, void* user, lf_stats* stats);
 
 /* v^T K u by full 3D quadrature without forming K (referenceBilinear,
  * include/lamfast/assembly.hpp; assembly.cpp:247-318): host coefficient

@@ -193,6 +193,23 @@ class FastTerms:
                                         cols.ctypes.data_as(POINTER(c_int32)), _d(vals), ctypes.byref(nnz)))
         return rp, cols[:nnz.value], vals[:nnz.value]
 
+    def row_offsets(self, t0, t1):
+        """Slab-local row offsets of thickness rows [t0, t1) (no values)."""
+        rows = 3 * self.prob.n_s * (t1 - t0)
+        rp = np.zeros(rows + 1, dtype=np.int64)
+        nnz = c_int64()
+        self.o._check(self.o.lib.orc_fast_slab(self.h, t0, t1, rp.ctypes.data_as(POINTER(c_int64)), None, None,
+                                               ctypes.byref(nnz)))
+        return rp
+
+    def function_offset(self, f):
+        """Global CSR offset of the first entry of function f = i_t n_s + i_s."""
+        ns = self.prob.n_s
+        t, i = divmod(f, ns)
+        if t >= self.prob.n_t:
+            return self.nnz_before(self.prob.n_t)
+        return self.nnz_before(t) + int(self.row_offsets(t, t + 1)[3 * i])
+
     def nnz_before(self, t):
         nnz = c_int64()
         self.o._check(self.o.lib.orc_fast_slab(self.h, 0, t, None, None, None, ctypes.byref(nnz)))

@@ -7,17 +7,17 @@ runs as hand-written sm_100a CUDA kernels behind a C ABI
 Python host layer over that ABI; see DESIGN.md.
 """
 from .abi import LamfastError, library
-from .assembler import (CSR, Plan, assemble_fast, assemble_slab, reference_bilinear, assemble_standard, assemble_voigt_free,
+from .assembler import (CSR, Plan, assemble_fast, assemble_range, assemble_slab, assemble_stream, reference_bilinear, assemble_standard, assemble_voigt_free,
                         assemble_with, combine_operators, compute_inplane_operators,
                         compute_thickness_operators, device_csr_stats, pattern_size, release_memory,
-                        slab_bounds)
+                        slab_bounds, slab_bounds_functions)
 from .problem import (LaminateProblem, baseline_config, baseline_orthotropic, c0_knots,
                       cube_problem, equal_interfaces, isotropic, pagano, plate, sizes,
                       uniform_knots)
 
 __all__ = [
     "reference_bilinear",
-    "assemble_slab",
+    "assemble_slab", "assemble_range", "assemble_stream", "slab_bounds_functions",
     "LamfastError", "library", "CSR", "Plan", "assemble_fast", "assemble_standard",
     "assemble_voigt_free", "assemble_with", "combine_operators", "compute_inplane_operators",
     "compute_thickness_operators", "device_csr_stats", "pattern_size", "release_memory", "slab_bounds",

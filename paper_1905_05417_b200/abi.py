@@ -103,8 +103,12 @@ SIGNATURES = [
     ("lf_pattern_size", c_int, [_P(Problem), c_int, _P(c_int64), _P(c_int64)]),
     ("lf_slab_bounds", c_int, [_P(Problem), c_int, c_int, c_int, _P(c_int32), _P(c_int32),
                                _P(c_int64), _P(c_int64), _P(c_int64), _P(c_int64)]),
+    ("lf_slab_bounds_functions", c_int, [_P(Problem), c_int, c_int, c_int, _P(c_int64), _P(c_int64),
+                                         _P(c_int64), _P(c_int64), _P(c_int64), _P(c_int64)]),
     ("lf_plan_create", c_int, [_P(Problem), c_int, c_int, c_void_p, c_int32, c_int32,
                                _P(c_void_p)]),
+    ("lf_plan_create_range", c_int, [_P(Problem), c_int, c_int, c_void_p, c_int64, c_int64,
+                                     _P(c_void_p)]),
     ("lf_plan_destroy", c_int, [c_void_p]),
     ("lf_plan_info", c_int, [c_void_p, _P(c_int64), _P(c_int64), _P(c_int64), _P(c_int64)]),
     ("lf_plan_build_pattern", c_int, [c_void_p, c_void_p, c_void_p]),
@@ -118,6 +122,9 @@ SIGNATURES = [
     ("lf_reference_bilinear", c_int, [_P(Problem), _P(c_double), _P(c_double), c_int, _P(c_double)]),
     ("lf_assemble_slab", c_int, [_P(Problem), c_int, c_int, c_int32, c_int32, c_void_p, c_void_p,
                                  c_void_p, _P(Stats)]),
+    ("lf_assemble_range", c_int, [_P(Problem), c_int, c_int, c_int64, c_int64, c_void_p, c_void_p,
+                                  c_void_p, _P(Stats)]),
+    ("lf_assemble_stream", c_int, [_P(Problem), c_int, c_int, c_int64, c_void_p, c_void_p, _P(Stats)]),
     ("lf_inplane_operators", c_int, [_P(Problem), _P(c_double), c_int, _P(c_double),
                                      _P(c_char), _P(Stats)]),
     ("lf_inplane_operators_bracket", c_int, [_P(Problem), _P(c_double), c_int,
@@ -139,6 +146,10 @@ SIGNATURES = [
     ("lf_plan_symmetry_sq", c_int, [c_void_p, c_void_p, _P(c_double)]),
     ("lf_release_memory", c_int, [c_int]),
 ]
+
+# lf_chunk_sink
+CHUNK_SINK = ctypes.CFUNCTYPE(c_int, c_void_p, c_int64, c_int64, c_int64, c_int64, POINTER(c_int64),
+                              POINTER(c_int32), POINTER(c_double))
 
 _lib = None
 

@@ -71,6 +71,48 @@ def slab_bounds(prob: LaminateProblem, n_parts: int, part: int, backend: str = "
             "nnz_begin": z0.value, "nnz_end": z1.value}
 
 
+def slab_bounds_functions(prob: LaminateProblem, n_parts: int, part: int, backend: str = "fast") -> dict:
+    """Row slab cut at function boundaries (f = i_t * n_s + i_s), balanced by
+    nnz to within one function (lf_slab_bounds_functions)."""
+    lib = abi.library()
+    c = prob.to_c()
+    f0, f1, r0, r1, z0, z1 = (c_int64() for _ in range(6))
+    abi.check(lib.lf_slab_bounds_functions(byref(c), abi.BACKENDS[backend], n_parts, part, byref(f0), byref(f1),
+                                           byref(r0), byref(r1), byref(z0), byref(z1)))
+    return {"f_begin": f0.value, "f_end": f1.value, "row_begin": r0.value, "row_end": r1.value,
+            "nnz_begin": z0.value, "nnz_end": z1.value}
+
+
+def assemble_stream(prob: LaminateProblem, sink, backend: str = "fast", device: int = 0,
+                    max_chunk_nnz: int = 0) -> abi.Stats:
+    """Streams the whole matrix through ``sink(row_begin, rows, nnz_begin,
+    row_ptr, cols, values)`` chunk by chunk (lf_assemble_stream); the numpy
+    arrays are views of pinned staging memory valid only during the call.
+    A falsy return continues, a truthy one aborts."""
+    lib = abi.library()
+    c = prob.to_c()
+    err = []
+
+    def cb(_user, row_begin, rows, nnz_begin, nnz, rp, cols, vals):
+        try:
+            r = np.ctypeslib.as_array(rp, shape=(rows + 1,))
+            cc = np.ctypeslib.as_array(cols, shape=(nnz,)) if nnz else np.zeros(0, np.int32)
+            vv = np.ctypeslib.as_array(vals, shape=(nnz,)) if nnz else np.zeros(0)
+            return 1 if sink(row_begin, rows, nnz_begin, r, cc, vv) else 0
+        except Exception as exc:  # re-raised below
+            err.append(exc)
+            return 1
+
+    fn = abi.CHUNK_SINK(cb)
+    st = abi.Stats()
+    status = lib.lf_assemble_stream(byref(c), abi.BACKENDS[backend], device, max_chunk_nnz,
+                                    ctypes.cast(fn, c_void_p), None, byref(st))
+    if err:
+        raise err[0]
+    abi.check(status)
+    return st
+
+
 def assemble_with(backend: str, prob: LaminateProblem, device: int = 0,
                   out: Optional[Tuple[np.ndarray, np.ndarray, np.ndarray]] = None) -> CSR:
     """One-shot assembly into host buffers (pinned buffers may be passed in
@@ -108,6 +150,28 @@ def assemble_slab(prob: LaminateProblem, t_begin: int, t_end: int, backend: str 
     ptrs = [a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data for a in out]
     st = abi.Stats()
     abi.check(lib.lf_assemble_slab(byref(c), abi.BACKENDS[backend], device, t_begin, t_end, *ptrs, byref(st)))
+    rp, cols, vals = out
+    nnz = int(rp[rows])
+    return CSR(rp[:rows + 1], cols[:nnz], vals[:nnz], st)
+
+
+def assemble_range(prob: LaminateProblem, f_begin: int, f_end: int, backend: str = "fast", device: int = 0,
+                   out: Optional[Tuple] = None) -> CSR:
+    """One-shot assembly of the functions [f_begin, f_end) (rows 3 f_begin ..
+    3 f_end) into host buffers (lf_assemble_range): a slab cut inside
+    thickness rows, row offsets rebased to 0, global columns."""
+    lib = abi.library()
+    c = prob.to_c()
+    rows = 3 * (f_end - f_begin)
+    if out is None:
+        plan = Plan(prob, backend, device, f_begin=f_begin, f_end=f_end)
+        nnz = plan.nnz
+        plan.close()
+        out = (np.empty(rows + 1, dtype=np.int64), np.empty(max(nnz, 1), dtype=np.int32),
+               np.empty(max(nnz, 1), dtype=np.float64))
+    ptrs = [a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data for a in out]
+    st = abi.Stats()
+    abi.check(lib.lf_assemble_range(byref(c), abi.BACKENDS[backend], device, f_begin, f_end, *ptrs, byref(st)))
     rp, cols, vals = out
     nnz = int(rp[rows])
     return CSR(rp[:rows + 1], cols[:nnz], vals[:nnz], st)
@@ -202,7 +266,11 @@ class Plan:
     streams only)."""
 
     def __init__(self, prob: LaminateProblem, backend: str = "fast", device: int = 0,
-                 t_begin: int = 0, t_end: int = -1, stream=None):
+                 t_begin: int = 0, t_end: int = -1, stream=None, f_begin: Optional[int] = None,
+                 f_end: Optional[int] = None):
+        """Rows of the thickness functions [t_begin, t_end), or -- with
+        f_begin / f_end -- of the functions [f_begin, f_end) (a slab cut
+        inside thickness rows, lf_plan_create_range)."""
         self.lib = abi.library()
         self.prob = prob
         self.backend = backend
@@ -210,8 +278,12 @@ class Plan:
         self._c = prob.to_c()
         h = c_void_p()
         sp = c_void_p(stream) if stream else None
-        abi.check(self.lib.lf_plan_create(byref(self._c), abi.BACKENDS[backend], device, sp,
-                                          t_begin, t_end, byref(h)))
+        if f_begin is not None:
+            abi.check(self.lib.lf_plan_create_range(byref(self._c), abi.BACKENDS[backend], device, sp,
+                                                    f_begin, -1 if f_end is None else f_end, byref(h)))
+        else:
+            abi.check(self.lib.lf_plan_create(byref(self._c), abi.BACKENDS[backend], device, sp,
+                                              t_begin, t_end, byref(h)))
         self.handle = h
         rows, nnz, r0, z0 = c_int64(), c_int64(), c_int64(), c_int64()
         abi.check(self.lib.lf_plan_info(h, byref(rows), byref(nnz), byref(r0), byref(z0)))

@@ -15,6 +15,8 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <thread>
+#include <tuple>
 #include <utility>
 #include <vector>
 
@@ -323,10 +325,38 @@ void alloc_element_scratch(DeviceArena& ar, lfb::DevTables& d, int n_terms) {
     d.Pe = ar.alloc<double>(per_term * static_cast<std::size_t>(d.pe_terms));
 }
 
-void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void* stream, int t0, int t1) {
+/// Functions per thickness row (n_u n_v) of a problem, 0 if its in-plane knot
+/// counts are not valid (the setup then reports the error).
+int64_t functions_per_row(const lf_problem* p) {
+    if (!p)
+        return 0;
+    const int64_t nu = p->n_knots_u - p->degree_u - 1, nv = p->n_knots_v - p->degree_v - 1;
+    return nu > 0 && nv > 0 ? nu * nv : 0;
+}
+
+/// Function range of the thickness rows [t0, t1) (t1 < 0: all).
+std::pair<int64_t, int64_t> thickness_range(const lf_problem* p, int t0, int t1) {
+    const int64_t ns = functions_per_row(p);
+    return {static_cast<int64_t>(t0) * ns, t1 < 0 ? -1 : static_cast<int64_t>(t1) * ns};
+}
+
+/// Output-range fields of the device tables (row offsets slab-local).
+void set_range(const lfb::Range& r, lfb::DevTables& d) {
+    d.t0 = r.t0;
+    d.t1 = r.t1;
+    d.s0 = r.s0;
+    d.s1 = r.s1;
+    d.f0 = r.f0;
+    d.f1 = r.f1;
+    d.out_base = r.out_base;
+    d.rp_base = 0;
+    d.nnz_slab = r.nnz;
+}
+
+void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void* stream, int64_t f0, int64_t f1) {
     if (!p)
         raise(LF_ERR_INVALID_ARGUMENT, "null problem");
-    plan->setup = lfb::buildSetup(*p, backend, t0, t1 < 0 ? -1 : t1);
+    plan->setup = lfb::buildSetupRange(*p, backend, f0, f1);
     use_device(device);
     plan->device = device;
     if (stream) {
@@ -360,10 +390,10 @@ void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void
         d.sym = (dmax <= 1e-15 * amax && !std::getenv("LAMFAST_NO_SYM")) ? 1 : 0;
     }
     d.layer_config = ar.upload(s.layup.layer_config);
-    d.t0 = s.t0;
-    d.t1 = s.t1;
+    set_range(lfb::rangeOf(s, s.f0, s.f1), d);
+    d.w_t0 = s.t0;
+    d.w_t1 = s.t1;
     d.n_pairs = s.n_pairs;
-    d.nnz_slab = s.nnz;
     if (backend != LF_BACKEND_STANDARD) {
         d.W = ar.alloc<double>(static_cast<std::size_t>(std::max<long long>(1, d.n_pairs)) * d.n_terms * 4);
         d.Wmask = ar.alloc<unsigned>(static_cast<std::size_t>(std::max<long long>(1, d.n_pairs)) * d.n_passes);
@@ -380,56 +410,58 @@ void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void
     CK(cudaStreamSynchronize(plan->stream)); // the uploads' host sources are temporaries
 }
 
-int plan_launch(lf_plan* plan, double* values, bool timed = true) {
+/// Setup kernels of one assembly, everything before the values: basis and
+/// thickness weights (W), the 1D integrals / C~ (affine) or the general P.
+/// Asynchronous on `s`; returns the number of kernels launched.
+int plan_prepare(lf_plan* plan, cudaStream_t s) {
     const lfb::DevTables& d = plan->d;
     int launches = 0;
-    cudaStream_t s = plan->stream;
-    auto events = [&]() {
-        std::pair<cudaEvent_t, cudaEvent_t> ev;
-        if (!plan->free_events.empty()) {
-            ev = plan->free_events.back();
-            plan->free_events.pop_back();
-        } else {
-            CK(cudaEventCreate(&ev.first));
-            CK(cudaEventCreate(&ev.second));
-        }
-        return ev;
-    };
     if (plan->setup.backend == LF_BACKEND_STANDARD) {
         CK(static_cast<cudaError_t>(lfb::launch_basis(d, false, s)));
-        ++launches;
-        if (!timed) {
-            CK(static_cast<cudaError_t>(lfb::launch_standard(d, values, plan->setup.nnz, s, &launches)));
-            return launches;
-        }
-        const auto ev = events(); // brackets the coloured standard kernels
-        CK(cudaEventRecord(ev.first, s));
-        CK(static_cast<cudaError_t>(lfb::launch_standard(d, values, plan->setup.nnz, s, &launches)));
-        CK(cudaEventRecord(ev.second, s));
-        plan->pending.push_back(ev);
-        return launches;
+        return 1;
     }
     if (d.affine) {
         // one fused setup launch: U, V, thickness-pair weights, Ct
         CK(static_cast<cudaError_t>(lfb::launch_prepare_affine(d, s)));
-        ++launches;
-    } else {
-        CK(static_cast<cudaError_t>(lfb::launch_basis(d, false, s)));
-        ++launches;
-        if (d.n_pairs > 0) {
-            CK(static_cast<cudaError_t>(lfb::launch_thickness_pairs(d, s)));
-            ++launches;
-        }
-        CK(static_cast<cudaError_t>(lfb::launch_inplane_general(d, s)));
-        launches += lfb::inplane_general_launches(d);
+        return 1;
     }
-    if (!timed) {
+    CK(static_cast<cudaError_t>(lfb::launch_basis(d, false, s)));
+    ++launches;
+    if (d.n_pairs > 0) {
+        CK(static_cast<cudaError_t>(lfb::launch_thickness_pairs(d, s)));
+        ++launches;
+    }
+    CK(static_cast<cudaError_t>(lfb::launch_inplane_general(d, s)));
+    return launches + lfb::inplane_general_launches(d);
+}
+
+/// The value kernels of the output range of `d` (the plan's own range or a
+/// sub-range of it) into `values`, after plan_prepare.
+int plan_values(lf_plan* plan, const lfb::DevTables& d, double* values, cudaStream_t s) {
+    int launches = 0;
+    if (plan->setup.backend == LF_BACKEND_STANDARD)
+        CK(static_cast<cudaError_t>(lfb::launch_standard(d, values, d.nnz_slab, s, &launches)));
+    else
         CK(static_cast<cudaError_t>(lfb::launch_combine(d, values, 0, s, &launches)));
-        return launches;
+    return launches;
+}
+
+int plan_launch(lf_plan* plan, double* values, bool timed = true) {
+    cudaStream_t s = plan->stream;
+    int launches = plan_prepare(plan, s);
+    if (!timed)
+        return launches + plan_values(plan, plan->d, values, s);
+    // CUDA events around the dominant kernels (combine, or the coloured standard launches)
+    std::pair<cudaEvent_t, cudaEvent_t> ev;
+    if (!plan->free_events.empty()) {
+        ev = plan->free_events.back();
+        plan->free_events.pop_back();
+    } else {
+        CK(cudaEventCreate(&ev.first));
+        CK(cudaEventCreate(&ev.second));
     }
-    const auto ev = events();
     CK(cudaEventRecord(ev.first, s));
-    CK(static_cast<cudaError_t>(lfb::launch_combine(d, values, 0, s, &launches)));
+    launches += plan_values(plan, plan->d, values, s);
     CK(cudaEventRecord(ev.second, s));
     plan->pending.push_back(ev);
     if (plan->pending.size() > 4096)
@@ -621,11 +653,37 @@ int lf_slab_bounds(const lf_problem* p, int backend, int n_parts, int part, int3
     });
 }
 
+int lf_slab_bounds_functions(const lf_problem* p, int backend, int n_parts, int part, int64_t* f_begin,
+                             int64_t* f_end, int64_t* row_begin, int64_t* row_end, int64_t* nnz_begin,
+                             int64_t* nnz_end) {
+    return guarded([&] {
+        const lfb::Setup s = lfb::buildSetup(*p, backend, 0, -1);
+        int64_t f0 = 0, f1 = 0;
+        lfb::slabBoundsFunctions(s, n_parts, part, &f0, &f1);
+        *f_begin = f0;
+        *f_end = f1;
+        *row_begin = 3 * f0;
+        *row_end = 3 * f1;
+        *nnz_begin = lfb::functionOffset(s, f0);
+        *nnz_end = lfb::functionOffset(s, f1);
+    });
+}
+
 int lf_plan_create(const lf_problem* p, int backend, int device, void* cuda_stream, int32_t t_begin, int32_t t_end,
                    lf_plan** out) {
     return guarded([&] {
         auto plan = std::make_unique<lf_plan>();
-        plan_init(plan.get(), p, backend, device, cuda_stream, t_begin, t_end);
+        const auto r = thickness_range(p, t_begin, t_end);
+        plan_init(plan.get(), p, backend, device, cuda_stream, r.first, r.second);
+        *out = plan.release();
+    });
+}
+
+int lf_plan_create_range(const lf_problem* p, int backend, int device, void* cuda_stream, int64_t f_begin,
+                         int64_t f_end, lf_plan** out) {
+    return guarded([&] {
+        auto plan = std::make_unique<lf_plan>();
+        plan_init(plan.get(), p, backend, device, cuda_stream, f_begin, f_end);
         *out = plan.release();
     });
 }
@@ -718,51 +776,261 @@ static OneShotStreams& one_shot_streams(int device) {
     return st;
 }
 
-static int assemble_one_shot(const lf_problem* p, int backend, int device, int t0, int t1, int64_t* row_ptr,
-                             int32_t* cols, double* values, lf_stats* stats) {
+/// Pinned host staging of one-shot calls whose destination is pageable (or
+/// a chunk sink): two slots, kept per (thread, device) and grown on demand,
+/// so a call does not pay for pinning fresh host pages.
+struct Staging {
+    void* slot[2] = {nullptr, nullptr};
+    std::size_t bytes = 0;
+    ~Staging() {
+        for (void* p : slot)
+            if (p)
+                cudaFreeHost(p);
+    }
+    void reserve(std::size_t n) {
+        if (n <= bytes)
+            return;
+        for (void*& p : slot) {
+            if (p)
+                CK(cudaFreeHost(p));
+            p = nullptr;
+        }
+        bytes = 0;
+        for (void*& p : slot)
+            CK(cudaHostAlloc(&p, n, cudaHostAllocDefault));
+        bytes = n;
+    }
+};
+
+static Staging& host_staging(int device) {
+    thread_local std::vector<std::unique_ptr<Staging>> per_device;
+    if (static_cast<int>(per_device.size()) <= device)
+        per_device.resize(static_cast<std::size_t>(device) + 1);
+    auto& st = per_device[static_cast<std::size_t>(device)];
+    if (!st)
+        st = std::make_unique<Staging>();
+    return *st;
+}
+
+static bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+/// memcpy of several (dst, src, bytes) pieces on up to 16 host threads: a
+/// pageable destination takes ~50 GB/s only with several cores copying.
+static void parallel_copy(const std::vector<std::tuple<void*, const void*, std::size_t>>& jobs) {
+    std::size_t total = 0;
+    for (const auto& j : jobs)
+        total += std::get<2>(j);
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const unsigned nt = static_cast<unsigned>(std::max<std::size_t>(1, std::min<std::size_t>(hw, total >> 24)));
+    if (nt <= 1) {
+        for (const auto& j : jobs)
+            std::memcpy(std::get<0>(j), std::get<1>(j), std::get<2>(j));
+        return;
+    }
+    // cut the concatenated byte range into nt equal pieces
+    auto work = [&](unsigned t) {
+        const std::size_t lo = total * t / nt, hi = total * (t + 1) / nt;
+        std::size_t off = 0;
+        for (const auto& j : jobs) {
+            const std::size_t n = std::get<2>(j);
+            const std::size_t a = std::max(lo, off), b = std::min(hi, off + n);
+            if (a < b)
+                std::memcpy(static_cast<char*>(std::get<0>(j)) + (a - off),
+                            static_cast<const char*>(std::get<1>(j)) + (a - off), b - a);
+            off += n;
+        }
+    };
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < nt; ++t)
+        th.emplace_back(work, t);
+    work(0);
+    for (auto& x : th)
+        x.join();
+}
+
+/// Function cuts [f0 = c_0 < c_1 < ... < c_K = f1] of chunks holding at most
+/// max_nnz values each (at least one function per chunk).
+static std::vector<int64_t> chunk_cuts(const lfb::Setup& s, int64_t f0, int64_t f1, int64_t max_nnz) {
+    std::vector<int64_t> cuts{f0};
+    int64_t cur = f0;
+    while (cur < f1) {
+        const int64_t base = lfb::functionOffset(s, cur);
+        int64_t lo = cur + 1, hi = f1;
+        while (lo < hi) {
+            const int64_t mid = lo + (hi - lo + 1) / 2;
+            if (lfb::functionOffset(s, mid) - base <= max_nnz)
+                lo = mid;
+            else
+                hi = mid - 1;
+        }
+        cur = lo;
+        cuts.push_back(cur);
+    }
+    return cuts;
+}
+
+/// Destination of a one-shot assembly: the caller's host arrays for the whole
+/// range (row offsets from 0 at the range start), or a chunk sink.
+struct OneShotOut {
+    int64_t* row_ptr = nullptr;
+    int32_t* cols = nullptr;
+    double* values = nullptr;
+    lf_chunk_sink sink = nullptr;
+    void* user = nullptr;
+};
+
+/// The one-shot pipeline: the range is cut into chunks of at most
+/// `chunk_nnz` values; each chunk's pattern and values are computed into one
+/// of two device slots on the plan's stream while the other slot's chunk
+/// crosses PCIe on the side stream, so the CSR may be larger than HBM (it
+/// only has to fit the host).  Pinned destinations receive the D2H directly;
+/// pageable ones (and sinks) go through two pinned staging slots, emptied by
+/// host threads while the next chunk is copied.
+static void run_one_shot(lf_plan& plan, OneShotStreams& st, int64_t chunk_nnz, const OneShotOut& out) {
+    const lfb::Setup& s = plan.setup;
+    const std::vector<int64_t> cuts = chunk_cuts(s, s.f0, s.f1, chunk_nnz);
+    const std::size_t K = cuts.size() - 1;
+    std::vector<lfb::Range> rg(K);
+    int64_t max_rows = 0, max_nnz = 0;
+    for (std::size_t k = 0; k < K; ++k) {
+        rg[k] = lfb::rangeOf(s, cuts[k], cuts[k + 1]);
+        max_rows = std::max(max_rows, rg[k].rows);
+        max_nnz = std::max(max_nnz, rg[k].nnz);
+    }
+    const bool staged = out.sink || !(is_pinned(out.row_ptr) && is_pinned(out.cols) && is_pinned(out.values));
+    // device slots (two only when there is more than one chunk)
+    const int nslot = K > 1 ? 2 : 1;
+    const std::size_t rp_bytes = sizeof(int64_t) * static_cast<std::size_t>(max_rows + 1);
+    const std::size_t col_bytes = sizeof(int32_t) * static_cast<std::size_t>(std::max<int64_t>(1, max_nnz));
+    const std::size_t val_bytes = sizeof(double) * static_cast<std::size_t>(std::max<int64_t>(1, max_nnz));
+    std::vector<std::unique_ptr<DeviceBuffer>> drp, dcols, dvals;
+    for (int b = 0; b < nslot; ++b) {
+        drp.push_back(std::make_unique<DeviceBuffer>(rp_bytes, plan.stream));
+        dcols.push_back(std::make_unique<DeviceBuffer>(col_bytes, plan.stream));
+        dvals.push_back(std::make_unique<DeviceBuffer>(val_bytes, plan.stream));
+    }
+    // staging slot layout: values | columns | row offsets (8-byte aligned)
+    const std::size_t so_cols = val_bytes, so_rp = val_bytes + ((col_bytes + 7) & ~std::size_t(7));
+    Staging* stg = nullptr;
+    if (staged) {
+        stg = &host_staging(plan.device);
+        stg->reserve(so_rp + rp_bytes);
+    }
+    struct Events {
+        cudaEvent_t e[4] = {nullptr, nullptr, nullptr, nullptr};
+        ~Events() {
+            for (auto x : e)
+                if (x)
+                    cudaEventDestroy(x);
+        }
+    } ev;
+    for (auto& x : ev.e)
+        CK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    cudaEvent_t* ready = ev.e;    // [2] slot computed (plan stream)
+    cudaEvent_t* drained = ev.e + 2; // [2] slot copied out (side stream)
+    cudaStream_t cs = plan.stream, xs = st.side;
+    plan_prepare(&plan, cs);
+    auto finish = [&](std::size_t j) { // host side of chunk j (staged only)
+        const int b = static_cast<int>(j % 2);
+        CK(cudaEventSynchronize(drained[b]));
+        const lfb::Range& r = rg[j];
+        const char* base = static_cast<const char*>(stg->slot[b]);
+        const double* v = reinterpret_cast<const double*>(base);
+        const int32_t* c = reinterpret_cast<const int32_t*>(base + so_cols);
+        const int64_t* rp = reinterpret_cast<const int64_t*>(base + so_rp);
+        if (out.sink) {
+            if (out.sink(out.user, r.row_begin, r.rows, r.nnz_begin, r.nnz, rp, c, v) != 0)
+                raise(LF_ERR_RUNTIME, "lf_assemble_stream: the chunk sink aborted the assembly");
+            return;
+        }
+        const std::size_t ro = static_cast<std::size_t>(r.row_begin - s.row_begin);
+        const std::size_t zo = static_cast<std::size_t>(r.nnz_begin - s.nnz_begin);
+        parallel_copy({{out.values + zo, v, sizeof(double) * static_cast<std::size_t>(r.nnz)},
+                       {out.cols + zo, c, sizeof(int32_t) * static_cast<std::size_t>(r.nnz)},
+                       {out.row_ptr + ro, rp, sizeof(int64_t) * static_cast<std::size_t>(r.rows + 1)}});
+    };
+    for (std::size_t k = 0; k < K; ++k) {
+        const int b = static_cast<int>(k % 2);
+        const lfb::Range& r = rg[k];
+        lfb::DevTables d = plan.d;
+        set_range(r, d);
+        d.rp_base = out.sink ? 0 : r.nnz_begin - s.nnz_begin; // sinks get chunk-local row offsets
+        if (k >= 2)
+            CK(cudaStreamWaitEvent(cs, drained[b], 0)); // the slot's previous chunk has left the device
+        auto* rpd = static_cast<long long*>(drp[static_cast<std::size_t>(b % nslot)]->p);
+        auto* cd = static_cast<int*>(dcols[static_cast<std::size_t>(b % nslot)]->p);
+        auto* vd = static_cast<double*>(dvals[static_cast<std::size_t>(b % nslot)]->p);
+        CK(static_cast<cudaError_t>(lfb::launch_pattern(d, rpd, cd, cs)));
+        if (r.nnz > 0)
+            plan_values(&plan, d, vd, cs);
+        CK(cudaEventRecord(ready[b], cs));
+        CK(cudaStreamWaitEvent(xs, ready[b], 0));
+        const std::size_t nv = static_cast<std::size_t>(r.nnz), nr = static_cast<std::size_t>(r.rows + 1);
+        if (staged) {
+            char* base = static_cast<char*>(stg->slot[b]);
+            copy_d2h(base, vd, sizeof(double) * nv, xs);
+            copy_d2h(base + so_cols, cd, sizeof(int32_t) * nv, xs);
+            copy_d2h(base + so_rp, rpd, sizeof(int64_t) * nr, xs);
+        } else {
+            const std::size_t ro = static_cast<std::size_t>(r.row_begin - s.row_begin);
+            const std::size_t zo = static_cast<std::size_t>(r.nnz_begin - s.nnz_begin);
+            copy_d2h(out.values + zo, vd, sizeof(double) * nv, xs);
+            copy_d2h(out.cols + zo, cd, sizeof(int32_t) * nv, xs);
+            copy_d2h(out.row_ptr + ro, rpd, sizeof(int64_t) * nr, xs);
+        }
+        CK(cudaEventRecord(drained[b], xs));
+        if (staged && k >= 1)
+            finish(k - 1);
+    }
+    if (staged && K > 0)
+        finish(K - 1);
+    CK(cudaStreamSynchronize(xs));
+    CK(cudaStreamSynchronize(cs));
+    CK(cudaGetLastError());
+}
+
+/// Values per chunk of a one-shot call: whole range in one chunk when its CSR
+/// fits half the free device memory and 2 GiB, else chunks of that size (so
+/// the D2H of one overlaps the compute of the next).  `requested` > 0 caps it.
+static int64_t default_chunk_nnz(int64_t requested) {
+    std::size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    const double per_nnz = 12.5; // value + column + a share of the row offsets
+    const double slot = std::min<double>(2.0 * (1ull << 30), 0.45 * static_cast<double>(free_b));
+    int64_t n = std::max<int64_t>(1 << 20, static_cast<int64_t>(slot / per_nnz));
+    if (requested > 0)
+        n = std::min(n, requested);
+    return n;
+}
+
+static int assemble_one_shot(const lf_problem* p, int backend, int device, int64_t f0, int64_t f1, bool whole,
+                             const OneShotOut& out, int64_t chunk_nnz, lf_stats* stats) {
     return guarded([&] {
         use_device(device);
         OneShotStreams& streams = one_shot_streams(device);
         lf_plan plan;
-        plan_init(&plan, p, backend, device, streams.main, t0, t1);
-            const lfb::Setup& s = plan.setup;
+        plan_init(&plan, p, backend, device, streams.main, f0, f1);
+        const lfb::Setup& s = plan.setup;
         if (s.nnz == 0) {
-            if (t0 == 0 && t1 < 0) // the whole matrix: SparseMatrixBuilder::finalize (sparse.cpp:15-18)
+            if (whole) // the whole matrix: SparseMatrixBuilder::finalize (sparse.cpp:15-18)
                 raise(LF_ERR_LOGIC, "SparseMatrixBuilder: nothing accumulated");
-            std::fill(row_ptr, row_ptr + s.rows + 1, int64_t(0)); // an empty slab: every row empty
+            if (out.sink) {
+                std::vector<int64_t> zeros(static_cast<std::size_t>(s.rows + 1), 0);
+                if (out.sink(out.user, s.row_begin, s.rows, s.nnz_begin, 0, zeros.data(), nullptr, nullptr) != 0)
+                    raise(LF_ERR_RUNTIME, "lf_assemble_stream: the chunk sink aborted the assembly");
+            } else {
+                std::fill(out.row_ptr, out.row_ptr + s.rows + 1, int64_t(0)); // an empty slab: every row empty
+            }
             return;
         }
-        const std::size_t rows = static_cast<std::size_t>(s.rows);
-        const std::size_t nnz = static_cast<std::size_t>(s.nnz);
-        DeviceBuffer drp(sizeof(int64_t) * (rows + 1), plan.stream);
-        DeviceBuffer dcols(sizeof(int32_t) * nnz, plan.stream);
-        DeviceBuffer dvals(sizeof(double) * nnz, plan.stream);
-        // the pattern and its read-back run on a side stream, so the values are
-        // computed while the row offsets and columns cross PCIe
-        struct Side {
-            cudaStream_t s = nullptr;
-            cudaEvent_t e = nullptr;
-            ~Side() {
-                if (s)
-                    cudaStreamSynchronize(s);
-                if (e)
-                    cudaEventDestroy(e);
-            }
-        } side;
-        side.s = streams.side;
-        CK(cudaEventCreateWithFlags(&side.e, cudaEventDisableTiming));
-        CK(cudaEventRecord(side.e, plan.stream)); // buffers allocated (stream-ordered)
-        CK(cudaStreamWaitEvent(side.s, side.e, 0));
-        cudaStream_t ps = side.s;
-        CK(static_cast<cudaError_t>(lfb::launch_pattern(plan.d, static_cast<long long*>(drp.p),
-                                                        static_cast<int*>(dcols.p), ps)));
-        copy_d2h(row_ptr, drp.p, sizeof(int64_t) * (rows + 1), ps);
-        copy_d2h(cols, dcols.p, sizeof(int32_t) * nnz, ps);
-        plan_launch(&plan, static_cast<double*>(dvals.p));
-        copy_d2h(values, dvals.p, sizeof(double) * nnz, plan.stream);
-        CK(cudaStreamSynchronize(ps));
-        CK(cudaStreamSynchronize(plan.stream));
-        CK(cudaGetLastError());
+        run_one_shot(plan, streams, default_chunk_nnz(chunk_nnz), out);
         if (stats) {
             stats->qpoint_visits += s.stats.qpoint_visits;
             stats->frame_evaluations += s.stats.frame_evaluations;
@@ -773,12 +1041,42 @@ static int assemble_one_shot(const lf_problem* p, int backend, int device, int t
 
 int lf_assemble(const lf_problem* p, int backend, int device, int64_t* row_ptr, int32_t* cols, double* values,
                 lf_stats* stats) {
-    return assemble_one_shot(p, backend, device, 0, -1, row_ptr, cols, values, stats);
+    OneShotOut out;
+    out.row_ptr = row_ptr;
+    out.cols = cols;
+    out.values = values;
+    return assemble_one_shot(p, backend, device, 0, -1, true, out, 0, stats);
 }
 
 int lf_assemble_slab(const lf_problem* p, int backend, int device, int32_t t_begin, int32_t t_end, int64_t* row_ptr,
                      int32_t* cols, double* values, lf_stats* stats) {
-    return assemble_one_shot(p, backend, device, t_begin, t_end, row_ptr, cols, values, stats);
+    OneShotOut out;
+    out.row_ptr = row_ptr;
+    out.cols = cols;
+    out.values = values;
+    const auto r = thickness_range(p, t_begin, t_end);
+    return assemble_one_shot(p, backend, device, r.first, r.second, false, out, 0, stats);
+}
+
+int lf_assemble_range(const lf_problem* p, int backend, int device, int64_t f_begin, int64_t f_end,
+                      int64_t* row_ptr, int32_t* cols, double* values, lf_stats* stats) {
+    OneShotOut out;
+    out.row_ptr = row_ptr;
+    out.cols = cols;
+    out.values = values;
+    return assemble_one_shot(p, backend, device, f_begin, f_end, false, out, 0, stats);
+}
+
+int lf_assemble_stream(const lf_problem* p, int backend, int device, int64_t max_chunk_nnz, lf_chunk_sink sink,
+                       void* user, lf_stats* stats) {
+    if (!sink) {
+        g_error = "lf_assemble_stream: null sink";
+        return LF_ERR_INVALID_ARGUMENT;
+    }
+    OneShotOut out;
+    out.sink = sink;
+    out.user = user;
+    return assemble_one_shot(p, backend, device, 0, -1, true, out, max_chunk_nnz, stats);
 }
 
 int lf_reference_bilinear(const lf_problem* p, const double* v, const double* u, int device, double* out) {
@@ -912,8 +1210,8 @@ int lf_thickness_operators(int32_t degree_t, int32_t n_knots_t, const double* kn
                 on[static_cast<std::size_t>(l) * L + l] = 1;
             }
             upload_terms(ar, d, L, L, tab, lam, on);
-            d.t0 = 0;
-            d.t1 = s.n_t;
+            d.t0 = d.w_t0 = 0;
+            d.t1 = d.w_t1 = s.n_t;
             d.n_pairs = s.at.total;
             d.W = ar.alloc<double>(static_cast<std::size_t>(d.n_pairs) * L * 4);
             d.Wmask = ar.alloc<unsigned>(static_cast<std::size_t>(d.n_pairs) * d.n_passes);
@@ -1009,8 +1307,13 @@ int lf_combine(const lf_problem* p, int32_t n_terms, const double* blocks, const
             d.n_terms = n_terms;
             d.n_passes = (n_terms + 7) / 8;
             d.affine = 0;
-            d.t0 = 0;
-            d.t1 = nt;
+            d.t0 = d.w_t0 = 0;
+            d.t1 = d.w_t1 = nt;
+            d.s0 = 0;
+            d.s1 = s.n_s;
+            d.f0 = 0;
+            d.f1 = static_cast<long long>(nt) * s.n_s;
+            d.out_base = d.rp_base = 0;
             d.n_pairs = at.total;
             d.nnz_slab = nnz;
             // P: banded -> entry layout

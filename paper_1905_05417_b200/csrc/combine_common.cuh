@@ -75,10 +75,15 @@ __device__ __forceinline__ void affine_p(const DevTables& d, int iu, int iv, int
 // term's range are predicated off (no shared-memory wavefront, no FMA).  With
 // EPT = 2 every weight load feeds two outputs.
 struct RowInfo {
-    long long base; // 9 S_s (pre_t[it] - pre_t[t0]): slab offset of row block it
-    int lt;         // L_t(it)
+    long long base; // 9 S_s (pre_t[it] - pre_t[t0]) - out_base: range offset of row block it
+    int lt;         // L_t(it) | edge << 8 (edge bit 0: row t0 starts at s0; bit 1: row t1-1 ends at s1)
     unsigned mask;  // union of term masks over the row's pairs (this pass)
 };
+
+/// Row of a range that starts or ends inside it (see DevTables::s0 / s1).
+__device__ __forceinline__ int row_edge(const DevTables& d, int it) {
+    return (it == d.t0 && d.s0 > 0 ? 1 : 0) | (it == d.t1 - 1 && d.s1 < d.ns ? 2 : 0);
+}
 
 template <int NT, int EPT, int LT, bool ACCUM, bool SMEM = false, typename WP = const double4*>
 __device__ __forceinline__ void combine_row(const double (&P)[EPT][NT][4], WP w,
@@ -285,13 +290,14 @@ __device__ __forceinline__ void stage_rows_block(const DevTables& d, int it0, in
                                                  int nthreads) {
     const int t_first = pass * 8;
     const long long pre0 = __ldg(d.pre_t + d.t0);
+    const long long preW = __ldg(d.pre_t + d.w_t0); // W / Wmask index base (the plan's rows)
     const long long nine_S = 9 * d.S_s;
     const unsigned* mask_base = d.Wmask + (long long)pass * d.n_pairs;
     const int T = d.n_terms;
     // stage rows: RowInfo, per-term neighbour ranges, weights s_w[row][k][t]
     for (int rr = tid; rr < nrow; rr += nthreads) {
         const int it = it0 + rr;
-        const long long pfx = __ldg(d.pre_t + it) - pre0;
+        const long long pfx = __ldg(d.pre_t + it) - preW;
         const int lt = __ldg(d.len_t + it);
         unsigned m = 0;
         unsigned char lo[NT], hi[NT];
@@ -310,8 +316,8 @@ __device__ __forceinline__ void stage_rows_block(const DevTables& d, int it0, in
                     hi[t] = (unsigned char)(k + 1);
                 }
         }
-        s_row[rr].base = nine_S * pfx;
-        s_row[rr].lt = lt;
+        s_row[rr].base = nine_S * (__ldg(d.pre_t + it) - pre0) - d.out_base;
+        s_row[rr].lt = lt | row_edge(d, it) << 8;
         s_row[rr].mask = m;
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
@@ -327,7 +333,7 @@ __device__ __forceinline__ void stage_rows_block(const DevTables& d, int it0, in
         const int it = it0 + rr;
         double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
         if (k < __ldg(d.len_t + it)) {
-            const long long q = __ldg(d.pre_t + it) - pre0 + k;
+            const long long q = __ldg(d.pre_t + it) - preW + k;
             const double2* src = reinterpret_cast<const double2*>(d.W + ((q * T) + t_first + t) * 4);
             const double2 lo2 = __ldg(src), hi2 = __ldg(src + 1);
             v = make_double4(lo2.x, lo2.y, hi2.x, hi2.y);

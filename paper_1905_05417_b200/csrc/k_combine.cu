@@ -27,7 +27,7 @@ __device__ __forceinline__ void combine_body(const DevTables& d, double* __restr
     double* o_thread[EPT];
     long long A[EPT];
     int B[EPT];
-    bool live[EPT];
+    bool live[EPT], in_s0[EPT], in_s1[EPT]; // in_s0/1: entry's function is >= s0 / < s1 (partial rows)
 #pragma unroll
     for (int x = 0; x < EPT; ++x) {
         // entry of slot x: e = blockIdx*256*EPT + warp*32*EPT + x*32 + lane, so
@@ -42,6 +42,8 @@ __device__ __forceinline__ void combine_body(const DevTables& d, double* __restr
             ++is;
         const long long ebase = __ldg(d.es_pre + is);
         const int r = (int)(ec - ebase);
+        in_s0[x] = is >= d.s0;
+        in_s1[x] = is < d.s1;
         const int iu = is % d.nu, iv = is / d.nu;
         const int Lu = __ldg(d.len_u + iu), Lv = __ldg(d.len_v + iv);
         B[x] = 3 * Lu * Lv; // row segment length per thickness neighbour
@@ -79,13 +81,19 @@ __device__ __forceinline__ void combine_body(const DevTables& d, double* __restr
             continue;
         for (int rr = 0; rr < nrow; ++rr) {
             const RowInfo ri = s_row[rr];
+            const int lt = ri.lt & 0xff, edge = ri.lt >> 8;
+            // entries of a partial first / last row outside the range are not written
+            bool lv[EPT];
+#pragma unroll
+            for (int x = 0; x < EPT; ++x)
+                lv[x] = edge ? live[x] && (!(edge & 1) || in_s0[x]) && (!(edge & 2) || in_s1[x]) : live[x];
             double* o[EPT];
 #pragma unroll
             for (int x = 0; x < EPT; ++x)
-                o[x] = o_thread[x] + ri.base + (long long)ri.lt * A[x];
+                o[x] = o_thread[x] + ri.base + (long long)lt * A[x];
 #pragma unroll
             for (int x = 0; x < EPT; ++x)
-                LF_CHECK(!live[x] || (o[x] >= out && o[x] + (long long)(ri.lt - 1) * B[x] < out + d.nnz_slab));
+                LF_CHECK(!lv[x] || (o[x] >= out && o[x] + (long long)(lt - 1) * B[x] < out + d.nnz_slab));
             const double4* w = s_w + rr * lt_max * NT;
             const unsigned char* kr = s_kr + rr * NT * 2;
 #ifndef LF_NO_MASKED_ROWS
@@ -102,23 +110,23 @@ __device__ __forceinline__ void combine_body(const DevTables& d, double* __restr
 #define LF_MASKED_MIN_NT 4
 #endif
             if constexpr (EPT >= 2 && NT <= 4 && NT >= LF_MASKED_MIN_NT && !ACCUM) {
-                if (((LF_MASKED_LTS >> 5) & 1) && ri.lt == 5 && row_masked<NT, EPT, 5>(ri.mask, P, w, o, B, live))
+                if (((LF_MASKED_LTS >> 5) & 1) && lt == 5 && row_masked<NT, EPT, 5>(ri.mask, P, w, o, B, lv))
                     continue;
-                if (((LF_MASKED_LTS >> 3) & 1) && ri.lt == 3 && row_masked<NT, EPT, 3>(ri.mask, P, w, o, B, live))
+                if (((LF_MASKED_LTS >> 3) & 1) && lt == 3 && row_masked<NT, EPT, 3>(ri.mask, P, w, o, B, lv))
                     continue;
             }
 #endif
             // EPT >= 2: k-outer rows (EPT live accumulators; C4 2.66 -> 2.53 ms,
             // C3 1.39 -> 1.33 ms with two entries per thread); EPT = 1: the
             // LT-unrolled form keeps more independent FMA chains in flight
-            switch (ri.lt) {
-            case 1: row_dispatch<NT, EPT, 1, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
-            case 2: row_dispatch<NT, EPT, 2, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
-            case 3: row_dispatch<NT, EPT, 3, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
-            case 4: row_dispatch<NT, EPT, 4, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
-            case 5: row_dispatch<NT, EPT, 5, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
-            case 7: row_dispatch<NT, EPT, 7, ACCUM>(P, w, ri.mask, kr, o, B, live); break;
-            default: combine_row_dyn<NT, EPT, ACCUM>(P, w, ri.lt, ri.mask, o, B, live); break;
+            switch (lt) {
+            case 1: row_dispatch<NT, EPT, 1, ACCUM>(P, w, ri.mask, kr, o, B, lv); break;
+            case 2: row_dispatch<NT, EPT, 2, ACCUM>(P, w, ri.mask, kr, o, B, lv); break;
+            case 3: row_dispatch<NT, EPT, 3, ACCUM>(P, w, ri.mask, kr, o, B, lv); break;
+            case 4: row_dispatch<NT, EPT, 4, ACCUM>(P, w, ri.mask, kr, o, B, lv); break;
+            case 5: row_dispatch<NT, EPT, 5, ACCUM>(P, w, ri.mask, kr, o, B, lv); break;
+            case 7: row_dispatch<NT, EPT, 7, ACCUM>(P, w, ri.mask, kr, o, B, lv); break;
+            default: combine_row_dyn<NT, EPT, ACCUM>(P, w, lt, ri.mask, o, B, lv); break;
             }
         }
     }

@@ -423,8 +423,11 @@ __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard(const DevTables d,
             const int at = al / el.nl2, as = al % el.nl2;
             const int bt = be / el.nl2, bs = be % el.nl2;
             const int it = ft + at, jt = ft + bt;
-            const bool row_i = it >= d.t0 && it < d.t1;
-            const bool row_j = d.sym && al != be && jt >= d.t0 && jt < d.t1;
+            // rows of functions (it, is) / (jt, js) inside the output range [f0, f1)
+            const long long gi = (long long)it * d.ns + (el.fv + as / (d.pu + 1)) * d.nu + el.fu + as % (d.pu + 1);
+            const long long gj = (long long)jt * d.ns + (el.fv + bs / (d.pu + 1)) * d.nu + el.fu + bs % (d.pu + 1);
+            const bool row_i = gi >= d.f0 && gi < d.f1;
+            const bool row_j = d.sym && al != be && gj >= d.f0 && gj < d.f1;
             if (!row_i && !row_j)
                 continue;
             double acc[9];
@@ -480,7 +483,7 @@ __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard(const DevTables d,
                 const int slot = (jv - d.lo_v[iv]) * Lu + (ju - d.lo_u[iu]);
                 const int Lt = d.len_t[rt];
                 const long long pos = 9 * d.S_s * (d.pre_t[rt] - pre0) + (long long)Lt * d.es_pre[is] +
-                                      (long long)(ct_ - d.lo_t[rt]) * B + 3 * slot;
+                                      (long long)(ct_ - d.lo_t[rt]) * B + 3 * slot - d.out_base;
                 LF_CHECK(pos >= 0 && pos + 2LL * Lt * B + 2 < d.nnz_slab && ct_ >= d.lo_t[rt] &&
                          ct_ < d.lo_t[rt] + Lt);
 #pragma unroll
@@ -631,17 +634,16 @@ __global__ void k_pattern_rows(const DevTables d, long long* __restrict__ row_pt
     if (r > rows)
         return;
     if (r == rows) {
-        row_ptr[rows] = 9 * d.S_s * (d.pre_t[d.t1] - d.pre_t[d.t0]);
+        row_ptr[rows] = d.rp_base + d.nnz_slab;
         return;
     }
-    const long long per_t = 3LL * d.ns;
-    const int it = d.t0 + (int)(r / per_t);
-    const long long rr = r % per_t;
-    const int is = (int)(rr / 3), a = (int)(rr % 3);
+    const long long g = d.f0 + r / 3; // function i_t * ns + i_s of row r
+    const int it = (int)(g / d.ns), is = (int)(g % d.ns), a = (int)(r % 3);
     const int iu = is % d.nu, iv = is / d.nu;
     const int B = 3 * d.len_u[iu] * d.len_v[iv];
     const int Lt = d.len_t[it];
-    row_ptr[r] = 9 * d.S_s * (d.pre_t[it] - d.pre_t[d.t0]) + (long long)Lt * (d.es_pre[is] + (long long)a * B);
+    row_ptr[r] = d.rp_base + 9 * d.S_s * (d.pre_t[it] - d.pre_t[d.t0]) +
+                 (long long)Lt * (d.es_pre[is] + (long long)a * B) - d.out_base;
 }
 
 /// Columns of the slab's CSR.  Thread slots are warp-contiguous (a warp owns
@@ -655,7 +657,7 @@ __global__ void __launch_bounds__(kBlock) k_pattern_cols(const DevTables d, int*
     int* o0[kColsEpt];
     int B[kColsEpt], col_s[kColsEpt];
     long long A[kColsEpt];
-    bool live[kColsEpt];
+    bool live[kColsEpt], in_s0[kColsEpt], in_s1[kColsEpt];
 #pragma unroll
     for (int x = 0; x < kColsEpt; ++x) {
         const long long e = (long long)blockIdx.x * kBlock * kColsEpt + (threadIdx.x >> 5) * 32 * kColsEpt +
@@ -667,6 +669,8 @@ __global__ void __launch_bounds__(kBlock) k_pattern_cols(const DevTables d, int*
             ++is;
         const long long ebase = __ldg(d.es_pre + is);
         const int r = (int)(ec - ebase);
+        in_s0[x] = is >= d.s0;
+        in_s1[x] = is < d.s1;
         const int iu = is % d.nu, iv = is / d.nu;
         const int Lu = __ldg(d.len_u + iu), Lv = __ldg(d.len_v + iv);
         B[x] = 3 * Lu * Lv;
@@ -682,17 +686,22 @@ __global__ void __launch_bounds__(kBlock) k_pattern_cols(const DevTables d, int*
     const long long pre0 = __ldg(d.pre_t + d.t0);
     for (int it = it_begin; it < it_end; ++it) {
         const int Lt = __ldg(d.len_t + it);
-        const long long base = 9 * d.S_s * (__ldg(d.pre_t + it) - pre0);
+        const long long base = 9 * d.S_s * (__ldg(d.pre_t + it) - pre0) - d.out_base;
         const int c0 = 3 * d.ns * __ldg(d.lo_t + it);
+        const int edge = row_edge(d, it);
+        bool lv[kColsEpt];
 #pragma unroll
         for (int x = 0; x < kColsEpt; ++x)
-            LF_CHECK(!live[x] || (base + (long long)Lt * A[x] + (o0[x] - cols) >= 0 &&
-                                  base + (long long)Lt * A[x] + (long long)(Lt - 1) * B[x] + (o0[x] - cols) <
-                                      d.nnz_slab));
+            lv[x] = live[x] && (!(edge & 1) || in_s0[x]) && (!(edge & 2) || in_s1[x]);
+#pragma unroll
+        for (int x = 0; x < kColsEpt; ++x)
+            LF_CHECK(!lv[x] || (base + (long long)Lt * A[x] + (o0[x] - cols) >= 0 &&
+                                base + (long long)Lt * A[x] + (long long)(Lt - 1) * B[x] + (o0[x] - cols) <
+                                    d.nnz_slab));
         for (int k = 0; k < Lt; ++k) {
 #pragma unroll
             for (int x = 0; x < kColsEpt; ++x)
-                if (live[x])
+                if (lv[x])
                     __stcs(o0[x] + base + (long long)Lt * A[x] + (long long)k * B[x], c0 + 3 * d.ns * k + col_s[x]);
         }
     }
@@ -846,17 +855,20 @@ __global__ void __launch_bounds__(256) k_plan_symmetry(const DevTables d, const 
         const long long pre0 = __ldg(d.pre_t + d.t0), nine_S = 9 * d.S_s;
         const int it0 = d.t0 + blockIdx.y * t_chunk, it1 = min(d.t1, it0 + t_chunk);
         for (int it = it0; it < it1; ++it) {
+            const long long gi = (long long)it * d.ns + is;
+            if (gi < d.f0 || gi >= d.f1)
+                continue; // partial first / last row
             const int Lt = __ldg(d.len_t + it), lot = __ldg(d.lo_t + it);
-            const long long base_i = nine_S * (__ldg(d.pre_t + it) - pre0);
+            const long long base_i = nine_S * (__ldg(d.pre_t + it) - pre0) - d.out_base;
             for (int k = 0; k < Lt; ++k) {
                 const int jt = lot + k;
-                if (jt < d.t0 || jt >= d.t1)
+                const long long gj = (long long)jt * d.ns + js;
+                if (gj < d.f0 || gj >= d.f1)
                     continue; // mirror row block outside the slab
-                const long long gi = (long long)it * d.ns + is, gj = (long long)jt * d.ns + js;
                 if (gi > gj)
                     continue;
                 const int Ltj = __ldg(d.len_t + jt);
-                const long long base_j = nine_S * (__ldg(d.pre_t + jt) - pre0);
+                const long long base_j = nine_S * (__ldg(d.pre_t + jt) - pre0) - d.out_base;
                 const double* own = v + base_i + (long long)Lt * esi + (long long)k * Bi + 3 * slot;
                 const double* mir = v + base_j + (long long)Ltj * esj + (long long)(it - __ldg(d.lo_t + jt)) * Bj +
                                     3 * slot_m;
@@ -927,7 +939,7 @@ int launch_inplane_general(const DevTables& d, cudaStream_t stream) {
 int inplane_general_launches(const DevTables& d) { return 2 * ((d.n_terms + d.pe_terms - 1) / d.pe_terms); }
 
 int launch_pattern(const DevTables& d, long long* row_ptr, int* cols, cudaStream_t stream) {
-    const long long rows = 3LL * d.ns * (d.t1 - d.t0);
+    const long long rows = 3 * (d.f1 - d.f0);
     k_pattern_rows<<<(unsigned)((rows + 1 + 255) / 256), 256, 0, stream>>>(d, row_ptr, rows);
     if (d.E > 0 && d.t1 > d.t0) {
         const int nt = d.t1 - d.t0;

@@ -143,9 +143,9 @@ __global__ void k_thickness_pairs(DevTables d) {
     if (gw >= d.n_pairs)
         return;
     const long long pp = gw;
-    // locate (it, k): pre_t[it] - pre_t[t0] <= pp < pre_t[it+1] - pre_t[t0]
-    const long long target = pp + d.pre_t[d.t0];
-    int lo = d.t0, hi = d.t1; // it in [t0, t1)
+    // locate (it, k): pre_t[it] - pre_t[w_t0] <= pp < pre_t[it+1] - pre_t[w_t0]
+    const long long target = pp + d.pre_t[d.w_t0];
+    int lo = d.w_t0, hi = d.w_t1; // it in [w_t0, w_t1)
     while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
         if (d.pre_t[mid] <= target)
@@ -313,8 +313,8 @@ __device__ void integral_1d(const double* kn, const int* first, const double* sl
 /// one thread).
 template <int P>
 __device__ void thickness_pair_warp(const DevTables& d, long long pp, int lane) {
-    const long long target = pp + d.pre_t[d.t0];
-    int lo = d.t0, hi = d.t1;
+    const long long target = pp + d.pre_t[d.w_t0];
+    int lo = d.w_t0, hi = d.w_t1;
     while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
         if (d.pre_t[mid] <= target)

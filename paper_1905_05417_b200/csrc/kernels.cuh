@@ -86,10 +86,18 @@ struct DevTables {
     double* Pg;                                // [T][4][E] (general geometry)
     double* Pe;     // element-local P of a batch of pe_terms terms: [term][el][4][nl2][3][nl2][3]
     int pe_terms;   // terms per batch
-    // slab
-    int t0, t1;
+    // output range: the functions f = i_t * ns + i_s in [f0, f1), covering
+    // thickness rows [t0, t1) -- row t0 from in-plane function s0, row t1 - 1
+    // up to s1 (exclusive).  Entry (it, is, ...) of the range is written at
+    // 9 S_s (pre_t[it] - pre_t[t0]) + L_t(it) es_pre[is] + ... - out_base;
+    // row offsets get rp_base added (0: slab-local CSR).
+    int t0, t1, s0, s1;
+    long long f0, f1, out_base, rp_base;
+    // thickness rows whose pair weights W / Wmask hold (the plan's slab;
+    // a streamed sub-range reads the plan's W)
+    int w_t0, w_t1;
     long long n_pairs, E;
-    long long nnz_slab; // values of this plan's slab (bounds checks in LF_DEBUG_CHECKS builds)
+    long long nnz_slab; // values of this range (bounds checks in LF_DEBUG_CHECKS builds)
 };
 
 // Launchers (all asynchronous on `stream`).  Return cudaError_t as int.

@@ -599,6 +599,65 @@ Setup buildSpaceSetup(const lf_problem& p, bool need_geometry) {
     return s;
 }
 
+int64_t functionOffset(const Setup& s, int64_t f) {
+    const int64_t F = static_cast<int64_t>(s.n_t) * s.n_s;
+    if (f >= F)
+        return 9 * s.S_s * s.at.pre[static_cast<std::size_t>(s.n_t)];
+    const int t = static_cast<int>(f / s.n_s), is = static_cast<int>(f % s.n_s);
+    return 9 * s.S_s * s.at.pre[static_cast<std::size_t>(t)] +
+           static_cast<int64_t>(s.at.len[static_cast<std::size_t>(t)]) * s.es_pre[static_cast<std::size_t>(is)];
+}
+
+Range rangeOf(const Setup& s, int64_t f0, int64_t f1) {
+    const int64_t F = static_cast<int64_t>(s.n_t) * s.n_s;
+    if (f1 < 0)
+        f1 = F;
+    if (f0 < 0 || f0 > f1 || f1 > F)
+        raise(LF_ERR_INVALID_ARGUMENT, "row slab out of range");
+    Range r;
+    r.f0 = f0;
+    r.f1 = f1;
+    r.rows = 3 * (f1 - f0);
+    r.row_begin = 3 * f0;
+    r.nnz_begin = functionOffset(s, f0);
+    if (f0 == f1) { // empty slab
+        r.t0 = r.t1 = static_cast<int>(std::min<int64_t>(f0 / s.n_s, s.n_t));
+        r.s0 = 0;
+        r.s1 = s.n_s;
+        return r;
+    }
+    r.t0 = static_cast<int>(f0 / s.n_s);
+    r.s0 = static_cast<int>(f0 % s.n_s);
+    r.t1 = static_cast<int>((f1 + s.n_s - 1) / s.n_s);
+    r.s1 = static_cast<int>(f1 - static_cast<int64_t>(r.t1 - 1) * s.n_s);
+    r.out_base = static_cast<int64_t>(s.at.len[static_cast<std::size_t>(r.t0)]) * s.es_pre[static_cast<std::size_t>(r.s0)];
+    r.n_pairs = s.at.pre[static_cast<std::size_t>(r.t1)] - s.at.pre[static_cast<std::size_t>(r.t0)];
+    r.nnz = functionOffset(s, f1) - r.nnz_begin;
+    return r;
+}
+
+void applyRange(Setup& s, int64_t f0, int64_t f1) {
+    const Range r = rangeOf(s, f0, f1);
+    s.f0 = r.f0;
+    s.f1 = r.f1;
+    s.t0 = r.t0;
+    s.t1 = r.t1;
+    s.s0 = r.s0;
+    s.s1 = r.s1;
+    s.out_base = r.out_base;
+    s.rows = r.rows;
+    s.row_begin = r.row_begin;
+    s.n_pairs = r.n_pairs;
+    s.nnz_begin = r.nnz_begin;
+    s.nnz = r.nnz;
+}
+
+Setup buildSetupRange(const lf_problem& p, int backend, int64_t f0, int64_t f1) {
+    Setup s = buildSetup(p, backend, 0, -1);
+    applyRange(s, f0, f1);
+    return s;
+}
+
 Setup buildSetup(const lf_problem& p, int backend, int t0, int t1) {
     if (backend != LF_BACKEND_FAST && backend != LF_BACKEND_STANDARD && backend != LF_BACKEND_VOIGT_FREE)
         raise(LF_ERR_INVALID_ARGUMENT, "unknown backend");
@@ -714,13 +773,7 @@ Setup buildSetup(const lf_problem& p, int backend, int t0, int t1) {
         t1 = s.n_t;
     if (t0 < 0 || t0 > t1 || t1 > s.n_t)
         raise(LF_ERR_INVALID_ARGUMENT, "row slab out of range");
-    s.t0 = t0;
-    s.t1 = t1;
-    s.rows = 3LL * s.n_s * (t1 - t0);
-    s.row_begin = 3LL * s.n_s * t0;
-    s.n_pairs = s.at.pre[static_cast<std::size_t>(t1)] - s.at.pre[static_cast<std::size_t>(t0)];
-    s.nnz = 9 * s.S_s * s.n_pairs;
-    s.nnz_begin = 9 * s.S_s * s.at.pre[static_cast<std::size_t>(t0)];
+    applyRange(s, static_cast<int64_t>(t0) * s.n_s, static_cast<int64_t>(t1) * s.n_s);
 
     // analytic AssemblyStats (test_fast.cpp:343-351, test_assembly.cpp:249-253)
     const int64_t per_build = static_cast<int64_t>(s.spu.size() * s.spv.size()) * s.nqu * s.nqv;
@@ -760,6 +813,35 @@ void slabBounds(const Setup& s, int n_parts, int part, int* t0, int* t1) {
     };
     *t0 = cut(part);
     *t1 = std::max(*t0, cut(part + 1));
+}
+
+void slabBoundsFunctions(const Setup& s, int n_parts, int part, int64_t* f0, int64_t* f1) {
+    if (n_parts < 1 || part < 0 || part >= n_parts)
+        raise(LF_ERR_INVALID_ARGUMENT, "slab: bad part");
+    // cut at function boundaries, balanced by nnz: the prefix functionOffset
+    // is nondecreasing in f, so the closest cut is found by bisection
+    const int64_t F = static_cast<int64_t>(s.n_t) * s.n_s;
+    const int64_t total = functionOffset(s, F);
+    auto cut = [&](int k) -> int64_t {
+        if (k == 0)
+            return 0;
+        if (k == n_parts)
+            return F;
+        const long double target = static_cast<long double>(total) * k / n_parts;
+        int64_t lo = 0, hi = F; // first f with offset >= target lies in [lo, hi]
+        while (lo < hi) {
+            const int64_t mid = lo + (hi - lo) / 2;
+            if (static_cast<long double>(functionOffset(s, mid)) < target)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        if (lo > 0 && target - functionOffset(s, lo - 1) < functionOffset(s, lo) - target)
+            --lo;
+        return lo;
+    };
+    *f0 = cut(part);
+    *f1 = std::max(*f0, cut(part + 1));
 }
 
 } // namespace lfb

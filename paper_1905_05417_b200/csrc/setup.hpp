@@ -132,8 +132,12 @@ struct Setup {
     int64_t S_s = 0;                    // in-plane pairs
     std::vector<int64_t> es_pre;        // [n_s + 1] = 9 * P_s(i_s)
     int n_u = 0, n_v = 0, n_t = 0, n_s = 0;
-    // slab
-    int t0 = 0, t1 = 0;
+    // slab: the functions f = i_t * n_s + i_s in [f0, f1) (rows 3 f0 .. 3 f1);
+    // they cover the thickness rows [t0, t1), the first from in-plane
+    // function s0, the last up to s1 (exclusive); out_base = L_t(t0) *
+    // es_pre[s0] is the offset of (t0, s0) inside thickness row t0's block
+    int t0 = 0, t1 = 0, s0 = 0, s1 = 0;
+    int64_t f0 = 0, f1 = 0, out_base = 0;
     int64_t rows = 0, nnz = 0, row_begin = 0, nnz_begin = 0, n_pairs = 0;
     // stats of one assembly (analytic)
     lf_stats stats{};
@@ -141,6 +145,19 @@ struct Setup {
 
 /// Builds the setup of `backend` for thickness rows [t0, t1) (t1 < 0: all).
 Setup buildSetup(const lf_problem& p, int backend, int t0, int t1);
+/// The same for the functions [f0, f1) (f = i_t * n_s + i_s; f1 < 0: all):
+/// row slabs cut inside a thickness row.
+Setup buildSetupRange(const lf_problem& p, int backend, int64_t f0, int64_t f1);
+/// Sizes and offsets of the functions [f0, f1) of a full setup (f1 < 0: to the end).
+struct Range {
+    int t0 = 0, t1 = 0, s0 = 0, s1 = 0;
+    int64_t f0 = 0, f1 = 0, out_base = 0, rows = 0, row_begin = 0, nnz = 0, nnz_begin = 0, n_pairs = 0;
+};
+Range rangeOf(const Setup& s, int64_t f0, int64_t f1);
+/// Restricts a setup to the functions [f0, f1) (slab sizes and offsets).
+void applyRange(Setup& s, int64_t f0, int64_t f1);
+/// Global CSR offset of the first entry of function f (f = n_t * n_s: nnz).
+int64_t functionOffset(const Setup& s, int64_t f);
 
 /// Space-only setup (knots, spans, quadrature, adjacency) used by the
 /// operator-level entry points.
@@ -148,5 +165,8 @@ Setup buildSpaceSetup(const lf_problem& p, bool need_geometry);
 
 /// Row slab of n_parts balanced by nnz at thickness-function boundaries.
 void slabBounds(const Setup& full, int n_parts, int part, int* t0, int* t1);
+/// Row slab of n_parts balanced by nnz at function boundaries (cuts inside
+/// thickness rows): functions [f0, f1).
+void slabBoundsFunctions(const Setup& full, int n_parts, int part, int64_t* f0, int64_t* f1);
 
 } // namespace lfb

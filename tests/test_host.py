@@ -191,3 +191,30 @@ def test_report_format_round_trip():
     assert lines[2].split(",")[7] == ""  # empty rel_diff cell when unavailable
     back = R.parse_json(R.emit_json(rep))
     assert back == rep
+
+
+@pytest.mark.parametrize("name,parts", [("C5", 8), ("C5", 3), ("C4", 8), ("C2", 7)])
+def test_function_slab_bounds_balance_and_oracle_offsets(oracle, name, parts):
+    """lf_slab_bounds_functions (host only): the parts tile [0, n_t n_s),
+    their nnz are balanced to within one function's row block (C5 x 8: the
+    thickness-function cuts of round 1 had max/mean 1.069), and every cut's
+    global offset equals the oracle's row offset of that function."""
+    import paper_1905_05417_b200 as lf
+    prob = P.baseline_config(name)
+    terms = oracle.fast_terms(prob, want_values=False)
+    prev, nnz = 0, []
+    for part in range(parts):
+        b = lf.slab_bounds_functions(prob, parts, part)
+        assert b["f_begin"] == prev and b["f_end"] >= b["f_begin"]
+        assert b["row_begin"] == 3 * b["f_begin"] and b["row_end"] == 3 * b["f_end"]
+        assert b["nnz_begin"] == terms.function_offset(b["f_begin"])
+        assert b["nnz_end"] == terms.function_offset(b["f_end"])
+        nnz.append(b["nnz_end"] - b["nnz_begin"])
+        prev = b["f_end"]
+    assert prev == prob.n_s * prob.n_t
+    assert sum(nnz) == P.sizes(prob)["nnz"]
+    # within one function's row block (3 rows of at most 3 (2p+1)^2 L_t entries)
+    assert max(nnz) - sum(nnz) / parts <= 9 * 49 * 5
+    if name == "C5":
+        assert max(nnz) / (sum(nnz) / parts) <= 1.000001
+    terms.close()
