@@ -7,12 +7,21 @@ One step = one complete fast assembly (assembleFast: basis evaluation,
 thickness integrals, in-plane operators, combination into the FP64 CSR
 values) of the workload, inputs resident in HBM.  Workload at N=1: BASELINE
 config C4 (128x64 elements, p=2, 128 plies, 1.92e9 nnz, 23 GB CSR) -- the
-largest BASELINE config that fits one B200 (C5 is 203 GB).  With N ranks
-(torchrun) the path partitions into row slabs, one per GPU, no
-collective on the data path.  Default --scaling weak: the laminate of the
-config family grows with N (N x 128 plies for C4) and each rank assembles one
-nnz-balanced slab of it, i.e. one C4's worth of rows per GPU; --scaling strong
-splits the fixed config across the N GPUs instead.
+largest BASELINE config that fits one B200 with its pattern (C5 is 203 GB).
+With N ranks (torchrun) the path partitions into row slabs,
+one per GPU, cut at function boundaries and balanced by nnz, no collective on
+the data path.  Default --scaling weak: the laminate of the config family
+grows with N (N x 128 plies for C4) and each rank assembles one slab of it,
+i.e. one C4's worth of rows per GPU; --scaling strong splits the fixed config
+across the N GPUs instead.
+
+Also in the line (each its own timed region, never inside the headline one):
+  c5            BASELINE C5 (the scaling case, 1.69e10 nnz) split over the N
+                ranks (strong scaling): per-rank device time, max over ranks,
+                balance, roofline; at N=1 also its streamed e2e (203 GB
+                through lf_assemble_stream into pinned host staging);
+  e2e_dropin    the C++ drop-in's assembleFast (std::vector result in
+                pageable memory) timed by build/dropin_e2e.
 
 Reported beside the device number:
   e2e           the same metric through the C-ABI one-shot call lf_assemble
@@ -65,6 +74,10 @@ def parse():
                     help="weak: N x the config's plies, one slab per GPU; strong: the config split N ways")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the multi-rank path on fewer GPUs than ranks")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 strong-scaling sub-measurement")
+    ap.add_argument("--no-dropin", action="store_true", help="skip the C++ drop-in e2e timing")
+    ap.add_argument("--no-oracle-check", action="store_true",
+                    help="N>1: skip the per-rank oracle comparison of one sampled thickness row")
     return ap.parse_args()
 
 
@@ -128,9 +141,11 @@ class ClockSampler:
 
 
 def reference_arm(args, rank, world):
-    """--impl reference: the reference's own CPU fast assembler (oracle/_ref)."""
+    """--impl reference: the reference's own CPU fast assembler (oracle/_ref),
+    all host threads, on a bounded sample of the workload family."""
     if rank != 0:
         return
+    import resource
     from oracle.checkers import Reference
     from paper_1905_05417_b200 import problem as P
     if not Reference.available():
@@ -141,27 +156,40 @@ def reference_arm(args, rank, world):
     plies = choose_sample_plies(ref, args, threads, budget_s=150.0)
     prob = P.baseline_config(args.config, plies=plies)
     nnz = P.sizes(prob)["nnz"]
+    full_plies = len(P.baseline_config(args.config).layers)
     for _ in range(args.warmup):
         ref.assemble(prob, "fast", threads)
     times = []
+    ru0 = resource.getrusage(resource.RUSAGE_SELF)
     for _ in range(args.steps):
         t0 = time.perf_counter()
         ref.assemble(prob, "fast", threads)
         times.append(time.perf_counter() - t0)
-    sec = sum(times) / len(times)
+    ru1 = resource.getrusage(resource.RUSAGE_SELF)
+    cpu_s = (ru1.ru_utime - ru0.ru_utime) + (ru1.ru_stime - ru0.ru_stime)
+    wall = sum(times)
+    sec = wall / len(times)
     value = nnz / sec
-    sample = (f"{args.config} family with {plies} plies instead of "
-              f"{len(P.baseline_config(args.config).layers)} (same elements, degree, materials); "
-              f"{nnz} nnz per step")
+    sample = (f"{args.config} family with {plies} plies instead of {full_plies} (same elements, degree, "
+              f"materials); {nnz} nnz per step")
     line = {
         "impl": "reference", "metric": "assembled stiffness nnz/s (FP64 CSR)", "value": value,
         "unit": "nnz/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "backend": "fast", "sample_plies": plies,
-                   "nnz_per_step": nnz},
+                   "nnz_per_step": nnz, "same_config": plies == full_plies,
+                   "same_config_reason": None if plies == full_plies else
+                   (f"the full {args.config} takes minutes per step on the host (reference ~8e6 nnz/s vs "
+                    f"{P.sizes(P.baseline_config(args.config))['nnz']:.3g} nnz), so each step is the "
+                    f"first {plies} plies of the same laminate; the reference's rate is flat in the "
+                    f"ply count (profiles/r2_cpu_ply_trend.txt)")},
         "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": threads, "kind": "reference",
-                         "sample": sample},
+                         "sample": sample, "threads_requested": threads,
+                         "effective_parallelism": cpu_s / wall if wall > 0 else None,
+                         "note": "AssemblyOptions.threads = all host threads; the reference's "
+                                 "SparseMatrixBuilder merge and stable_sort run on one thread, so the "
+                                 "measured CPU-time/wall ratio is the effective parallelism"},
         "e2e": {"value": value, "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -210,6 +238,52 @@ def cpu_baseline(args):
                       f"reference sources compiled with the Eigen subset, threads={threads}"}
 
 
+def device_step_time(plans, vals_ptrs, steps, warmup, stream, world, dist_backend):
+    """Event-timed steps of the given plans (one step = every plan once),
+    barrier + synchronize on both sides, max over ranks.  Returns (ms per
+    step, combine ms per step, combine launches, launches per step)."""
+    import torch
+    import torch.distributed as dist
+
+    def step():
+        for p, v in zip(plans, vals_ptrs):
+            p.assemble(v)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    for p in plans:
+        p.kernel_time(reset=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    k_ms = k_n = 0
+    for p in plans:
+        a, b = p.kernel_time(reset=True)
+        k_ms += a
+        k_n += b
+    local = (ms / steps, k_ms / steps)
+    t = torch.tensor(list(local), dtype=torch.float64)
+    per_rank = [local]
+    if world > 1:
+        tc = t.cuda() if dist_backend == "nccl" else t
+        gathered = [torch.empty_like(tc) for _ in range(world)]
+        dist.all_gather(gathered, tc)
+        per_rank = [tuple(float(x) for x in g.cpu()) for g in gathered]
+    return {"ms_per_step": max(r[0] for r in per_rank), "combine_ms_per_step": k_ms / steps,
+            "combine_launches": k_n, "launches_per_step": sum(p.launch_count for p in plans),
+            "per_rank_ms": [r[0] for r in per_rank], "local_ms": local[0]}
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -219,6 +293,12 @@ def main():
         reference_arm(args, rank, world)
         return
 
+    if world > 1:
+        # NCCL's own log (stderr) records the communicator size per rank
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        # the per-rank oracle check shares the host cores
+        os.environ.setdefault("OMP_NUM_THREADS", str(max(1, (os.cpu_count() or 1) // world)))
     import torch
     import torch.distributed as dist
     import paper_1905_05417_b200 as lf
@@ -235,28 +315,27 @@ def main():
     plies = base_plies * world if args.scaling == "weak" else base_plies
     prob = P.baseline_config(args.config, plies=plies)
     sz = P.sizes(prob)
-    bounds = lf.slab_bounds(prob, world, rank) if world > 1 else {"t_begin": 0, "t_end": prob.n_t}
+    # this rank's slab: functions [f_begin, f_end), cut inside thickness rows,
+    # balanced by nnz to within one function
+    bounds = (lf.slab_bounds_functions(prob, world, rank) if world > 1 else
+              {"f_begin": 0, "f_end": prob.n_s * prob.n_t, "row_begin": 0, "nnz_begin": 0})
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
 
-    # this rank's slab; split into sequential sub-slab passes when its values
-    # do not fit in HBM next to the workspace (C5: 135 GB of values)
-    free, _ = torch.cuda.mem_get_info()
-    full = lf.Plan(prob, "fast", device, bounds["t_begin"], bounds["t_end"], stream=stream.cuda_stream)
-    # pattern + values resident when both fit; else values only (C5: 135 GB of
-    # values fit one B200, the 67 GB of columns beside them do not), in as few
+    # pattern + values resident when both fit; else values only, in as few
     # sequential sub-slab passes as the values need
+    free, _ = torch.cuda.mem_get_info()
+    full = lf.Plan(prob, "fast", device, stream=stream.cuda_stream, f_begin=bounds["f_begin"],
+                   f_end=bounds["f_end"])
     with_pattern = full.nnz * 12 + full.rows * 8 <= int(0.85 * free)
     passes = 1 if with_pattern else max(1, -(-full.nnz * 8 // int(0.9 * free)))
-    if not with_pattern and os.environ.get("LAMFAST_BENCH_PASSES"):
-        passes = max(passes, int(os.environ["LAMFAST_BENCH_PASSES"]))
     if passes == 1:
         plans = [full]
     else:
         full.close()
-        nt = bounds["t_end"] - bounds["t_begin"]
-        cuts = [bounds["t_begin"] + (nt * k) // passes for k in range(passes + 1)]
-        plans = [lf.Plan(prob, "fast", device, cuts[k], cuts[k + 1], stream=stream.cuda_stream)
+        f0, f1 = bounds["f_begin"], bounds["f_end"]
+        cuts = [f0 + ((f1 - f0) * k) // passes for k in range(passes + 1)]
+        plans = [lf.Plan(prob, "fast", device, stream=stream.cuda_stream, f_begin=cuts[k], f_end=cuts[k + 1])
                  for k in range(passes)]
     vals = torch.empty(max(p.nnz for p in plans), dtype=torch.float64, device="cuda")
     rp = cols = None
@@ -281,49 +360,17 @@ def main():
         pattern = {"ms": pms, "bytes": pbytes, "gbs": pbytes / (pms / 1e3) / 1e9,
                    "kernels": "k_pattern_rows + k_pattern_cols"}
 
-    def step():
-        for p in plans:
-            p.assemble(vals.data_ptr())
-
     sampler = ClockSampler(device)
     sampler.start()
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    for p in plans:
-        p.kernel_time(reset=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(args.steps):
-        step()
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    timing = device_step_time(plans, [vals.data_ptr()] * len(plans), args.steps, args.warmup, stream, world,
+                              args.dist_backend)
     clocks = sampler.stop()
-    ms_total = ev0.elapsed_time(ev1)
-    k_ms = k_n = 0
-    for p in plans:
-        a, b = p.kernel_time(reset=True)
-        k_ms += a
-        k_n += b
-    launches = sum(p.launch_count for p in plans) * args.steps
+    ms_per_step = timing["ms_per_step"]
+    launches = timing["launches_per_step"] * args.steps
     rank_nnz = sum(p.nnz for p in plans)
     # combine kernel: average duration of one launch over all sub-slabs -> bytes/s
-    k_avg_ms = k_ms / max(k_n, 1)
+    k_avg_ms = timing["combine_ms_per_step"] * args.steps / max(timing["combine_launches"], 1)
     k_bytes = rank_nnz * 8 / len(plans)
-    t = torch.tensor([ms_total, k_ms / max(args.steps, 1)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX) if args.dist_backend == "nccl" else None
-        if args.dist_backend != "nccl":
-            tc = t.cpu()
-            dist.all_reduce(tc, op=dist.ReduceOp.MAX)
-            t = tc
-    ms_total = float(t[0])
-    ms_per_step = ms_total / args.steps
     total_nnz = sz["nnz"]
     value = total_nnz / (ms_per_step / 1e3)
 
@@ -332,15 +379,23 @@ def main():
     if world == 1 and with_pattern:
         st = lf.device_csr_stats(plans[0].rows, rp.data_ptr(), cols.data_ptr(), vals.data_ptr(),
                                  stream.cuda_stream)
-        verify = {"fro_norm": st["fro_sq"] ** 0.5, "symmetry_rel": (st["sym_sq"] / st["fro_sq"]) ** 0.5}
+        verify = {"fro_norm": st["fro_sq"] ** 0.5, "symmetry_rel": (st["sym_sq"] / st["fro_sq"]) ** 0.5,
+                  "symmetry_rel_closed_form": (plans[0].symmetry_sq(vals.data_ptr()) / st["fro_sq"]) ** 0.5}
     elif world > 1 and with_pattern:
-        # gather of slab summaries (verification only, never timed)
         from paper_1905_05417_b200 import distributed as D
         s = D.slab_summary(rp, cols, vals[:plans[0].nnz], bounds["row_begin"], bounds["nnz_begin"])
+        if not args.no_oracle_check:  # verification leg, outside the timed region
+            from oracle.checkers import slab_oracle_delta
+            s = D.with_field(s, "oracle_rel_dk", slab_oracle_delta(prob, bounds["f_begin"], bounds["f_end"], rp,
+                                                                    cols, vals[:plans[0].nnz]))
         parts = D.gather_summaries(s.cuda() if args.dist_backend == "nccl" else s)
         tot = D.combine_summaries(parts)
         verify = {"fro_norm": tot["fro_sq"] ** 0.5, "nnz_gathered": int(tot["nnz"]),
-                  "rows_gathered": int(tot["rows"]), "pattern_hash": tot["pattern_hash"]}
+                  "rows_gathered": int(tot["rows"]), "pattern_hash": tot["pattern_hash"],
+                  "pattern_hash_closed_form_ok": int(tot["nnz"]) == total_nnz and int(tot["rows"]) == sz["dim"],
+                  "oracle_max_rel_dk_per_rank": [float(p[D.FIELD_INDEX["oracle_rel_dk"]]) for p in parts]
+                  if not args.no_oracle_check else None,
+                  "nccl_ranks": world}
         # full-slab gather to rank 0 over NCCL where the whole K fits there
         fits = torch.tensor([1.0 if (sz["nnz"] * 12 + sz["dim"] * 8) * 2 <= 0.8 * torch.cuda.mem_get_info()[0]
                              else 0.0], dtype=torch.float64, device="cuda")
@@ -367,14 +422,18 @@ def main():
                 "kernel": "k_combine (K4)", "bytes_per_launch": k_bytes,
                 "kernel_ms": k_avg_ms, "peak_source": peak_src,
                 "step_frac": value * 8 / (world * hbm * 1e9)}
+    # ncu DRAM traffic is attached only to the exact workload it was captured on
     traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(traffic_file):
         try:
             with open(traffic_file) as f:
                 tj = json.load(f).get(args.config)
-            if tj:
+            if tj and world == 1 and passes == 1 and plies == base_plies:
                 roofline["traffic"] = tj["dram_bytes_per_launch"]
                 roofline["traffic_source"] = tj["source"]
+            elif tj:
+                roofline["traffic_note"] = (f"ncu traffic is from the 1-GPU {args.config} capture; this "
+                                            f"line's per-rank workload differs, so traffic is null")
         except Exception:
             pass
     del rp, cols, vals
@@ -402,13 +461,7 @@ def main():
         pass
 
     e2e = None
-    if args.no_e2e:
-        e2e = None
-    elif not with_pattern:
-        e2e = {"value": None, "unit": "nnz/s",
-               "unavailable": f"the {args.config} CSR ({total_nnz * 12 / 1e9:.0f} GB) does not fit one "
-                              f"device for a one-shot host-buffer call"}
-    else:
+    if not args.no_e2e:
         try:
             if world == 1:
                 e2e = measure_e2e(args, prob, device, total_nnz)
@@ -416,6 +469,11 @@ def main():
                 e2e = measure_e2e_slab(args, prob, device, rank, world, bounds, total_nnz)
         except Exception as exc:  # e.g. pinned host memory limits: reported, the device line stands
             e2e = {"value": None, "unit": "nnz/s", "error": f"{type(exc).__name__}: {exc}"[:300]}
+    lf.release_memory(device)
+
+    e2e_dropin = None
+    if world == 1 and not args.no_dropin:
+        e2e_dropin = measure_e2e_dropin(args)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -432,6 +490,13 @@ def main():
         except Exception as exc:  # reported, not fatal
             standard = {"error": str(exc)}
 
+    c5 = None
+    if not args.no_c5 and args.config != "C5":
+        try:
+            c5 = measure_c5(args, device, rank, world, stream, hbm)
+        except Exception as exc:  # reported, not fatal
+            c5 = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
     if rank == 0:
         line = {
             "metric": "assembled stiffness nnz/s (FP64 CSR)", "value": value, "unit": "nnz/s",
@@ -445,13 +510,119 @@ def main():
                        "distinct_materials": prob.distinct_configs(),
                        "l2": "output > L2 (values %.1f GB vs 126 MB L2); no flush needed"
                              % (total_nnz * 8 / 1e9),
-                       "parallelism": f"row-slab x{world}", "slab_passes_per_gpu": passes},
-            "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
-            "clocks": clocks, "verify": verify, "standard": standard, "pattern": pattern,
+                       "parallelism": f"row-slab x{world}", "slab_cuts": "function boundaries, nnz-balanced",
+                       "slab_passes_per_gpu": passes},
+            "roofline": roofline, "e2e": e2e, "e2e_dropin": e2e_dropin, "cpu_baseline": cpu,
+            "gpu_launches": launches, "clocks": clocks, "verify": verify, "standard": standard,
+            "pattern": pattern, "per_rank_ms": timing["per_rank_ms"], "c5": c5,
         }
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def measure_c5(args, device, rank, world, stream, hbm):
+    """BASELINE C5 (the scaling case: 192x192 p=3, 128 random-angle plies,
+    1.69e10 nnz) split over the N ranks by function-level nnz-balanced slabs
+    (strong scaling): per-rank device time of the whole hot path, max over
+    ranks; at N=1 also its streamed e2e.  Pattern resident where it fits,
+    else values only (1 GPU: 135 GB of values)."""
+    import torch
+    import paper_1905_05417_b200 as lf
+    from paper_1905_05417_b200 import problem as P
+    prob = P.baseline_config("C5")
+    total = P.sizes(prob)["nnz"]
+    b = lf.slab_bounds_functions(prob, world, rank) if world > 1 else {"f_begin": 0, "f_end": prob.n_s * prob.n_t}
+    torch.cuda.empty_cache()
+    free, _ = torch.cuda.mem_get_info()
+    plan = lf.Plan(prob, "fast", device, stream=stream.cuda_stream, f_begin=b["f_begin"], f_end=b["f_end"])
+    nnz = plan.nnz
+    with_pattern = nnz * 12 + plan.rows * 8 <= int(0.85 * free)
+    if not with_pattern and nnz * 8 > int(0.9 * free):
+        plan.close()
+        return {"error": f"rank {rank}: the C5 slab's values ({nnz * 8 / 1e9:.0f} GB) do not fit"}
+    vals = torch.empty(nnz, dtype=torch.float64, device="cuda")
+    rp = cols = None
+    if with_pattern:
+        rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
+        cols = torch.empty(nnz, dtype=torch.int32, device="cuda")
+        plan.build_pattern(rp.data_ptr(), cols.data_ptr())
+    steps, warmup = max(3, min(args.steps, 10)), 2
+    sampler = ClockSampler(device)
+    sampler.start()
+    t = device_step_time([plan], [vals.data_ptr()], steps, warmup, stream, world, args.dist_backend)
+    clocks = sampler.stop()
+    k_ms = t["combine_ms_per_step"]
+    out = {"workload": "C5 (192x192, p=3, 128 plies, 4 materials), row slabs at function boundaries",
+           "scaling": "strong", "nnz": total, "steps": steps, "warmup": warmup,
+           "ms_per_step": t["ms_per_step"], "value": total / (t["ms_per_step"] / 1e3), "unit": "nnz/s",
+           "per_rank_ms": t["per_rank_ms"],
+           "balance_max_over_mean": max(t["per_rank_ms"]) / (sum(t["per_rank_ms"]) / len(t["per_rank_ms"])),
+           "rank0_nnz": nnz, "pattern_resident": with_pattern, "clocks": clocks,
+           "roofline": {"bound": "hbm", "kernel": "k_combine (K4)", "achieved": nnz * 8 / (k_ms / 1e3) / 1e9,
+                        "peak": hbm, "frac": nnz * 8 / (k_ms / 1e3) / 1e9 / hbm, "unit": "GB/s",
+                        "step_frac": total * 8 / (t["ms_per_step"] / 1e3) / (world * hbm * 1e9)}}
+    if with_pattern:
+        st = lf.device_csr_stats(plan.rows, rp.data_ptr(), cols.data_ptr(), vals.data_ptr(), stream.cuda_stream)
+        out["rank0_fro_norm"] = st["fro_sq"] ** 0.5
+    plan.close()
+    del vals, rp, cols
+    torch.cuda.empty_cache()
+    if world == 1 and not args.no_e2e:
+        out["e2e_stream"] = measure_stream_e2e(prob, device, total)
+    lf.release_memory(device)
+    return out
+
+
+def measure_stream_e2e(prob, device, total_nnz):
+    """C5's 203 GB CSR (more than HBM and than this host's RAM) streamed
+    through lf_assemble_stream: every chunk computed on the device and copied
+    into pinned host staging, handed to a sink that sums its values (so the
+    bytes are really read on the host).  One warm-up call, one timed."""
+    import ctypes
+    import numpy as np
+    from paper_1905_05417_b200 import abi
+    lib = abi.library()
+    c = prob.to_c()
+    acc = {"sum": 0.0, "chunks": 0, "bytes": 0}
+
+    def sink(_u, row_begin, rows, nnz_begin, nnz, rp, cols, vals):
+        acc["chunks"] += 1
+        acc["bytes"] += (rows + 1) * 8 + nnz * 12
+        acc["sum"] += float(np.ctypeslib.as_array(vals, shape=(nnz,))[::4096].sum()) if nnz else 0.0
+        return 0
+
+    fn = abi.CHUNK_SINK(sink)
+    st = abi.Stats()
+    times = []
+    for _ in range(2):
+        acc.update(sum=0.0, chunks=0, bytes=0)
+        t0 = time.perf_counter()
+        abi.check(lib.lf_assemble_stream(ctypes.byref(c), abi.LF_BACKEND_FAST, device, 0,
+                                         ctypes.cast(fn, ctypes.c_void_p), None, ctypes.byref(st)))
+        times.append(time.perf_counter() - t0)
+    sec = times[-1]
+    return {"value": total_nnz / sec, "unit": "nnz/s", "ms": sec * 1e3, "chunks": acc["chunks"],
+            "d2h_bytes": acc["bytes"], "d2h_gbs": acc["bytes"] / sec / 1e9, "warmup_ms": times[0] * 1e3,
+            "call": "lf_assemble_stream(LF_BACKEND_FAST) -> pinned host staging -> sink (sampled sum)"}
+
+
+def measure_e2e_dropin(args):
+    """The C++ drop-in as a reference-API caller uses it: lamfast::assembleFast
+    returning a StiffnessMatrix of std::vectors (pageable memory), timed by
+    build/dropin_e2e (3 calls after a warm-up)."""
+    exe = os.path.join(ROOT, "build", "dropin_e2e")
+    if not os.path.exists(exe):
+        return {"unavailable": "build/dropin_e2e not built"}
+    try:
+        r = subprocess.run([exe, args.config if args.config in ("C2", "C3", "C4") else "C4", "3"],
+                           capture_output=True, text=True, timeout=600)
+        out = json.loads(r.stdout.strip().splitlines()[-1])
+        out["unit"] = "nnz/s"
+        out["call"] = "lamfast::assembleFast(setup) -> StiffnessMatrix (std::vector, pageable)"
+        return out
+    except Exception as exc:
+        return {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
 
 def measure_standard(args, prob, device, stream):
@@ -556,7 +727,7 @@ def measure_e2e_slab(args, prob, device, rank, world, bounds, total_nnz):
     import torch
     import torch.distributed as dist
     import paper_1905_05417_b200 as lf
-    probe = lf.Plan(prob, "fast", device, bounds["t_begin"], bounds["t_end"])
+    probe = lf.Plan(prob, "fast", device, f_begin=bounds["f_begin"], f_end=bounds["f_end"])
     rows, nnz = probe.rows, probe.nnz
     probe.close()
     # every rank must get its buffers before any enters a collective
@@ -575,7 +746,7 @@ def measure_e2e_slab(args, prob, device, rank, world, bounds, total_nnz):
         return {"value": None, "unit": "nnz/s", "error": err or "buffer allocation failed on another rank"}
 
     def once():
-        lf.assemble_slab(prob, bounds["t_begin"], bounds["t_end"], "fast", device, out=out)
+        lf.assemble_range(prob, bounds["f_begin"], bounds["f_end"], "fast", device, out=out)
 
     once()
     dist.barrier()
@@ -595,7 +766,7 @@ def measure_e2e_slab(args, prob, device, rank, world, bounds, total_nnz):
     dist.all_reduce(d2h)
     return {"value": total_nnz / sec, "unit": "nnz/s", "h2d_bytes_per_step": int(h2d) * world,
             "d2h_bytes_per_step": int(d2h[0]), "ms_per_step": sec * 1e3, "steps": n,
-            "call": "per rank: lf_assemble_slab (setup + table H2D, pattern, values, slab CSR D2H)"}
+            "call": "per rank: lf_assemble_range (setup + table H2D, pattern, values, slab CSR D2H)"}
 
 
 if __name__ == "__main__":

@@ -387,3 +387,33 @@ def csr_rel_diff(a, b):
     d = sp.linalg.norm(A - B) if (A - B).nnz else 0.0
     den = max(np.sqrt(np.dot(a[2], a[2])), np.sqrt(np.dot(b[2], b[2])))
     return 0.0 if den == 0 else d / den
+
+
+def slab_oracle_delta(prob: LaminateProblem, f_begin: int, f_end: int, row_ptr, cols, values) -> float:
+    """max |K - K_oracle| / max |K_oracle| over one sampled thickness row of a
+    rank's row slab: the functions of the thickness row that
+    holds the slab's middle function, restricted to the slab [f_begin, f_end)
+    (row_ptr / cols / values: the slab's CSR, rows from 3 f_begin, any array
+    type), compared with the oracle's rows of that thickness function.  A
+    pattern mismatch returns +inf."""
+    import torch
+    ns = prob.n_s
+    if f_end <= f_begin:
+        return 0.0
+    t = ((f_begin + f_end) // 2) // ns
+    g0, g1 = max(f_begin, t * ns), min(f_end, (t + 1) * ns)
+    terms = Oracle().fast_terms(prob)
+    orp, oc, ov = terms.slab(t, t + 1)
+    terms.close()
+    a, b = 3 * (g0 - t * ns), 3 * (g1 - t * ns)
+    want = (orp[a:b + 1] - orp[a], oc[orp[a]:orp[b]], ov[orp[a]:orp[b]])
+    rp = torch.as_tensor(row_ptr)
+    la, lb = 3 * (g0 - f_begin), 3 * (g1 - f_begin)
+    z0, z1 = int(rp[la]), int(rp[lb])
+    got_rp = (rp[la:lb + 1] - z0).cpu().numpy()
+    got_c = torch.as_tensor(cols)[z0:z1].cpu().numpy()
+    got_v = torch.as_tensor(values)[z0:z1].cpu().numpy()
+    if not (np.array_equal(got_rp, want[0]) and np.array_equal(got_c, want[1])):
+        return float("inf")
+    scale = float(np.abs(want[2]).max()) if len(want[2]) else 0.0
+    return float(np.abs(got_v - want[2]).max()) / scale if scale else 0.0

@@ -777,33 +777,105 @@ int orc_inplane_operators(const lf_problem* p, const double d[36], double* block
 /* ---------------------------------------------------------------------- */
 /* thickness operators (fast.cpp:170-209)                                   */
 
-static int thickness_operators(const orc_kv* kt, int n_layers, const double* ifc, int npts,
-                               double* q /* [L][4][nt][nt] */, char* occ /* [nt][nt] */) {
+/* Per-layer thickness integrals Q_l (fast.cpp:170-209), each held as the
+ * dense block of the functions its cells touch: block[l] covers functions
+ * [lo[l], lo[l] + w[l]) and stores [4][w][w].  Accumulation order per entry
+ * is the reference's (cells in order, points in order). */
+typedef struct {
+    int n_layers;
+    int* lo;
+    int* w;
+    double** q;
+} orc_tblocks;
+
+static void tblocks_free(orc_tblocks* b) {
+    for (int l = 0; l < b->n_layers; ++l)
+        free(b->q[l]);
+    free(b->q);
+    free(b->lo);
+    free(b->w);
+}
+
+static int thickness_blocks(const orc_kv* kt, int n_layers, const double* ifc, int npts, orc_tblocks* tb,
+                            char* occ /* [nt][nt] */) {
     const int nt = kt->n, p = kt->p;
-    memset(q, 0, sizeof(double) * (size_t)n_layers * 4 * nt * nt);
+    memset(tb, 0, sizeof *tb);
     memset(occ, 0, (size_t)nt * nt);
     orc_cell* cells = NULL;
     const int nc = thickness_cells(kt, n_layers, ifc, npts, &cells);
     if (nc < 0)
         return -nc;
+    tb->n_layers = n_layers;
+    tb->lo = malloc(sizeof(int) * (size_t)n_layers);
+    tb->w = calloc((size_t)n_layers, sizeof(int));
+    tb->q = calloc((size_t)n_layers, sizeof(double*));
+    int* hi = malloc(sizeof(int) * (size_t)n_layers);
+    for (int l = 0; l < n_layers; ++l) {
+        tb->lo[l] = nt;
+        hi[l] = -1;
+    }
+    /* function range of each layer's cells */
+    for (int c = 0; c < nc; ++c)
+        for (int k = 0; k < npts; ++k) {
+            double v[ORC_MAXP + 1], dd[ORC_MAXP + 1];
+            const int first = kv_eval(kt, cells[c].pts[k], v, dd);
+            const int l = cells[c].layer;
+            if (first < tb->lo[l])
+                tb->lo[l] = first;
+            if (first + p > hi[l])
+                hi[l] = first + p;
+        }
+    for (int l = 0; l < n_layers; ++l) {
+        if (hi[l] < tb->lo[l])
+            tb->lo[l] = 0, hi[l] = -1;
+        tb->w[l] = hi[l] - tb->lo[l] + 1;
+        tb->q[l] = calloc((size_t)4 * tb->w[l] * tb->w[l] + 1, sizeof(double));
+    }
+    free(hi);
     for (int c = 0; c < nc; ++c) {
-        double* fam = q + (size_t)cells[c].layer * 4 * nt * nt;
+        const int l = cells[c].layer, w = tb->w[l], lo = tb->lo[l];
+        double* fam = tb->q[l];
+        const size_t ww = (size_t)w * w;
         for (int k = 0; k < npts; ++k) {
             const double wq = cells[c].wts[k];
             double v[ORC_MAXP + 1], dd[ORC_MAXP + 1];
             const int first = kv_eval(kt, cells[c].pts[k], v, dd);
             for (int a = 0; a <= p; ++a)
                 for (int b = 0; b <= p; ++b) {
-                    const size_t ij = (size_t)(first + a) * nt + (first + b);
-                    fam[0 * nt * nt + ij] += wq * v[a] * v[b];
-                    fam[1 * nt * nt + ij] += wq * v[a] * dd[b];
-                    fam[2 * nt * nt + ij] += wq * dd[a] * v[b];
-                    fam[3 * nt * nt + ij] += wq * dd[a] * dd[b];
-                    occ[ij] = 1;
+                    const size_t ij = (size_t)(first + a - lo) * w + (first + b - lo);
+                    fam[0 * ww + ij] += wq * v[a] * v[b];
+                    fam[1 * ww + ij] += wq * v[a] * dd[b];
+                    fam[2 * ww + ij] += wq * dd[a] * v[b];
+                    fam[3 * ww + ij] += wq * dd[a] * dd[b];
+                    occ[(size_t)(first + a) * nt + (first + b)] = 1;
                 }
         }
     }
     free(cells);
+    return LF_OK;
+}
+
+/* thick[(f * nt + i) * nt + j] += weight * Q_l (family-major dense [4][nt][nt]). */
+static void add_layer_block(const orc_tblocks* tb, int l, double weight, int nt, double* thick) {
+    const int w = tb->w[l], lo = tb->lo[l];
+    const size_t nn = (size_t)nt * nt, ww = (size_t)w * w;
+    for (int f = 0; f < 4; ++f)
+        for (int i = 0; i < w; ++i)
+            for (int j = 0; j < w; ++j)
+                thick[f * nn + (size_t)(lo + i) * nt + (lo + j)] += weight * tb->q[l][f * ww + (size_t)i * w + j];
+}
+
+static int thickness_operators(const orc_kv* kt, int n_layers, const double* ifc, int npts,
+                               double* q /* [L][4][nt][nt] */, char* occ /* [nt][nt] */) {
+    const int nt = kt->n;
+    orc_tblocks tb;
+    const int st = thickness_blocks(kt, n_layers, ifc, npts, &tb, occ);
+    if (st)
+        return st;
+    memset(q, 0, sizeof(double) * (size_t)n_layers * 4 * nt * nt);
+    for (int l = 0; l < n_layers; ++l)
+        add_layer_block(&tb, l, 1.0, nt, q + (size_t)l * 4 * nt * nt);
+    tblocks_free(&tb);
     return LF_OK;
 }
 
@@ -854,12 +926,12 @@ static int build_terms(const orc_space* s, const lf_problem* p, orc_terms* terms
     double* cd = malloc(sizeof(double) * 36 * (size_t)L);
     int ncfg = 0;
     int st = orc_layup(p, &ncfg, cfg, cd);
-    double* q = NULL;
+    orc_tblocks tb;
+    memset(&tb, 0, sizeof tb);
     memset(terms, 0, sizeof *terms);
     if (st)
         goto done;
-    q = malloc(sizeof(double) * (size_t)L * 4 * nt * nt);
-    if ((st = thickness_operators(&s->kt, L, p->interfaces, s->nqt, q, occ)))
+    if ((st = thickness_blocks(&s->kt, L, p->interfaces, s->nqt, &tb, occ)))
         goto done;
     const size_t nn = (size_t)nt * nt;
     if (!p->decompose_angles) {
@@ -871,8 +943,7 @@ static int build_terms(const orc_space* s, const lf_problem* p, orc_terms* terms
             for (int l = 0; l < L; ++l) {
                 if (cfg[l] != c || !layer_active(p, l))
                     continue;
-                for (size_t k = 0; k < 4 * nn; ++k)
-                    terms->thick[(size_t)c * 4 * nn + k] += q[(size_t)l * 4 * nn + k];
+                add_layer_block(&tb, l, 1.0, nt, terms->thick + (size_t)c * 4 * nn);
             }
         }
     } else {
@@ -909,9 +980,7 @@ static int build_terms(const orc_space* s, const lf_problem* p, orc_terms* terms
                         continue;
                     const double c = cos(p->layers[l].angle), sn = sin(p->layers[l].angle);
                     const double weight[5] = {1.0, c * c * c * c, c * c * c * sn, c * c, c * sn};
-                    for (size_t e = 0; e < 4 * nn; ++e)
-                        terms->thick[(size_t)t * 4 * nn + e] +=
-                            weight[k] * q[(size_t)l * 4 * nn + e];
+                    add_layer_block(&tb, l, weight[k], nt, terms->thick + (size_t)t * 4 * nn);
                 }
             }
         }
@@ -924,7 +993,8 @@ static int build_terms(const orc_space* s, const lf_problem* p, orc_terms* terms
         stats->operator_builds += terms->n;
     }
 done:
-    free(q);
+    if (tb.q)
+        tblocks_free(&tb);
     free(cfg);
     free(cd);
     return st;

@@ -1,9 +1,9 @@
 """Row-slab sharding across GPUs.
 
 The assembly has no exchange step: rank r of N assembles the contiguous row
-slab ``slab_bounds(prob, N, r)`` (cut at thickness-function boundaries,
-balanced by nnz) into its own HBM, with row offsets rebased to 0 and global
-column indices.  Collectives (NCCL over NVLink on GPUs, gloo on CPU) are used
+slab ``slab_bounds_functions(prob, N, r)`` (cut at function boundaries, i.e.
+inside thickness rows, balanced by nnz to within one function) into its own
+HBM, with row offsets rebased to 0 and global column indices.  Collectives (NCCL over NVLink on GPUs, gloo on CPU) are used
 only for verification -- gathering per-slab summaries -- never inside the
 timed assembly.
 """
@@ -12,10 +12,11 @@ from __future__ import annotations
 import os
 from typing import Dict, List
 
-from .assembler import slab_bounds
+from .assembler import slab_bounds, slab_bounds_functions
 from .problem import LaminateProblem
 
-SUMMARY_FIELDS = ("rows", "nnz", "fro_sq", "checksum", "max_abs", "pattern_hash")
+SUMMARY_FIELDS = ("rows", "nnz", "fro_sq", "checksum", "max_abs", "pattern_hash", "oracle_rel_dk")
+FIELD_INDEX = {k: i for i, k in enumerate(SUMMARY_FIELDS)}
 HASH_P = (1 << 31) - 1  # pattern hashes are sums mod this prime: exact in float64 across ranks
 
 
@@ -26,7 +27,9 @@ def env_rank():
 
 
 def slab_for_rank(prob: LaminateProblem, rank: int, world: int, backend: str = "fast") -> Dict[str, int]:
-    return slab_bounds(prob, world, rank, backend)
+    """This rank's row slab: functions [f_begin, f_end), nnz-balanced (cuts
+    inside thickness rows)."""
+    return slab_bounds_functions(prob, world, rank, backend)
 
 
 def _mix(x):
@@ -83,8 +86,16 @@ def slab_summary(row_ptr, cols, values, row_begin: int = 0, nnz_begin: int = 0):
     w = (c.to(torch.int64) % 97 + 1).to(torch.float64)
     ph = pattern_hash(rp, c, row_begin, nnz_begin)
     return torch.tensor([float(len(rp) - 1), float(nnz), float((v * v).sum()),
-                         float((v * w).sum()), float(v.abs().max()) if nnz else 0.0, float(ph)],
+                         float((v * w).sum()), float(v.abs().max()) if nnz else 0.0, float(ph), -1.0],
                         dtype=torch.float64)
+
+
+def with_field(summary, name: str, value: float):
+    """A copy of a slab summary with one field set (e.g. the oracle_rel_dk a
+    verification leg computed for this rank's slab)."""
+    s = summary.clone()
+    s[FIELD_INDEX[name]] = float(value)
+    return s
 
 
 def gather_summaries(summary, group=None) -> List:
@@ -104,7 +115,7 @@ def combine_summaries(parts) -> Dict[str, float]:
     tot = {k: 0.0 for k in SUMMARY_FIELDS}
     for p in parts:
         for i, k in enumerate(SUMMARY_FIELDS):
-            tot[k] = max(tot[k], float(p[i])) if k == "max_abs" else tot[k] + float(p[i])
+            tot[k] = max(tot[k], float(p[i])) if k in ("max_abs", "oracle_rel_dk") else tot[k] + float(p[i])
     tot["pattern_hash"] = int(tot["pattern_hash"]) % HASH_P
     return tot
 

@@ -31,11 +31,21 @@ def _worker(rank, world, port, config, q):
     from paper_1905_05417_b200 import problem as P
     prob = P.baseline_config(config)
     r, w, _ = D.env_rank()
-    b = D.slab_for_rank(prob, r, w)
-    rp, cols, vals = Oracle().assemble(prob, "fast", b["t_begin"], b["t_end"])
+    b = D.slab_for_rank(prob, r, w)  # functions [f_begin, f_end): cut inside a thickness row
+    ns = prob.n_s
+    t0, t1 = b["f_begin"] // ns, -(-b["f_end"] // ns)
+    trp, tcols, tvals = Oracle().assemble(prob, "fast", t0, t1)
+    a, e = 3 * (b["f_begin"] - t0 * ns), 3 * (b["f_end"] - t0 * ns)
+    rp, cols, vals = trp[a:e + 1] - trp[a], tcols[trp[a]:trp[e]], tvals[trp[a]:trp[e]]
     assert rp[0] == 0 and int(rp[-1]) == b["nnz_end"] - b["nnz_begin"]
     s = D.slab_summary(torch.from_numpy(rp), torch.from_numpy(cols), torch.from_numpy(vals),
                        b["row_begin"], b["nnz_begin"])
+    # the per-rank oracle comparison of one sampled thickness row (here of the
+    # oracle's own slab: exactly 0)
+    from oracle.checkers import slab_oracle_delta
+    s = D.with_field(s, "oracle_rel_dk", slab_oracle_delta(prob, b["f_begin"], b["f_end"], torch.from_numpy(rp),
+                                                            torch.from_numpy(cols), torch.from_numpy(vals)))
+    assert float(s[D.FIELD_INDEX["oracle_rel_dk"]]) == 0.0
     parts = D.gather_summaries(s)
     full = D.gather_csr(torch.from_numpy(rp), torch.from_numpy(cols), torch.from_numpy(vals), dst=0)
     if rank == 0:
@@ -70,6 +80,7 @@ def test_two_rank_slabs_reproduce_full_matrix(config, oracle):
     assert got["checksum"] == pytest.approx(full["checksum"], rel=1e-12)
     assert got["max_abs"] == full["max_abs"]
     assert got["pattern_hash"] == full["pattern_hash"]
+    assert got["oracle_rel_dk"] == 0.0
     # the full-slab gather reassembles the single-rank matrix exactly
     assert np.array_equal(gathered[0], rp) and np.array_equal(gathered[1], cols)
     assert np.array_equal(gathered[2], vals)
