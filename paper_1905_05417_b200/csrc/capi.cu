@@ -340,6 +340,17 @@ std::pair<int64_t, int64_t> thickness_range(const lf_problem* p, int t0, int t1)
     return {static_cast<int64_t>(t0) * ns, t1 < 0 ? -1 : static_cast<int64_t>(t1) * ns};
 }
 
+/// Smallest term count that takes the coefficient form of the combine
+/// (affine geometry).  Below it the per-term form keeps the entry's P in
+/// registers (4 FMA per active term and value); from 9 terms on the
+/// per-term form would need a second read-modify-write pass.  Measured:
+/// profiles/r2_eform.txt.  LAMFAST_EFORM_MIN_TERMS overrides it (A/B runs).
+int eform_min_terms() {
+    if (const char* e = std::getenv("LAMFAST_EFORM_MIN_TERMS"))
+        return std::max(1, std::atoi(e));
+    return 9;
+}
+
 /// Output-range fields of the device tables (row offsets slab-local).
 void set_range(const lfb::Range& r, lfb::DevTables& d) {
     d.t0 = r.t0;
@@ -400,6 +411,9 @@ void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void
         if (!d.affine) {
             d.Pg = ar.alloc<double>(static_cast<std::size_t>(d.n_terms) * 4 * static_cast<std::size_t>(d.E));
             alloc_element_scratch(ar, d, d.n_terms);
+        } else if (d.n_terms >= eform_min_terms()) {
+            // coefficient form of the combine: one pass for any term count
+            d.Etab = ar.alloc<double>(static_cast<std::size_t>(std::max<long long>(1, d.n_pairs)) * lfb::kEPair);
         }
     }
     // graph replay for launch-bound plans (<= 64M values, or any standard plan:
@@ -423,7 +437,10 @@ int plan_prepare(lf_plan* plan, cudaStream_t s) {
     if (d.affine) {
         // one fused setup launch: U, V, thickness-pair weights, Ct
         CK(static_cast<cudaError_t>(lfb::launch_prepare_affine(d, s)));
-        return 1;
+        if (!d.Etab)
+            return 1;
+        CK(static_cast<cudaError_t>(lfb::launch_pair_coeffs(d, s)));
+        return 2;
     }
     CK(static_cast<cudaError_t>(lfb::launch_basis(d, false, s)));
     ++launches;

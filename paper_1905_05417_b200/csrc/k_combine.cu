@@ -201,6 +201,136 @@ void combine_one(const DevTables& d, double* out, int pass, int t_chunk, int sta
                                                         false);
 }
 
+// ---------------------------------------------------------------------------
+// Coefficient form of K4 for affine geometry with many operator terms
+// (decompose_angles: 5 per material; laminates with > 8 distinct angles).
+// With a constant frame every term's P is linear in the same nine 2D
+// integrals I_xy of the entry, so the whole sum over terms and families
+//   K = sum_t sum_f W[pair][t][f] P_{t,f} = sum_xy I_xy E[pair][ab][xy],
+//   E[pair][ab][xy] = sum_t Ct[t][xy][ab] W[pair][t][f(xy)]
+// costs 9 FMA per value whatever the term count.  E (720 B per thickness
+// pair) is formed once per assembly by k_pair_coeffs; the combine keeps the
+// entry's nine I_xy in registers and streams E rows through shared memory.
+// One launch, every value written once (the per-term form needed one
+// read-modify-write pass per 8 terms: 24 B/nnz of traffic for 10 terms).
+__global__ void k_pair_coeffs(const DevTables d) {
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= d.n_pairs * 81)
+        return;
+    const long long pp = g / 81;
+    const int r = (int)(g - pp * 81), ab = r / 9, xy = r - 9 * ab;
+    // family of xy: {00,01,10,11} -> P11, {02,12} -> P12, {20,21} -> P21, 22 -> P22
+    const int x = xy / 3, y = xy - 3 * x;
+    const int f = (x < 2 && y < 2) ? 0 : (x < 2) ? 1 : (y < 2) ? 2 : 3;
+    double e = 0.0;
+    for (int t = 0; t < d.n_terms; ++t)
+        e = fma(d.Ct[(long long)t * 81 + xy * 9 + ab], d.W[(pp * d.n_terms + t) * 4 + f], e);
+    d.Etab[pp * kEPair + ab * kEStride + xy] = e;
+}
+
+template <int EPT, int BT>
+__global__ void __launch_bounds__(BT, 2) k_combine_e(const DevTables d, double* __restrict__ out, int t_chunk,
+                                                     int stage_rows, int lt_max) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    RowInfo* s_row = reinterpret_cast<RowInfo*>(smem_raw);
+    double* s_e = reinterpret_cast<double*>(smem_raw + ((stage_rows * sizeof(RowInfo) + 15) & ~15));
+    double I[EPT][9];
+    double* o_thread[EPT];
+    long long A[EPT];
+    int B[EPT], eoff[EPT]; // eoff: ab * kEStride
+    bool live[EPT], in_s0[EPT], in_s1[EPT];
+#pragma unroll
+    for (int x = 0; x < EPT; ++x) {
+        const long long e = (long long)blockIdx.x * BT * EPT + (threadIdx.x >> 5) * 32 * EPT + x * 32 +
+                            (threadIdx.x & 31);
+        live[x] = e < d.E;
+        const long long ec = live[x] ? e : d.E - 1;
+        int is = __ldg(d.blk_is + ec / kBlock);
+        while (__ldg(d.es_pre + is + 1) <= ec)
+            ++is;
+        const long long ebase = __ldg(d.es_pre + is);
+        const int r = (int)(ec - ebase);
+        in_s0[x] = is >= d.s0;
+        in_s1[x] = is < d.s1;
+        const int iu = is % d.nu, iv = is / d.nu;
+        const int Lu = __ldg(d.len_u + iu), Lv = __ldg(d.len_v + iv);
+        B[x] = 3 * Lu * Lv;
+        const int a = r / B[x];
+        const int rem = r - a * B[x];
+        A[x] = ebase + (long long)a * B[x];
+        o_thread[x] = out + (long long)rem;
+        const int sl = rem / 3, b = rem - 3 * sl;
+        const int sv = sl / Lu, su = sl - sv * Lu;
+        eoff[x] = (3 * a + b) * kEStride;
+        const double* U = d.U + ((long long)iu * d.bu + su) * 4;
+        const double* V = d.V + ((long long)iv * d.bv + sv) * 4;
+        const double u0 = __ldg(U), u1 = __ldg(U + 1), u2 = __ldg(U + 2), u3 = __ldg(U + 3);
+        const double v0 = __ldg(V), v1 = __ldg(V + 1), v2 = __ldg(V + 2), v3 = __ldg(V + 3);
+        // xy = 3x + y, x/y: 0 -> d/du, 1 -> d/dv, 2 -> value (affine_p)
+        I[x][0] = u3 * v0; I[x][1] = u2 * v1; I[x][2] = u2 * v0;
+        I[x][3] = u1 * v2; I[x][4] = u0 * v3; I[x][5] = u0 * v2;
+        I[x][6] = u1 * v0; I[x][7] = u0 * v1; I[x][8] = u0 * v0;
+    }
+    const int it_begin = d.t0 + blockIdx.y * t_chunk;
+    const int it_end = min(d.t1, it_begin + t_chunk);
+    const long long pre0 = __ldg(d.pre_t + d.t0), preW = __ldg(d.pre_t + d.w_t0), nine_S = 9 * d.S_s;
+    for (int it0 = it_begin; it0 < it_end; it0 += stage_rows) {
+        const int nrow = min(stage_rows, it_end - it0);
+        if (it0 != it_begin)
+            __syncthreads();
+        for (int rr = threadIdx.x; rr < nrow; rr += BT) {
+            const int it = it0 + rr;
+            s_row[rr].base = nine_S * (__ldg(d.pre_t + it) - pre0) - d.out_base;
+            s_row[rr].lt = __ldg(d.len_t + it) | row_edge(d, it) << 8;
+            s_row[rr].mask = 0;
+        }
+        // E rows of the staged thickness rows: s_e[row][k][kEPair] (16-byte chunks)
+        const int per_row = lt_max * kEPair / 2;
+        for (int idx = threadIdx.x; idx < nrow * per_row; idx += BT) {
+            const int rr = idx / per_row, h = idx - rr * per_row;
+            const int k = (2 * h) / kEPair;
+            const int it = it0 + rr;
+            double2 v = make_double2(0.0, 0.0);
+            if (k < __ldg(d.len_t + it)) {
+                const long long q = __ldg(d.pre_t + it) - preW + k;
+                v = __ldg(reinterpret_cast<const double2*>(d.Etab + q * kEPair) + (2 * h - k * kEPair) / 2);
+            }
+            reinterpret_cast<double2*>(s_e)[idx] = v;
+        }
+        __syncthreads();
+        for (int rr = 0; rr < nrow; ++rr) {
+            const RowInfo ri = s_row[rr];
+            const int lt = ri.lt & 0xff, edge = ri.lt >> 8;
+            bool lv[EPT];
+#pragma unroll
+            for (int x = 0; x < EPT; ++x)
+                lv[x] = edge ? live[x] && (!(edge & 1) || in_s0[x]) && (!(edge & 2) || in_s1[x]) : live[x];
+            const double* er = s_e + (long long)rr * lt_max * kEPair;
+            for (int k = 0; k < lt; ++k) {
+#pragma unroll
+                for (int x = 0; x < EPT; ++x) {
+                    const double2* c = reinterpret_cast<const double2*>(er + k * kEPair + eoff[x]);
+                    const double2 c01 = c[0], c23 = c[1], c45 = c[2], c67 = c[3];
+                    const double c8 = er[k * kEPair + eoff[x] + 8];
+                    double acc = I[x][0] * c01.x;
+                    acc = fma(I[x][1], c01.y, acc);
+                    acc = fma(I[x][2], c23.x, acc);
+                    acc = fma(I[x][3], c23.y, acc);
+                    acc = fma(I[x][4], c45.x, acc);
+                    acc = fma(I[x][5], c45.y, acc);
+                    acc = fma(I[x][6], c67.x, acc);
+                    acc = fma(I[x][7], c67.y, acc);
+                    acc = fma(I[x][8], c8, acc);
+                    double* o = o_thread[x] + ri.base + (long long)lt * A[x] + (long long)k * B[x];
+                    LF_CHECK(!lv[x] || (o >= out && o < out + d.nnz_slab));
+                    if (lv[x])
+                        store_value(o, acc);
+                }
+            }
+        }
+    }
+}
+
 } // namespace
 
 int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t stream, int* launches) {
@@ -232,6 +362,21 @@ int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t st
     }
     const unsigned nchunk = (unsigned)((nt + t_chunk - 1) / t_chunk);
     const int lt_max = std::max(1, d.lt_max);
+    if (d.Etab) {
+        // coefficient form: one launch for any term count; ~40 KB of staged E rows
+        constexpr int EPT = 2, BT = 256;
+        int stage_rows = (int)((40 * 1024) / ((size_t)lt_max * kEPair * sizeof(double)));
+        stage_rows = std::max(1, std::min(stage_rows, t_chunk));
+        const size_t smem = ((stage_rows * sizeof(RowInfo) + 15) & ~size_t(15)) +
+                            (size_t)stage_rows * lt_max * kEPair * sizeof(double);
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(k_combine_e<EPT, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const dim3 grid((unsigned)((d.E + (long long)BT * EPT - 1) / ((long long)BT * EPT)), nchunk);
+        k_combine_e<EPT, BT><<<grid, BT, smem, stream>>>(d, out, t_chunk, stage_rows, lt_max);
+        if (launches)
+            ++*launches;
+        return (int)cudaGetLastError();
+    }
     for (int pass = 0; pass < d.n_passes; ++pass) {
         const int nterm = std::min(8, d.n_terms - 8 * pass);
         const bool accum = pass > 0;
@@ -254,5 +399,13 @@ int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t st
     return (int)cudaGetLastError();
 }
 
+
+int launch_pair_coeffs(const DevTables& d, cudaStream_t stream) {
+    if (d.n_pairs == 0)
+        return 0;
+    const long long n = d.n_pairs * 81;
+    k_pair_coeffs<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(d);
+    return (int)cudaGetLastError();
+}
 
 } // namespace lfb

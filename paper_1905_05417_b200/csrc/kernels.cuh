@@ -84,6 +84,10 @@ struct DevTables {
     double* W;                                 // [n_pairs][T][4]
     unsigned* Wmask;                           // [n_passes][n_pairs]
     double* Pg;                                // [T][4][E] (general geometry)
+    // coefficient form of the combine (affine geometry, many terms): per
+    // thickness pair E[pair][ab][xy] = sum_t Ct[t][xy][ab] W[pair][t][f(xy)],
+    // padded to kEStride doubles per ab; nullptr -> the per-term form
+    double* Etab;
     double* Pe;     // element-local P of a batch of pe_terms terms: [term][el][4][nl2][3][nl2][3]
     int pe_terms;   // terms per batch
     // output range: the functions f = i_t * ns + i_s in [f0, f1), covering
@@ -100,6 +104,9 @@ struct DevTables {
     long long nnz_slab; // values of this range (bounds checks in LF_DEBUG_CHECKS builds)
 };
 
+constexpr int kEStride = 10; // doubles per (pair, ab) row of Etab (9 used; 16-byte rows)
+constexpr int kEPair = 9 * kEStride;
+
 // Launchers (all asynchronous on `stream`).  Return cudaError_t as int.
 int launch_basis(const DevTables& d, bool with_ct, cudaStream_t stream);
 int launch_thickness_pairs(const DevTables& d, cudaStream_t stream);
@@ -114,6 +121,8 @@ int launch_affine_export(const DevTables& d, cudaStream_t stream);
 /// block row; returns the number of kernels launched via *launches.
 int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t stream,
                    int* launches);
+/// Coefficient form: Etab from W and Ct (after the setup kernels).
+int launch_pair_coeffs(const DevTables& d, cudaStream_t stream);
 int launch_pattern(const DevTables& d, long long* row_ptr, int* cols, cudaStream_t stream);
 int launch_standard(const DevTables& d, double* values, long long nnz, cudaStream_t stream,
                     int* launches);

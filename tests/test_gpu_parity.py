@@ -121,11 +121,56 @@ def test_decompose_angles(gpu, oracle):
 
 
 def test_many_terms_multi_pass(gpu, oracle):
-    """More than 8 operator terms exercises the accumulate passes of K4."""
+    """More than 8 operator terms: the coefficient form of K4 on affine maps,
+    the accumulate passes on general (skewed) ones."""
     angles = [0.1 * k for k in range(11)]
-    prob = P.cube_problem(2, 2, 2, angles)
+    for geom in ("flat", "skewed"):
+        prob = P.cube_problem(2, 2, 2, angles, geometry=geom)
+        got = gpu.assemble_fast(prob)
+        assert got.stats.operator_builds == 11
+        assert_csr_match(got.astuple(), oracle.assemble(prob, "fast"), RTOL)
+
+
+@pytest.mark.parametrize("min_terms", ["9", "1"])
+@pytest.mark.parametrize("case", ["16 angles", "decompose C2", "mixed C0", "slab"])
+def test_coefficient_form_matches_oracle(gpu, oracle, monkeypatch, min_terms, case):
+    """The coefficient form of the combine (one pass, 9 FMA per value for any
+    term count; default from 9 terms, forced for every term count with
+    LAMFAST_EFORM_MIN_TERMS=1) against the oracle: a 16-distinct-angle
+    laminate, decompose_angles with two materials (10 terms), mixed degrees
+    with C0 thickness knots, and a row slab cut inside a thickness row."""
+    import torch
+    monkeypatch.setenv("LAMFAST_EFORM_MIN_TERMS", min_terms)
+    if case == "16 angles":
+        prob = P.plate(2, 6, 5, [(P.baseline_orthotropic(), -1.5 + 0.2 * k) for k in range(16)], thickness=0.2)
+    elif case == "decompose C2":
+        base = P.baseline_config("C2")
+        layers = [(P.isotropic(0.5, 0.3), 0.0) if k % 3 == 1 else l for k, l in enumerate(base.layers)]
+        prob = base.replace(layers=layers, decompose_angles=True)
+    elif case == "mixed C0":
+        prob = P.LaminateProblem(
+            degree_u=2, degree_v=3, degree_t=2, knots_u=P.uniform_knots(2, 3),
+            knots_v=P.uniform_knots(3, 2), knots_t=P.c0_knots(2, 3), interfaces=P.equal_interfaces(3),
+            layers=[(P.baseline_orthotropic(), 0.0), (P.isotropic(0.5, 0.3), 0.0),
+                    (P.baseline_orthotropic(), 0.6)])
+    else:
+        prob = P.plate(2, 6, 5, [(P.baseline_orthotropic(), -1.5 + 0.2 * k) for k in range(12)], thickness=0.2)
+        ns = prob.n_s
+        f0, f1 = ns + 5, 4 * ns - 7
+        plan = gpu.Plan(prob, "fast", 0, f_begin=f0, f_end=f1)
+        rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
+        cols = torch.empty(plan.nnz, dtype=torch.int32, device="cuda")
+        vals = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
+        plan.build_pattern(rp.data_ptr(), cols.data_ptr())
+        plan.assemble(vals.data_ptr())
+        plan.synchronize()
+        trp, tc, tv = oracle.assemble(prob, "fast", 1, 4)
+        a, e = 3 * (f0 - ns), 3 * (f1 - ns)
+        want = (trp[a:e + 1] - trp[a], tc[trp[a]:trp[e]], tv[trp[a]:trp[e]])
+        assert_csr_match((rp.cpu().numpy(), cols.cpu().numpy(), vals.cpu().numpy()), want, RTOL)
+        plan.close()
+        return
     got = gpu.assemble_fast(prob)
-    assert got.stats.operator_builds == 11
     assert_csr_match(got.astuple(), oracle.assemble(prob, "fast"), RTOL)
 
 

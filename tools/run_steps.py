@@ -19,6 +19,8 @@ ap.add_argument("--plies", type=int, default=0)
 ap.add_argument("--calibrate", action="store_true")
 ap.add_argument("--geometry", default="planar", choices=["planar", "bilinear"])
 ap.add_argument("--decompose", action="store_true", help="AssemblyOptions::decompose_angles")
+ap.add_argument("--distinct", type=int, default=0,
+                help="replace the layup by the orthotropic material at N distinct angles, cycling")
 a = ap.parse_args()
 if a.calibrate:
     # same-box write-only and copy bandwidth of a buffer the size of C4's values
@@ -47,6 +49,9 @@ if a.geometry == "bilinear":  # non-affine map: general in-plane path (k_inplane
                                                    1.02 * lx, 1.03 * ly, 0.01))
 if a.decompose:
     prob = prob.replace(decompose_angles=True)
+if a.distinct:
+    prob = prob.replace(layers=[(lf.baseline_orthotropic(), -1.5 + 3.0 * (k % a.distinct) / a.distinct)
+                                for k in range(len(prob.layers))])
 s = torch.cuda.Stream()
 torch.cuda.set_stream(s)
 plan = lf.Plan(prob, a.backend, 0, stream=s.cuda_stream)
