@@ -228,48 +228,49 @@ __global__ void k_pair_coeffs(const DevTables d) {
     d.Etab[pp * kEPair + ab * kEStride + xy] = e;
 }
 
-template <int EPT, int BT>
-__global__ void __launch_bounds__(BT, 2) k_combine_e(const DevTables d, double* __restrict__ out, int t_chunk,
-                                                     int stage_rows, int lt_max) {
+// One thread per in-plane entry triple (i_s, a, slot): the nine I_xy depend
+// on (i_s, slot) only, so the thread forms the three values b = 0..2 of its
+// (a, slot) from the 27 coefficients E[pair][3a + b][xy].  Consecutive lanes
+// hold consecutive slots of one row segment (warp-uniform a except at segment
+// ends), so the coefficient loads are shared-memory broadcasts and a warp's
+// three stores per (row, neighbour) cover one contiguous 768-byte run.
+// Per value: 9 FMA and 1/3 of a 16-byte broadcast load group.
+template <int BT>
+__global__ void __launch_bounds__(BT) k_combine_e3(const DevTables d, double* __restrict__ out, int t_chunk,
+                                                   int stage_rows, int lt_max) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     RowInfo* s_row = reinterpret_cast<RowInfo*>(smem_raw);
     double* s_e = reinterpret_cast<double*>(smem_raw + ((stage_rows * sizeof(RowInfo) + 15) & ~15));
-    double I[EPT][9];
-    double* o_thread[EPT];
-    long long A[EPT];
-    int B[EPT], eoff[EPT]; // eoff: ab * kEStride
-    bool live[EPT], in_s0[EPT], in_s1[EPT];
-#pragma unroll
-    for (int x = 0; x < EPT; ++x) {
-        const long long e = (long long)blockIdx.x * BT * EPT + (threadIdx.x >> 5) * 32 * EPT + x * 32 +
-                            (threadIdx.x & 31);
-        live[x] = e < d.E;
-        const long long ec = live[x] ? e : d.E - 1;
-        int is = __ldg(d.blk_is + ec / kBlock);
-        while (__ldg(d.es_pre + is + 1) <= ec)
-            ++is;
-        const long long ebase = __ldg(d.es_pre + is);
-        const int r = (int)(ec - ebase);
-        in_s0[x] = is >= d.s0;
-        in_s1[x] = is < d.s1;
-        const int iu = is % d.nu, iv = is / d.nu;
-        const int Lu = __ldg(d.len_u + iu), Lv = __ldg(d.len_v + iv);
-        B[x] = 3 * Lu * Lv;
-        const int a = r / B[x];
-        const int rem = r - a * B[x];
-        A[x] = ebase + (long long)a * B[x];
-        o_thread[x] = out + (long long)rem;
-        const int sl = rem / 3, b = rem - 3 * sl;
+    const long long nq = d.E / 3; // entry triples (b = 0, 1, 2 of one (i_s, a, slot))
+    const long long q = (long long)blockIdx.x * BT + threadIdx.x;
+    const bool live = q < nq;
+    const long long e = 3 * (live ? q : nq - 1);
+    int is = __ldg(d.blk_is + e / kBlock);
+    while (__ldg(d.es_pre + is + 1) <= e)
+        ++is;
+    const long long ebase = __ldg(d.es_pre + is);
+    const int r = (int)(e - ebase);
+    const bool in_s0 = is >= d.s0, in_s1 = is < d.s1;
+    const int iu = is % d.nu, iv = is / d.nu;
+    const int Lu = __ldg(d.len_u + iu), Lv = __ldg(d.len_v + iv);
+    const int B = 3 * Lu * Lv;
+    const int a = r / B;
+    const int rem = r - a * B; // 3 * slot
+    const long long A = ebase + (long long)a * B;
+    double* const o_thread = out + rem;
+    const int coff = 3 * a * kEStride;
+    double I[9];
+    {
+        const int sl = rem / 3;
         const int sv = sl / Lu, su = sl - sv * Lu;
-        eoff[x] = (3 * a + b) * kEStride;
         const double* U = d.U + ((long long)iu * d.bu + su) * 4;
         const double* V = d.V + ((long long)iv * d.bv + sv) * 4;
         const double u0 = __ldg(U), u1 = __ldg(U + 1), u2 = __ldg(U + 2), u3 = __ldg(U + 3);
         const double v0 = __ldg(V), v1 = __ldg(V + 1), v2 = __ldg(V + 2), v3 = __ldg(V + 3);
         // xy = 3x + y, x/y: 0 -> d/du, 1 -> d/dv, 2 -> value (affine_p)
-        I[x][0] = u3 * v0; I[x][1] = u2 * v1; I[x][2] = u2 * v0;
-        I[x][3] = u1 * v2; I[x][4] = u0 * v3; I[x][5] = u0 * v2;
-        I[x][6] = u1 * v0; I[x][7] = u0 * v1; I[x][8] = u0 * v0;
+        I[0] = u3 * v0; I[1] = u2 * v1; I[2] = u2 * v0;
+        I[3] = u1 * v2; I[4] = u0 * v3; I[5] = u0 * v2;
+        I[6] = u1 * v0; I[7] = u0 * v1; I[8] = u0 * v0;
     }
     const int it_begin = d.t0 + blockIdx.y * t_chunk;
     const int it_end = min(d.t1, it_begin + t_chunk);
@@ -292,39 +293,44 @@ __global__ void __launch_bounds__(BT, 2) k_combine_e(const DevTables d, double* 
             const int it = it0 + rr;
             double2 v = make_double2(0.0, 0.0);
             if (k < __ldg(d.len_t + it)) {
-                const long long q = __ldg(d.pre_t + it) - preW + k;
-                v = __ldg(reinterpret_cast<const double2*>(d.Etab + q * kEPair) + (2 * h - k * kEPair) / 2);
+                const long long pq = __ldg(d.pre_t + it) - preW + k;
+                v = __ldg(reinterpret_cast<const double2*>(d.Etab + pq * kEPair) + (2 * h - k * kEPair) / 2);
             }
             reinterpret_cast<double2*>(s_e)[idx] = v;
         }
         __syncthreads();
+        if (!live)
+            continue;
         for (int rr = 0; rr < nrow; ++rr) {
             const RowInfo ri = s_row[rr];
             const int lt = ri.lt & 0xff, edge = ri.lt >> 8;
-            bool lv[EPT];
-#pragma unroll
-            for (int x = 0; x < EPT; ++x)
-                lv[x] = edge ? live[x] && (!(edge & 1) || in_s0[x]) && (!(edge & 2) || in_s1[x]) : live[x];
-            const double* er = s_e + (long long)rr * lt_max * kEPair;
+            const bool lv = !edge || ((!(edge & 1) || in_s0) && (!(edge & 2) || in_s1));
+            double* const o = o_thread + ri.base + (long long)lt * A;
+            const double* er = s_e + (long long)rr * lt_max * kEPair + coff;
             for (int k = 0; k < lt; ++k) {
+                const double2* c = reinterpret_cast<const double2*>(er + k * kEPair);
+                double v[3];
 #pragma unroll
-                for (int x = 0; x < EPT; ++x) {
-                    const double2* c = reinterpret_cast<const double2*>(er + k * kEPair + eoff[x]);
-                    const double2 c01 = c[0], c23 = c[1], c45 = c[2], c67 = c[3];
-                    const double c8 = er[k * kEPair + eoff[x] + 8];
-                    double acc = I[x][0] * c01.x;
-                    acc = fma(I[x][1], c01.y, acc);
-                    acc = fma(I[x][2], c23.x, acc);
-                    acc = fma(I[x][3], c23.y, acc);
-                    acc = fma(I[x][4], c45.x, acc);
-                    acc = fma(I[x][5], c45.y, acc);
-                    acc = fma(I[x][6], c67.x, acc);
-                    acc = fma(I[x][7], c67.y, acc);
-                    acc = fma(I[x][8], c8, acc);
-                    double* o = o_thread[x] + ri.base + (long long)lt * A[x] + (long long)k * B[x];
-                    LF_CHECK(!lv[x] || (o >= out && o < out + d.nnz_slab));
-                    if (lv[x])
-                        store_value(o, acc);
+                for (int b = 0; b < 3; ++b) {
+                    // coefficients of value b: er[k][10 b + xy], xy < 9 (five 16-byte loads)
+                    const double2 c0 = c[5 * b], c1 = c[5 * b + 1], c2 = c[5 * b + 2], c3 = c[5 * b + 3],
+                                  c4 = c[5 * b + 4];
+                    double acc = I[0] * c0.x;
+                    acc = fma(I[1], c0.y, acc);
+                    acc = fma(I[2], c1.x, acc);
+                    acc = fma(I[3], c1.y, acc);
+                    acc = fma(I[4], c2.x, acc);
+                    acc = fma(I[5], c2.y, acc);
+                    acc = fma(I[6], c3.x, acc);
+                    acc = fma(I[7], c3.y, acc);
+                    v[b] = fma(I[8], c4.x, acc);
+                }
+                double* ok = o + (long long)k * B;
+                LF_CHECK(!lv || (ok >= out && ok + 2 < out + d.nnz_slab));
+                if (lv) {
+                    store_value(ok, v[0]);
+                    store_value(ok + 1, v[1]);
+                    store_value(ok + 2, v[2]);
                 }
             }
         }
@@ -363,16 +369,17 @@ int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t st
     const unsigned nchunk = (unsigned)((nt + t_chunk - 1) / t_chunk);
     const int lt_max = std::max(1, d.lt_max);
     if (d.Etab) {
-        // coefficient form: one launch for any term count; ~40 KB of staged E rows
-        constexpr int EPT = 2, BT = 256;
-        int stage_rows = (int)((40 * 1024) / ((size_t)lt_max * kEPair * sizeof(double)));
+        // coefficient form: one launch for any term count; ~32 KB of staged E rows
+        constexpr int BT = 256;
+        int stage_rows = (int)((32 * 1024) / ((size_t)lt_max * kEPair * sizeof(double)));
         stage_rows = std::max(1, std::min(stage_rows, t_chunk));
         const size_t smem = ((stage_rows * sizeof(RowInfo) + 15) & ~size_t(15)) +
                             (size_t)stage_rows * lt_max * kEPair * sizeof(double);
         if (smem > 48 * 1024)
-            cudaFuncSetAttribute(k_combine_e<EPT, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        const dim3 grid((unsigned)((d.E + (long long)BT * EPT - 1) / ((long long)BT * EPT)), nchunk);
-        k_combine_e<EPT, BT><<<grid, BT, smem, stream>>>(d, out, t_chunk, stage_rows, lt_max);
+            cudaFuncSetAttribute(k_combine_e3<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const long long nq = d.E / 3;
+        const dim3 grid((unsigned)((nq + BT - 1) / BT), nchunk);
+        k_combine_e3<BT><<<grid, BT, smem, stream>>>(d, out, t_chunk, stage_rows, lt_max);
         if (launches)
             ++*launches;
         return (int)cudaGetLastError();

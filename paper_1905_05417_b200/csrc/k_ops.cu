@@ -349,15 +349,64 @@ __global__ void k_inplane_gather(const DevTables d, int t0) {
 // K6: standard full-3D quadrature (assembly.cpp:134-245), one block per
 // (element, thickness span) of one colour, accumulated straight into the
 // precomputed CSR (the duplicate summation of sparse.cpp:30-55).
+//
+// The local block of a pair (al, be) = ((at, as), (bt, bs)) is
+//   K[ab] = sum_cells sum_q2 sum_q3 sum_xy Ct_q2[xy][ab] X_al[x] X_be[y] w3,
+//   X_al = (du N_as T_at, dv N_as T_at, N_as T'_at)   (assembly.cpp:203-206).
+// The 3D Gauss rule is a tensor product and the pulled-back Ct of a cell
+// does not vary with q3, so the thickness points are summed first, exactly:
+//   sum_q3 X_al[x] X_be[y] w3 = g_as[x] g_bs[y] tau[at][bt][x==2][y==2],
+//   tau[at][bt][i][j] = sum_q3 T^(i)_at T^(j)_bt w3     (per cell, 36 values),
+// so a (pair, q2) costs 18 products + 81 FMA, with no thickness loop.  Each
+// thread takes a group of KP pairs sharing al (KP consecutive be), so every
+// broadcast load of a Ct row feeds KP x 9 FMA (ncu, the one-pair form: FP64
+// pipe 43%, shared-memory loads as the second stall; profiles/r1_ncu_standard_c3.txt).
+// Measured (profiles/r2_k6_ab.txt, C3 / C4 ms): one pair per thread 87 / 88;
+// KP = 2 at <= 128 registers (16 warps/SM) 78 / 85; KP = 3, 4 at 197-228
+// registers (8 warps/SM) 120-136 / 183-200 -- the += into the CSR needs the
+// warps to hide its load latency.
 #ifndef LF_K6_MINB
-#define LF_K6_MINB 3 // <= 80 registers: 24 warps/SM (C3 standard 95.7 -> 87.2 ms)
+#define LF_K6_MINB 2
 #endif
+#ifndef LF_K6_PAIRS
+#define LF_K6_PAIRS 2
+#endif
+constexpr int kK6Pairs = LF_K6_PAIRS; // pairs per thread
+
+/// Pair group g of an element block: al and the first be of kK6Pairs
+/// consecutive be (be >= al when the tables are symmetric).
+__device__ __forceinline__ void k6_group(int g, int nl3, bool sym, int& al, int& be0) {
+    if (sym) {
+        al = 0;
+        int per = (nl3 + kK6Pairs - 1) / kK6Pairs;
+        while (g >= per) {
+            g -= per;
+            ++al;
+            per = (nl3 - al + kK6Pairs - 1) / kK6Pairs;
+        }
+        be0 = al + g * kK6Pairs;
+    } else {
+        const int per = (nl3 + kK6Pairs - 1) / kK6Pairs;
+        al = g / per;
+        be0 = (g % per) * kK6Pairs;
+    }
+}
+
+__host__ __device__ inline int k6_groups(int nl3, bool sym) {
+    if (!sym)
+        return nl3 * ((nl3 + kK6Pairs - 1) / kK6Pairs);
+    int n = 0;
+    for (int al = 0; al < nl3; ++al)
+        n += (nl3 - al + kK6Pairs - 1) / kK6Pairs;
+    return n;
+}
+
 __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard(const DevTables d, double* __restrict__ values, int cu, int cv, int ct, int nchunk) {
     extern __shared__ double sm[];
     ElemInfo el;
     el.eu = cu + blockIdx.x * (d.pu + 1);
     el.ev = cv + blockIdx.y * (d.pv + 1);
-    // blockIdx.z = (span of this thickness colour, chunk of the local pairs):
+    // blockIdx.z = (span of this thickness colour, chunk of the pair groups):
     // few elements per colour (small plates, many plies per span) still fill
     // the GPU; chunks own disjoint pairs, so their writes never overlap
     const int chunk = blockIdx.z % nchunk;
@@ -384,96 +433,124 @@ __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard(const DevTables d,
     double* tv = ctq + el.nq2 * 90; // nqt * ntl values, then derivatives
     double* td = tv + d.nqt * ntl;
     double* w3 = td + d.nqt * ntl;
+    double* tau = w3 + d.nqt; // [at][bt][i][j]
     element_tables(d, el, gh, w2);
     const int e_index = el.ev * d.nspu + el.eu;
     const long long pre0 = d.pre_t[d.t0];
-    for (int c = c0; c < c1; ++c) {
-        __syncthreads();
-        const int cfg = d.layer_config[d.cell_layer[c]];
-        pullback_tables(d, e_index, el.nq2, w2, d.term_table + (long long)cfg * 81, ctq);
-        for (int idx = threadIdx.x; idx < d.nqt * ntl; idx += blockDim.x) {
-            const int q = idx / ntl, a = idx % ntl;
-            const long long h = (long long)c * d.nqt + q;
-            const int sh = ft - d.Bt_first[h]; // 0 unless a point rounds onto a knot
-            const int aa = a + sh;
-            const bool ok = aa >= 0 && aa <= d.pt;
-            tv[idx] = ok ? d.Bt_val[h * ntl + aa] : 0.0;
-            td[idx] = ok ? d.Bt_der[h * ntl + aa] : 0.0;
+    const bool sym = d.sym != 0;
+    const int ngroup = k6_groups(nl3, sym);
+    const int per = (ngroup + nchunk - 1) / nchunk;
+    const int g_end = min(ngroup, (chunk + 1) * per);
+    // this thread's pair groups: at most ceil(per / blockDim) (one, normally)
+    for (int g = chunk * per + threadIdx.x; g - threadIdx.x < g_end; g += blockDim.x) {
+        const bool g_live = g < g_end;
+        int al = 0, be0 = 0;
+        if (g_live)
+            k6_group(g, nl3, sym, al, be0);
+        const int at = al / el.nl2, as = al % el.nl2;
+        int bs[kK6Pairs], bt[kK6Pairs];
+        bool pv[kK6Pairs];
+#pragma unroll
+        for (int p = 0; p < kK6Pairs; ++p) {
+            const int be = be0 + p;
+            pv[p] = g_live && be < nl3;
+            const int bec = pv[p] ? be : al;
+            bt[p] = bec / el.nl2;
+            bs[p] = bec % el.nl2;
         }
-        for (int q = threadIdx.x; q < d.nqt; q += blockDim.x)
-            w3[q] = d.cell_wts[(long long)c * d.nqt + q];
-        __syncthreads();
-        const int npair = d.sym ? nl3 * (nl3 + 1) / 2 : nl3 * nl3;
-        const int per = (npair + nchunk - 1) / nchunk;
-        const int p_end = min(npair, (chunk + 1) * per);
-        for (int pr = chunk * per + threadIdx.x; pr < p_end; pr += blockDim.x) {
-            int al, be;
-            if (d.sym) { // triangular index: be >= al
-                al = 0;
-                int rest = pr;
-                while (rest >= nl3 - al) {
-                    rest -= nl3 - al;
-                    ++al;
-                }
-                be = al + rest;
-            } else {
-                al = pr / nl3;
-                be = pr % nl3;
-            }
-            const int at = al / el.nl2, as = al % el.nl2;
-            const int bt = be / el.nl2, bs = be % el.nl2;
-            const int it = ft + at, jt = ft + bt;
-            // rows of functions (it, is) / (jt, js) inside the output range [f0, f1)
-            const long long gi = (long long)it * d.ns + (el.fv + as / (d.pu + 1)) * d.nu + el.fu + as % (d.pu + 1);
-            const long long gj = (long long)jt * d.ns + (el.fv + bs / (d.pu + 1)) * d.nu + el.fu + bs % (d.pu + 1);
-            const bool row_i = gi >= d.f0 && gi < d.f1;
-            const bool row_j = d.sym && al != be && gj >= d.f0 && gj < d.f1;
-            if (!row_i && !row_j)
-                continue;
-            double acc[9];
+        double acc[kK6Pairs][9];
+#pragma unroll
+        for (int p = 0; p < kK6Pairs; ++p)
 #pragma unroll
             for (int k = 0; k < 9; ++k)
-                acc[k] = 0.0;
+                acc[p][k] = 0.0;
+        for (int c = c0; c < c1; ++c) {
+            __syncthreads();
+            const int cfg = d.layer_config[d.cell_layer[c]];
+            pullback_tables(d, e_index, el.nq2, w2, d.term_table + (long long)cfg * 81, ctq);
+            for (int idx = threadIdx.x; idx < d.nqt * ntl; idx += blockDim.x) {
+                const int q = idx / ntl, a = idx % ntl;
+                const long long h = (long long)c * d.nqt + q;
+                const int sh = ft - d.Bt_first[h]; // 0 unless a point rounds onto a knot
+                const int aa = a + sh;
+                const bool ok = aa >= 0 && aa <= d.pt;
+                tv[idx] = ok ? d.Bt_val[h * ntl + aa] : 0.0;
+                td[idx] = ok ? d.Bt_der[h * ntl + aa] : 0.0;
+            }
+            for (int q = threadIdx.x; q < d.nqt; q += blockDim.x)
+                w3[q] = d.cell_wts[(long long)c * d.nqt + q];
+            __syncthreads();
+            for (int idx = threadIdx.x; idx < ntl * ntl * 4; idx += blockDim.x) {
+                const int a = idx / (4 * ntl), b = (idx / 4) % ntl, i = (idx >> 1) & 1, j = idx & 1;
+                double s = 0.0;
+                for (int q3 = 0; q3 < d.nqt; ++q3)
+                    s += (i ? td : tv)[q3 * ntl + a] * (j ? td : tv)[q3 * ntl + b] * w3[q3];
+                tau[idx] = s;
+            }
+            __syncthreads();
+            if (!g_live)
+                continue;
+            double tp[kK6Pairs][4];
+#pragma unroll
+            for (int p = 0; p < kK6Pairs; ++p)
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    tp[p][k] = tau[(at * ntl + bt[p]) * 4 + k];
             for (int q2 = 0; q2 < el.nq2; ++q2) {
                 const double* ga = gh + (q2 * el.nl2 + as) * 3;
-                const double* gb = gh + (q2 * el.nl2 + bs) * 3;
-                // the thickness points of the cell share the in-plane C~: sum the
-                // 9 gradient products over q3 first, then contract once with C~
-                double S[9];
+                const double a0 = ga[0], a1 = ga[1], a2 = ga[2];
+                double gb[kK6Pairs][3];
 #pragma unroll
-                for (int xy = 0; xy < 9; ++xy)
-                    S[xy] = 0.0;
-                for (int q3 = 0; q3 < d.nqt; ++q3) {
-                    const double Ta = tv[q3 * ntl + at], Tda = td[q3 * ntl + at];
-                    const double Tb = tv[q3 * ntl + bt], Tdb = td[q3 * ntl + bt];
-                    // grad_hat = (du T, dv T, val T') (assembly.cpp:203-206)
-                    const double xa[3] = {ga[0] * Ta, ga[1] * Ta, ga[2] * Tda};
-                    const double xb[3] = {gb[0] * Tb * w3[q3], gb[1] * Tb * w3[q3], gb[2] * Tdb * w3[q3]};
-#pragma unroll
-                    for (int x = 0; x < 3; ++x)
-#pragma unroll
-                        for (int y = 0; y < 3; ++y)
-                            S[3 * x + y] += xa[x] * xb[y];
+                for (int p = 0; p < kK6Pairs; ++p) {
+                    const double* b = gh + (q2 * el.nl2 + bs[p]) * 3;
+                    gb[p][0] = b[0];
+                    gb[p][1] = b[1];
+                    gb[p][2] = b[2];
                 }
                 const double2* C2 = reinterpret_cast<const double2*>(ctq + q2 * 90);
 #pragma unroll
                 for (int xy = 0; xy < 9; ++xy) {
+                    const int x = xy / 3, y = xy % 3;
+                    const double gx = x == 0 ? a0 : x == 1 ? a1 : a2;
+                    const double2 r0 = C2[xy * 5], r1 = C2[xy * 5 + 1], r2 = C2[xy * 5 + 2], r3 = C2[xy * 5 + 3],
+                                  r4 = C2[xy * 5 + 4];
 #pragma unroll
-                    for (int h = 0; h < 5; ++h) {
-                        const double2 c = C2[xy * 5 + h];
-                        acc[2 * h] += c.x * S[xy];
-                        if (2 * h + 1 < 9)
-                            acc[2 * h + 1] += c.y * S[xy];
+                    for (int p = 0; p < kK6Pairs; ++p) {
+                        const double s = gx * gb[p][y] * tp[p][(x == 2 ? 2 : 0) + (y == 2 ? 1 : 0)];
+                        acc[p][0] = fma(r0.x, s, acc[p][0]);
+                        acc[p][1] = fma(r0.y, s, acc[p][1]);
+                        acc[p][2] = fma(r1.x, s, acc[p][2]);
+                        acc[p][3] = fma(r1.y, s, acc[p][3]);
+                        acc[p][4] = fma(r2.x, s, acc[p][4]);
+                        acc[p][5] = fma(r2.y, s, acc[p][5]);
+                        acc[p][6] = fma(r3.x, s, acc[p][6]);
+                        acc[p][7] = fma(r3.y, s, acc[p][7]);
+                        acc[p][8] = fma(r4.x, s, acc[p][8]);
                     }
                 }
             }
+        }
+        if (!g_live)
+            continue;
+        const int it = ft + at;
+        const long long gi = (long long)it * d.ns + (el.fv + as / (d.pu + 1)) * d.nu + el.fu + as % (d.pu + 1);
+#pragma unroll
+        for (int p = 0; p < kK6Pairs; ++p) {
+            if (!pv[p])
+                continue;
+            const int jt = ft + bt[p];
+            const long long gj =
+                (long long)jt * d.ns + (el.fv + bs[p] / (d.pu + 1)) * d.nu + el.fu + bs[p] % (d.pu + 1);
+            // rows of functions (it, is) / (jt, js) inside the output range [f0, f1)
+            const bool row_i = gi >= d.f0 && gi < d.f1;
+            const bool row_j = sym && al != be0 + p && gj >= d.f0 && gj < d.f1;
             // K(i,j)[a][b] into row block i; with symmetric tables also
             // K(j,i)[b][a] = K(i,j)[a][b] into row block j (same element, so the
             // colouring still makes the += race-free)
             for (int side = 0; side < 2; ++side) {
                 if (side == 0 ? !row_i : !row_j)
                     continue;
-                const int ls = side ? bs : as, ms = side ? as : bs;
+                const int ls = side ? bs[p] : as, ms = side ? as : bs[p];
                 const int rt = side ? jt : it, ct_ = side ? it : jt;
                 const int iu = el.fu + ls % (d.pu + 1), iv = el.fv + ls / (d.pu + 1);
                 const int ju = el.fu + ms % (d.pu + 1), jv = el.fv + ms / (d.pu + 1);
@@ -490,7 +567,7 @@ __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard(const DevTables d,
                 for (int a = 0; a < 3; ++a)
 #pragma unroll
                     for (int b = 0; b < 3; ++b)
-                        values[pos + (long long)a * Lt * B + b] += side ? acc[3 * b + a] : acc[3 * a + b];
+                        values[pos + (long long)a * Lt * B + b] += side ? acc[p][3 * b + a] : acc[p][3 * a + b];
             }
         }
     }
@@ -654,23 +731,26 @@ __global__ void k_pattern_rows(const DevTables d, long long* __restrict__ row_pt
 template <int kColsEpt>
 __global__ void __launch_bounds__(kBlock) k_pattern_cols(const DevTables d, int* __restrict__ cols,
                                                          int t_chunk) {
-    int* o0[kColsEpt];
-    int B[kColsEpt], col_s[kColsEpt];
-    long long A[kColsEpt];
-    bool live[kColsEpt], in_s0[kColsEpt], in_s1[kColsEpt];
+    // per entry: row-segment length B, offset in the segment, in-plane entry
+    // base A (< E < 2^31, checked by the launcher) and column; 32-bit each
+    int B[kColsEpt], col_s[kColsEpt], rem_x[kColsEpt], A[kColsEpt];
+    // bit x: entry x is live / its function is >= s0 / < s1 (partial first and
+    // last rows); packed so that 16 entries per thread stay within 255 registers
+    // without spilling (three bool arrays took the C4 build from 1.44 to 2.2 ms)
+    unsigned live = 0, in_s0 = 0, in_s1 = 0;
 #pragma unroll
     for (int x = 0; x < kColsEpt; ++x) {
         const long long e = (long long)blockIdx.x * kBlock * kColsEpt + (threadIdx.x >> 5) * 32 * kColsEpt +
                             x * 32 + (threadIdx.x & 31);
-        live[x] = e < d.E;
-        const long long ec = live[x] ? e : d.E - 1;
+        live |= (e < d.E ? 1u : 0u) << x;
+        const long long ec = e < d.E ? e : d.E - 1;
         int is = __ldg(d.blk_is + ec / kBlock);
         while (__ldg(d.es_pre + is + 1) <= ec)
             ++is;
         const long long ebase = __ldg(d.es_pre + is);
         const int r = (int)(ec - ebase);
-        in_s0[x] = is >= d.s0;
-        in_s1[x] = is < d.s1;
+        in_s0 |= (is >= d.s0 ? 1u : 0u) << x;
+        in_s1 |= (is < d.s1 ? 1u : 0u) << x;
         const int iu = is % d.nu, iv = is / d.nu;
         const int Lu = __ldg(d.len_u + iu), Lv = __ldg(d.len_v + iv);
         B[x] = 3 * Lu * Lv;
@@ -678,8 +758,8 @@ __global__ void __launch_bounds__(kBlock) k_pattern_cols(const DevTables d, int*
         const int s = rem / 3, b = rem % 3;
         const int jv = __ldg(d.lo_v + iv) + s / Lu, ju = __ldg(d.lo_u + iu) + s % Lu;
         col_s[x] = 3 * (jv * d.nu + ju) + b;
-        A[x] = ebase + (long long)a * B[x];
-        o0[x] = cols + rem;
+        A[x] = (int)(ebase + (long long)a * B[x]);
+        rem_x[x] = rem;
     }
     const int it_begin = d.t0 + blockIdx.y * t_chunk;
     const int it_end = min(d.t1, it_begin + t_chunk);
@@ -689,20 +769,18 @@ __global__ void __launch_bounds__(kBlock) k_pattern_cols(const DevTables d, int*
         const long long base = 9 * d.S_s * (__ldg(d.pre_t + it) - pre0) - d.out_base;
         const int c0 = 3 * d.ns * __ldg(d.lo_t + it);
         const int edge = row_edge(d, it);
-        bool lv[kColsEpt];
+        const unsigned lv = live & ((edge & 1) ? in_s0 : ~0u) & ((edge & 2) ? in_s1 : ~0u);
 #pragma unroll
         for (int x = 0; x < kColsEpt; ++x)
-            lv[x] = live[x] && (!(edge & 1) || in_s0[x]) && (!(edge & 2) || in_s1[x]);
-#pragma unroll
-        for (int x = 0; x < kColsEpt; ++x)
-            LF_CHECK(!lv[x] || (base + (long long)Lt * A[x] + (o0[x] - cols) >= 0 &&
-                                base + (long long)Lt * A[x] + (long long)(Lt - 1) * B[x] + (o0[x] - cols) <
+            LF_CHECK(!((lv >> x) & 1u) || (base + (long long)Lt * A[x] + rem_x[x] >= 0 &&
+                                base + (long long)Lt * A[x] + (long long)(Lt - 1) * B[x] + rem_x[x] <
                                     d.nnz_slab));
         for (int k = 0; k < Lt; ++k) {
 #pragma unroll
             for (int x = 0; x < kColsEpt; ++x)
-                if (lv[x])
-                    __stcs(o0[x] + base + (long long)Lt * A[x] + (long long)k * B[x], c0 + 3 * d.ns * k + col_s[x]);
+                if ((lv >> x) & 1u)
+                    __stcs(cols + base + (long long)Lt * A[x] + (long long)k * B[x] + rem_x[x],
+                           c0 + 3 * d.ns * k + col_s[x]);
         }
     }
 }
@@ -940,6 +1018,8 @@ int inplane_general_launches(const DevTables& d) { return 2 * ((d.n_terms + d.pe
 
 int launch_pattern(const DevTables& d, long long* row_ptr, int* cols, cudaStream_t stream) {
     const long long rows = 3 * (d.f1 - d.f0);
+    if (d.E >= (1LL << 31))
+        return (int)cudaErrorInvalidValue; // in-plane entry space beyond 32-bit offsets
     k_pattern_rows<<<(unsigned)((rows + 1 + 255) / 256), 256, 0, stream>>>(d, row_ptr, rows);
     if (d.E > 0 && d.t1 > d.t0) {
         const int nt = d.t1 - d.t0;
@@ -963,16 +1043,16 @@ int launch_standard(const DevTables& d, double* values, long long nnz, cudaStrea
     cudaMemsetAsync(values, 0, sizeof(double) * (size_t)nnz, stream);
     const int nl2 = (d.pu + 1) * (d.pv + 1), nq2 = d.nqu * d.nqv, ntl = d.pt + 1;
     const size_t smem = sizeof(double) * ((size_t)nq2 * nl2 * 3 + nq2 + 1 + (size_t)nq2 * 90 +
-                                          2 * (size_t)d.nqt * ntl + d.nqt);
+                                          2 * (size_t)d.nqt * ntl + d.nqt + 4 * (size_t)ntl * ntl);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_standard, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int gx = (d.nspu + d.pu) / (d.pu + 1), gy = (d.nspv + d.pv) / (d.pv + 1), gz = (d.nspt + d.pt) / (d.pt + 1);
-    // split the local pairs of each (element, span) over enough blocks for
-    // ~4 blocks per SM per colour launch (chunks of >= 256 pairs)
+    // split the pair groups of each (element, span) over enough blocks for
+    // ~4 blocks per SM per colour launch (chunks of >= 128 groups)
     const int nl3 = nl2 * ntl;
-    const int npair = d.sym ? nl3 * (nl3 + 1) / 2 : nl3 * nl3;
+    const int ngroup = k6_groups(nl3, d.sym != 0);
     const long long blocks = (long long)gx * gy * gz;
-    int nchunk = (int)std::min<long long>((148LL * 4 + blocks - 1) / blocks, (npair + 255) / 256);
+    int nchunk = (int)std::min<long long>((148LL * 4 + blocks - 1) / blocks, (ngroup + 127) / 128);
     nchunk = std::max(1, std::min(nchunk, 65535 / std::max(1, gz)));
     const dim3 grid(gx, gy, gz * nchunk);
     for (int ct = 0; ct <= d.pt; ++ct)

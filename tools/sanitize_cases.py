@@ -49,6 +49,17 @@ plan.synchronize()
 st = lf.device_csr_stats(plan.rows, rp.data_ptr(), cols.data_ptr(), vals.data_ptr())
 out.append(st["fro_sq"])
 plan.close()
+# coefficient-form combine (12 terms) on a function range cut inside thickness rows
+many12 = P.plate(2, 6, 5, [(P.baseline_orthotropic(), -1.5 + 0.2 * k) for k in range(12)], thickness=0.2)
+plan = lf.Plan(many12, "fast", 0, f_begin=many12.n_s + 5, f_end=4 * many12.n_s - 7)
+rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
+cols = torch.empty(plan.nnz, dtype=torch.int32, device="cuda")
+vals = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
+plan.build_pattern(rp.data_ptr(), cols.data_ptr())
+plan.assemble(vals.data_ptr())
+plan.synchronize()
+out.append(float(vals.sum()))
+plan.close()
 # a BASELINE-size plan (C3): the large-slab pattern kernel (16 entries per thread) and the
 # 4-term combine with the branch-free bodies
 c3 = P.baseline_config("C3")
