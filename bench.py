@@ -490,6 +490,13 @@ def main():
         except Exception as exc:  # reported, not fatal
             standard = {"error": str(exc)}
 
+    many = None
+    if world == 1 and with_pattern and not args.no_standard:
+        try:
+            many = measure_many_terms(args, prob, device, stream, hbm)
+        except Exception as exc:  # reported, not fatal
+            many = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
     c5 = None
     if not args.no_c5 and args.config != "C5":
         try:
@@ -514,7 +521,7 @@ def main():
                        "slab_passes_per_gpu": passes},
             "roofline": roofline, "e2e": e2e, "e2e_dropin": e2e_dropin, "cpu_baseline": cpu,
             "gpu_launches": launches, "clocks": clocks, "verify": verify, "standard": standard,
-            "pattern": pattern, "per_rank_ms": timing["per_rank_ms"], "c5": c5,
+            "pattern": pattern, "per_rank_ms": timing["per_rank_ms"], "c5": c5, "many_terms": many,
         }
         print(json.dumps(line))
     if world > 1:
@@ -666,6 +673,35 @@ def measure_standard(args, prob, device, stream):
                 "value": nnz / dt, "unit": "nnz/s", "cores": threads, "kind": "reference",
                 "sample": f"{args.config} family with 1 ply ({nnz} nnz), one assembleStandard, "
                           f"reference sources compiled with the Eigen subset, threads={threads}"}
+    return out
+
+
+def measure_many_terms(args, prob, device, stream, hbm):
+    """Side measurement: the same workload with many operator terms, which
+    takes the coefficient form of the combine (one launch, 9 FMA per value
+    whatever the term count): AssemblyOptions.decompose_angles (five terms
+    per material) and the orthotropic ply at 16 distinct angles.  Device time
+    per step (CUDA events) and k_combine's HBM fraction, values in the same
+    precomputed pattern."""
+    import torch
+    import paper_1905_05417_b200 as lf
+    orth = lf.baseline_orthotropic()
+    cases = {"decompose_angles": prob.replace(decompose_angles=True),
+             "16_distinct_angles": prob.replace(layers=[(orth, -1.5 + 3.0 * (k % 16) / 16)
+                                                        for k in range(len(prob.layers))])}
+    out = {}
+    for name, pr in cases.items():
+        plan = lf.Plan(pr, "fast", device, stream=stream.cuda_stream)
+        vals = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
+        t = device_step_time([plan], [vals.data_ptr()], max(3, min(args.steps, 10)), 2, stream, 1, "nccl")
+        k_ms = t["combine_ms_per_step"]
+        out[name] = {"ms_per_step": t["ms_per_step"], "value": plan.nnz / (t["ms_per_step"] / 1e3),
+                     "unit": "nnz/s", "operator_builds": plan.stats().operator_builds,
+                     "launches_per_step": plan.launch_count,
+                     "combine_ms": k_ms, "combine_frac_of_hbm": plan.nnz * 8 / (k_ms / 1e3) / 1e9 / hbm}
+        plan.close()
+        del vals
+        torch.cuda.empty_cache()
     return out
 
 

@@ -342,13 +342,16 @@ std::pair<int64_t, int64_t> thickness_range(const lf_problem* p, int t0, int t1)
 
 /// Smallest term count that takes the coefficient form of the combine
 /// (affine geometry).  Below it the per-term form keeps the entry's P in
-/// registers (4 FMA per active term and value); from 9 terms on the
-/// per-term form would need a second read-modify-write pass.  Measured:
-/// profiles/r2_eform.txt.  LAMFAST_EFORM_MIN_TERMS overrides it (A/B runs).
+/// registers (4 FMA per active term and value); the coefficient form costs
+/// 9 FMA per value whatever the term count, and from 9 terms on the
+/// per-term form would need a second read-modify-write pass.  Measured
+/// crossover (profiles/r2_coef_threshold.txt): per-term faster up to 6-7
+/// distinct angles on C4 and C3, the coefficient form from 8.
+/// LAMFAST_EFORM_MIN_TERMS overrides it (A/B runs).
 int eform_min_terms() {
     if (const char* e = std::getenv("LAMFAST_EFORM_MIN_TERMS"))
         return std::max(1, std::atoi(e));
-    return 9;
+    return 8;
 }
 
 /// Output-range fields of the device tables (row offsets slab-local).

@@ -24,6 +24,13 @@ __device__ __forceinline__ void store_value(double* p, double v) {
 #endif
 }
 
+/// Predicated streaming store (no branch around it).
+__device__ __forceinline__ void store_value_if(double* p, double v, unsigned pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.cs.f64 [%0], %1;\n\t}" ::"l"(p),
+                 "d"(v), "r"(pred)
+                 : "memory");
+}
+
 __device__ __forceinline__ int find_is(const long long* es_pre, int ns, long long e) {
     int lo = 0, hi = ns; // es_pre[lo] <= e < es_pre[hi]
     while (hi - lo > 1) {

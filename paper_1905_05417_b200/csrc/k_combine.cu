@@ -228,49 +228,98 @@ __global__ void k_pair_coeffs(const DevTables d) {
     d.Etab[pp * kEPair + ab * kEStride + xy] = e;
 }
 
-// One thread per in-plane entry triple (i_s, a, slot): the nine I_xy depend
-// on (i_s, slot) only, so the thread forms the three values b = 0..2 of its
-// (a, slot) from the 27 coefficients E[pair][3a + b][xy].  Consecutive lanes
-// hold consecutive slots of one row segment (warp-uniform a except at segment
-// ends), so the coefficient loads are shared-memory broadcasts and a warp's
-// three stores per (row, neighbour) cover one contiguous 768-byte run.
-// Per value: 9 FMA and 1/3 of a 16-byte broadcast load group.
-template <int BT>
-__global__ void __launch_bounds__(BT) k_combine_e3(const DevTables d, double* __restrict__ out, int t_chunk,
-                                                   int stage_rows, int lt_max) {
+// Thread mapping.  A warp owns 32 consecutive in-plane pairs (i_s, slot) of
+// one row-component a (the pairs of each a are padded to a multiple of 32, so
+// a is warp-uniform and every coefficient load is a shared-memory broadcast).
+// Per (row, neighbour) the warp writes the 96 values (pair, b) of its pairs:
+// lane t stores values j = t + 32 m, m = 0..2, i.e. pair j / 3 and b = j % 3,
+// so each of its three stores is one contiguous 256-byte run across the warp
+// (except where a segment of the row ends).  Since 32 = 2 mod 3, a lane's
+// three values carry the three different b, so the lane keeps, for every b,
+// the nine I_xy of the pair it stores with that b (J[b], selected once) and
+// forms w_b = sum_xy J[b][xy] E[pair][3a + b][xy] with the same broadcast
+// coefficient rows as every other lane.  With NS sets of 32 pairs per warp
+// every broadcast feeds NS FMA per lane.  Measured (C4 / C3 combine ms,
+// profiles/r2_eform_*.txt, r2_coef_*.txt): one entry per thread 5.62 / 2.80;
+// one triple per thread with 24-byte-stride stores 5.66 / 2.67 (ncu: LSU
+// data pipe 74%, three shared wavefronts per coefficient load); this mapping
+// 4.39 / 1.98, with split FMA chains and component-local staging 4.09 / 1.78
+// (NS = 1, 16 warps/SM), NS = 2 at 254 registers (8 warps/SM) 4.04 / 1.75.
+// The per-term form it replaces above 7 terms needs one read-modify-write
+// pass per 8 terms: C4 decompose_angles 14.6 ms, 16 distinct angles 12.3 ms.
+template <int BT, int NS, int MINB>
+__global__ void __launch_bounds__(BT, MINB) k_combine_coef(const DevTables d, double* __restrict__ out, int t_chunk,
+                                                           int stage_rows, int lt_max, long long s_pad) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     RowInfo* s_row = reinterpret_cast<RowInfo*>(smem_raw);
     double* s_e = reinterpret_cast<double*>(smem_raw + ((stage_rows * sizeof(RowInfo) + 15) & ~15));
-    const long long nq = d.E / 3; // entry triples (b = 0, 1, 2 of one (i_s, a, slot))
-    const long long q = (long long)blockIdx.x * BT + threadIdx.x;
-    const bool live = q < nq;
-    const long long e = 3 * (live ? q : nq - 1);
-    int is = __ldg(d.blk_is + e / kBlock);
-    while (__ldg(d.es_pre + is + 1) <= e)
-        ++is;
-    const long long ebase = __ldg(d.es_pre + is);
-    const int r = (int)(e - ebase);
-    const bool in_s0 = is >= d.s0, in_s1 = is < d.s1;
-    const int iu = is % d.nu, iv = is / d.nu;
-    const int Lu = __ldg(d.len_u + iu), Lv = __ldg(d.len_v + iv);
-    const int B = 3 * Lu * Lv;
-    const int a = r / B;
-    const int rem = r - a * B; // 3 * slot
-    const long long A = ebase + (long long)a * B;
-    double* const o_thread = out + rem;
-    const int coff = 3 * a * kEStride;
-    double I[9];
-    {
-        const int sl = rem / 3;
-        const int sv = sl / Lu, su = sl - sv * Lu;
-        const double* U = d.U + ((long long)iu * d.bu + su) * 4;
-        const double* V = d.V + ((long long)iv * d.bv + sv) * 4;
-        const double u0 = __ldg(U), u1 = __ldg(U + 1), u2 = __ldg(U + 2), u3 = __ldg(U + 3);
-        const double v0 = __ldg(V), v1 = __ldg(V + 1), v2 = __ldg(V + 2), v3 = __ldg(V + 3);
-        // xy = 3x + y, x/y: 0 -> d/du, 1 -> d/dv, 2 -> value (affine_p)
-        I[0] = u3 * v0; I[1] = u2 * v1; I[2] = u2 * v0;
-        I[3] = u1 * v2; I[4] = u0 * v3; I[5] = u0 * v2;
-        I[6] = u1 * v0; I[7] = u0 * v1; I[8] = u0 * v0;
+    const int lane = threadIdx.x & 31;
+    // first pair slot of the warp; the warp owns NS sets of 32 consecutive pairs
+    const long long w0 = ((long long)blockIdx.x * BT + threadIdx.x - lane) * NS;
+    const int a = (int)(w0 / s_pad);
+    const bool warp_live = a < 3;
+    const long long ps0 = w0 - (long long)a * s_pad;
+    // the block stages only the coefficient rows ab = 3 a + b of the
+    // components its warps carry (one a, or two where the block straddles)
+    const int a_lo = (int)min(2LL, (long long)blockIdx.x * BT * NS / s_pad);
+    const int a_hi = (int)min(2LL, ((long long)blockIdx.x * BT + BT - 1) * NS / s_pad);
+    const int k_stride = 3 * (a_hi - a_lo + 1) * kEStride; // doubles per staged (row, k)
+    const int coff = 3 * (min(a, 2) - a_lo) * kEStride;
+    double J[NS][3][9];
+    int A[NS][3], B[NS][3], R[NS][3], bsel[3];
+    unsigned live = 0, in_s0 = 0, in_s1 = 0; // bit 3 s + m
+#pragma unroll
+    for (int m = 0; m < 3; ++m)
+        bsel[m] = (lane + 32 * m) % 3;
+#pragma unroll
+    for (int st = 0; st < NS; ++st)
+#pragma unroll
+        for (int m = 0; m < 3; ++m) {
+            const int j = lane + 32 * m;
+            const int b = bsel[m];
+            const long long ps = ps0 + 32 * st + j / 3;
+            const bool lv = warp_live && ps < d.S_s;
+            live |= (lv ? 1u : 0u) << (3 * st + m);
+            const long long e = 9 * (lv ? ps : d.S_s - 1);
+            int is = __ldg(d.blk_is + e / kBlock);
+            while (__ldg(d.es_pre + is + 1) <= e)
+                ++is;
+            const long long ebase = __ldg(d.es_pre + is);
+            const int slot = (int)((e - ebase) / 9);
+            in_s0 |= (is >= d.s0 ? 1u : 0u) << (3 * st + m);
+            in_s1 |= (is < d.s1 ? 1u : 0u) << (3 * st + m);
+            const int iu = is % d.nu, iv = is / d.nu;
+            const int Lu = __ldg(d.len_u + iu), Lv = __ldg(d.len_v + iv);
+            B[st][m] = 3 * Lu * Lv;
+            A[st][m] = (int)(ebase + (long long)min(a, 2) * B[st][m]);
+            R[st][m] = 3 * slot + b;
+            const int sv = slot / Lu, su = slot - sv * Lu;
+            const double* U = d.U + ((long long)iu * d.bu + su) * 4;
+            const double* V = d.V + ((long long)iv * d.bv + sv) * 4;
+            const double u0 = __ldg(U), u1 = __ldg(U + 1), u2 = __ldg(U + 2), u3 = __ldg(U + 3);
+            const double v0 = __ldg(V), v1 = __ldg(V + 1), v2 = __ldg(V + 2), v3 = __ldg(V + 3);
+            // xy = 3x + y, x/y: 0 -> d/du, 1 -> d/dv, 2 -> value (affine_p)
+            const double I[9] = {u3 * v0, u2 * v1, u2 * v0, u1 * v2, u0 * v3, u0 * v2, u1 * v0, u0 * v1, u0 * v0};
+            // J[st][b] = I of the value this lane stores with component b
+#pragma unroll
+            for (int bb = 0; bb < 3; ++bb)
+#pragma unroll
+                for (int xy = 0; xy < 9; ++xy)
+                    if (bb == b)
+                        J[st][bb][xy] = I[xy];
+        }
+    // staging assignment: a row's lt_max * k_stride / 2 chunks spread over the
+    // block, st_rows rows per pass (st_h < 0: more chunks per row than threads)
+    const int row_chunks = lt_max * (k_stride / 2);
+    const int st_rows = BT / row_chunks;
+    int st_r = 0, st_k = 0, st_h = -1;
+    if (st_rows > 0 && (int)threadIdx.x < st_rows * row_chunks) {
+        st_r = threadIdx.x / row_chunks;
+        const int r = threadIdx.x - st_r * row_chunks;
+        st_k = r / (k_stride / 2);
+        st_h = r - st_k * (k_stride / 2);
+    } else if (st_rows > 0) {
+        st_h = -2; // idle in staging
     }
     const int it_begin = d.t0 + blockIdx.y * t_chunk;
     const int it_end = min(d.t1, it_begin + t_chunk);
@@ -285,18 +334,32 @@ __global__ void __launch_bounds__(BT) k_combine_e3(const DevTables d, double* __
             s_row[rr].lt = __ldg(d.len_t + it) | row_edge(d, it) << 8;
             s_row[rr].mask = 0;
         }
-        // E rows of the staged thickness rows: s_e[row][k][kEPair] (16-byte chunks)
-        const int per_row = lt_max * kEPair / 2;
-        for (int idx = threadIdx.x; idx < nrow * per_row; idx += BT) {
-            const int rr = idx / per_row, h = idx - rr * per_row;
-            const int k = (2 * h) / kEPair;
-            const int it = it0 + rr;
-            double2 v = make_double2(0.0, 0.0);
-            if (k < __ldg(d.len_t + it)) {
-                const long long pq = __ldg(d.pre_t + it) - preW + k;
-                v = __ldg(reinterpret_cast<const double2*>(d.Etab + pq * kEPair) + (2 * h - k * kEPair) / 2);
+        // coefficient rows of the staged thickness rows: s_e[row][k][k_stride]
+        // (16-byte chunks); each thread copies the same (k, chunk) of every
+        // rows_per_pass-th row, its indices fixed for the whole kernel
+        if (st_rows > 0) {
+            for (int rr = st_r; st_h >= 0 && rr < nrow; rr += st_rows) {
+                const int it = it0 + rr;
+                double2 v = make_double2(0.0, 0.0);
+                if (st_k < __ldg(d.len_t + it)) {
+                    const long long pq = __ldg(d.pre_t + it) - preW + st_k;
+                    v = __ldg(reinterpret_cast<const double2*>(d.Etab + pq * kEPair + 3 * a_lo * kEStride) + st_h);
+                }
+                reinterpret_cast<double2*>(s_e)[(rr * lt_max + st_k) * (k_stride / 2) + st_h] = v;
             }
-            reinterpret_cast<double2*>(s_e)[idx] = v;
+        } else {
+            const int per_k = k_stride / 2;
+            for (int idx = threadIdx.x; idx < nrow * lt_max * per_k; idx += BT) {
+                const int rk = idx / per_k, h = idx - rk * per_k;
+                const int rr = rk / lt_max, k = rk - rr * lt_max;
+                const int it = it0 + rr;
+                double2 v = make_double2(0.0, 0.0);
+                if (k < __ldg(d.len_t + it)) {
+                    const long long pq = __ldg(d.pre_t + it) - preW + k;
+                    v = __ldg(reinterpret_cast<const double2*>(d.Etab + pq * kEPair + 3 * a_lo * kEStride) + h);
+                }
+                reinterpret_cast<double2*>(s_e)[idx] = v;
+            }
         }
         __syncthreads();
         if (!live)
@@ -304,34 +367,48 @@ __global__ void __launch_bounds__(BT) k_combine_e3(const DevTables d, double* __
         for (int rr = 0; rr < nrow; ++rr) {
             const RowInfo ri = s_row[rr];
             const int lt = ri.lt & 0xff, edge = ri.lt >> 8;
-            const bool lv = !edge || ((!(edge & 1) || in_s0) && (!(edge & 2) || in_s1));
-            double* const o = o_thread + ri.base + (long long)lt * A;
-            const double* er = s_e + (long long)rr * lt_max * kEPair + coff;
+            const unsigned lv = live & ((edge & 1) ? in_s0 : ~0u) & ((edge & 2) ? in_s1 : ~0u);
+            double* o[NS][3];
+#pragma unroll
+            for (int st = 0; st < NS; ++st)
+#pragma unroll
+                for (int m = 0; m < 3; ++m)
+                    o[st][m] = out + ri.base + (long long)lt * A[st][m] + R[st][m];
+            const double* er = s_e + (long long)rr * lt_max * k_stride + coff;
             for (int k = 0; k < lt; ++k) {
-                const double2* c = reinterpret_cast<const double2*>(er + k * kEPair);
-                double v[3];
+                const double2* c = reinterpret_cast<const double2*>(er + k * k_stride);
+                double w[NS][3];
 #pragma unroll
                 for (int b = 0; b < 3; ++b) {
-                    // coefficients of value b: er[k][10 b + xy], xy < 9 (five 16-byte loads)
+                    // coefficients of component b: er[k][10 b + xy], xy < 9 (five 16-byte
+                    // broadcasts, each feeding NS FMA per lane); two partial sums per value
+                    // halve the dependent FMA chain
                     const double2 c0 = c[5 * b], c1 = c[5 * b + 1], c2 = c[5 * b + 2], c3 = c[5 * b + 3],
                                   c4 = c[5 * b + 4];
-                    double acc = I[0] * c0.x;
-                    acc = fma(I[1], c0.y, acc);
-                    acc = fma(I[2], c1.x, acc);
-                    acc = fma(I[3], c1.y, acc);
-                    acc = fma(I[4], c2.x, acc);
-                    acc = fma(I[5], c2.y, acc);
-                    acc = fma(I[6], c3.x, acc);
-                    acc = fma(I[7], c3.y, acc);
-                    v[b] = fma(I[8], c4.x, acc);
+#pragma unroll
+                    for (int st = 0; st < NS; ++st) {
+                        const double* Jb = J[st][b];
+                        double s0 = Jb[0] * c0.x, s1 = Jb[1] * c0.y;
+                        s0 = fma(Jb[2], c1.x, s0);
+                        s1 = fma(Jb[3], c1.y, s1);
+                        s0 = fma(Jb[4], c2.x, s0);
+                        s1 = fma(Jb[5], c2.y, s1);
+                        s0 = fma(Jb[6], c3.x, s0);
+                        s1 = fma(Jb[7], c3.y, s1);
+                        s0 = fma(Jb[8], c4.x, s0);
+                        w[st][b] = s0 + s1;
+                    }
                 }
-                double* ok = o + (long long)k * B;
-                LF_CHECK(!lv || (ok >= out && ok + 2 < out + d.nnz_slab));
-                if (lv) {
-                    store_value(ok, v[0]);
-                    store_value(ok + 1, v[1]);
-                    store_value(ok + 2, v[2]);
-                }
+#pragma unroll
+                for (int st = 0; st < NS; ++st)
+#pragma unroll
+                    for (int m = 0; m < 3; ++m) {
+                        const double val = bsel[m] == 0 ? w[st][0] : bsel[m] == 1 ? w[st][1] : w[st][2];
+                        const unsigned bit = (lv >> (3 * st + m)) & 1u;
+                        LF_CHECK(!bit || (o[st][m] >= out && o[st][m] < out + d.nnz_slab));
+                        store_value_if(o[st][m], val, bit);
+                        o[st][m] += B[st][m];
+                    }
             }
         }
     }
@@ -369,17 +446,31 @@ int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t st
     const unsigned nchunk = (unsigned)((nt + t_chunk - 1) / t_chunk);
     const int lt_max = std::max(1, d.lt_max);
     if (d.Etab) {
-        // coefficient form: one launch for any term count; ~32 KB of staged E rows
-        constexpr int BT = 256;
-        int stage_rows = (int)((32 * 1024) / ((size_t)lt_max * kEPair * sizeof(double)));
+        // coefficient form: one launch for any term count; ~32 KB of staged
+        // coefficient rows (two components a per block at most when a
+        // component's pairs fill a block, else all three)
+#ifndef LF_COEF_BT
+#define LF_COEF_BT 256
+#endif
+#ifndef LF_COEF_NS
+#define LF_COEF_NS 2
+#endif
+#ifndef LF_COEF_MINB
+#define LF_COEF_MINB 1
+#endif
+        constexpr int BT = LF_COEF_BT, NS = LF_COEF_NS, MINB = LF_COEF_MINB;
+        const long long s_pad = (d.S_s + 32 * NS - 1) / (32 * NS) * (32 * NS); // pairs per component, warp-padded
+        const int nab = s_pad >= (long long)BT * NS ? 6 : 9;
+        int stage_rows = (int)((32 * 1024) / ((size_t)lt_max * nab * kEStride * sizeof(double)));
         stage_rows = std::max(1, std::min(stage_rows, t_chunk));
         const size_t smem = ((stage_rows * sizeof(RowInfo) + 15) & ~size_t(15)) +
-                            (size_t)stage_rows * lt_max * kEPair * sizeof(double);
+                            (size_t)stage_rows * lt_max * nab * kEStride * sizeof(double);
+        auto kern = k_combine_coef<BT, NS, MINB>;
         if (smem > 48 * 1024)
-            cudaFuncSetAttribute(k_combine_e3<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        const long long nq = d.E / 3;
-        const dim3 grid((unsigned)((nq + BT - 1) / BT), nchunk);
-        k_combine_e3<BT><<<grid, BT, smem, stream>>>(d, out, t_chunk, stage_rows, lt_max);
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const long long warps = 3 * s_pad / (32 * NS);
+        const dim3 grid((unsigned)((warps * 32 + BT - 1) / BT), nchunk);
+        kern<<<grid, BT, smem, stream>>>(d, out, t_chunk, stage_rows, lt_max, s_pad);
         if (launches)
             ++*launches;
         return (int)cudaGetLastError();

@@ -401,6 +401,27 @@ __host__ __device__ inline int k6_groups(int nl3, bool sym) {
     return n;
 }
 
+/// CSR position of value (0, 0) of block K(i, j), i = (rt, local in-plane ls),
+/// j = (ct, local ms), of an element; value (a, b) is at + a Lt B + b.
+__device__ __forceinline__ long long k6_pos(const DevTables& d, const ElemInfo& el, int ls, int ms, int rt, int ct,
+                                            long long pre0, long long& LtB) {
+    const int iu = el.fu + ls % (d.pu + 1), iv = el.fv + ls / (d.pu + 1);
+    const int ju = el.fu + ms % (d.pu + 1), jv = el.fv + ms / (d.pu + 1);
+    const int is = iv * d.nu + iu;
+    const int Lu = d.len_u[iu], Lv = d.len_v[iv];
+    const int B = 3 * Lu * Lv;
+    const int slot = (jv - d.lo_v[iv]) * Lu + (ju - d.lo_u[iu]);
+    const int Lt = d.len_t[rt];
+    LtB = (long long)Lt * B;
+    LF_CHECK(ct >= d.lo_t[rt] && ct < d.lo_t[rt] + Lt);
+    return 9 * d.S_s * (d.pre_t[rt] - pre0) + (long long)Lt * d.es_pre[is] + (long long)(ct - d.lo_t[rt]) * B +
+           3 * slot - d.out_base;
+}
+
+#ifndef LF_K6_PREFETCH
+#define LF_K6_PREFETCH 1
+#endif
+
 __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard(const DevTables d, double* __restrict__ values, int cu, int cv, int ct, int nchunk) {
     extern __shared__ double sm[];
     ElemInfo el;
@@ -464,6 +485,34 @@ __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard(const DevTables d,
 #pragma unroll
             for (int k = 0; k < 9; ++k)
                 acc[p][k] = 0.0;
+        const int it = ft + at;
+        const long long gi = (long long)it * d.ns + (el.fv + as / (d.pu + 1)) * d.nu + el.fu + as % (d.pu + 1);
+#if LF_K6_PREFETCH
+        // the group's += targets are read only after the quadrature loop: ask L2
+        // for their lines now, so the read-modify-write at the end hits L2
+        if (g_live) {
+#pragma unroll
+            for (int p = 0; p < kK6Pairs; ++p) {
+                if (!pv[p])
+                    continue;
+                const int jt = ft + bt[p];
+                const long long gj =
+                    (long long)jt * d.ns + (el.fv + bs[p] / (d.pu + 1)) * d.nu + el.fu + bs[p] % (d.pu + 1);
+                for (int side = 0; side < 2; ++side) {
+                    const bool row = side == 0 ? gi >= d.f0 && gi < d.f1
+                                               : sym && al != be0 + p && gj >= d.f0 && gj < d.f1;
+                    if (!row)
+                        continue;
+                    long long LtB;
+                    const long long pos = side ? k6_pos(d, el, bs[p], as, jt, it, pre0, LtB)
+                                               : k6_pos(d, el, as, bs[p], it, jt, pre0, LtB);
+#pragma unroll
+                    for (int a = 0; a < 3; ++a)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(values + pos + a * LtB));
+                }
+            }
+        }
+#endif
         for (int c = c0; c < c1; ++c) {
             __syncthreads();
             const int cfg = d.layer_config[d.cell_layer[c]];
@@ -532,8 +581,6 @@ __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard(const DevTables d,
         }
         if (!g_live)
             continue;
-        const int it = ft + at;
-        const long long gi = (long long)it * d.ns + (el.fv + as / (d.pu + 1)) * d.nu + el.fu + as % (d.pu + 1);
 #pragma unroll
         for (int p = 0; p < kK6Pairs; ++p) {
             if (!pv[p])
@@ -550,24 +597,15 @@ __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard(const DevTables d,
             for (int side = 0; side < 2; ++side) {
                 if (side == 0 ? !row_i : !row_j)
                     continue;
-                const int ls = side ? bs[p] : as, ms = side ? as : bs[p];
-                const int rt = side ? jt : it, ct_ = side ? it : jt;
-                const int iu = el.fu + ls % (d.pu + 1), iv = el.fv + ls / (d.pu + 1);
-                const int ju = el.fu + ms % (d.pu + 1), jv = el.fv + ms / (d.pu + 1);
-                const int is = iv * d.nu + iu;
-                const int Lu = d.len_u[iu], Lv = d.len_v[iv];
-                const int B = 3 * Lu * Lv;
-                const int slot = (jv - d.lo_v[iv]) * Lu + (ju - d.lo_u[iu]);
-                const int Lt = d.len_t[rt];
-                const long long pos = 9 * d.S_s * (d.pre_t[rt] - pre0) + (long long)Lt * d.es_pre[is] +
-                                      (long long)(ct_ - d.lo_t[rt]) * B + 3 * slot - d.out_base;
-                LF_CHECK(pos >= 0 && pos + 2LL * Lt * B + 2 < d.nnz_slab && ct_ >= d.lo_t[rt] &&
-                         ct_ < d.lo_t[rt] + Lt);
+                long long LtB;
+                const long long pos = side ? k6_pos(d, el, bs[p], as, jt, it, pre0, LtB)
+                                           : k6_pos(d, el, as, bs[p], it, jt, pre0, LtB);
+                LF_CHECK(pos >= 0 && pos + 2 * LtB + 2 < d.nnz_slab);
 #pragma unroll
                 for (int a = 0; a < 3; ++a)
 #pragma unroll
                     for (int b = 0; b < 3; ++b)
-                        values[pos + (long long)a * Lt * B + b] += side ? acc[p][3 * b + a] : acc[p][3 * a + b];
+                        values[pos + a * LtB + b] += side ? acc[p][3 * b + a] : acc[p][3 * a + b];
             }
         }
     }
