@@ -542,12 +542,21 @@ def measure_c5(args, device, rank, world, stream, hbm):
     b = lf.slab_bounds_functions(prob, world, rank) if world > 1 else {"f_begin": 0, "f_end": prob.n_s * prob.n_t}
     torch.cuda.empty_cache()
     free, _ = torch.cuda.mem_get_info()
+    free //= max(1, -(-world // max(1, torch.cuda.device_count())))  # ranks sharing a GPU (code-path runs)
     plan = lf.Plan(prob, "fast", device, stream=stream.cuda_stream, f_begin=b["f_begin"], f_end=b["f_end"])
     nnz = plan.nnz
     with_pattern = nnz * 12 + plan.rows * 8 <= int(0.85 * free)
-    if not with_pattern and nnz * 8 > int(0.9 * free):
+    fits = with_pattern or nnz * 8 <= int(0.9 * free)
+    if world > 1:  # every rank takes the same branch (the timing below has collectives)
+        import torch.distributed as dist
+        flags = torch.tensor([1.0 if fits else 0.0, 1.0 if with_pattern else 0.0], dtype=torch.float64)
+        if args.dist_backend == "nccl":
+            flags = flags.cuda()
+        dist.all_reduce(flags, op=dist.ReduceOp.MIN)
+        fits, with_pattern = bool(flags[0] > 0), bool(flags[1] > 0)
+    if not fits:
         plan.close()
-        return {"error": f"rank {rank}: the C5 slab's values ({nnz * 8 / 1e9:.0f} GB) do not fit"}
+        return {"error": f"the C5 slab's values ({nnz * 8 / 1e9:.0f} GB on rank {rank}) do not fit on every rank"}
     vals = torch.empty(nnz, dtype=torch.float64, device="cuda")
     rp = cols = None
     if with_pattern:
@@ -705,8 +714,17 @@ def measure_many_terms(args, prob, device, stream, hbm):
     return out
 
 
+def host_columns() -> bool:
+    """One-shot calls write the CSR columns on the host (lf_pattern_columns)
+    unless LAMFAST_HOST_COLS=0; then only row offsets and values cross PCIe."""
+    return os.environ.get("LAMFAST_HOST_COLS", "1") != "0"
+
+
 def measure_e2e(args, prob, device, total_nnz):
-    """lf_assemble (drop-in for assembleFast) with pinned host buffers."""
+    """lf_assemble (drop-in for assembleFast) with pinned host buffers.  The
+    columns are written by host threads while row offsets and values cross
+    PCIe (default); the same call with the device pattern copied over PCIe
+    (LAMFAST_HOST_COLS=0) is timed beside it."""
     import torch
     from paper_1905_05417_b200 import abi
     lib = abi.library()
@@ -721,38 +739,53 @@ def measure_e2e(args, prob, device, total_nnz):
         abi.check(lib.lf_assemble(ctypes.byref(c), abi.LF_BACKEND_FAST, device, rp.data_ptr(),
                                   cols.data_ptr(), vals.data_ptr(), ctypes.byref(st)))
 
-    once()  # warm-up (allocator pool, module load)
-    n = max(1, args.e2e_steps)
-    per = []
-    t0 = time.perf_counter()
-    for _ in range(n):
-        t1 = time.perf_counter()
-        once()
-        per.append(time.perf_counter() - t1)
-    sec = (time.perf_counter() - t0) / n
+    def timed(n):
+        once()  # warm-up (allocator pool, module load)
+        per = []
+        t0 = time.perf_counter()
+        for _ in range(n):
+            t1 = time.perf_counter()
+            once()
+            per.append(time.perf_counter() - t1)
+        return (time.perf_counter() - t0) / n, per
+
+    hc = host_columns()
+    sec, per = timed(max(1, args.e2e_steps))
+    alt = None
+    if hc:  # the device-pattern variant of the same call, for comparison
+        os.environ["LAMFAST_HOST_COLS"] = "0"
+        try:
+            alt_sec, _ = timed(2)
+            alt = {"ms_per_step": alt_sec * 1e3, "value": total_nnz / alt_sec,
+                   "d2h_bytes_per_step": rp.numel() * 8 + total_nnz * 12}
+        finally:
+            os.environ.pop("LAMFAST_HOST_COLS", None)
     h2d = sum(a.nbytes for a in prob._keep if hasattr(a, "nbytes"))
-    d2h = rp.numel() * 8 + total_nnz * 12
-    # the e2e roofline: a plain pinned D2H of the same three arrays on this box
+    d2h = rp.numel() * 8 + total_nnz * (8 if hc else 12)
+    # the e2e roofline: a plain pinned D2H of the arrays that cross PCIe
     # (device tensors of the CSR's sizes into the same pinned buffers), after
     # the timed region, best of 2
     dev = f"cuda:{device}"
-    srcs = [torch.empty_like(rp, device=dev), torch.empty_like(cols, device=dev),
-            torch.empty_like(vals, device=dev)]
+    hosts = (rp, vals) if hc else (rp, cols, vals)
+    srcs = [torch.empty_like(h, device=dev) for h in hosts]
     best = 0.0
     for _ in range(2):
         torch.cuda.synchronize()
         t1 = time.perf_counter()
-        for h, dsrc in zip((rp, cols, vals), srcs):
+        for h, dsrc in zip(hosts, srcs):
             h.copy_(dsrc)
         torch.cuda.synchronize()
         best = max(best, d2h / (time.perf_counter() - t1) / 1e9)
-    del rp, cols, vals, srcs
+    del rp, cols, vals, srcs, hosts
     return {"value": total_nnz / sec, "unit": "nnz/s", "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "ms_per_step": sec * 1e3, "steps": n,
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": sec * 1e3, "steps": len(per),
             "call": "lf_assemble(LF_BACKEND_FAST) -> host CSR (row_ptr, cols, values)",
+            "columns": "written on the host (closed form, lf_pattern_columns) while row offsets and values "
+                       "cross PCIe" if hc else "device pattern copied over PCIe",
             "ms_median": statistics.median(per) * 1e3,
-            "d2h_gbs_measured": best, "d2h_probe": "plain pinned D2H of the same arrays, best of 2",
-            "pcie_frac": (d2h / sec / 1e9) / best if best else None}
+            "d2h_gbs_measured": best, "d2h_probe": "plain pinned D2H of the arrays that cross PCIe, best of 2",
+            "pcie_frac": (d2h / sec / 1e9) / best if best else None,
+            "device_columns": alt}
 
 
 def measure_e2e_slab(args, prob, device, rank, world, bounds, total_nnz):
@@ -796,7 +829,7 @@ def measure_e2e_slab(args, prob, device, rank, world, bounds, total_nnz):
     dist.all_reduce(dt, op=dist.ReduceOp.MAX)
     sec = float(dt[0])
     h2d = sum(a.nbytes for a in prob._keep if hasattr(a, "nbytes"))
-    d2h = torch.tensor([float((rows + 1) * 8 + nnz * 12)], dtype=torch.float64)
+    d2h = torch.tensor([float((rows + 1) * 8 + nnz * (8 if host_columns() else 12))], dtype=torch.float64)
     if args.dist_backend == "nccl":
         d2h = d2h.cuda()
     dist.all_reduce(d2h)

@@ -160,6 +160,14 @@ int lf_layup_configs(const lf_problem* p, int32_t* n_configs, int32_t* layer_con
  * produced by `backend` (the standard backend drops thickness spans whose
  * cells are all masked by active_layers, assembly.cpp:184-186). */
 int lf_pattern_size(const lf_problem* p, int backend, int64_t* dim, int64_t* nnz);
+/* Column indices of the CSR rows of the functions [f_begin, f_end) (rows
+ * 3 f_begin .. 3 f_end; f_end < 0: to the end), written on the host into
+ * cols[0 .. *nnz) -- the same closed form k_pattern_cols writes on the device
+ * (the column half of SparseMatrixBuilder::finalize, sparse.cpp:30-55).
+ * cols == NULL: only *nnz.  One-shot calls into host arrays use it so that
+ * the columns do not cross PCIe.  Host-only: no device is needed. */
+int lf_pattern_columns(const lf_problem* p, int backend, int64_t f_begin, int64_t f_end, int32_t* cols,
+                       int64_t* nnz);
 /* Row slab `part` of `n_parts`, cut at thickness-function boundaries and
  * balanced by nnz.  Rows [row_begin, row_end) hold entries
  * [nnz_begin, nnz_end) of the global CSR. */

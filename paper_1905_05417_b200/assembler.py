@@ -60,6 +60,19 @@ def pattern_size(prob: LaminateProblem, backend: str = "fast") -> Tuple[int, int
     return dim.value, nnz.value
 
 
+def pattern_columns(prob: LaminateProblem, f_begin: int = 0, f_end: int = -1, backend: str = "fast") -> np.ndarray:
+    """Host-written CSR columns of the functions [f_begin, f_end)
+    (lf_pattern_columns: the closed form k_pattern_cols writes on the device)."""
+    lib = abi.library()
+    c = prob.to_c()
+    n = c_int64()
+    abi.check(lib.lf_pattern_columns(byref(c), abi.BACKENDS[backend], f_begin, f_end, None, byref(n)))
+    cols = np.empty(max(1, n.value), dtype=np.int32)
+    abi.check(lib.lf_pattern_columns(byref(c), abi.BACKENDS[backend], f_begin, f_end,
+                                     cols.ctypes.data_as(POINTER(c_int32)), byref(n)))
+    return cols[:n.value]
+
+
 def slab_bounds(prob: LaminateProblem, n_parts: int, part: int, backend: str = "fast") -> dict:
     lib = abi.library()
     c = prob.to_c()

@@ -650,11 +650,71 @@ int lf_layup_configs(const lf_problem* p, int32_t* n_configs, int32_t* layer_con
     });
 }
 
+/// Whether one-shot calls into host arrays write the columns on the host
+/// (default) instead of building them on the device and copying them over
+/// PCIe.  The columns are a closed form of the adjacency tables (4 B/nnz, a
+/// third of the CSR); host threads write them into the destination while the
+/// values (8 B/nnz) and row offsets cross PCIe.  LAMFAST_HOST_COLS=0 restores
+/// the device pattern (A/B runs, tests).
+static bool host_columns_enabled() {
+    const char* e = std::getenv("LAMFAST_HOST_COLS");
+    return !(e && e[0] == '0');
+}
+
+/// Host threads writing the columns of the functions [f0, f1) into `cols`
+/// (offset 0 = the first entry of f0), cut into equal-nnz pieces.
+struct HostColumns {
+    std::vector<std::thread> th;
+    HostColumns(const lfb::Setup& s, int64_t f0, int64_t f1, int32_t* cols) {
+        const int64_t base = lfb::functionOffset(s, f0), total = lfb::functionOffset(s, f1) - base;
+        const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        const unsigned nt = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(hw, total >> 22)));
+        std::vector<int64_t> cut{f0};
+        for (unsigned t = 1; t < nt; ++t) { // first function whose offset reaches t/nt of the entries
+            const int64_t target = base + total * t / nt;
+            int64_t lo = cut.back(), hi = f1;
+            while (lo < hi) {
+                const int64_t mid = lo + (hi - lo) / 2;
+                if (lfb::functionOffset(s, mid) < target)
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+            cut.push_back(lo);
+        }
+        cut.push_back(f1);
+        for (unsigned t = 0; t < nt; ++t) {
+            const int64_t a = cut[t], b = cut[t + 1];
+            if (a < b)
+                th.emplace_back([&s, a, b, cols, base] { lfb::fillColumns(s, a, b, cols + (lfb::functionOffset(s, a) - base)); });
+        }
+    }
+    void join() {
+        for (auto& x : th)
+            if (x.joinable())
+                x.join();
+    }
+    ~HostColumns() { join(); }
+};
+
 int lf_pattern_size(const lf_problem* p, int backend, int64_t* dim, int64_t* nnz) {
     return guarded([&] {
         const lfb::Setup s = lfb::buildSetup(*p, backend, 0, -1);
         *dim = 3LL * s.n_s * s.n_t;
         *nnz = s.nnz;
+    });
+}
+
+int lf_pattern_columns(const lf_problem* p, int backend, int64_t f_begin, int64_t f_end, int32_t* cols,
+                       int64_t* nnz) {
+    return guarded([&] {
+        if (!p || !nnz)
+            raise(LF_ERR_INVALID_ARGUMENT, "lf_pattern_columns: null argument");
+        const lfb::Setup s = lfb::buildSetup(*p, backend, 0, -1);
+        const lfb::Range r = lfb::rangeOf(s, f_begin, f_end);
+        *nnz = r.nnz;
+        if (cols)
+            HostColumns(s, r.f0, r.f1, cols).join();
     });
 }
 
@@ -924,7 +984,9 @@ static void run_one_shot(lf_plan& plan, OneShotStreams& st, int64_t chunk_nnz, c
         max_rows = std::max(max_rows, rg[k].rows);
         max_nnz = std::max(max_nnz, rg[k].nnz);
     }
-    const bool staged = out.sink || !(is_pinned(out.row_ptr) && is_pinned(out.cols) && is_pinned(out.values));
+    const bool host_cols = !out.sink && host_columns_enabled();
+    const bool staged =
+        out.sink || !(is_pinned(out.row_ptr) && (host_cols || is_pinned(out.cols)) && is_pinned(out.values));
     // device slots (two only when there is more than one chunk)
     const int nslot = K > 1 ? 2 : 1;
     const std::size_t rp_bytes = sizeof(int64_t) * static_cast<std::size_t>(max_rows + 1);
@@ -933,7 +995,7 @@ static void run_one_shot(lf_plan& plan, OneShotStreams& st, int64_t chunk_nnz, c
     std::vector<std::unique_ptr<DeviceBuffer>> drp, dcols, dvals;
     for (int b = 0; b < nslot; ++b) {
         drp.push_back(std::make_unique<DeviceBuffer>(rp_bytes, plan.stream));
-        dcols.push_back(std::make_unique<DeviceBuffer>(col_bytes, plan.stream));
+        dcols.push_back(std::make_unique<DeviceBuffer>(host_cols ? sizeof(int32_t) : col_bytes, plan.stream));
         dvals.push_back(std::make_unique<DeviceBuffer>(val_bytes, plan.stream));
     }
     // staging slot layout: values | columns | row offsets (8-byte aligned)
@@ -956,6 +1018,10 @@ static void run_one_shot(lf_plan& plan, OneShotStreams& st, int64_t chunk_nnz, c
     cudaEvent_t* ready = ev.e;    // [2] slot computed (plan stream)
     cudaEvent_t* drained = ev.e + 2; // [2] slot copied out (side stream)
     cudaStream_t cs = plan.stream, xs = st.side;
+    // columns on the host, concurrently with the whole device pipeline
+    std::unique_ptr<HostColumns> hc;
+    if (host_cols)
+        hc = std::make_unique<HostColumns>(s, s.f0, s.f1, out.cols);
     plan_prepare(&plan, cs);
     auto finish = [&](std::size_t j) { // host side of chunk j (staged only)
         const int b = static_cast<int>(j % 2);
@@ -972,9 +1038,13 @@ static void run_one_shot(lf_plan& plan, OneShotStreams& st, int64_t chunk_nnz, c
         }
         const std::size_t ro = static_cast<std::size_t>(r.row_begin - s.row_begin);
         const std::size_t zo = static_cast<std::size_t>(r.nnz_begin - s.nnz_begin);
-        parallel_copy({{out.values + zo, v, sizeof(double) * static_cast<std::size_t>(r.nnz)},
-                       {out.cols + zo, c, sizeof(int32_t) * static_cast<std::size_t>(r.nnz)},
-                       {out.row_ptr + ro, rp, sizeof(int64_t) * static_cast<std::size_t>(r.rows + 1)}});
+        if (host_cols)
+            parallel_copy({{out.values + zo, v, sizeof(double) * static_cast<std::size_t>(r.nnz)},
+                           {out.row_ptr + ro, rp, sizeof(int64_t) * static_cast<std::size_t>(r.rows + 1)}});
+        else
+            parallel_copy({{out.values + zo, v, sizeof(double) * static_cast<std::size_t>(r.nnz)},
+                           {out.cols + zo, c, sizeof(int32_t) * static_cast<std::size_t>(r.nnz)},
+                           {out.row_ptr + ro, rp, sizeof(int64_t) * static_cast<std::size_t>(r.rows + 1)}});
     };
     for (std::size_t k = 0; k < K; ++k) {
         const int b = static_cast<int>(k % 2);
@@ -987,7 +1057,7 @@ static void run_one_shot(lf_plan& plan, OneShotStreams& st, int64_t chunk_nnz, c
         auto* rpd = static_cast<long long*>(drp[static_cast<std::size_t>(b % nslot)]->p);
         auto* cd = static_cast<int*>(dcols[static_cast<std::size_t>(b % nslot)]->p);
         auto* vd = static_cast<double*>(dvals[static_cast<std::size_t>(b % nslot)]->p);
-        CK(static_cast<cudaError_t>(lfb::launch_pattern(d, rpd, cd, cs)));
+        CK(static_cast<cudaError_t>(lfb::launch_pattern(d, rpd, host_cols ? nullptr : cd, cs)));
         if (r.nnz > 0)
             plan_values(&plan, d, vd, cs);
         CK(cudaEventRecord(ready[b], cs));
@@ -996,13 +1066,15 @@ static void run_one_shot(lf_plan& plan, OneShotStreams& st, int64_t chunk_nnz, c
         if (staged) {
             char* base = static_cast<char*>(stg->slot[b]);
             copy_d2h(base, vd, sizeof(double) * nv, xs);
-            copy_d2h(base + so_cols, cd, sizeof(int32_t) * nv, xs);
+            if (!host_cols)
+                copy_d2h(base + so_cols, cd, sizeof(int32_t) * nv, xs);
             copy_d2h(base + so_rp, rpd, sizeof(int64_t) * nr, xs);
         } else {
             const std::size_t ro = static_cast<std::size_t>(r.row_begin - s.row_begin);
             const std::size_t zo = static_cast<std::size_t>(r.nnz_begin - s.nnz_begin);
             copy_d2h(out.values + zo, vd, sizeof(double) * nv, xs);
-            copy_d2h(out.cols + zo, cd, sizeof(int32_t) * nv, xs);
+            if (!host_cols)
+                copy_d2h(out.cols + zo, cd, sizeof(int32_t) * nv, xs);
             copy_d2h(out.row_ptr + ro, rpd, sizeof(int64_t) * nr, xs);
         }
         CK(cudaEventRecord(drained[b], xs));
@@ -1013,6 +1085,8 @@ static void run_one_shot(lf_plan& plan, OneShotStreams& st, int64_t chunk_nnz, c
         finish(K - 1);
     CK(cudaStreamSynchronize(xs));
     CK(cudaStreamSynchronize(cs));
+    if (hc)
+        hc->join();
     CK(cudaGetLastError());
 }
 

@@ -1059,7 +1059,7 @@ int launch_pattern(const DevTables& d, long long* row_ptr, int* cols, cudaStream
     if (d.E >= (1LL << 31))
         return (int)cudaErrorInvalidValue; // in-plane entry space beyond 32-bit offsets
     k_pattern_rows<<<(unsigned)((rows + 1 + 255) / 256), 256, 0, stream>>>(d, row_ptr, rows);
-    if (d.E > 0 && d.t1 > d.t0) {
+    if (cols && d.E > 0 && d.t1 > d.t0) { // cols == nullptr: row offsets only
         const int nt = d.t1 - d.t0;
         auto launch = [&](auto kern, int ept) {
             const long long nblk = (d.E + (long long)kBlock * ept - 1) / ((long long)kBlock * ept);

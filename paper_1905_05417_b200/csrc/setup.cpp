@@ -608,6 +608,27 @@ int64_t functionOffset(const Setup& s, int64_t f) {
            static_cast<int64_t>(s.at.len[static_cast<std::size_t>(t)]) * s.es_pre[static_cast<std::size_t>(is)];
 }
 
+void fillColumns(const Setup& s, int64_t f_lo, int64_t f_hi, int32_t* cols) {
+    // row block of function f = (i_t, i_s): rows a = 0..2, each L_t segments
+    // (neighbour j_t) of 3 L_s columns ordered (j_s, b); for a
+    // fixed (a, j_t, j_v) the 3 L_u columns are consecutive integers
+    const int nu = s.n_u, ns = s.n_s;
+    for (int64_t f = f_lo; f < f_hi; ++f) {
+        const int it = static_cast<int>(f / ns), is = static_cast<int>(f % ns);
+        const int iu = is % nu, iv = is / nu;
+        const int Lt = s.at.len[static_cast<std::size_t>(it)], lot = s.at.lo[static_cast<std::size_t>(it)];
+        const int Lu = s.au.len[static_cast<std::size_t>(iu)], lou = s.au.lo[static_cast<std::size_t>(iu)];
+        const int Lv = s.av.len[static_cast<std::size_t>(iv)], lov = s.av.lo[static_cast<std::size_t>(iv)];
+        for (int a = 0; a < 3; ++a)
+            for (int k = 0; k < Lt; ++k)
+                for (int sv = 0; sv < Lv; ++sv) {
+                    const int32_t c0 = 3 * ((lot + k) * ns + (lov + sv) * nu + lou);
+                    for (int i = 0; i < 3 * Lu; ++i)
+                        *cols++ = c0 + i;
+                }
+    }
+}
+
 Range rangeOf(const Setup& s, int64_t f0, int64_t f1) {
     const int64_t F = static_cast<int64_t>(s.n_t) * s.n_s;
     if (f1 < 0)

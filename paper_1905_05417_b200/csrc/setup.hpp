@@ -159,6 +159,10 @@ void applyRange(Setup& s, int64_t f0, int64_t f1);
 /// Global CSR offset of the first entry of function f (f = n_t * n_s: nnz).
 int64_t functionOffset(const Setup& s, int64_t f);
 
+/// Host writer of the closed-form CSR columns of the functions [f_lo, f_hi)
+/// (the same pattern k_pattern_cols writes), into cols[0 ..).
+void fillColumns(const Setup& s, int64_t f_lo, int64_t f_hi, int32_t* cols);
+
 /// Space-only setup (knots, spans, quadrature, adjacency) used by the
 /// operator-level entry points.
 Setup buildSpaceSetup(const lf_problem& p, bool need_geometry);

@@ -75,9 +75,13 @@ def test_function_range_plans_are_rows_of_the_full_matrix(gpu, oracle, backend, 
             assert_csr_match(got, _oracle_rows(oracle, prob, backend, f0, f1), RTOL)
 
 
-def test_function_range_one_shot_and_balanced_bounds(gpu):
+@pytest.mark.parametrize("host_cols", ["1", "0"])
+def test_function_range_one_shot_and_balanced_bounds(gpu, monkeypatch, host_cols):
     """lf_assemble_range equals the plan's rows, and lf_slab_bounds_functions'
-    parts tile the matrix with nnz balanced to within one function."""
+    parts tile the matrix with nnz balanced to within one function; with the
+    columns written on the host (default) and copied from the device pattern
+    (LAMFAST_HOST_COLS=0)."""
+    monkeypatch.setenv("LAMFAST_HOST_COLS", host_cols)
     prob = P.baseline_config("C2")
     full = gpu.assemble_fast(prob).astuple()
     parts = 5
@@ -147,11 +151,14 @@ def test_stream_sink_abort_is_reported(gpu):
 
 
 @pytest.mark.slow
-def test_c4_one_shot_chunked_into_pageable_host_memory(gpu):
+@pytest.mark.parametrize("host_cols", ["1", "0"])
+def test_c4_one_shot_chunked_into_pageable_host_memory(gpu, monkeypatch, host_cols):
     """Full C4 (1.92e9 nnz, 23 GB: 12 chunks of <= 2 GiB) through lf_assemble
     into pageable numpy arrays (staged through pinned buffers by host
-    threads) equals the device-resident plan's CSR bitwise."""
+    threads) equals the device-resident plan's CSR bitwise: with the columns
+    written by host threads (default) and with the device pattern copied."""
     import torch
+    monkeypatch.setenv("LAMFAST_HOST_COLS", host_cols)
     prob = P.baseline_config("C4")
     got = gpu.assemble_fast(prob)
     plan = gpu.Plan(prob, "fast", 0)

@@ -218,3 +218,30 @@ def test_function_slab_bounds_balance_and_oracle_offsets(oracle, name, parts):
     if name == "C5":
         assert max(nnz) / (sum(nnz) / parts) <= 1.000001
     terms.close()
+
+
+@pytest.mark.parametrize("case", ["C1", "C2", "mixed", "masked-standard", "range"])
+def test_host_pattern_columns_match_oracle(oracle, case):
+    """lf_pattern_columns (host-written closed-form columns, what one-shot
+    calls into host arrays use instead of copying the device pattern) equals
+    the oracle's CSR columns, bit for bit."""
+    backend, f0, f1 = "fast", 0, -1
+    if case in ("C1", "C2"):
+        prob = P.baseline_config(case)
+    elif case == "mixed":
+        prob = P.LaminateProblem(
+            degree_u=2, degree_v=3, degree_t=2, knots_u=P.uniform_knots(2, 3), knots_v=P.uniform_knots(3, 2),
+            knots_t=P.c0_knots(2, 3), interfaces=P.equal_interfaces(3),
+            layers=[(P.baseline_orthotropic(), 0.0), (P.isotropic(0.5, 0.3), 0.0), (P.baseline_orthotropic(), 0.6)])
+    elif case == "masked-standard":
+        prob, backend = P.baseline_config("C1").replace(active_layers=[0, 3]), "standard"
+    else:
+        prob = P.baseline_config("C2")
+        f0, f1 = prob.n_s + 5, 4 * prob.n_s - 7
+    rp, cols, _ = oracle.assemble(prob, backend)
+    got = lf.pattern_columns(prob, f0, f1, backend)
+    if f1 < 0:
+        want = cols
+    else:
+        want = cols[rp[3 * f0]:rp[3 * f1]]
+    assert got.dtype == np.int32 and np.array_equal(got, want)
