@@ -600,11 +600,12 @@ def measure_stream_e2e(prob, device, total_nnz):
     from paper_1905_05417_b200 import abi
     lib = abi.library()
     c = prob.to_c()
-    acc = {"sum": 0.0, "chunks": 0, "bytes": 0}
+    acc = {"sum": 0.0, "chunks": 0, "bytes": 0, "pcie": 0}
 
     def sink(_u, row_begin, rows, nnz_begin, nnz, rp, cols, vals):
         acc["chunks"] += 1
         acc["bytes"] += (rows + 1) * 8 + nnz * 12
+        acc["pcie"] += (rows + 1) * 8 + nnz * (8 if host_columns() else 12)
         acc["sum"] += float(np.ctypeslib.as_array(vals, shape=(nnz,))[::4096].sum()) if nnz else 0.0
         return 0
 
@@ -612,14 +613,17 @@ def measure_stream_e2e(prob, device, total_nnz):
     st = abi.Stats()
     times = []
     for _ in range(2):
-        acc.update(sum=0.0, chunks=0, bytes=0)
+        acc.update(sum=0.0, chunks=0, bytes=0, pcie=0)
         t0 = time.perf_counter()
         abi.check(lib.lf_assemble_stream(ctypes.byref(c), abi.LF_BACKEND_FAST, device, 0,
                                          ctypes.cast(fn, ctypes.c_void_p), None, ctypes.byref(st)))
         times.append(time.perf_counter() - t0)
     sec = times[-1]
     return {"value": total_nnz / sec, "unit": "nnz/s", "ms": sec * 1e3, "chunks": acc["chunks"],
-            "d2h_bytes": acc["bytes"], "d2h_gbs": acc["bytes"] / sec / 1e9, "warmup_ms": times[0] * 1e3,
+            "csr_bytes": acc["bytes"], "d2h_bytes": acc["pcie"], "d2h_gbs": acc["pcie"] / sec / 1e9,
+            "warmup_ms": times[0] * 1e3,
+            "columns": "written on the host per chunk into the staging slot while its values cross PCIe"
+                       if host_columns() else "device pattern copied over PCIe",
             "call": "lf_assemble_stream(LF_BACKEND_FAST) -> pinned host staging -> sink (sampled sum)"}
 
 

@@ -984,7 +984,7 @@ static void run_one_shot(lf_plan& plan, OneShotStreams& st, int64_t chunk_nnz, c
         max_rows = std::max(max_rows, rg[k].rows);
         max_nnz = std::max(max_nnz, rg[k].nnz);
     }
-    const bool host_cols = !out.sink && host_columns_enabled();
+    const bool host_cols = host_columns_enabled();
     const bool staged =
         out.sink || !(is_pinned(out.row_ptr) && (host_cols || is_pinned(out.cols)) && is_pinned(out.values));
     // device slots (two only when there is more than one chunk)
@@ -1018,9 +1018,11 @@ static void run_one_shot(lf_plan& plan, OneShotStreams& st, int64_t chunk_nnz, c
     cudaEvent_t* ready = ev.e;    // [2] slot computed (plan stream)
     cudaEvent_t* drained = ev.e + 2; // [2] slot copied out (side stream)
     cudaStream_t cs = plan.stream, xs = st.side;
-    // columns on the host, concurrently with the whole device pipeline
-    std::unique_ptr<HostColumns> hc;
-    if (host_cols)
+    // columns on the host, concurrently with the whole device pipeline (host
+    // arrays), or per chunk into the staging slot while the chunk's values
+    // cross PCIe (sinks)
+    std::unique_ptr<HostColumns> hc, slot_hc[2];
+    if (host_cols && !out.sink)
         hc = std::make_unique<HostColumns>(s, s.f0, s.f1, out.cols);
     plan_prepare(&plan, cs);
     auto finish = [&](std::size_t j) { // host side of chunk j (staged only)
@@ -1031,6 +1033,8 @@ static void run_one_shot(lf_plan& plan, OneShotStreams& st, int64_t chunk_nnz, c
         const double* v = reinterpret_cast<const double*>(base);
         const int32_t* c = reinterpret_cast<const int32_t*>(base + so_cols);
         const int64_t* rp = reinterpret_cast<const int64_t*>(base + so_rp);
+        if (slot_hc[b])
+            slot_hc[b]->join();
         if (out.sink) {
             if (out.sink(out.user, r.row_begin, r.rows, r.nnz_begin, r.nnz, rp, c, v) != 0)
                 raise(LF_ERR_RUNTIME, "lf_assemble_stream: the chunk sink aborted the assembly");
@@ -1078,6 +1082,9 @@ static void run_one_shot(lf_plan& plan, OneShotStreams& st, int64_t chunk_nnz, c
             copy_d2h(out.row_ptr + ro, rpd, sizeof(int64_t) * nr, xs);
         }
         CK(cudaEventRecord(drained[b], xs));
+        if (host_cols && out.sink) // this chunk's columns, into its staging slot, while its values cross PCIe
+            slot_hc[b] = std::make_unique<HostColumns>(s, r.f0, r.f1,
+                                                       reinterpret_cast<int32_t*>(static_cast<char*>(stg->slot[b]) + so_cols));
         if (staged && k >= 1)
             finish(k - 1);
     }

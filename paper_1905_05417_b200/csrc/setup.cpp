@@ -2,6 +2,10 @@
 // /root/reference/proj.
 #include "setup.hpp"
 
+#if defined(__SSE2__)
+#include <immintrin.h>
+#endif
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -608,11 +612,64 @@ int64_t functionOffset(const Setup& s, int64_t f) {
            static_cast<int64_t>(s.at.len[static_cast<std::size_t>(t)]) * s.es_pre[static_cast<std::size_t>(is)];
 }
 
+namespace {
+
+/// Streaming writer of consecutive int32 runs: 16-byte non-temporal stores
+/// (no read-for-ownership of the destination lines, which would double the
+/// host memory traffic while the values' DMA is writing the same memory).
+struct ColumnWriter {
+    int32_t* p;
+    alignas(16) int32_t buf[4];
+    int n = 0;
+    explicit ColumnWriter(int32_t* dst) : p(dst) {}
+    void put(int32_t v) {
+#if defined(__SSE2__)
+        if (n == 0 && (reinterpret_cast<std::uintptr_t>(p) & 15) != 0) { // head: align the destination
+            *p++ = v;
+            return;
+        }
+        buf[n++] = v;
+        if (n == 4) {
+            _mm_stream_si128(reinterpret_cast<__m128i*>(p), _mm_load_si128(reinterpret_cast<const __m128i*>(buf)));
+            p += 4;
+            n = 0;
+        }
+#else
+        *p++ = v;
+#endif
+    }
+    /// c0, c0 + 1, ..., c0 + len - 1
+    void run(int32_t c0, int len) {
+#if defined(__SSE2__)
+        while (len > 0 && (n != 0 || (reinterpret_cast<std::uintptr_t>(p) & 15) != 0)) {
+            put(c0++);
+            --len;
+        }
+        const __m128i step = _mm_set_epi32(3, 2, 1, 0);
+        for (; len >= 4; len -= 4, c0 += 4, p += 4)
+            _mm_stream_si128(reinterpret_cast<__m128i*>(p), _mm_add_epi32(_mm_set1_epi32(c0), step));
+#endif
+        for (; len > 0; --len)
+            put(c0++);
+    }
+    void finish() {
+        for (int i = 0; i < n; ++i)
+            *p++ = buf[i];
+        n = 0;
+#if defined(__SSE2__)
+        _mm_sfence();
+#endif
+    }
+};
+
+} // namespace
+
 void fillColumns(const Setup& s, int64_t f_lo, int64_t f_hi, int32_t* cols) {
     // row block of function f = (i_t, i_s): rows a = 0..2, each L_t segments
     // (neighbour j_t) of 3 L_s columns ordered (j_s, b); for a
     // fixed (a, j_t, j_v) the 3 L_u columns are consecutive integers
     const int nu = s.n_u, ns = s.n_s;
+    ColumnWriter w(cols);
     for (int64_t f = f_lo; f < f_hi; ++f) {
         const int it = static_cast<int>(f / ns), is = static_cast<int>(f % ns);
         const int iu = is % nu, iv = is / nu;
@@ -621,12 +678,10 @@ void fillColumns(const Setup& s, int64_t f_lo, int64_t f_hi, int32_t* cols) {
         const int Lv = s.av.len[static_cast<std::size_t>(iv)], lov = s.av.lo[static_cast<std::size_t>(iv)];
         for (int a = 0; a < 3; ++a)
             for (int k = 0; k < Lt; ++k)
-                for (int sv = 0; sv < Lv; ++sv) {
-                    const int32_t c0 = 3 * ((lot + k) * ns + (lov + sv) * nu + lou);
-                    for (int i = 0; i < 3 * Lu; ++i)
-                        *cols++ = c0 + i;
-                }
+                for (int sv = 0; sv < Lv; ++sv)
+                    w.run(3 * ((lot + k) * ns + (lov + sv) * nu + lou), 3 * Lu);
     }
+    w.finish();
 }
 
 Range rangeOf(const Setup& s, int64_t f0, int64_t f1) {

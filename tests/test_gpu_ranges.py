@@ -102,13 +102,19 @@ def test_function_range_one_shot_and_balanced_bounds(gpu, monkeypatch, host_cols
 
 
 @pytest.mark.parametrize("backend", ["fast", "standard"])
-def test_streamed_chunks_equal_one_shot(gpu, backend):
+@pytest.mark.parametrize("host_cols", ["1", "0"])
+def test_streamed_chunks_equal_one_shot(gpu, monkeypatch, backend, host_cols):
     """lf_assemble_stream with small chunks (many chunks, chunk edges inside
     thickness rows) delivers, in row order, exactly the one-shot CSR; the
-    pinned and pageable destinations of lf_assemble give the same arrays."""
+    pinned and pageable destinations of lf_assemble give the same arrays.
+    Columns written by host threads (per chunk into the staging slot for the
+    sink) and copied from the device pattern (LAMFAST_HOST_COLS=0); the
+    reference CSR comes from the device-pattern path."""
     import torch
     prob = P.baseline_config("C2")
+    monkeypatch.setenv("LAMFAST_HOST_COLS", "0")
     want = gpu.assemble_with(backend, prob).astuple()
+    monkeypatch.setenv("LAMFAST_HOST_COLS", host_cols)
     got_rp, got_c, got_v = [np.zeros(1, np.int64)], [], []
     seen = {"rows": 0, "nnz": 0, "chunks": 0}
 
