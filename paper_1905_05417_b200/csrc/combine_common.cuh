@@ -149,6 +149,9 @@ __device__ __forceinline__ void combine_row_k(const double (&P)[EPT][NT][4], WP 
                                               unsigned mask, const unsigned char* __restrict__ kr,
                                               double* const (&o)[EPT], const int (&B)[EPT], const bool (&live)[EPT]) {
     int klo[NT], khi[NT];
+#ifdef LF_STORE_ONLY
+    mask = 0; // diagnostic build: identical store pattern, no weight loads / FMAs
+#endif
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
         klo[t] = (mask & (1u << t)) ? kr[2 * t] : LT;
@@ -229,6 +232,9 @@ template <int NT, int EPT, int LT, typename WP = const double4*>
 __device__ __forceinline__ bool row_masked(unsigned mask, const double (&P)[EPT][NT][4],
                                            WP w, double* const (&o)[EPT],
                                            const int (&B)[EPT], const bool (&live)[EPT]) {
+#ifdef LF_STORE_ONLY
+    return false;
+#endif
     switch (mask) {
 #define LF_ROW_M(m)                                                  \
     case m:                                                          \

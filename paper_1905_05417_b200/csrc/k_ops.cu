@@ -171,7 +171,23 @@ __device__ __forceinline__ long long pe_local(int f, int al, int a, int be, int 
     return ((((long long)f * nl2 + al) * 3 + a) * nl2 + be) * 3 + b;
 }
 
-__global__ void k_inplane_elem(const DevTables d, int t0) {
+/// Phase 1: one block per (element, term); a thread takes one family f, one
+/// al and kK2bPairs consecutive be, so every broadcast load of a C~ row
+/// (warp-uniform f) feeds kK2bPairs x 9 FMA (the one-pair form loaded a row
+/// per 9 FMA: C3 1.10 ms, FP64 pipe 4%, profiles/r1_k2b.txt).
+#ifndef LF_K2B_PAIRS
+#define LF_K2B_PAIRS 4
+#endif
+#ifndef LF_K2B_MINB
+#define LF_K2B_MINB 2
+#endif
+constexpr int kK2bPairs = LF_K2B_PAIRS;
+
+__host__ __device__ inline int k2b_family_slots(int nl2) {
+    return (nl2 * ((nl2 + kK2bPairs - 1) / kK2bPairs) + 31) / 32 * 32;
+}
+
+__global__ void __launch_bounds__(256, LF_K2B_MINB) k_inplane_elem(const DevTables d, int t0) {
     extern __shared__ double sm[];
     const int e_index = blockIdx.x;
     const int t = t0 + blockIdx.y;
@@ -196,50 +212,67 @@ __global__ void k_inplane_elem(const DevTables d, int t0) {
     const int nel = d.nspu * d.nspv;
     const long long per_el = 36LL * el.nl2 * el.nl2;
     double* pe = d.Pe + ((long long)blockIdx.y * nel + e_index) * per_el;
-    const int npair = el.nl2 * el.nl2;
-    const int qstride = (npair + 31) & ~31;
-    for (int idx = threadIdx.x; idx < 4 * qstride; idx += blockDim.x) {
-        const int f = idx / qstride;
-        const int pr = idx - f * qstride;
-        if (pr >= npair)
+    const int ngroup = (el.nl2 + kK2bPairs - 1) / kK2bPairs;
+    const int fslots = k2b_family_slots(el.nl2);
+    for (int idx = threadIdx.x; idx < 4 * fslots; idx += blockDim.x) {
+        const int f = idx / fslots;
+        const int g = idx - f * fslots;
+        if (g >= el.nl2 * ngroup)
             continue;
-        const int al = pr / el.nl2, be = pr % el.nl2;
+        const int al = g / ngroup, be0 = (g - al * ngroup) * kK2bPairs;
         const int nxy = f == 0 ? 4 : f == 3 ? 1 : 2;
         int xys[4];
         xys[0] = f == 0 ? 0 : f == 1 ? 2 : f == 2 ? 6 : 8;
         xys[1] = f == 0 ? 1 : f == 1 ? 5 : 7;
         xys[2] = 3;
         xys[3] = 4;
-        double acc[9];
+        int bes[kK2bPairs];
 #pragma unroll
-        for (int k = 0; k < 9; ++k)
-            acc[k] = 0.0;
+        for (int p = 0; p < kK2bPairs; ++p)
+            bes[p] = min(be0 + p, el.nl2 - 1);
+        double acc[kK2bPairs][9];
+#pragma unroll
+        for (int p = 0; p < kK2bPairs; ++p)
+#pragma unroll
+            for (int k = 0; k < 9; ++k)
+                acc[p][k] = 0.0;
         for (int q = 0; q < el.nq2; ++q) {
             const double* ga = gh + (q * el.nl2 + al) * 3;
-            const double* gb = gh + (q * el.nl2 + be) * 3;
             const double* C = ctq + q * 90;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 if (u < nxy) {
                     const int xy = xys[u];
-                    const double sxy = ga[xy / 3] * gb[xy % 3];
+                    const double gx = ga[xy / 3];
                     const double2* C2 = reinterpret_cast<const double2*>(C + xy * 10);
+                    const double2 c0 = C2[0], c1 = C2[1], c2 = C2[2], c3 = C2[3], c4 = C2[4];
 #pragma unroll
-                    for (int h = 0; h < 5; ++h) {
-                        const double2 c = C2[h];
-                        acc[2 * h] += c.x * sxy;
-                        if (2 * h + 1 < 9)
-                            acc[2 * h + 1] += c.y * sxy;
+                    for (int p = 0; p < kK2bPairs; ++p) {
+                        const double sxy = gx * gh[(q * el.nl2 + bes[p]) * 3 + xy % 3];
+                        acc[p][0] = fma(c0.x, sxy, acc[p][0]);
+                        acc[p][1] = fma(c0.y, sxy, acc[p][1]);
+                        acc[p][2] = fma(c1.x, sxy, acc[p][2]);
+                        acc[p][3] = fma(c1.y, sxy, acc[p][3]);
+                        acc[p][4] = fma(c2.x, sxy, acc[p][4]);
+                        acc[p][5] = fma(c2.y, sxy, acc[p][5]);
+                        acc[p][6] = fma(c3.x, sxy, acc[p][6]);
+                        acc[p][7] = fma(c3.y, sxy, acc[p][7]);
+                        acc[p][8] = fma(c4.x, sxy, acc[p][8]);
                     }
                 }
             }
         }
-        LF_CHECK(pe_local(f, al, 2, be, 2, el.nl2) < per_el);
 #pragma unroll
-        for (int a = 0; a < 3; ++a)
+        for (int p = 0; p < kK2bPairs; ++p) {
+            if (be0 + p >= el.nl2)
+                continue;
+            LF_CHECK(pe_local(f, al, 2, be0 + p, 2, el.nl2) < per_el);
 #pragma unroll
-            for (int b = 0; b < 3; ++b)
-                pe[pe_local(f, al, a, be, b, el.nl2)] = acc[3 * a + b];
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b)
+                    pe[pe_local(f, al, a, be0 + p, b, el.nl2)] = acc[p][3 * a + b];
+        }
     }
 }
 
@@ -1030,7 +1063,7 @@ int launch_inplane_general(const DevTables& d, cudaStream_t stream) {
     // two-phase: element-local P (one launch per term batch), then the gather
     const int nl2 = (d.pu + 1) * (d.pv + 1), nq2 = d.nqu * d.nqv;
     const size_t smem = sizeof(double) * ((size_t)nq2 * nl2 * 3 + nq2 + 1 + (size_t)nq2 * 90);
-    const int threads = std::min(512, 4 * ((nl2 * nl2 + 31) / 32 * 32)); // one thread per (local pair, family)
+    const int threads = std::min(256, 4 * k2b_family_slots(nl2)); // one thread per (family, al, be group)
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_inplane_elem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const unsigned nel = (unsigned)(d.nspu * d.nspv);
