@@ -367,7 +367,8 @@ void set_range(const lfb::Range& r, lfb::DevTables& d) {
     d.nnz_slab = r.nnz;
 }
 
-void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void* stream, int64_t f0, int64_t f1) {
+void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void* stream, int64_t f0, int64_t f1,
+               bool want_values = true) {
     if (!p)
         raise(LF_ERR_INVALID_ARGUMENT, "null problem");
     plan->setup = lfb::buildSetupRange(*p, backend, f0, f1);
@@ -408,6 +409,22 @@ void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void
     d.w_t0 = s.t0;
     d.w_t1 = s.t1;
     d.n_pairs = s.n_pairs;
+    if (backend == LF_BACKEND_STANDARD) {
+        d.spt_first_h = s.spt_first.data();
+        if (want_values) {
+            // two-phase K6: element-local blocks of as many spans per batch as
+            // fit ~4 GB (or a fifth of the free memory), one span at least
+            const std::size_t nl3 = static_cast<std::size_t>(d.pu + 1) * (d.pv + 1) * (d.pt + 1);
+            const std::size_t per_blk = 9 * (d.sym ? nl3 * (nl3 + 1) / 2 : nl3 * nl3);
+            const std::size_t per_span = static_cast<std::size_t>(d.nspu) * d.nspv * per_blk * sizeof(double);
+            std::size_t free_b = 0, total_b = 0;
+            CK(cudaMemGetInfo(&free_b, &total_b));
+            const std::size_t budget = std::min<std::size_t>(std::size_t(4) << 30, free_b / 5);
+            d.ks_batch = static_cast<int>(std::max<std::size_t>(
+                1, std::min<std::size_t>(static_cast<std::size_t>(d.nspt), budget / std::max<std::size_t>(1, per_span))));
+            d.Ks = ar.alloc<double>(per_span / sizeof(double) * static_cast<std::size_t>(d.ks_batch));
+        }
+    }
     if (backend != LF_BACKEND_STANDARD) {
         d.W = ar.alloc<double>(static_cast<std::size_t>(std::max<long long>(1, d.n_pairs)) * d.n_terms * 4);
         d.Wmask = ar.alloc<unsigned>(static_cast<std::size_t>(std::max<long long>(1, d.n_pairs)) * d.n_passes);
@@ -1185,7 +1202,7 @@ int lf_reference_bilinear(const lf_problem* p, const double* v, const double* u,
         if (!p || !v || !u || !out)
             raise(LF_ERR_INVALID_ARGUMENT, "referenceBilinear: null argument");
         lf_plan plan;
-        plan_init(&plan, p, LF_BACKEND_STANDARD, device, nullptr, 0, -1);
+        plan_init(&plan, p, LF_BACKEND_STANDARD, device, nullptr, 0, -1, false);
         const lfb::DevTables& d = plan.d;
         const std::size_t n = 3 * static_cast<std::size_t>(plan.setup.n_s) * static_cast<std::size_t>(d.nt);
         const std::size_t nblk = static_cast<std::size_t>(d.nspu) * d.nspv * d.nspt;

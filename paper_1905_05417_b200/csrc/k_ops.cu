@@ -7,7 +7,8 @@
 //      k_inplane_gather   (fast.cpp:54-168 / voigt_free.cpp:142-248)
 //  (K4 k_combine, the hot kernel, is in k_combine.cu)
 //  K5  k_pattern_*        closed-form CSR row offsets and columns
-//  K6  k_standard         full 3D quadrature cross-check, coloured
+//  K6  k_standard_local + full 3D quadrature cross-check, two-phase
+//      k_standard_gather
 //                         (assembly.cpp:134-245)
 //  K7  verification       ||K||_F, K x, ||A-B||_F, ||K-K^T||_F (sparse.cpp:66-139)
 #include <cuda_runtime.h>
@@ -379,9 +380,8 @@ __global__ void k_inplane_gather(const DevTables d, int t0) {
 }
 
 // ---------------------------------------------------------------------------
-// K6: standard full-3D quadrature (assembly.cpp:134-245), one block per
-// (element, thickness span) of one colour, accumulated straight into the
-// precomputed CSR (the duplicate summation of sparse.cpp:30-55).
+// K6: standard full-3D quadrature (assembly.cpp:134-245), the reference's
+// element loop with its full in-plane quadrature, in two phases (below).
 //
 // The local block of a pair (al, be) = ((at, as), (bt, bs)) is
 //   K[ab] = sum_cells sum_q2 sum_q3 sum_xy Ct_q2[xy][ab] X_al[x] X_be[y] w3,
@@ -394,10 +394,12 @@ __global__ void k_inplane_gather(const DevTables d, int t0) {
 // thread takes a group of KP pairs sharing al (KP consecutive be), so every
 // broadcast load of a Ct row feeds KP x 9 FMA (ncu, the one-pair form: FP64
 // pipe 43%, shared-memory loads as the second stall; profiles/r1_ncu_standard_c3.txt).
-// Measured (profiles/r2_k6_ab.txt, C3 / C4 ms): one pair per thread 87 / 88;
-// KP = 2 at <= 128 registers (16 warps/SM) 78 / 85; KP = 3, 4 at 197-228
-// registers (8 warps/SM) 120-136 / 183-200 -- the += into the CSR needs the
-// warps to hide its load latency.
+// Measured (C3 / C4 ms, profiles/r2_k6_*.txt): round 1 (one pair per thread,
+// q3 loop, 48 coloured launches of += into the CSR) 87 / 88; tau + KP = 2,
+// coloured, 78 / 85 (KP = 3, 4 at 197-228 registers: 120-200, the += needs
+// warps to hide its loads), + L2 prefetch of the += targets 76.5 / 81.5;
+// two-phase 62.6 / 82.0, with the pair-symmetric gather (every stored block
+// read once) 60.1 / 80.7 (KP = 3, 4 at 8 warps/SM: 76-78 / 99-106).
 #ifndef LF_K6_MINB
 #define LF_K6_MINB 2
 #endif
@@ -434,42 +436,32 @@ __host__ __device__ inline int k6_groups(int nl3, bool sym) {
     return n;
 }
 
-/// CSR position of value (0, 0) of block K(i, j), i = (rt, local in-plane ls),
-/// j = (ct, local ms), of an element; value (a, b) is at + a Lt B + b.
-__device__ __forceinline__ long long k6_pos(const DevTables& d, const ElemInfo& el, int ls, int ms, int rt, int ct,
-                                            long long pre0, long long& LtB) {
-    const int iu = el.fu + ls % (d.pu + 1), iv = el.fv + ls / (d.pu + 1);
-    const int ju = el.fu + ms % (d.pu + 1), jv = el.fv + ms / (d.pu + 1);
-    const int is = iv * d.nu + iu;
-    const int Lu = d.len_u[iu], Lv = d.len_v[iv];
-    const int B = 3 * Lu * Lv;
-    const int slot = (jv - d.lo_v[iv]) * Lu + (ju - d.lo_u[iu]);
-    const int Lt = d.len_t[rt];
-    LtB = (long long)Lt * B;
-    LF_CHECK(ct >= d.lo_t[rt] && ct < d.lo_t[rt] + Lt);
-    return 9 * d.S_s * (d.pre_t[rt] - pre0) + (long long)Lt * d.es_pre[is] + (long long)(ct - d.lo_t[rt]) * B +
-           3 * slot - d.out_base;
+// ---------------------------------------------------------------------------
+// K6, two-phase form: phase 1 (k_standard_local) computes every (element,
+// span) block's local pairs into the scratch Ks -- all elements and spans of
+// a batch in one launch, coalesced stores, no colours, no read-modify-write
+// of the CSR; phase 2 (k_standard_gather) has one thread per (row block,
+// in-plane pair) sum, for each thickness neighbour, the <= (pt+1)(pu+1)(pv+1)
+// local blocks that contain both functions in a fixed (span, ev, eu) order
+// (deterministic) and add the 9 values into the CSR once per batch.
+
+/// Triangular index of the local pair (al, be), al <= be, or the full one.
+__device__ __forceinline__ int k6_pair_index(int al, int be, int nl3, bool sym) {
+    return sym ? al * nl3 - (al * (al - 1)) / 2 + (be - al) : al * nl3 + be;
 }
 
-#ifndef LF_K6_PREFETCH
-#define LF_K6_PREFETCH 1
-#endif
-
-__global__ void __launch_bounds__(256, LF_K6_MINB) k_standard(const DevTables d, double* __restrict__ values, int cu, int cv, int ct, int nchunk) {
+__global__ void __launch_bounds__(256, LF_K6_MINB) k_standard_local(const DevTables d, int ks0) {
     extern __shared__ double sm[];
     ElemInfo el;
-    el.eu = cu + blockIdx.x * (d.pu + 1);
-    el.ev = cv + blockIdx.y * (d.pv + 1);
-    // blockIdx.z = (span of this thickness colour, chunk of the pair groups):
-    // few elements per colour (small plates, many plies per span) still fill
-    // the GPU; chunks own disjoint pairs, so their writes never overlap
-    const int chunk = blockIdx.z % nchunk;
-    const int ks = ct + (blockIdx.z / nchunk) * (d.pt + 1);
-    if (el.eu >= d.nspu || el.ev >= d.nspv || ks >= d.nspt)
+    const int e_index = blockIdx.x;
+    el.eu = e_index % d.nspu;
+    el.ev = e_index / d.nspu;
+    const int ks = ks0 + blockIdx.y;
+    if (ks >= d.nspt)
         return;
     const int c0 = d.span_cell0[ks], c1 = d.span_cell0[ks + 1];
     if (c0 == c1)
-        return; // span with no unmasked cell (assembly.cpp:185-186)
+        return; // span with no unmasked cell: phase 2 skips it
     if (d.spt_first[ks] + d.pt < d.t0 || d.spt_first[ks] >= d.t1)
         return; // no row of this span lies in the slab
     el.fu = d.spu_first[el.eu];
@@ -484,100 +476,64 @@ __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard(const DevTables d,
     double* gh = sm;
     double* w2 = gh + el.nq2 * el.nl2 * 3;
     double* ctq = sm + ((el.nq2 * el.nl2 * 3 + el.nq2 + 1) & ~1); // nq2 * 90, 16-byte aligned
-    double* tv = ctq + el.nq2 * 90; // nqt * ntl values, then derivatives
+    double* tv = ctq + el.nq2 * 90;
     double* td = tv + d.nqt * ntl;
     double* w3 = td + d.nqt * ntl;
     double* tau = w3 + d.nqt; // [at][bt][i][j]
     element_tables(d, el, gh, w2);
-    const int e_index = el.ev * d.nspu + el.eu;
-    const long long pre0 = d.pre_t[d.t0];
     const bool sym = d.sym != 0;
     const int ngroup = k6_groups(nl3, sym);
-    const int per = (ngroup + nchunk - 1) / nchunk;
-    const int g_end = min(ngroup, (chunk + 1) * per);
-    // this thread's pair groups: at most ceil(per / blockDim) (one, normally)
-    for (int g = chunk * per + threadIdx.x; g - threadIdx.x < g_end; g += blockDim.x) {
-        const bool g_live = g < g_end;
-        int al = 0, be0 = 0;
-        if (g_live)
-            k6_group(g, nl3, sym, al, be0);
-        const int at = al / el.nl2, as = al % el.nl2;
-        int bs[kK6Pairs], bt[kK6Pairs];
-        bool pv[kK6Pairs];
-#pragma unroll
-        for (int p = 0; p < kK6Pairs; ++p) {
-            const int be = be0 + p;
-            pv[p] = g_live && be < nl3;
-            const int bec = pv[p] ? be : al;
-            bt[p] = bec / el.nl2;
-            bs[p] = bec % el.nl2;
+    const long long per_blk = 9LL * (sym ? nl3 * (nl3 + 1) / 2 : nl3 * nl3);
+    double* kb = d.Ks + ((long long)blockIdx.y * (d.nspu * d.nspv) + e_index) * per_blk;
+    for (int c = c0; c < c1; ++c) {
+        __syncthreads();
+        const int cfg = d.layer_config[d.cell_layer[c]];
+        pullback_tables(d, e_index, el.nq2, w2, d.term_table + (long long)cfg * 81, ctq);
+        for (int idx = threadIdx.x; idx < d.nqt * ntl; idx += blockDim.x) {
+            const int q = idx / ntl, a = idx % ntl;
+            const long long h = (long long)c * d.nqt + q;
+            const int sh = ft - d.Bt_first[h]; // 0 unless a point rounds onto a knot
+            const int aa = a + sh;
+            const bool ok = aa >= 0 && aa <= d.pt;
+            tv[idx] = ok ? d.Bt_val[h * ntl + aa] : 0.0;
+            td[idx] = ok ? d.Bt_der[h * ntl + aa] : 0.0;
         }
-        double acc[kK6Pairs][9];
-#pragma unroll
-        for (int p = 0; p < kK6Pairs; ++p)
-#pragma unroll
-            for (int k = 0; k < 9; ++k)
-                acc[p][k] = 0.0;
-        const int it = ft + at;
-        const long long gi = (long long)it * d.ns + (el.fv + as / (d.pu + 1)) * d.nu + el.fu + as % (d.pu + 1);
-#if LF_K6_PREFETCH
-        // the group's += targets are read only after the quadrature loop: ask L2
-        // for their lines now, so the read-modify-write at the end hits L2
-        if (g_live) {
+        for (int q = threadIdx.x; q < d.nqt; q += blockDim.x)
+            w3[q] = d.cell_wts[(long long)c * d.nqt + q];
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < ntl * ntl * 4; idx += blockDim.x) {
+            const int a = idx / (4 * ntl), b = (idx / 4) % ntl, i = (idx >> 1) & 1, j = idx & 1;
+            double s = 0.0;
+            for (int q3 = 0; q3 < d.nqt; ++q3)
+                s += (i ? td : tv)[q3 * ntl + a] * (j ? td : tv)[q3 * ntl + b] * w3[q3];
+            tau[idx] = s;
+        }
+        __syncthreads();
+        for (int g = threadIdx.x; g < ngroup; g += blockDim.x) {
+            int al, be0;
+            k6_group(g, nl3, sym, al, be0);
+            const int at = al / el.nl2, as = al % el.nl2;
+            int bs[kK6Pairs], bt[kK6Pairs];
+            bool pv[kK6Pairs];
 #pragma unroll
             for (int p = 0; p < kK6Pairs; ++p) {
-                if (!pv[p])
-                    continue;
-                const int jt = ft + bt[p];
-                const long long gj =
-                    (long long)jt * d.ns + (el.fv + bs[p] / (d.pu + 1)) * d.nu + el.fu + bs[p] % (d.pu + 1);
-                for (int side = 0; side < 2; ++side) {
-                    const bool row = side == 0 ? gi >= d.f0 && gi < d.f1
-                                               : sym && al != be0 + p && gj >= d.f0 && gj < d.f1;
-                    if (!row)
-                        continue;
-                    long long LtB;
-                    const long long pos = side ? k6_pos(d, el, bs[p], as, jt, it, pre0, LtB)
-                                               : k6_pos(d, el, as, bs[p], it, jt, pre0, LtB);
-#pragma unroll
-                    for (int a = 0; a < 3; ++a)
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(values + pos + a * LtB));
-                }
+                const int be = be0 + p;
+                pv[p] = be < nl3;
+                const int bec = pv[p] ? be : al;
+                bt[p] = bec / el.nl2;
+                bs[p] = bec % el.nl2;
             }
-        }
-#endif
-        for (int c = c0; c < c1; ++c) {
-            __syncthreads();
-            const int cfg = d.layer_config[d.cell_layer[c]];
-            pullback_tables(d, e_index, el.nq2, w2, d.term_table + (long long)cfg * 81, ctq);
-            for (int idx = threadIdx.x; idx < d.nqt * ntl; idx += blockDim.x) {
-                const int q = idx / ntl, a = idx % ntl;
-                const long long h = (long long)c * d.nqt + q;
-                const int sh = ft - d.Bt_first[h]; // 0 unless a point rounds onto a knot
-                const int aa = a + sh;
-                const bool ok = aa >= 0 && aa <= d.pt;
-                tv[idx] = ok ? d.Bt_val[h * ntl + aa] : 0.0;
-                td[idx] = ok ? d.Bt_der[h * ntl + aa] : 0.0;
-            }
-            for (int q = threadIdx.x; q < d.nqt; q += blockDim.x)
-                w3[q] = d.cell_wts[(long long)c * d.nqt + q];
-            __syncthreads();
-            for (int idx = threadIdx.x; idx < ntl * ntl * 4; idx += blockDim.x) {
-                const int a = idx / (4 * ntl), b = (idx / 4) % ntl, i = (idx >> 1) & 1, j = idx & 1;
-                double s = 0.0;
-                for (int q3 = 0; q3 < d.nqt; ++q3)
-                    s += (i ? td : tv)[q3 * ntl + a] * (j ? td : tv)[q3 * ntl + b] * w3[q3];
-                tau[idx] = s;
-            }
-            __syncthreads();
-            if (!g_live)
-                continue;
+            double acc[kK6Pairs][9];
             double tp[kK6Pairs][4];
 #pragma unroll
-            for (int p = 0; p < kK6Pairs; ++p)
+            for (int p = 0; p < kK6Pairs; ++p) {
+#pragma unroll
+                for (int k = 0; k < 9; ++k)
+                    acc[p][k] = 0.0;
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                     tp[p][k] = tau[(at * ntl + bt[p]) * 4 + k];
+            }
             for (int q2 = 0; q2 < el.nq2; ++q2) {
                 const double* ga = gh + (q2 * el.nl2 + as) * 3;
                 const double a0 = ga[0], a1 = ga[1], a2 = ga[2];
@@ -611,35 +567,131 @@ __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard(const DevTables d,
                     }
                 }
             }
-        }
-        if (!g_live)
-            continue;
 #pragma unroll
-        for (int p = 0; p < kK6Pairs; ++p) {
-            if (!pv[p])
-                continue;
-            const int jt = ft + bt[p];
-            const long long gj =
-                (long long)jt * d.ns + (el.fv + bs[p] / (d.pu + 1)) * d.nu + el.fu + bs[p] % (d.pu + 1);
-            // rows of functions (it, is) / (jt, js) inside the output range [f0, f1)
-            const bool row_i = gi >= d.f0 && gi < d.f1;
-            const bool row_j = sym && al != be0 + p && gj >= d.f0 && gj < d.f1;
-            // K(i,j)[a][b] into row block i; with symmetric tables also
-            // K(j,i)[b][a] = K(i,j)[a][b] into row block j (same element, so the
-            // colouring still makes the += race-free)
-            for (int side = 0; side < 2; ++side) {
-                if (side == 0 ? !row_i : !row_j)
+            for (int p = 0; p < kK6Pairs; ++p) {
+                if (!pv[p])
                     continue;
-                long long LtB;
-                const long long pos = side ? k6_pos(d, el, bs[p], as, jt, it, pre0, LtB)
-                                           : k6_pos(d, el, as, bs[p], it, jt, pre0, LtB);
-                LF_CHECK(pos >= 0 && pos + 2 * LtB + 2 < d.nnz_slab);
+                double* o = kb + 9LL * k6_pair_index(al, be0 + p, nl3, sym);
+                LF_CHECK(o >= kb && o + 9 <= kb + per_blk);
+#pragma unroll
+                for (int k = 0; k < 9; ++k)
+                    o[k] = c == c0 ? acc[p][k] : o[k] + acc[p][k]; // a block's own scratch: no race
+            }
+        }
+    }
+}
+
+/// Phase 2: thread per (thickness row it of the batch, in-plane pair
+/// (i_s, slot)); for every neighbour j_t of it, the 3x3 block K(i, j) is the
+/// sum over the batch's spans and the elements containing both in-plane
+/// functions of the local blocks in Ks, added into the CSR.  With symmetric
+/// tables only blocks al <= be are stored; local order follows the global
+/// function order, so the thread with i < j reads its blocks directly
+/// (consecutive slots: consecutive blocks) and also adds the transpose into
+/// row block j, the thread with i > j does nothing unless j lies outside the
+/// output range (then it reads the transposed blocks itself): every stored
+/// block is read once.
+__global__ void __launch_bounds__(256) k_standard_gather(const DevTables d, double* __restrict__ values, int ks0,
+                                                         int ks1, int it_lo) {
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; // in-plane pair
+    const int it = it_lo + blockIdx.y;
+    if (q >= d.S_s || it < d.t0 || it >= d.t1)
+        return;
+    const long long e = 9 * q;
+    int is = __ldg(d.blk_is + e / kBlock);
+    while (__ldg(d.es_pre + is + 1) <= e)
+        ++is;
+    const long long gi = (long long)it * d.ns + is;
+    if (gi < d.f0 || gi >= d.f1)
+        return; // partial first / last row of a function range
+    const int slot = (int)((e - __ldg(d.es_pre + is)) / 9);
+    const int iu = is % d.nu, iv = is / d.nu;
+    const int Lu = __ldg(d.len_u + iu), Lv = __ldg(d.len_v + iv);
+    const int sv = slot / Lu, su = slot - sv * Lu;
+    const int ju = __ldg(d.lo_u + iu) + su, jv = __ldg(d.lo_v + iv) + sv;
+    const int js = jv * d.nu + ju;
+    const int B = 3 * Lu * Lv;
+    const int nl2 = (d.pu + 1) * (d.pv + 1), ntl = d.pt + 1, nl3 = nl2 * ntl;
+    const bool sym = d.sym != 0;
+    const long long per_blk = 9LL * (sym ? nl3 * (nl3 + 1) / 2 : nl3 * nl3);
+    const int nel = d.nspu * d.nspv;
+    // elements containing both in-plane functions: first[e] <= min, max <= first[e] + p
+    const int umin = min(iu, ju), umax = max(iu, ju), vmin = min(iv, jv), vmax = max(iv, jv);
+    const int eu_lo = span_lower(d.spu_first, d.nspu, umax - d.pu);
+    const int ev_lo = span_lower(d.spv_first, d.nspv, vmax - d.pv);
+    const int Lt = __ldg(d.len_t + it), lot = __ldg(d.lo_t + it);
+    const long long pre0 = __ldg(d.pre_t + d.t0), nine_S = 9 * d.S_s;
+    const long long row0 = nine_S * (__ldg(d.pre_t + it) - pre0) + (long long)Lt * __ldg(d.es_pre + is) + 3 * slot -
+                           d.out_base;
+    for (int k = 0; k < Lt; ++k) {
+        const int jt = lot + k;
+        const long long gj = (long long)jt * d.ns + js;
+        const bool j_in = gj >= d.f0 && gj < d.f1;
+        // which blocks this thread writes: K(i,j) always (row i is ours), K(j,i)
+        // too when i < j and row j is ours; a thread with i > j and row j ours
+        // leaves both to that row's thread
+        if (sym && gi > gj && j_in)
+            continue;
+        const bool mirror = sym && gi < gj && j_in;
+        const bool transposed = sym && gi > gj; // stored block is (be, al)
+        const int tmin = min(it, jt), tmax = max(it, jt);
+        double acc[9];
+#pragma unroll
+        for (int x = 0; x < 9; ++x)
+            acc[x] = 0.0;
+        bool any = false;
+        for (int ks = max(ks0, span_lower(d.spt_first, d.nspt, tmax - d.pt)); ks < ks1; ++ks) {
+            const int ft = __ldg(d.spt_first + ks);
+            if (ft > tmin)
+                break;
+            if (__ldg(d.span_cell0 + ks) == __ldg(d.span_cell0 + ks + 1))
+                continue; // masked span (assembly.cpp:185-186)
+            const int at = it - ft, bt = jt - ft;
+            for (int ev = ev_lo; ev < d.nspv && __ldg(d.spv_first + ev) <= vmin; ++ev) {
+                const int fv = __ldg(d.spv_first + ev);
+                for (int eu = eu_lo; eu < d.nspu && __ldg(d.spu_first + eu) <= umin; ++eu) {
+                    const int fu = __ldg(d.spu_first + eu);
+                    const int al = at * nl2 + (iv - fv) * (d.pu + 1) + (iu - fu);
+                    const int be = bt * nl2 + (jv - fv) * (d.pu + 1) + (ju - fu);
+                    const double* kb = d.Ks + ((long long)(ks - ks0) * nel + ev * d.nspu + eu) * per_blk;
+                    any = true;
+                    if (!transposed) {
+                        const double* src = kb + 9LL * k6_pair_index(al, be, nl3, sym);
+#pragma unroll
+                        for (int x = 0; x < 9; ++x)
+                            acc[x] += __ldg(src + x);
+                    } else { // K(i,j) = K(j,i)^T
+                        const double* src = kb + 9LL * k6_pair_index(be, al, nl3, sym);
+#pragma unroll
+                        for (int a = 0; a < 3; ++a)
+#pragma unroll
+                            for (int b = 0; b < 3; ++b)
+                                acc[3 * a + b] += __ldg(src + 3 * b + a);
+                    }
+                }
+            }
+        }
+        if (!any)
+            continue;
+        const long long pos = row0 + (long long)k * B;
+        LF_CHECK(pos >= 0 && pos + 2LL * Lt * B + 2 < d.nnz_slab);
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b)
+                values[pos + (long long)a * Lt * B + b] += acc[3 * a + b];
+        if (mirror) { // K(j,i)[b][a] = K(i,j)[a][b], in row block j
+            const int Luj = __ldg(d.len_u + ju), Lvj = __ldg(d.len_v + jv);
+            const int Bj = 3 * Luj * Lvj, Ltj = __ldg(d.len_t + jt);
+            const int slot_m = (iv - __ldg(d.lo_v + jv)) * Luj + (iu - __ldg(d.lo_u + ju));
+            const long long posj = nine_S * (__ldg(d.pre_t + jt) - pre0) + (long long)Ltj * __ldg(d.es_pre + js) +
+                                   (long long)(it - __ldg(d.lo_t + jt)) * Bj + 3 * slot_m - d.out_base;
+            LF_CHECK(posj >= 0 && posj + 2LL * Ltj * Bj + 2 < d.nnz_slab);
+#pragma unroll
+            for (int b = 0; b < 3; ++b)
 #pragma unroll
                 for (int a = 0; a < 3; ++a)
-#pragma unroll
-                    for (int b = 0; b < 3; ++b)
-                        values[pos + a * LtB + b] += side ? acc[p][3 * b + a] : acc[p][3 * a + b];
-            }
+                    values[posj + (long long)b * Ltj * Bj + a] += acc[3 * a + b];
         }
     }
 }
@@ -1115,24 +1167,31 @@ int launch_standard(const DevTables& d, double* values, long long nnz, cudaStrea
     const int nl2 = (d.pu + 1) * (d.pv + 1), nq2 = d.nqu * d.nqv, ntl = d.pt + 1;
     const size_t smem = sizeof(double) * ((size_t)nq2 * nl2 * 3 + nq2 + 1 + (size_t)nq2 * 90 +
                                           2 * (size_t)d.nqt * ntl + d.nqt + 4 * (size_t)ntl * ntl);
+    if (!d.Ks)
+        return (int)cudaErrorInvalidValue; // the plan allocates the scratch for every standard assembly
+    // two-phase: batches of ks_batch spans, local blocks then the gather
     if (smem > 48 * 1024)
-        cudaFuncSetAttribute(k_standard, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int gx = (d.nspu + d.pu) / (d.pu + 1), gy = (d.nspv + d.pv) / (d.pv + 1), gz = (d.nspt + d.pt) / (d.pt + 1);
-    // split the pair groups of each (element, span) over enough blocks for
-    // ~4 blocks per SM per colour launch (chunks of >= 128 groups)
-    const int nl3 = nl2 * ntl;
-    const int ngroup = k6_groups(nl3, d.sym != 0);
-    const long long blocks = (long long)gx * gy * gz;
-    int nchunk = (int)std::min<long long>((148LL * 4 + blocks - 1) / blocks, (ngroup + 127) / 128);
-    nchunk = std::max(1, std::min(nchunk, 65535 / std::max(1, gz)));
-    const dim3 grid(gx, gy, gz * nchunk);
-    for (int ct = 0; ct <= d.pt; ++ct)
-        for (int cv = 0; cv <= d.pv; ++cv)
-            for (int cu = 0; cu <= d.pu; ++cu) {
-                k_standard<<<grid, 256, smem, stream>>>(d, values, cu, cv, ct, nchunk);
-                if (launches)
-                    ++*launches;
-            }
+        cudaFuncSetAttribute(k_standard_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // spans with a row in the slab
+    int ks_lo = 0, ks_hi = d.nspt;
+    while (ks_lo < d.nspt && d.spt_first_h[ks_lo] + d.pt < d.t0)
+        ++ks_lo;
+    while (ks_hi > ks_lo && d.spt_first_h[ks_hi - 1] >= d.t1)
+        --ks_hi;
+    const unsigned nel = (unsigned)(d.nspu * d.nspv);
+    for (int ks0 = ks_lo; ks0 < ks_hi; ks0 += d.ks_batch) {
+        const int ks1 = std::min(ks_hi, ks0 + d.ks_batch);
+        k_standard_local<<<dim3(nel, (unsigned)(ks1 - ks0)), 256, smem, stream>>>(d, ks0);
+        // rows of the batch's spans inside the slab
+        const int it_lo = std::max(d.t0, d.spt_first_h[ks0]);
+        const int it_hi = std::min(d.t1, d.spt_first_h[ks1 - 1] + d.pt + 1);
+        if (it_hi > it_lo) {
+            const dim3 grid((unsigned)((d.S_s + 255) / 256), (unsigned)(it_hi - it_lo));
+            k_standard_gather<<<grid, 256, 0, stream>>>(d, values, ks0, ks1, it_lo);
+        }
+        if (launches)
+            *launches += 2;
+    }
     return (int)cudaGetLastError();
 }
 

@@ -90,6 +90,11 @@ struct DevTables {
     double* Etab;
     double* Pe;     // element-local P of a batch of pe_terms terms: [term][el][4][nl2][3][nl2][3]
     int pe_terms;   // terms per batch
+    // two-phase standard assembly (K6): element-local blocks of a batch of
+    // ks_batch thickness spans, Ks[span][el][pair][9] (pair: al <= be when sym)
+    double* Ks;
+    int ks_batch;
+    const int* spt_first_h; // host copy of spt_first (the launcher's batch bounds)
     // output range: the functions f = i_t * ns + i_s in [f0, f1), covering
     // thickness rows [t0, t1) -- row t0 from in-plane function s0, row t1 - 1
     // up to s1 (exclusive).  Entry (it, is, ...) of the range is written at

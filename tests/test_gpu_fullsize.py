@@ -58,3 +58,48 @@ def test_full_size_boundary_slabs_match_oracle(gpu, oracle, name):
             assert b["nnz_begin"] == terms.nnz_before(b["t_begin"])
             assert b["nnz_end"] == terms.nnz_before(b["t_end"])
     terms.close()
+
+
+def _device_range(gpu, prob, f0, f1):
+    import torch
+    plan = gpu.Plan(prob, "fast", 0, f_begin=f0, f_end=f1)
+    rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
+    cols = torch.empty(max(1, plan.nnz), dtype=torch.int32, device="cuda")
+    vals = torch.empty(max(1, plan.nnz), dtype=torch.float64, device="cuda")
+    plan.build_pattern(rp.data_ptr(), cols.data_ptr())
+    plan.assemble(vals.data_ptr())
+    plan.synchronize()
+    out = (rp.cpu().numpy(), cols[:plan.nnz].cpu().numpy(), vals[:plan.nnz].cpu().numpy())
+    info = {"nnz_begin": plan.nnz_begin, "row_begin": plan.row_begin, "nnz": plan.nnz}
+    plan.close()
+    del rp, cols, vals
+    torch.cuda.empty_cache()
+    return out, info
+
+
+@pytest.mark.parametrize("parts", [8, 3])
+def test_c5_function_range_cuts_match_oracle(gpu, oracle, parts):
+    """The multi-GPU cuts of C5 fall inside thickness rows
+    (lf_slab_bounds_functions).  Around every cut of the 8- and 3-way splits,
+    a function range straddling it (the last 40 functions of one part and the
+    first 40 of the next, plus the matrix's first and last 40) is assembled
+    as its own plan and equals the oracle's rows (pattern bit-exact, values
+    within 1e-12 * max|K|), at global offsets up to 1.69e10 (> 2^32) that
+    must equal the oracle's function offsets."""
+    prob = P.baseline_config("C5")
+    terms = oracle.fast_terms(prob)
+    ns, F = prob.n_s, prob.n_s * prob.n_t
+    cuts = [gpu.slab_bounds_functions(prob, parts, k)["f_begin"] for k in range(1, parts)]
+    windows = [(0, 40), (F - 40, F)] + [(c - 40, c + 40) for c in cuts]
+    for f0, f1 in windows:
+        got, info = _device_range(gpu, prob, f0, f1)
+        assert info["nnz_begin"] == terms.function_offset(f0)
+        assert info["nnz_begin"] + info["nnz"] == terms.function_offset(f1)
+        assert info["row_begin"] == 3 * f0
+        t0, t1 = f0 // ns, (f1 - 1) // ns + 1
+        rp, cols, vals = terms.slab(t0, t1)
+        a, e = 3 * (f0 - t0 * ns), 3 * (f1 - t0 * ns)
+        want = (rp[a:e + 1] - rp[a], cols[rp[a]:rp[e]], vals[rp[a]:rp[e]])
+        assert_csr_match(got, want, RTOL)
+    assert max(terms.function_offset(c) for c in cuts) > 2 ** 32 or parts == 3
+    terms.close()
