@@ -271,6 +271,7 @@ struct lf_plan {
     lfb::Setup setup;
     DeviceArena arena;
     lfb::DevTables d{};
+    lfb::K6Const k6c{}; // standard backend, affine map: K6 phase-1 tables (n_cfg = 0: not used)
     int launches = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> free_events, pending;
     double kernel_ms = 0.0;
@@ -411,6 +412,23 @@ void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void
     d.n_pairs = s.n_pairs;
     if (backend == LF_BACKEND_STANDARD) {
         d.spt_first_h = s.spt_first.data();
+        // affine map: det G C G per configuration for K6 phase 1 (kernel parameter)
+        const int n_cfg = static_cast<int>(s.term_table.size() / 81);
+        const char* kc = std::getenv("LAMFAST_K6_CONST");
+        if (d.affine && n_cfg <= lfb::kK6MaxCfg && !(kc && kc[0] == '0')) {
+            plan->k6c.n_cfg = n_cfg;
+            for (int c = 0; c < n_cfg; ++c)
+                for (int xy = 0; xy < 9; ++xy)
+                    for (int ik = 0; ik < 9; ++ik) {
+                        const int x = xy / 3, y = xy % 3;
+                        double acc = 0.0; // pullback_tables' order (k_ops.cu), without the in-plane weight
+                        for (int j = 0; j < 3; ++j)
+                            for (int l = 0; l < 3; ++l)
+                                acc += d.G[3 * x + j] * d.G[3 * y + l] *
+                                       s.term_table[static_cast<std::size_t>(c) * 81 + (3 * j + l) * 9 + ik];
+                        plan->k6c.C[c][xy * 9 + ik] = d.det * acc;
+                    }
+        }
         if (want_values) {
             // two-phase K6: element-local blocks of as many spans per batch as
             // fit ~4 GB (or a fifth of the free memory), one span at least
@@ -477,7 +495,7 @@ int plan_prepare(lf_plan* plan, cudaStream_t s) {
 int plan_values(lf_plan* plan, const lfb::DevTables& d, double* values, cudaStream_t s) {
     int launches = 0;
     if (plan->setup.backend == LF_BACKEND_STANDARD)
-        CK(static_cast<cudaError_t>(lfb::launch_standard(d, values, d.nnz_slab, s, &launches)));
+        CK(static_cast<cudaError_t>(lfb::launch_standard(d, values, d.nnz_slab, s, &launches, &plan->k6c)));
     else
         CK(static_cast<cudaError_t>(lfb::launch_combine(d, values, 0, s, &launches)));
     return launches;

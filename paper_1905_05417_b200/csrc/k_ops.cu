@@ -450,7 +450,14 @@ __device__ __forceinline__ int k6_pair_index(int al, int be, int nl3, bool sym) 
     return sym ? al * nl3 - (al * (al - 1)) / 2 + (be - al) : al * nl3 + be;
 }
 
-__global__ void __launch_bounds__(256, LF_K6_MINB) k_standard_local(const DevTables d, int ks0) {
+/// CONSTC: affine map with the per-configuration tables in the kernel
+/// parameter `cst` (det G C G; the in-plane weight multiplies the basis
+/// products instead), so the inner loop's table reads are constant-bank
+/// loads rather than shared-memory broadcasts, and no per-cell pull-back
+/// table is built.
+template <bool CONSTC>
+__global__ void __launch_bounds__(256, LF_K6_MINB) k_standard_local(const DevTables d, int ks0,
+                                                                    const __grid_constant__ K6Const cst) {
     extern __shared__ double sm[];
     ElemInfo el;
     const int e_index = blockIdx.x;
@@ -488,7 +495,9 @@ __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard_local(const DevTab
     for (int c = c0; c < c1; ++c) {
         __syncthreads();
         const int cfg = d.layer_config[d.cell_layer[c]];
-        pullback_tables(d, e_index, el.nq2, w2, d.term_table + (long long)cfg * 81, ctq);
+        if constexpr (!CONSTC)
+            pullback_tables(d, e_index, el.nq2, w2, d.term_table + (long long)cfg * 81, ctq);
+        const double* Cc = cst.C[CONSTC ? cfg : 0];
         for (int idx = threadIdx.x; idx < d.nqt * ntl; idx += blockDim.x) {
             const int q = idx / ntl, a = idx % ntl;
             const long long h = (long long)c * d.nqt + q;
@@ -536,7 +545,9 @@ __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard_local(const DevTab
             }
             for (int q2 = 0; q2 < el.nq2; ++q2) {
                 const double* ga = gh + (q2 * el.nl2 + as) * 3;
-                const double a0 = ga[0], a1 = ga[1], a2 = ga[2];
+                // CONSTC: the in-plane weight goes with the al side
+                const double wq = CONSTC ? w2[q2] : 1.0;
+                const double a0 = ga[0] * wq, a1 = ga[1] * wq, a2 = ga[2] * wq;
                 double gb[kK6Pairs][3];
 #pragma unroll
                 for (int p = 0; p < kK6Pairs; ++p) {
@@ -550,8 +561,17 @@ __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard_local(const DevTab
                 for (int xy = 0; xy < 9; ++xy) {
                     const int x = xy / 3, y = xy % 3;
                     const double gx = x == 0 ? a0 : x == 1 ? a1 : a2;
-                    const double2 r0 = C2[xy * 5], r1 = C2[xy * 5 + 1], r2 = C2[xy * 5 + 2], r3 = C2[xy * 5 + 3],
-                                  r4 = C2[xy * 5 + 4];
+                    double2 r0, r1, r2, r3, r4;
+                    if constexpr (CONSTC) {
+                        r0 = make_double2(Cc[xy * 9 + 0], Cc[xy * 9 + 1]);
+                        r1 = make_double2(Cc[xy * 9 + 2], Cc[xy * 9 + 3]);
+                        r2 = make_double2(Cc[xy * 9 + 4], Cc[xy * 9 + 5]);
+                        r3 = make_double2(Cc[xy * 9 + 6], Cc[xy * 9 + 7]);
+                        r4 = make_double2(Cc[xy * 9 + 8], 0.0);
+                    } else {
+                        r0 = C2[xy * 5], r1 = C2[xy * 5 + 1], r2 = C2[xy * 5 + 2], r3 = C2[xy * 5 + 3],
+                        r4 = C2[xy * 5 + 4];
+                    }
 #pragma unroll
                     for (int p = 0; p < kK6Pairs; ++p) {
                         const double s = gx * gb[p][y] * tp[p][(x == 2 ? 2 : 0) + (y == 2 ? 1 : 0)];
@@ -1162,7 +1182,8 @@ int launch_pattern(const DevTables& d, long long* row_ptr, int* cols, cudaStream
     return (int)cudaGetLastError();
 }
 
-int launch_standard(const DevTables& d, double* values, long long nnz, cudaStream_t stream, int* launches) {
+int launch_standard(const DevTables& d, double* values, long long nnz, cudaStream_t stream, int* launches,
+                    const K6Const* cst) {
     cudaMemsetAsync(values, 0, sizeof(double) * (size_t)nnz, stream);
     const int nl2 = (d.pu + 1) * (d.pv + 1), nq2 = d.nqu * d.nqv, ntl = d.pt + 1;
     const size_t smem = sizeof(double) * ((size_t)nq2 * nl2 * 3 + nq2 + 1 + (size_t)nq2 * 90 +
@@ -1170,8 +1191,12 @@ int launch_standard(const DevTables& d, double* values, long long nnz, cudaStrea
     if (!d.Ks)
         return (int)cudaErrorInvalidValue; // the plan allocates the scratch for every standard assembly
     // two-phase: batches of ks_batch spans, local blocks then the gather
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(k_standard_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const bool constc = cst && cst->n_cfg > 0;
+    static const K6Const none{}; // n_cfg = 0
+    if (smem > 48 * 1024) {
+        cudaFuncSetAttribute(k_standard_local<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_standard_local<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
     // spans with a row in the slab
     int ks_lo = 0, ks_hi = d.nspt;
     while (ks_lo < d.nspt && d.spt_first_h[ks_lo] + d.pt < d.t0)
@@ -1181,7 +1206,10 @@ int launch_standard(const DevTables& d, double* values, long long nnz, cudaStrea
     const unsigned nel = (unsigned)(d.nspu * d.nspv);
     for (int ks0 = ks_lo; ks0 < ks_hi; ks0 += d.ks_batch) {
         const int ks1 = std::min(ks_hi, ks0 + d.ks_batch);
-        k_standard_local<<<dim3(nel, (unsigned)(ks1 - ks0)), 256, smem, stream>>>(d, ks0);
+        if (constc)
+            k_standard_local<true><<<dim3(nel, (unsigned)(ks1 - ks0)), 256, smem, stream>>>(d, ks0, *cst);
+        else
+            k_standard_local<false><<<dim3(nel, (unsigned)(ks1 - ks0)), 256, smem, stream>>>(d, ks0, none);
         // rows of the batch's spans inside the slab
         const int it_lo = std::max(d.t0, d.spt_first_h[ks0]);
         const int it_hi = std::min(d.t1, d.spt_first_h[ks1 - 1] + d.pt + 1);

@@ -109,6 +109,15 @@ struct DevTables {
     long long nnz_slab; // values of this range (bounds checks in LF_DEBUG_CHECKS builds)
 };
 
+/// Pulled-back contraction tables of an affine map without the in-plane
+/// weight, det G C G per material configuration, passed to K6 phase 1 as a
+/// kernel parameter (constant bank: no shared-memory loads in its inner loop).
+constexpr int kK6MaxCfg = 16;
+struct K6Const {
+    int n_cfg; // 0: not available (non-affine map or too many configurations)
+    double C[kK6MaxCfg][81];
+};
+
 constexpr int kEStride = 10; // doubles per (pair, ab) row of Etab (9 used; 16-byte rows)
 constexpr int kEPair = 9 * kEStride;
 
@@ -130,7 +139,7 @@ int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t st
 int launch_pair_coeffs(const DevTables& d, cudaStream_t stream);
 int launch_pattern(const DevTables& d, long long* row_ptr, int* cols, cudaStream_t stream);
 int launch_standard(const DevTables& d, double* values, long long nnz, cudaStream_t stream,
-                    int* launches);
+                    int* launches, const K6Const* cst = nullptr);
 
 /// Matrix-free v^T K u (referenceBilinear, assembly.cpp:247-318); partial holds
 /// nspu * nspv * nspt doubles, *out (device) the result.
