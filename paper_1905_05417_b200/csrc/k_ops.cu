@@ -450,11 +450,13 @@ __device__ __forceinline__ int k6_pair_index(int al, int be, int nl3, bool sym) 
     return sym ? al * nl3 - (al * (al - 1)) / 2 + (be - al) : al * nl3 + be;
 }
 
-/// CONSTC: affine map with the per-configuration tables in the kernel
-/// parameter `cst` (det G C G; the in-plane weight multiplies the basis
-/// products instead), so the inner loop's table reads are constant-bank
-/// loads rather than shared-memory broadcasts, and no per-cell pull-back
-/// table is built.
+/// CONSTC: affine map, the per-configuration tables det G C G come in the
+/// kernel parameter `cst`, so a cell's pulled-back table is w2[q] times one
+/// of them (one product per entry) instead of the frame contraction of
+/// pullback_tables (9 products and the frame loads per entry).  The inner
+/// loop reads the table from shared memory either way: reading it from the
+/// constant bank measured C4 71.5 ms but C3 65.1 against 60.1 ms (the
+/// register-indexed constant loads set the pace), profiles/r2_k6_const.txt.
 template <bool CONSTC>
 __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard_local(const DevTables d, int ks0,
                                                                     const __grid_constant__ K6Const cst) {
@@ -495,9 +497,15 @@ __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard_local(const DevTab
     for (int c = c0; c < c1; ++c) {
         __syncthreads();
         const int cfg = d.layer_config[d.cell_layer[c]];
-        if constexpr (!CONSTC)
+        if constexpr (CONSTC) { // affine: the pulled-back table is w2[q] times the configuration's
+            const double* Cc = cst.C[cfg];
+            for (int idx = threadIdx.x; idx < el.nq2 * 90; idx += blockDim.x) {
+                const int q = idx / 90, r = idx - 90 * q, xy = r / 10, ik = r - 10 * xy;
+                ctq[idx] = ik == 9 ? 0.0 : w2[q] * Cc[xy * 9 + ik];
+            }
+        } else {
             pullback_tables(d, e_index, el.nq2, w2, d.term_table + (long long)cfg * 81, ctq);
-        const double* Cc = cst.C[CONSTC ? cfg : 0];
+        }
         for (int idx = threadIdx.x; idx < d.nqt * ntl; idx += blockDim.x) {
             const int q = idx / ntl, a = idx % ntl;
             const long long h = (long long)c * d.nqt + q;
@@ -545,9 +553,7 @@ __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard_local(const DevTab
             }
             for (int q2 = 0; q2 < el.nq2; ++q2) {
                 const double* ga = gh + (q2 * el.nl2 + as) * 3;
-                // CONSTC: the in-plane weight goes with the al side
-                const double wq = CONSTC ? w2[q2] : 1.0;
-                const double a0 = ga[0] * wq, a1 = ga[1] * wq, a2 = ga[2] * wq;
+                const double a0 = ga[0], a1 = ga[1], a2 = ga[2];
                 double gb[kK6Pairs][3];
 #pragma unroll
                 for (int p = 0; p < kK6Pairs; ++p) {
@@ -561,17 +567,8 @@ __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard_local(const DevTab
                 for (int xy = 0; xy < 9; ++xy) {
                     const int x = xy / 3, y = xy % 3;
                     const double gx = x == 0 ? a0 : x == 1 ? a1 : a2;
-                    double2 r0, r1, r2, r3, r4;
-                    if constexpr (CONSTC) {
-                        r0 = make_double2(Cc[xy * 9 + 0], Cc[xy * 9 + 1]);
-                        r1 = make_double2(Cc[xy * 9 + 2], Cc[xy * 9 + 3]);
-                        r2 = make_double2(Cc[xy * 9 + 4], Cc[xy * 9 + 5]);
-                        r3 = make_double2(Cc[xy * 9 + 6], Cc[xy * 9 + 7]);
-                        r4 = make_double2(Cc[xy * 9 + 8], 0.0);
-                    } else {
-                        r0 = C2[xy * 5], r1 = C2[xy * 5 + 1], r2 = C2[xy * 5 + 2], r3 = C2[xy * 5 + 3],
-                        r4 = C2[xy * 5 + 4];
-                    }
+                    const double2 r0 = C2[xy * 5], r1 = C2[xy * 5 + 1], r2 = C2[xy * 5 + 2], r3 = C2[xy * 5 + 3],
+                                  r4 = C2[xy * 5 + 4];
 #pragma unroll
                     for (int p = 0; p < kK6Pairs; ++p) {
                         const double s = gx * gb[p][y] * tp[p][(x == 2 ? 2 : 0) + (y == 2 ? 1 : 0)];
