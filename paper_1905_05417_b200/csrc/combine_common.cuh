@@ -176,19 +176,6 @@ __device__ __forceinline__ void combine_row_k(const double (&P)[EPT][NT][4], WP 
                 }
             }
         }
-#ifdef LF_STORE_V2_TEST
-        // diagnostic (wrong values): the warp's 64 values as one 16-byte-aligned
-        // v2 store per lane at the warp's run, i.e. the ideal vector-store pattern
-        if constexpr (EPT == 2) {
-            double* p0 = o[0] + (long long)k * B[0];
-            unsigned long long a0 = __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(p0), 0);
-            a0 &= ~15ull;
-            double2* q = reinterpret_cast<double2*>(a0) + (threadIdx.x & 31);
-            if (live[0] && live[1])
-                __stcs(q, make_double2(acc[0], acc[1]));
-            continue;
-        }
-#endif
 #pragma unroll
         for (int x = 0; x < EPT; ++x)
             if (live[x])
