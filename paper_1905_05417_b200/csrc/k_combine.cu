@@ -368,12 +368,18 @@ __global__ void __launch_bounds__(BT, MINB) k_combine_coef(const DevTables d, do
             const RowInfo ri = s_row[rr];
             const int lt = ri.lt & 0xff, edge = ri.lt >> 8;
             const unsigned lv = live & ((edge & 1) ? in_s0 : ~0u) & ((edge & 2) ? in_s1 : ~0u);
-            double* o[NS][3];
+            // 32-bit offsets inside the row block (< 9 S_s L_t values) from one
+            // 64-bit row base: one IMAD.WIDE per store instead of 64-bit pointer arithmetic
+            double* const rowp = out + ri.base;
+            int o[NS][3];
+            bool sb[NS][3];
 #pragma unroll
             for (int st = 0; st < NS; ++st)
 #pragma unroll
-                for (int m = 0; m < 3; ++m)
-                    o[st][m] = out + ri.base + (long long)lt * A[st][m] + R[st][m];
+                for (int m = 0; m < 3; ++m) {
+                    o[st][m] = lt * A[st][m] + R[st][m];
+                    sb[st][m] = (lv >> (3 * st + m)) & 1u;
+                }
             const double* er = s_e + (long long)rr * lt_max * k_stride + coff;
             for (int k = 0; k < lt; ++k) {
                 const double2* c = reinterpret_cast<const double2*>(er + k * k_stride);
@@ -404,9 +410,9 @@ __global__ void __launch_bounds__(BT, MINB) k_combine_coef(const DevTables d, do
 #pragma unroll
                     for (int m = 0; m < 3; ++m) {
                         const double val = bsel[m] == 0 ? w[st][0] : bsel[m] == 1 ? w[st][1] : w[st][2];
-                        const unsigned bit = (lv >> (3 * st + m)) & 1u;
-                        LF_CHECK(!bit || (o[st][m] >= out && o[st][m] < out + d.nnz_slab));
-                        store_value_if(o[st][m], val, bit);
+                        double* const p = rowp + o[st][m];
+                        LF_CHECK(!sb[st][m] || (p >= out && p < out + d.nnz_slab));
+                        store_value_if(p, val, sb[st][m]);
                         o[st][m] += B[st][m];
                     }
             }
