@@ -31,6 +31,17 @@ __device__ __forceinline__ void store_value_if(double* p, double v, unsigned pre
                  : "memory");
 }
 
+/// 16-byte global -> shared asynchronous copy (L2 only), zero-filled when !ok.
+__device__ __forceinline__ void cp_async16(double* smem_dst, const double* gsrc, bool ok) {
+    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(gsrc), "r"(ok ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+/// all but the most recent committed group have landed (this thread's copies)
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 __device__ __forceinline__ int find_is(const long long* es_pre, int ns, long long e) {
     int lo = 0, hi = ns; // es_pre[lo] <= e < es_pre[hi]
     while (hi - lo > 1) {

@@ -251,8 +251,10 @@ template <int BT, int NS, int MINB>
 __global__ void __launch_bounds__(BT, MINB) k_combine_coef(const DevTables d, double* __restrict__ out, int t_chunk,
                                                            int stage_rows, int lt_max, long long s_pad) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    // s_row: the chunk's rows; two coefficient-row buffers, the next stage's
+    // cp.async copies in flight while the current one is consumed
     RowInfo* s_row = reinterpret_cast<RowInfo*>(smem_raw);
-    double* s_e = reinterpret_cast<double*>(smem_raw + ((stage_rows * sizeof(RowInfo) + 15) & ~15));
+    double* s_ebuf = reinterpret_cast<double*>(smem_raw + ((t_chunk * sizeof(RowInfo) + 15) & ~15));
     const int lane = threadIdx.x & 31;
     // first pair slot of the warp; the warp owns NS sets of 32 consecutive pairs
     const long long w0 = ((long long)blockIdx.x * BT + threadIdx.x - lane) * NS;
@@ -324,48 +326,52 @@ __global__ void __launch_bounds__(BT, MINB) k_combine_coef(const DevTables d, do
     const int it_begin = d.t0 + blockIdx.y * t_chunk;
     const int it_end = min(d.t1, it_begin + t_chunk);
     const long long pre0 = __ldg(d.pre_t + d.t0), preW = __ldg(d.pre_t + d.w_t0), nine_S = 9 * d.S_s;
-    for (int it0 = it_begin; it0 < it_end; it0 += stage_rows) {
-        const int nrow = min(stage_rows, it_end - it0);
-        if (it0 != it_begin)
-            __syncthreads();
-        for (int rr = threadIdx.x; rr < nrow; rr += BT) {
-            const int it = it0 + rr;
-            s_row[rr].base = nine_S * (__ldg(d.pre_t + it) - pre0) - d.out_base;
-            s_row[rr].lt = __ldg(d.len_t + it) | row_edge(d, it) << 8;
-            s_row[rr].mask = 0;
-        }
-        // coefficient rows of the staged thickness rows: s_e[row][k][k_stride]
-        // (16-byte chunks); each thread copies the same (k, chunk) of every
-        // rows_per_pass-th row, its indices fixed for the whole kernel
+    for (int rr = threadIdx.x; rr < it_end - it_begin; rr += BT) {
+        const int it = it_begin + rr;
+        s_row[rr].base = nine_S * (__ldg(d.pre_t + it) - pre0) - d.out_base;
+        s_row[rr].lt = __ldg(d.len_t + it) | row_edge(d, it) << 8;
+        s_row[rr].mask = 0;
+    }
+    const int stage_doubles = stage_rows * lt_max * k_stride;
+    const double* eb = d.Etab + 3 * a_lo * kEStride;
+    // issue the cp.async copies of stage rows [i0, i0 + stage_rows) into buf
+    // (16-byte chunks; neighbours k >= L_t(it) are zero-filled)
+    auto issue = [&](int i0, double* buf) {
+        const int nrow = min(stage_rows, it_end - i0);
+        const int per_k = k_stride / 2;
         if (st_rows > 0) {
             for (int rr = st_r; st_h >= 0 && rr < nrow; rr += st_rows) {
-                const int it = it0 + rr;
-                double2 v = make_double2(0.0, 0.0);
-                if (st_k < __ldg(d.len_t + it)) {
-                    const long long pq = __ldg(d.pre_t + it) - preW + st_k;
-                    v = __ldg(reinterpret_cast<const double2*>(d.Etab + pq * kEPair + 3 * a_lo * kEStride) + st_h);
-                }
-                reinterpret_cast<double2*>(s_e)[(rr * lt_max + st_k) * (k_stride / 2) + st_h] = v;
+                const int it = i0 + rr;
+                const bool ok = st_k < __ldg(d.len_t + it);
+                const double* src = ok ? eb + (__ldg(d.pre_t + it) - preW + st_k) * kEPair + 2 * st_h : eb;
+                cp_async16(buf + ((rr * lt_max + st_k) * per_k + st_h) * 2, src, ok);
             }
         } else {
-            const int per_k = k_stride / 2;
             for (int idx = threadIdx.x; idx < nrow * lt_max * per_k; idx += BT) {
                 const int rk = idx / per_k, h = idx - rk * per_k;
-                const int rr = rk / lt_max, k = rk - rr * lt_max;
-                const int it = it0 + rr;
-                double2 v = make_double2(0.0, 0.0);
-                if (k < __ldg(d.len_t + it)) {
-                    const long long pq = __ldg(d.pre_t + it) - preW + k;
-                    v = __ldg(reinterpret_cast<const double2*>(d.Etab + pq * kEPair + 3 * a_lo * kEStride) + h);
-                }
-                reinterpret_cast<double2*>(s_e)[idx] = v;
+                const int rr = rk / lt_max, kk = rk - rr * lt_max;
+                const int it = i0 + rr;
+                const bool ok = kk < __ldg(d.len_t + it);
+                const double* src = ok ? eb + (__ldg(d.pre_t + it) - preW + kk) * kEPair + 2 * h : eb;
+                cp_async16(buf + 2 * idx, src, ok);
             }
         }
+        cp_async_commit();
+    };
+    if (it_begin < it_end)
+        issue(it_begin, s_ebuf);
+    int stage = 0;
+    for (int it0 = it_begin; it0 < it_end; it0 += stage_rows, ++stage) {
+        const int nrow = min(stage_rows, it_end - it0);
+        double* const s_e = s_ebuf + (stage & 1) * stage_doubles;
+        if (it0 + stage_rows < it_end)
+            issue(it0 + stage_rows, s_ebuf + ((stage + 1) & 1) * stage_doubles);
+        else
+            cp_async_commit(); // empty group: the wait below always leaves one group pending
+        cp_async_wait1();
         __syncthreads();
-        if (!live)
-            continue;
-        for (int rr = 0; rr < nrow; ++rr) {
-            const RowInfo ri = s_row[rr];
+        for (int rr = 0; live && rr < nrow; ++rr) {
+            const RowInfo ri = s_row[it0 - it_begin + rr];
             const int lt = ri.lt & 0xff, edge = ri.lt >> 8;
             const unsigned lv = live & ((edge & 1) ? in_s0 : ~0u) & ((edge & 2) ? in_s1 : ~0u);
             // 32-bit offsets inside the row block (< 9 S_s L_t values) from one
@@ -417,7 +423,9 @@ __global__ void __launch_bounds__(BT, MINB) k_combine_coef(const DevTables d, do
                     }
             }
         }
+        __syncthreads(); // every warp is done with this buffer before the next issue refills it
     }
+    cp_async_wait0();
 }
 
 } // namespace
@@ -469,8 +477,9 @@ int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t st
         const int nab = s_pad >= (long long)BT * NS ? 6 : 9;
         int stage_rows = (int)((32 * 1024) / ((size_t)lt_max * nab * kEStride * sizeof(double)));
         stage_rows = std::max(1, std::min(stage_rows, t_chunk));
-        const size_t smem = ((stage_rows * sizeof(RowInfo) + 15) & ~size_t(15)) +
-                            (size_t)stage_rows * lt_max * nab * kEStride * sizeof(double);
+        // the chunk's rows + two coefficient-row stage buffers
+        const size_t smem = ((t_chunk * sizeof(RowInfo) + 15) & ~size_t(15)) +
+                            2 * (size_t)stage_rows * lt_max * nab * kEStride * sizeof(double);
         auto kern = k_combine_coef<BT, NS, MINB>;
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
