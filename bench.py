@@ -230,12 +230,18 @@ def cpu_baseline(args):
     plies = choose_sample_plies(ref, a, threads, budget_s=20.0)
     prob = P.baseline_config(args.config, plies=plies)
     nnz = P.sizes(prob)["nnz"]
+    import resource
+    ru0 = resource.getrusage(resource.RUSAGE_SELF)
     t0 = time.perf_counter()
     ref.assemble(prob, "fast", threads)
     dt = time.perf_counter() - t0
+    ru1 = resource.getrusage(resource.RUSAGE_SELF)
+    cpu_s = (ru1.ru_utime - ru0.ru_utime) + (ru1.ru_stime - ru0.ru_stime)
     return {"value": nnz / dt, "unit": "nnz/s", "cores": threads, "kind": "reference",
+            "effective_parallelism": cpu_s / dt if dt > 0 else None,
             "sample": f"{args.config} family with {plies} plies ({nnz} nnz), one assembleFast, "
-                      f"reference sources compiled with the Eigen subset, threads={threads}"}
+                      f"reference sources compiled with the Eigen subset, threads={threads} "
+                      f"(AssemblyOptions.threads; its merge and stable_sort are serial)"}
 
 
 def device_step_time(plans, vals_ptrs, steps, warmup, stream, world, dist_backend):
