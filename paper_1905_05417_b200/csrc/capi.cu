@@ -431,13 +431,15 @@ void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void
         }
         if (want_values) {
             // two-phase K6: element-local blocks of as many spans per batch as
-            // fit ~4 GB (or a fifth of the free memory), one span at least
+            // fit 4 GB, one span at least.  The batch size depends on the
+            // problem only (not on free memory) and batches are aligned to
+            // absolute span multiples (launch_standard), so a row slab sums
+            // its entries exactly as the whole matrix does: bitwise equal rows
+            // on any partition.
             const std::size_t nl3 = static_cast<std::size_t>(d.pu + 1) * (d.pv + 1) * (d.pt + 1);
             const std::size_t per_blk = 9 * (d.sym ? nl3 * (nl3 + 1) / 2 : nl3 * nl3);
             const std::size_t per_span = static_cast<std::size_t>(d.nspu) * d.nspv * per_blk * sizeof(double);
-            std::size_t free_b = 0, total_b = 0;
-            CK(cudaMemGetInfo(&free_b, &total_b));
-            const std::size_t budget = std::min<std::size_t>(std::size_t(4) << 30, free_b / 5);
+            const std::size_t budget = std::size_t(4) << 30;
             d.ks_batch = static_cast<int>(std::max<std::size_t>(
                 1, std::min<std::size_t>(static_cast<std::size_t>(d.nspt), budget / std::max<std::size_t>(1, per_span))));
             d.Ks = ar.alloc<double>(per_span / sizeof(double) * static_cast<std::size_t>(d.ks_batch));

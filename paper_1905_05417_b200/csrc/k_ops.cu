@@ -400,39 +400,38 @@ __global__ void k_inplane_gather(const DevTables d, int t0) {
 // warps to hide its loads), + L2 prefetch of the += targets 76.5 / 81.5;
 // two-phase 62.6 / 82.0, with the pair-symmetric gather (every stored block
 // read once) 60.1 / 80.7 (KP = 3, 4 at 8 warps/SM: 76-78 / 99-106).
-#ifndef LF_K6_MINB
-#define LF_K6_MINB 2
-#endif
-#ifndef LF_K6_PAIRS
-#define LF_K6_PAIRS 2
-#endif
-constexpr int kK6Pairs = LF_K6_PAIRS; // pairs per thread
+// Pairs per thread and blocks per SM are template parameters of phase 1:
+// p = 3 (nl3 = 48) runs best at KP = 2, 16 warps/SM (C3 56.3 ms against 67.3
+// at KP = 1, 32 warps); p <= 2 (nl3 = 27) the other way round (C4 67.7
+// against 75.7 ms), profiles/r2_k6_occ.txt.
 
-/// Pair group g of an element block: al and the first be of kK6Pairs
-/// consecutive be (be >= al when the tables are symmetric).
+/// Pair group g of an element block: al and the first be of KP consecutive
+/// be (be >= al when the tables are symmetric).
+template <int KP>
 __device__ __forceinline__ void k6_group(int g, int nl3, bool sym, int& al, int& be0) {
     if (sym) {
         al = 0;
-        int per = (nl3 + kK6Pairs - 1) / kK6Pairs;
+        int per = (nl3 + KP - 1) / KP;
         while (g >= per) {
             g -= per;
             ++al;
-            per = (nl3 - al + kK6Pairs - 1) / kK6Pairs;
+            per = (nl3 - al + KP - 1) / KP;
         }
-        be0 = al + g * kK6Pairs;
+        be0 = al + g * KP;
     } else {
-        const int per = (nl3 + kK6Pairs - 1) / kK6Pairs;
+        const int per = (nl3 + KP - 1) / KP;
         al = g / per;
-        be0 = (g % per) * kK6Pairs;
+        be0 = (g % per) * KP;
     }
 }
 
+template <int KP>
 __host__ __device__ inline int k6_groups(int nl3, bool sym) {
     if (!sym)
-        return nl3 * ((nl3 + kK6Pairs - 1) / kK6Pairs);
+        return nl3 * ((nl3 + KP - 1) / KP);
     int n = 0;
     for (int al = 0; al < nl3; ++al)
-        n += (nl3 - al + kK6Pairs - 1) / kK6Pairs;
+        n += (nl3 - al + KP - 1) / KP;
     return n;
 }
 
@@ -457,8 +456,8 @@ __device__ __forceinline__ int k6_pair_index(int al, int be, int nl3, bool sym) 
 /// loop reads the table from shared memory either way: reading it from the
 /// constant bank measured C4 71.5 ms but C3 65.1 against 60.1 ms (the
 /// register-indexed constant loads set the pace), profiles/r2_k6_const.txt.
-template <bool CONSTC>
-__global__ void __launch_bounds__(256, LF_K6_MINB) k_standard_local(const DevTables d, int ks0,
+template <bool CONSTC, int KP, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_standard_local(const DevTables d, int ks0,
                                                                     const __grid_constant__ K6Const cst) {
     extern __shared__ double sm[];
     ElemInfo el;
@@ -491,7 +490,7 @@ __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard_local(const DevTab
     double* tau = w3 + d.nqt; // [at][bt][i][j]
     element_tables(d, el, gh, w2);
     const bool sym = d.sym != 0;
-    const int ngroup = k6_groups(nl3, sym);
+    const int ngroup = k6_groups<KP>(nl3, sym);
     const long long per_blk = 9LL * (sym ? nl3 * (nl3 + 1) / 2 : nl3 * nl3);
     double* kb = d.Ks + ((long long)blockIdx.y * (d.nspu * d.nspv) + e_index) * per_blk;
     for (int c = c0; c < c1; ++c) {
@@ -528,22 +527,22 @@ __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard_local(const DevTab
         __syncthreads();
         for (int g = threadIdx.x; g < ngroup; g += blockDim.x) {
             int al, be0;
-            k6_group(g, nl3, sym, al, be0);
+            k6_group<KP>(g, nl3, sym, al, be0);
             const int at = al / el.nl2, as = al % el.nl2;
-            int bs[kK6Pairs], bt[kK6Pairs];
-            bool pv[kK6Pairs];
+            int bs[KP], bt[KP];
+            bool pv[KP];
 #pragma unroll
-            for (int p = 0; p < kK6Pairs; ++p) {
+            for (int p = 0; p < KP; ++p) {
                 const int be = be0 + p;
                 pv[p] = be < nl3;
                 const int bec = pv[p] ? be : al;
                 bt[p] = bec / el.nl2;
                 bs[p] = bec % el.nl2;
             }
-            double acc[kK6Pairs][9];
-            double tp[kK6Pairs][4];
+            double acc[KP][9];
+            double tp[KP][4];
 #pragma unroll
-            for (int p = 0; p < kK6Pairs; ++p) {
+            for (int p = 0; p < KP; ++p) {
 #pragma unroll
                 for (int k = 0; k < 9; ++k)
                     acc[p][k] = 0.0;
@@ -554,9 +553,9 @@ __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard_local(const DevTab
             for (int q2 = 0; q2 < el.nq2; ++q2) {
                 const double* ga = gh + (q2 * el.nl2 + as) * 3;
                 const double a0 = ga[0], a1 = ga[1], a2 = ga[2];
-                double gb[kK6Pairs][3];
+                double gb[KP][3];
 #pragma unroll
-                for (int p = 0; p < kK6Pairs; ++p) {
+                for (int p = 0; p < KP; ++p) {
                     const double* b = gh + (q2 * el.nl2 + bs[p]) * 3;
                     gb[p][0] = b[0];
                     gb[p][1] = b[1];
@@ -570,7 +569,7 @@ __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard_local(const DevTab
                     const double2 r0 = C2[xy * 5], r1 = C2[xy * 5 + 1], r2 = C2[xy * 5 + 2], r3 = C2[xy * 5 + 3],
                                   r4 = C2[xy * 5 + 4];
 #pragma unroll
-                    for (int p = 0; p < kK6Pairs; ++p) {
+                    for (int p = 0; p < KP; ++p) {
                         const double s = gx * gb[p][y] * tp[p][(x == 2 ? 2 : 0) + (y == 2 ? 1 : 0)];
                         acc[p][0] = fma(r0.x, s, acc[p][0]);
                         acc[p][1] = fma(r0.y, s, acc[p][1]);
@@ -585,7 +584,7 @@ __global__ void __launch_bounds__(256, LF_K6_MINB) k_standard_local(const DevTab
                 }
             }
 #pragma unroll
-            for (int p = 0; p < kK6Pairs; ++p) {
+            for (int p = 0; p < KP; ++p) {
                 if (!pv[p])
                     continue;
                 double* o = kb + 9LL * k6_pair_index(al, be0 + p, nl3, sym);
@@ -1190,10 +1189,12 @@ int launch_standard(const DevTables& d, double* values, long long nnz, cudaStrea
     // two-phase: batches of ks_batch spans, local blocks then the gather
     const bool constc = cst && cst->n_cfg > 0;
     static const K6Const none{}; // n_cfg = 0
-    if (smem > 48 * 1024) {
-        cudaFuncSetAttribute(k_standard_local<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_standard_local<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    }
+    const bool small = (d.pu + 1) * (d.pv + 1) * (d.pt + 1) <= 32; // nl3: p <= 2 layouts
+    auto local = [&](auto kern, unsigned nel, int ks0, int nks) {
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<dim3(nel, (unsigned)nks), 256, smem, stream>>>(d, ks0, constc ? *cst : none);
+    };
     // spans with a row in the slab
     int ks_lo = 0, ks_hi = d.nspt;
     while (ks_lo < d.nspt && d.spt_first_h[ks_lo] + d.pt < d.t0)
@@ -1201,12 +1202,15 @@ int launch_standard(const DevTables& d, double* values, long long nnz, cudaStrea
     while (ks_hi > ks_lo && d.spt_first_h[ks_hi - 1] >= d.t1)
         --ks_hi;
     const unsigned nel = (unsigned)(d.nspu * d.nspv);
-    for (int ks0 = ks_lo; ks0 < ks_hi; ks0 += d.ks_batch) {
-        const int ks1 = std::min(ks_hi, ks0 + d.ks_batch);
-        if (constc)
-            k_standard_local<true><<<dim3(nel, (unsigned)(ks1 - ks0)), 256, smem, stream>>>(d, ks0, *cst);
+    // batches aligned to absolute multiples of ks_batch (bitwise-identical sums on any slab)
+    for (int ks0 = ks_lo; ks0 < ks_hi;) {
+        const int ks1 = std::min(ks_hi, (ks0 / d.ks_batch + 1) * d.ks_batch);
+        if (small)
+            constc ? local(k_standard_local<true, 1, 4>, nel, ks0, ks1 - ks0)
+                   : local(k_standard_local<false, 1, 4>, nel, ks0, ks1 - ks0);
         else
-            k_standard_local<false><<<dim3(nel, (unsigned)(ks1 - ks0)), 256, smem, stream>>>(d, ks0, none);
+            constc ? local(k_standard_local<true, 2, 2>, nel, ks0, ks1 - ks0)
+                   : local(k_standard_local<false, 2, 2>, nel, ks0, ks1 - ks0);
         // rows of the batch's spans inside the slab
         const int it_lo = std::max(d.t0, d.spt_first_h[ks0]);
         const int it_hi = std::min(d.t1, d.spt_first_h[ks1 - 1] + d.pt + 1);
@@ -1216,6 +1220,7 @@ int launch_standard(const DevTables& d, double* values, long long nnz, cudaStrea
         }
         if (launches)
             *launches += 2;
+        ks0 = ks1;
     }
     return (int)cudaGetLastError();
 }

@@ -103,3 +103,30 @@ def test_c5_function_range_cuts_match_oracle(gpu, oracle, parts):
         assert_csr_match(got, want, RTOL)
     assert max(terms.function_offset(c) for c in cuts) > 2 ** 32 or parts == 3
     terms.close()
+
+
+def test_c3_standard_slab_rows_are_bitwise_rows_of_the_full_matrix(gpu):
+    """The standard (K6) two-phase assembly sums each entry per batch of
+    thickness spans; batches are aligned to absolute span multiples, so a row
+    slab whose rows straddle a batch boundary (C3: 12 spans per 4 GiB batch,
+    boundary between spans 11 and 12, i.e. at thickness function 24, shared by
+    both) gets bitwise the full matrix's rows."""
+    import torch
+    prob = P.baseline_config("C3")
+    ns = prob.n_s
+    full = gpu.Plan(prob, "standard", 0)
+    vals = torch.empty(full.nnz, dtype=torch.float64, device="cuda")
+    full.assemble(vals.data_ptr())
+    full.synchronize()
+    for f0, f1 in [(22 * ns + 17, 26 * ns - 5), (0, 3 * ns), (24 * ns, 25 * ns), (23 * ns + 3, 24 * ns + 9)]:
+        plan = gpu.Plan(prob, "standard", 0, f_begin=f0, f_end=f1)
+        sv = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
+        plan.assemble(sv.data_ptr())
+        plan.synchronize()
+        z0 = plan.nnz_begin
+        assert torch.equal(sv, vals[z0:z0 + plan.nnz]), (f0, f1)
+        plan.close()
+        del sv
+    full.close()
+    del vals
+    torch.cuda.empty_cache()
