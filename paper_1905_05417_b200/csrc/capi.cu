@@ -720,10 +720,16 @@ struct HostColumns {
             cut.push_back(lo);
         }
         cut.push_back(f1);
-        for (unsigned t = 0; t < nt; ++t) {
-            const int64_t a = cut[t], b = cut[t + 1];
-            if (a < b)
-                th.emplace_back([&s, a, b, cols, base] { lfb::fillColumns(s, a, b, cols + (lfb::functionOffset(s, a) - base)); });
+        try {
+            for (unsigned t = 0; t < nt; ++t) {
+                const int64_t a = cut[t], b = cut[t + 1];
+                if (a < b)
+                    th.emplace_back(
+                        [&s, a, b, cols, base] { lfb::fillColumns(s, a, b, cols + (lfb::functionOffset(s, a) - base)); });
+            }
+        } catch (...) { // no thread left running if one cannot be started
+            join();
+            throw;
         }
     }
     void join() {
