@@ -1,0 +1,8 @@
+# round-2: symmetric K2b (half the family blocks, transposes in the gather): parity and A/B
+set -x
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_debug_checks.py tests/test_gpu_fuzz.py tests/test_gpu_acceptance.py -q -x -m gpu > gpurun_out/r2_tests_k2bsym.log 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/r2_tests_k2bsym.log
+for rep in 1 2; do for m in sym nosym; do for c in C3 C4 C2; do
+  echo -n "$m $c: "; if [ $m = nosym ]; then export LAMFAST_NO_SYM=1; else unset LAMFAST_NO_SYM; fi
+  timeout 120 python tools/run_steps.py --config $c --geometry bilinear --steps 10 2>&1 | tail -1 | cut -c1-100; done; done; done > gpurun_out/r2_k2b_sym.txt 2>&1
+grep -v "^+" gpurun_out/r2_k2b_sym.txt
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_k2b_sym_launches.csv python tools/run_steps.py --config C3 --geometry bilinear --steps 1 > /dev/null 2>&1; echo "ncu rc=$?"
