@@ -244,6 +244,8 @@ void upload_thickness(const lfb::Setup& s, DeviceArena& ar, lfb::DevTables& d, c
     d.len_t = ar.upload(at.len);
     d.pre_t = reinterpret_cast<const long long*>(ar.upload(at.pre));
     d.lt_max = at.max_len;
+    d.len_t_h = at.len.data(); // `at` outlives the tables (the plan's setup)
+    d.pre_t_h = reinterpret_cast<const long long*>(at.pre.data());
     const std::size_t ntp = static_cast<std::size_t>(d.ncells) * d.nqt;
     d.Bt_val = ar.alloc<double>(ntp * (d.pt + 1));
     d.Bt_der = ar.alloc<double>(ntp * (d.pt + 1));
@@ -1447,6 +1449,8 @@ int lf_combine(const lf_problem* p, int32_t n_terms, const double* blocks, const
             d.lt_max = 0;
             for (int it = 0; it < nt; ++it)
                 d.lt_max = std::max(d.lt_max, at.len[static_cast<std::size_t>(it)]);
+            d.len_t_h = at.len.data();
+            d.pre_t_h = reinterpret_cast<const long long*>(at.pre.data());
             d.nt = nt;
             d.n_terms = n_terms;
             d.n_passes = (n_terms + 7) / 8;
