@@ -274,6 +274,7 @@ struct lf_plan {
     DeviceArena arena;
     lfb::DevTables d{};
     lfb::K6Const k6c{}; // standard backend, affine map: K6 phase-1 tables (n_cfg = 0: not used)
+    std::vector<unsigned> row_mask; // terms reaching each thickness row (host; orders the combine's row tiles)
     int launches = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> free_events, pending;
     double kernel_ms = 0.0;
@@ -446,6 +447,20 @@ void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void
                 1, std::min<std::size_t>(static_cast<std::size_t>(d.nspt), budget / std::max<std::size_t>(1, per_span))));
             d.Ks = ar.alloc<double>(per_span / sizeof(double) * static_cast<std::size_t>(d.ks_batch));
         }
+    }
+    if (backend != LF_BACKEND_STANDARD && s.n_terms <= 32) {
+        // terms with a contributing cell in the support of each thickness function
+        plan->row_mask.assign(static_cast<std::size_t>(s.n_t), 0u);
+        const int L = p->n_layers;
+        for (std::size_t c = 0; c < s.cell_first.size(); ++c) {
+            unsigned m = 0;
+            for (int t = 0; t < s.n_terms; ++t)
+                if (s.lam_on[static_cast<std::size_t>(t) * L + s.cell_layer[c]])
+                    m |= 1u << t;
+            for (int i = s.cell_first[c]; i <= s.cell_first[c] + s.kt.p && i < s.n_t; ++i)
+                plan->row_mask[static_cast<std::size_t>(i)] |= m;
+        }
+        d.row_mask_h = plan->row_mask.data();
     }
     if (backend != LF_BACKEND_STANDARD) {
         d.W = ar.alloc<double>(static_cast<std::size_t>(std::max<long long>(1, d.n_pairs)) * d.n_terms * 4);

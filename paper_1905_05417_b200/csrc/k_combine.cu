@@ -433,11 +433,11 @@ __global__ void __launch_bounds__(BT, MINB) k_combine_coef(const DevTables d, do
 int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t stream, int* launches) {
     if (d.E == 0 || d.t1 <= d.t0)
         return 0;
-    // position-owned form (line-aligned stores) for single-pass per-term plans,
-    // explicit t_chunk or LAMFAST_COMBINE=entry: the entry-owned kernel below
+    // LAMFAST_COMBINE=pos: the position-owned form (k_combine_pos.cu) for
+    // single-pass per-term plans; default: the entry-owned kernel below
     if (t_chunk <= 0 && !d.Etab && d.n_passes == 1) {
         const char* form = std::getenv("LAMFAST_COMBINE");
-        if (!(form && form[0] == 'e')) {
+        if (form && form[0] == 'p') {
             const int rc = launch_combine_pos(d, out, stream);
             if (rc >= 0) {
                 if (launches)

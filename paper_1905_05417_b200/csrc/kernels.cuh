@@ -99,6 +99,9 @@ struct DevTables {
     // classes from them per launch); nullptr: entry-owned combine only
     const int* len_t_h;
     const long long* pre_t_h;
+    // host: terms with a contributing cell per thickness row (bit t), the order
+    // of the rows inside a class; nullptr: rows stay in i_t order
+    const unsigned* row_mask_h;
     // output range: the functions f = i_t * ns + i_s in [f0, f1), covering
     // thickness rows [t0, t1) -- row t0 from in-plane function s0, row t1 - 1
     // up to s1 (exclusive).  Entry (it, is, ...) of the range is written at
