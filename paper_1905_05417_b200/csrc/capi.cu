@@ -244,8 +244,6 @@ void upload_thickness(const lfb::Setup& s, DeviceArena& ar, lfb::DevTables& d, c
     d.len_t = ar.upload(at.len);
     d.pre_t = reinterpret_cast<const long long*>(ar.upload(at.pre));
     d.lt_max = at.max_len;
-    d.len_t_h = at.len.data(); // `at` outlives the tables (the plan's setup)
-    d.pre_t_h = reinterpret_cast<const long long*>(at.pre.data());
     const std::size_t ntp = static_cast<std::size_t>(d.ncells) * d.nqt;
     d.Bt_val = ar.alloc<double>(ntp * (d.pt + 1));
     d.Bt_der = ar.alloc<double>(ntp * (d.pt + 1));
@@ -274,7 +272,6 @@ struct lf_plan {
     DeviceArena arena;
     lfb::DevTables d{};
     lfb::K6Const k6c{}; // standard backend, affine map: K6 phase-1 tables (n_cfg = 0: not used)
-    std::vector<unsigned> row_mask; // terms reaching each thickness row (host; orders the combine's row tiles)
     int launches = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> free_events, pending;
     double kernel_ms = 0.0;
@@ -447,20 +444,6 @@ void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void
                 1, std::min<std::size_t>(static_cast<std::size_t>(d.nspt), budget / std::max<std::size_t>(1, per_span))));
             d.Ks = ar.alloc<double>(per_span / sizeof(double) * static_cast<std::size_t>(d.ks_batch));
         }
-    }
-    if (backend != LF_BACKEND_STANDARD && s.n_terms <= 32) {
-        // terms with a contributing cell in the support of each thickness function
-        plan->row_mask.assign(static_cast<std::size_t>(s.n_t), 0u);
-        const int L = p->n_layers;
-        for (std::size_t c = 0; c < s.cell_first.size(); ++c) {
-            unsigned m = 0;
-            for (int t = 0; t < s.n_terms; ++t)
-                if (s.lam_on[static_cast<std::size_t>(t) * L + s.cell_layer[c]])
-                    m |= 1u << t;
-            for (int i = s.cell_first[c]; i <= s.cell_first[c] + s.kt.p && i < s.n_t; ++i)
-                plan->row_mask[static_cast<std::size_t>(i)] |= m;
-        }
-        d.row_mask_h = plan->row_mask.data();
     }
     if (backend != LF_BACKEND_STANDARD) {
         d.W = ar.alloc<double>(static_cast<std::size_t>(std::max<long long>(1, d.n_pairs)) * d.n_terms * 4);
@@ -1464,8 +1447,6 @@ int lf_combine(const lf_problem* p, int32_t n_terms, const double* blocks, const
             d.lt_max = 0;
             for (int it = 0; it < nt; ++it)
                 d.lt_max = std::max(d.lt_max, at.len[static_cast<std::size_t>(it)]);
-            d.len_t_h = at.len.data();
-            d.pre_t_h = reinterpret_cast<const long long*>(at.pre.data());
             d.nt = nt;
             d.n_terms = n_terms;
             d.n_passes = (n_terms + 7) / 8;

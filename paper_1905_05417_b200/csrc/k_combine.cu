@@ -433,19 +433,6 @@ __global__ void __launch_bounds__(BT, MINB) k_combine_coef(const DevTables d, do
 int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t stream, int* launches) {
     if (d.E == 0 || d.t1 <= d.t0)
         return 0;
-    // LAMFAST_COMBINE=pos: the position-owned form (k_combine_pos.cu) for
-    // single-pass per-term plans; default: the entry-owned kernel below
-    if (t_chunk <= 0 && !d.Etab && d.n_passes == 1) {
-        const char* form = std::getenv("LAMFAST_COMBINE");
-        if (form && form[0] == 'p') {
-            const int rc = launch_combine_pos(d, out, stream);
-            if (rc >= 0) {
-                if (launches)
-                    ++*launches;
-                return rc;
-            }
-        }
-    }
     const long long nblk = (d.E + kBlock - 1) / kBlock; // 256-entry sub-blocks
     const int nt = d.t1 - d.t0;
     if (t_chunk <= 0) {

@@ -95,13 +95,6 @@ struct DevTables {
     double* Ks;
     int ks_batch;
     const int* spt_first_h; // host copy of spt_first (the launcher's batch bounds)
-    // host copies of len_t / pre_t (the position-owned combine builds its row
-    // classes from them per launch); nullptr: entry-owned combine only
-    const int* len_t_h;
-    const long long* pre_t_h;
-    // host: terms with a contributing cell per thickness row (bit t), the order
-    // of the rows inside a class; nullptr: rows stay in i_t order
-    const unsigned* row_mask_h;
     // output range: the functions f = i_t * ns + i_s in [f0, f1), covering
     // thickness rows [t0, t1) -- row t0 from in-plane function s0, row t1 - 1
     // up to s1 (exclusive).  Entry (it, is, ...) of the range is written at
@@ -142,9 +135,6 @@ int launch_affine_export(const DevTables& d, cudaStream_t stream);
 /// block row; returns the number of kernels launched via *launches.
 int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t stream,
                    int* launches);
-/// Position-owned form of the combine (k_combine_pos.cu): line-aligned warp
-/// stores.  -1: outside its limits, the caller launches the entry-owned form.
-int launch_combine_pos(const DevTables& d, double* out, cudaStream_t stream);
 /// Coefficient form: Etab from W and Ct (after the setup kernels).
 int launch_pair_coeffs(const DevTables& d, cudaStream_t stream);
 int launch_pattern(const DevTables& d, long long* row_ptr, int* cols, cudaStream_t stream);

@@ -127,6 +127,75 @@ __device__ __forceinline__ PosDec decode_position(const DevTables& d, long long 
     return r;
 }
 
+/// Running decode of a lane's position across the consecutive 32-position
+/// groups of its warp: the in-plane function, row component, neighbour and
+/// offset inside the row segment advance by 32 values without a search or a
+/// division by a run-time row length.
+struct PosState {
+    int is, iu, iv, Lu, Lv, B; // in-plane function of the position, its neighbour counts, segment length 3 Lu Lv
+    int ebase;                 // first in-plane entry of is
+    int a, k, rem;             // row component, neighbour, offset inside the row segment
+    bool live;
+};
+
+__device__ __forceinline__ PosState start_position(const DevTables& d, long long o, int L, long long EL) {
+    PosState st;
+    st.live = o >= 0 && o < EL;
+    const unsigned oc = st.live ? (unsigned)o : 0u; // E L < 2^31 (launcher)
+    const unsigned e1 = oc / (unsigned)L;           // lies inside the entry range of the position's i_s
+    int is = __ldg(d.blk_is + e1 / kBlock);
+    while (__ldg(d.es_pre + is + 1) <= (long long)e1)
+        ++is;
+    st.is = is;
+    st.ebase = (int)__ldg(d.es_pre + is);
+    const int rr = (int)oc - L * st.ebase; // offset inside the (i_t, i_s) row block
+    st.iu = is % d.nu;
+    st.iv = is / d.nu;
+    st.Lu = __ldg(d.len_u + st.iu);
+    st.Lv = __ldg(d.len_v + st.iv);
+    st.B = 3 * st.Lu * st.Lv;
+    st.a = rr / (L * st.B);
+    const int r2 = rr - st.a * (L * st.B);
+    st.k = r2 / st.B;
+    st.rem = r2 - st.k * st.B;
+    return st;
+}
+
+/// 32 positions further (the position stays inside the class range: o + 32 < E L)
+__device__ __forceinline__ void advance_position(const DevTables& d, PosState& st, int L) {
+    st.rem += 32;
+    while (st.rem >= st.B) {
+        st.rem -= st.B;
+        if (++st.k == L) {
+            st.k = 0;
+            if (++st.a == 3) {
+                st.a = 0;
+                st.ebase += 3 * st.B; // 9 Lu Lv entries per in-plane function
+                ++st.is;
+                if (++st.iu == d.nu) {
+                    st.iu = 0;
+                    ++st.iv;
+                    st.Lv = __ldg(d.len_v + st.iv);
+                }
+                st.Lu = __ldg(d.len_u + st.iu);
+                st.B = 3 * st.Lu * st.Lv;
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ PosDec state_fields(const DevTables& d, const PosState& st) {
+    PosDec r;
+    const int s = st.rem / 3, b = st.rem - 3 * s;
+    const int sv = s / st.Lu, su = s - sv * st.Lu;
+    r.info = st.k | (3 * st.a + b) << 8 | (st.is >= d.s0 ? 1 << 12 : 0) | (st.is < d.s1 ? 1 << 13 : 0) |
+             (st.live ? 1 << 14 : 0);
+    r.uo = (st.iu * d.bu + su) * 4;
+    r.vo = (st.iv * d.bv + sv) * 4;
+    r.ec = st.ebase + st.a * st.B + st.rem;
+    return r;
+}
+
 /// Affine P of family j of one in-plane entry for NT terms (affine_p,
 /// combine_common.cuh, one family per lane): s_ct = C~ in shared memory.
 template <int NT>
@@ -160,13 +229,102 @@ __device__ __forceinline__ int tile_position(int tl, int n) {
     return 16 * (tl >> 1) + 4 * (n >> 1) + 2 * (tl & 1) + (n & 1);
 }
 
-template <int NT, int NTILE, bool AFFINE, int BT, int MINB>
+/// 32-bit shared-window address and loads through it: the row loop keeps no
+/// generic pointer to shared memory (the generic form rematerialised the
+/// window base, S2UR SR_CgaCtaId, once per row tile).
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ double lds_f64(unsigned a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint4 lds_u128(unsigned a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+
+/// Rows of one job for the warp's current positions and the neighbours
+/// (k0, k1): Pa / Pb are the B operands of the positions with neighbour k0 /
+/// k1 (exact zeros elsewhere), so a tile that holds both neighbours takes one
+/// DMMA per neighbour and nothing is selected inside the loop.  TWO = false:
+/// every position of the warp has neighbour k0.
+template <int NT, int NTILE, bool TWO>
+__device__ __forceinline__ void mma_rows(const DevTables& d, double* __restrict__ out, double* const o_lane,
+                                         const double (&Pa)[NTILE][NT], const double (&Pb)[NTILE][NT],
+                                         unsigned pair_a, unsigned pair_b, unsigned srow_a, unsigned sw_a0,
+                                         unsigned sw_a1, int nrow8, int rs, bool fast_store, const int (&qinfo)[NTILE / 2][4],
+                                         int k0, int k1) {
+    const unsigned w_step = (unsigned)rs * 8u * (unsigned)sizeof(double);
+    for (int rt = 0; rt < nrow8; rt += 8, srow_a += 8u * (unsigned)sizeof(PosRow), sw_a0 += w_step, sw_a1 += w_step) {
+        const uint4 ri = lds_u128(srow_a); // base (lo, hi), term mask of the tile, edge | tile edges << 8
+        const unsigned tmask = ri.z;
+        double D[NTILE][2];
+#pragma unroll
+        for (int tl = 0; tl < NTILE; ++tl)
+            D[tl][0] = D[tl][1] = 0.0;
+#ifndef LF_STORE_ONLY
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+            if (tmask & (1u << t)) {
+                const double a0 = lds_f64(sw_a0 + t * 32);
+                if constexpr (!TWO) {
+#pragma unroll
+                    for (int tl = 0; tl < NTILE; ++tl)
+                        dmma_884(D[tl][0], D[tl][1], a0, Pa[tl][t]);
+                } else {
+                    const double a1 = lds_f64(sw_a1 + t * 32);
+#pragma unroll
+                    for (int h = 0; h < NTILE / 2; ++h) {
+                        if (pair_a & (1u << h)) {
+                            dmma_884(D[2 * h][0], D[2 * h][1], a0, Pa[2 * h][t]);
+                            dmma_884(D[2 * h + 1][0], D[2 * h + 1][1], a0, Pa[2 * h + 1][t]);
+                        }
+                        if (pair_b & (1u << h)) {
+                            dmma_884(D[2 * h][0], D[2 * h][1], a1, Pb[2 * h][t]);
+                            dmma_884(D[2 * h + 1][0], D[2 * h + 1][1], a1, Pb[2 * h + 1][t]);
+                        }
+                    }
+                }
+            }
+#endif
+        const long long base = (long long)(((unsigned long long)ri.y << 32) | ri.x);
+        const int edge = (int)(ri.w & 0xffu);
+        if (fast_store && (ri.w >> 8) == 0) {
+            const bool row_ok = edge == 0; // padding rows of the last tile are not written
+            double* const p = o_lane + base;
+#pragma unroll
+            for (int h = 0; h < NTILE / 2; ++h) {
+                LF_CHECK(!row_ok || (p + 16 * h >= out && p + 16 * h + 3 < out + d.nnz_slab));
+                store_value4(p + 16 * h, D[2 * h][0], D[2 * h][1], D[2 * h + 1][0], D[2 * h + 1][1], row_ok);
+            }
+        } else {
+            // warps at the ends of the class range, warps with a third
+            // neighbour, and tiles with a partial first / last row of a
+            // function range: one predicated store per value
+#pragma unroll
+            for (int h = 0; h < NTILE / 2; ++h)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int info = qinfo[h][c];
+                    const unsigned flags = (info >> 12) & 3u;
+                    const int k = info & 0xff;
+                    const bool pred = ((info >> 14) & 1) && (k == k0 || k == k1) && edge < 4 &&
+                                      ((unsigned)edge & ~flags) == 0;
+                    double* const p = o_lane + base + 16 * h + c;
+                    LF_CHECK(!pred || (p >= out && p < out + d.nnz_slab));
+                    store_value_if(p, D[2 * h + (c >> 1)][c & 1], pred);
+                }
+        }
+    }
+}
+
+template <int NT, int NTILE, bool AFFINE, int BT, int MINB, int G>
 __global__ void __launch_bounds__(BT, MINB)
     k_combine_mma(const __grid_constant__ DevTables d, const __grid_constant__ PosParams pp,
                   double* __restrict__ out) {
-    static_assert(NTILE == 4 || NTILE == 8, "32 or 64 positions per warp");
-    constexpr int WP = 8 * NTILE;   // positions per warp
-    constexpr int ND = NTILE / 4;   // positions decoded per lane
+    static_assert(NTILE == 4, "32 positions per warp and group");
+    constexpr int WP = 8 * NTILE; // positions per warp and group
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // job of this block
     int jlo = 0, jhi = pp.n_jobs; // jobs[jlo].first_block <= blockIdx.x < jobs[jhi].first_block
@@ -188,7 +346,6 @@ __global__ void __launch_bounds__(BT, MINB)
 
     const int lane = threadIdx.x & 31, g = lane >> 2, j = lane & 3;
     const long long EL = d.E * L;
-    const long long tau_w = xb * ((BT / 32) * WP) + (threadIdx.x >> 5) * WP; // first position of the warp
 
     // stage C~, the job's rows and their weights s_w[row][k][term][family]
     if constexpr (AFFINE)
@@ -201,18 +358,23 @@ __global__ void __launch_bounds__(BT, MINB)
         for (int rr = threadIdx.x; rr < nrow8; rr += BT) {
             PosRow ri;
             ri.base = 0;
-            ri.mask = 0;
             ri.edge = 4;
-            if (rr < nrow) {
-                const int it = pp.rows[row0 + rr];
+            // term mask and edge bits of the row's 8-row tile
+            unsigned m = 0, te = 0;
+            for (int r8 = rr & ~7; r8 < (rr & ~7) + 8 && r8 < nrow; ++r8) {
+                const int it = pp.rows[row0 + r8];
                 const long long pre = __ldg(d.pre_t + it);
-                unsigned m = 0;
                 for (int k = 0; k < L; ++k)
                     m |= __ldg(d.Wmask + (pre - preW) + k);
-                ri.base = nine_S * (pre - pre0) - d.out_base - phi;
-                ri.mask = m;
+                te |= (unsigned)row_edge(d, it);
+            }
+            if (rr < nrow) {
+                const int it = pp.rows[row0 + rr];
+                ri.base = nine_S * (__ldg(d.pre_t + it) - pre0) - d.out_base - phi;
                 ri.edge = row_edge(d, it);
             }
+            ri.mask = m;
+            ri.edge |= (int)(te << 8);
             s_row[rr] = ri;
         }
         // a row's weights [k][term][family] are contiguous in W (single pass: n_terms = NT)
@@ -222,130 +384,105 @@ __global__ void __launch_bounds__(BT, MINB)
             if (rr < nrow)
                 src = reinterpret_cast<const double2*>(d.W) +
                       (__ldg(d.pre_t + pp.rows[row0 + rr]) - preW) * (NT * 2);
-            double2* dst = reinterpret_cast<double2*>(s_w + (size_t)rr * rs);
+            double* dst = s_w + (size_t)rr * rs;
             for (int c = lane; c < per_row; c += 32)
-                dst[c] = src ? __ldg(src + c) : make_double2(0.0, 0.0);
+                cp_async16(dst + 2 * c, src ? reinterpret_cast<const double*>(src + c) : d.W, src != nullptr);
         }
+        cp_async_commit();
+        cp_async_wait0();
     }
+    __syncthreads(); // C~, rows and weights visible; no block-wide barrier below
 
-    // decode the warp's positions, one (or two) per lane
-    PosDec dec[ND];
-#pragma unroll
-    for (int x = 0; x < ND; ++x)
-        dec[x] = decode_position(d, tau_w + 32 * x + lane - phi, L, EL);
-    unsigned kmask = 0, all_live = 1;
-#pragma unroll
-    for (int x = 0; x < ND; ++x) {
-        const bool lv = (dec[x].info >> 14) & 1;
-        kmask |= __reduce_or_sync(0xffffffffu, lv ? 1u << (dec[x].info & 0xff) : 0u);
-        all_live &= __all_sync(0xffffffffu, lv) ? 1u : 0u;
-    }
-    __syncthreads(); // s_ct (and the staged rows) visible
-    if (kmask == 0)
-        return; // no live position in this warp
+    const unsigned srow_a = smem_u32(s_row) + (unsigned)g * (unsigned)sizeof(PosRow);
+    const unsigned sw_g = smem_u32(s_w) + (unsigned)(g * rs + j) * (unsigned)sizeof(double);
 
-    // B operands: lane (g, j) holds family j of the position in column g of every tile
-    double P[NTILE][NT];
-    int ksel[NTILE];
-    unsigned tk[NTILE]; // neighbours present in the tile (bit k)
-#pragma unroll
-    for (int tl = 0; tl < NTILE; ++tl) {
-        const int q = tile_position(tl, g);
-        const int src = q & 31, x = q >> 5;
-        int info = 0, uo = 0, vo = 0, ec = 0;
-#pragma unroll
-        for (int xx = 0; xx < ND; ++xx) {
-            const int i0 = __shfl_sync(0xffffffffu, dec[xx].info, src);
-            const int i1 = __shfl_sync(0xffffffffu, AFFINE ? dec[xx].uo : dec[xx].ec, src);
-            const int i2 = __shfl_sync(0xffffffffu, dec[xx].vo, src);
-            if (xx == x) {
-                info = i0;
-                uo = ec = i1;
-                vo = i2;
-            }
+    // a warp owns G consecutive 32-position groups
+    const long long tau_w0 = (xb * (BT / 32) + (threadIdx.x >> 5)) * (long long)(G * WP);
+    PosState st;
+    st.live = false;
+    for (int grp = 0; grp < G; ++grp) {
+        const long long tau_w = tau_w0 + grp * WP; // first position of the warp in this group
+        if (tau_w - phi >= EL)
+            break;
+        // decode the warp's positions, one per lane: a full decode for the
+        // first group (and for lanes before the start of the class range),
+        // 32 values further after that
+        {
+            const long long o = tau_w + lane - phi;
+            if (grp == 0 || !st.live)
+                st = start_position(d, o, L, EL);
+            else if (o < EL)
+                advance_position(d, st, L);
+            else
+                st.live = false;
         }
-        const bool lv = (info >> 14) & 1;
-        ksel[tl] = lv ? (info & 0xff) : -1;
-        tk[tl] = __reduce_or_sync(0xffffffffu, lv ? 1u << (info & 0xff) : 0u);
-        if constexpr (AFFINE) {
-            family_p<NT>(d, s_ct, uo, vo, (info >> 8) & 15, j, P[tl]);
-        } else {
-#pragma unroll
-            for (int t = 0; t < NT; ++t)
-                P[tl][t] = __ldg(d.Pg + ((long long)t * 4 + j) * d.E + ec);
-        }
-        if (!lv) {
-#pragma unroll
-            for (int t = 0; t < NT; ++t)
-                P[tl][t] = 0.0;
-        }
-    }
-    const bool one_k = (kmask & (kmask - 1)) == 0; // every position of the warp has the same neighbour
+        const PosDec dec = state_fields(d, st);
+        const bool lv0 = (dec.info >> 14) & 1;
+        const unsigned kmask = __reduce_or_sync(0xffffffffu, lv0 ? 1u << (dec.info & 0xff) : 0u);
+        const bool all_live = __all_sync(0xffffffffu, lv0);
+        if (kmask == 0)
+            continue; // no live position in this warp
 
-    double* const o_lane = out + tau_w + 4 * j; // + 16 h: the lane's four positions of tile pair h
-    for (int rt = 0; rt < nrow8; rt += 8) {
-        const PosRow ri = s_row[rt + g];
-        const unsigned tmask = __reduce_or_sync(0xffffffffu, ri.mask);
-        const unsigned edge = __reduce_or_sync(0xffffffffu, (unsigned)ri.edge & 3u);
-        double D[NTILE][2];
+        // positions of the lane's tile columns and of its stored values
+        int tinfo[NTILE], tuo[NTILE], tvo[NTILE];
 #pragma unroll
-        for (int tl = 0; tl < NTILE; ++tl)
-            D[tl][0] = D[tl][1] = 0.0;
-        const double* wrow = s_w + (size_t)(rt + g) * rs + j;
-        if (one_k) {
-            const double* wk = wrow + (31 - __clz(kmask)) * (NT * 4);
+        for (int tl = 0; tl < NTILE; ++tl) {
+            const int src = tile_position(tl, g);
+            tinfo[tl] = __shfl_sync(0xffffffffu, dec.info, src);
+            tuo[tl] = __shfl_sync(0xffffffffu, AFFINE ? dec.uo : dec.ec, src);
+            tvo[tl] = __shfl_sync(0xffffffffu, dec.vo, src);
+        }
+        int qinfo[NTILE / 2][4];
 #pragma unroll
-            for (int t = 0; t < NT; ++t)
-                if (tmask & (1u << t)) {
-                    const double a = wk[t * 4];
+        for (int h = 0; h < NTILE / 2; ++h)
 #pragma unroll
-                    for (int tl = 0; tl < NTILE; ++tl)
-                        dmma_884(D[tl][0], D[tl][1], a, P[tl][t]);
+            for (int c = 0; c < 4; ++c)
+                qinfo[h][c] = __shfl_sync(0xffffffffu, dec.info, 16 * h + 4 * j + c);
+        double* const o_lane = out + tau_w + 4 * j; // + 16 h: the lane's four positions of tile pair h
+
+        // neighbours two at a time (a warp's 32 consecutive positions hold one
+        // or two; three only where the row segments are shorter than 32 values)
+        bool first = true;
+        for (unsigned kleft = kmask; kleft; first = false) {
+            const int k0 = __ffs(kleft) - 1;
+            kleft &= kleft - 1;
+            const bool two = kleft != 0;
+            const int k1 = two ? __ffs(kleft) - 1 : k0;
+            kleft &= kleft - 1;
+            const bool fast_store = all_live && first && kleft == 0;
+
+            // B operands: lane (g, j) holds family j of the position in column g of every tile
+            double Pa[NTILE][NT], Pb[NTILE][NT];
+            unsigned pair_a = 0, pair_b = 0;
+#pragma unroll
+            for (int tl = 0; tl < NTILE; ++tl) {
+                const int info = tinfo[tl];
+                const bool lv = (info >> 14) & 1;
+                const int k = lv ? (info & 0xff) : -1;
+                double P[NT];
+                if constexpr (AFFINE) {
+                    family_p<NT>(d, s_ct, tuo[tl], tvo[tl], (info >> 8) & 15, j, P);
+                } else {
+#pragma unroll
+                    for (int t = 0; t < NT; ++t)
+                        P[t] = __ldg(d.Pg + ((long long)t * 4 + j) * d.E + tuo[tl]);
                 }
-        } else {
-            for (unsigned km = kmask; km; km &= km - 1) {
-                const int k = __ffs(km) - 1;
-                const double* wk = wrow + k * (NT * 4);
 #pragma unroll
-                for (int t = 0; t < NT; ++t)
-                    if (tmask & (1u << t)) {
-                        const double a = wk[t * 4];
-#pragma unroll
-                        for (int tl = 0; tl < NTILE; ++tl)
-                            if (tk[tl] & (1u << k))
-                                dmma_884(D[tl][0], D[tl][1], a, ksel[tl] == k ? P[tl][t] : 0.0);
-                    }
-            }
-        }
-        if (all_live && edge == 0) {
-            const bool row_ok = ri.edge == 0; // padding rows of the last tile are not written
-            double* const p = o_lane + ri.base;
-#pragma unroll
-            for (int h = 0; h < NTILE / 2; ++h) {
-                LF_CHECK(!row_ok || (p + 16 * h >= out && p + 16 * h + 3 < out + d.nnz_slab));
-                store_value4(p + 16 * h, D[2 * h][0], D[2 * h][1], D[2 * h + 1][0], D[2 * h + 1][1], row_ok);
-            }
-        } else {
-            // warps at the ends of the class range, and tiles with a partial
-            // first / last row of a function range: one predicated store per value
-#pragma unroll
-            for (int h = 0; h < NTILE / 2; ++h)
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const int q = 16 * h + 4 * j + c;
-                    int info = 0;
-#pragma unroll
-                    for (int xx = 0; xx < ND; ++xx) {
-                        const int i0 = __shfl_sync(0xffffffffu, dec[xx].info, q & 31);
-                        if (xx == (q >> 5))
-                            info = i0;
-                    }
-                    const unsigned flags = (info >> 12) & 3u;
-                    const bool pred = ((info >> 14) & 1) && ri.edge < 4 && ((unsigned)ri.edge & ~flags) == 0;
-                    double* const p = o_lane + ri.base + 16 * h + c;
-                    LF_CHECK(!pred || (p >= out && p < out + d.nnz_slab));
-                    store_value_if(p, D[2 * h + (c >> 1)][c & 1], pred);
+                for (int t = 0; t < NT; ++t) {
+                    Pa[tl][t] = k == k0 ? P[t] : 0.0;
+                    Pb[tl][t] = (two && k == k1) ? P[t] : 0.0;
                 }
+                pair_a |= __any_sync(0xffffffffu, k == k0) ? 1u << (tl >> 1) : 0u;
+                pair_b |= __any_sync(0xffffffffu, two && k == k1) ? 1u << (tl >> 1) : 0u;
+            }
+            const unsigned sw_a0 = sw_g + (unsigned)(k0 * NT * 4) * (unsigned)sizeof(double);
+            const unsigned sw_a1 = sw_g + (unsigned)(k1 * NT * 4) * (unsigned)sizeof(double);
+            if (two)
+                mma_rows<NT, NTILE, true>(d, out, o_lane, Pa, Pb, pair_a, pair_b, srow_a, sw_a0, sw_a1, nrow8, rs,
+                                          fast_store, qinfo, k0, k1);
+            else
+                mma_rows<NT, NTILE, false>(d, out, o_lane, Pa, Pb, pair_a, pair_b, srow_a, sw_a0, sw_a1, nrow8, rs,
+                                           fast_store, qinfo, k0, k1);
         }
     }
 }
@@ -454,13 +591,16 @@ int combine_pos_launch(const DevTables& d, double* out, const PosConfig& cfg, cu
 #define LF_POS_BT 256
 #endif
 #ifndef LF_POS_MINB
-#define LF_POS_MINB 3
+#define LF_POS_MINB 2
 #endif
-    constexpr int BT = LF_POS_BT, MINB = NT * NTILE <= 20 ? LF_POS_MINB : 2; // 80 registers up to 5 terms
+#ifndef LF_POS_G
+#define LF_POS_G 4 // 32-position groups per warp: the staged rows and weights serve G * 256 positions
+#endif
+    constexpr int BT = LF_POS_BT, MINB = LF_POS_MINB, G = LF_POS_G;
     static thread_local PosParams pp;
     long long total_blocks = 0;
     size_t smem = 0;
-    if (!build_pos_params(d, out, NT, (BT / 32) * 8 * NTILE, cfg, pp, total_blocks, smem))
+    if (!build_pos_params(d, out, NT, G * (BT / 32) * 8 * NTILE, cfg, pp, total_blocks, smem))
         return -1;
     if (std::getenv("LAMFAST_POS_DEBUG")) {
         std::fprintf(stderr, "combine_pos: NT=%d NTILE=%d align=%d jobs=%d blocks=%lld smem=%zu\n", NT, NTILE,
@@ -475,9 +615,9 @@ int combine_pos_launch(const DevTables& d, double* out, const PosConfig& cfg, cu
         kern<<<(unsigned)total_blocks, BT, smem, s>>>(d, pp, out);
     };
     if (d.affine)
-        launch(k_combine_mma<NT, NTILE, true, BT, MINB>);
+        launch(k_combine_mma<NT, NTILE, true, BT, MINB, G>);
     else
-        launch(k_combine_mma<NT, NTILE, false, BT, MINB>);
+        launch(k_combine_mma<NT, NTILE, false, BT, MINB, G>);
     return (int)cudaGetLastError();
 }
 
@@ -493,21 +633,21 @@ int env_int(const char* name, int dflt) {
 /// classes than the parameter tables hold, no host copy of the thickness
 /// adjacency): the caller falls back to the entry-owned kernel.
 int launch_combine_pos(const DevTables& d, double* out, cudaStream_t stream) {
-    if (d.n_passes != 1 || d.n_terms < 1 || d.n_terms > 7 || d.Etab)
+    if (d.n_passes != 1 || d.n_terms < 1 || d.n_terms > 4 || d.Etab)
         return -1;
     PosConfig cfg;
     cfg.align = env_int("LAMFAST_POS_ALIGN", 0);
     cfg.min_rows = env_int("LAMFAST_POS_MIN_ROWS", 8);
     cfg.smem = (size_t)env_int("LAMFAST_POS_SMEM_KB", 72) * 1024;
     if (cfg.align <= 0) {
-        // widest phase granularity that leaves the classes enough rows to
-        // amortise a warp's position decode and P (>= 24 rows per class on average)
-        const int nt = d.t1 - d.t0;
+        // rows per class first (they amortise a warp's position decode and P),
+        // then the widest phase granularity that keeps them: 96 rows per
+        // class on average, or what 32-byte phases already give
         cfg.align = 4;
-        if (d.pre_t_h && d.len_t_h)
-            for (int A = 32; A > 4; A /= 2) {
+        if (d.pre_t_h && d.len_t_h) {
+            const long long addr0 = (long long)(reinterpret_cast<uintptr_t>(out) / sizeof(double));
+            auto rows_per_class = [&](int A) {
                 std::map<std::pair<int, long long>, int> cnt;
-                const long long addr0 = (long long)(reinterpret_cast<uintptr_t>(out) / sizeof(double));
                 for (int it = d.t0; it < d.t1; ++it) {
                     const long long base = 9 * d.S_s * (d.pre_t_h[it] - d.pre_t_h[d.t0]) - d.out_base;
                     ++cnt[{d.len_t_h[it], (((addr0 + base) % A) + A) % A}];
@@ -518,11 +658,15 @@ int launch_combine_pos(const DevTables& d, double* out, cudaStream_t stream) {
                         ++big;
                         big_rows += c.second;
                     }
-                if (big == 0 || big_rows >= 24 * big || nt < 24) {
+                return big ? (double)big_rows / big : 0.0;
+            };
+            const double want = std::min(96.0, rows_per_class(4));
+            for (int A = 32; A > 4; A /= 2)
+                if (rows_per_class(A) >= want) {
                     cfg.align = A;
                     break;
                 }
-            }
+        }
     }
     cfg.align = std::max(4, cfg.align / 4 * 4); // 256-bit stores need 32-byte aligned quads
 #ifndef LF_POS_NTILE
@@ -533,9 +677,7 @@ int launch_combine_pos(const DevTables& d, double* out, cudaStream_t stream) {
     case 2: return combine_pos_launch<2, LF_POS_NTILE>(d, out, cfg, stream);
     case 3: return combine_pos_launch<3, LF_POS_NTILE>(d, out, cfg, stream);
     case 4: return combine_pos_launch<4, LF_POS_NTILE>(d, out, cfg, stream);
-    case 5: return combine_pos_launch<5, LF_POS_NTILE>(d, out, cfg, stream);
-    case 6: return combine_pos_launch<6, LF_POS_NTILE>(d, out, cfg, stream);
-    default: return combine_pos_launch<7, LF_POS_NTILE>(d, out, cfg, stream);
+    default: return -1; // more terms: the split B operands would not fit the register file
     }
 }
 
