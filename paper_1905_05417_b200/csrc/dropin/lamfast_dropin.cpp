@@ -11,9 +11,11 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 #include <ostream>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 
 #include "lamfast/lamfast_b200.hpp"
 #include "lamfast_cuda.h"
@@ -40,12 +42,44 @@ void ok(int status) {
         rethrow(status);
 }
 
-/// A value-initialised std::vector of n elements for a CSR array (the
-/// reference's StiffnessMatrix type).  Large arrays ask for transparent huge
-/// pages between the allocation and the zero fill, so the first touch faults
-/// 2 MB pages instead of 4 KB ones: the zero fill of C4's 23 GB is what a
-/// fresh std::vector result costs, and with 4 KB faults it took 8.4 s on the
-/// GPU box against 0.41 s for the whole device assembly into pinned memory.
+/// Sets v's size to n <= capacity() without touching the elements (T trivial):
+/// the three-pointer representation {begin, end, end of storage} that
+/// libstdc++ and libc++ share is read back against data() / size() /
+/// capacity() first, and anything else leaves v alone (false).  This is the
+/// library-specific "resize without initialisation" that std::vector itself
+/// does not offer before a whole-array overwrite.
+template <class T>
+bool setSizeUninitialized(std::vector<T>& v, std::size_t n) {
+    static_assert(std::is_trivial_v<T>, "elements are overwritten, never constructed");
+    struct Rep {
+        T *begin, *end, *cap;
+    };
+    if constexpr (sizeof(std::vector<T>) != sizeof(Rep)) {
+        return false;
+    } else {
+        if (n > v.capacity() || v.data() == nullptr)
+            return false;
+        Rep r;
+        std::memcpy(&r, static_cast<const void*>(&v), sizeof r);
+        if (r.begin != v.data() || r.end != r.begin + v.size() || r.cap != r.begin + v.capacity())
+            return false;
+        r.end = r.begin + n;
+        std::memcpy(static_cast<void*>(&v), &r, sizeof r);
+        return v.size() == n;
+    }
+}
+
+/// A std::vector of n elements for a CSR array (the reference's
+/// StiffnessMatrix type) that the assembly call overwrites completely.
+/// - Large arrays ask for transparent huge pages between the allocation and
+///   the first touch, so the pages fault in as 2 MB instead of 4 KB: with 4 KB
+///   faults a fresh C4 result (23 GB) cost 8.4 s on the GPU box against 0.41 s
+///   for the whole device assembly into pinned memory.
+/// - The elements are not zero-filled (setSizeUninitialized): a value-
+///   initialising resize is a single-threaded 23 GB fill (2.7 of the 3.2 s a
+///   drop-in C4 call took with it), while the assembly's host threads touch
+///   and fill disjoint ranges in parallel.  LAMFAST_DROPIN_ZERO_FILL=1, or a
+///   standard library with another vector layout, takes the plain resize.
 template <class T>
 std::vector<T> csrArray(std::size_t n) {
     std::vector<T> v;
@@ -56,6 +90,12 @@ std::vector<T> csrArray(std::size_t n) {
         const std::uintptr_t a = (p + huge - 1) & ~(huge - 1), e = (p + n * sizeof(T)) & ~(huge - 1);
         if (e > a)
             madvise(reinterpret_cast<void*>(a), e - a, MADV_HUGEPAGE); // advisory: ignored where THP is off
+        static const bool zero_fill = [] {
+            const char* e = std::getenv("LAMFAST_DROPIN_ZERO_FILL");
+            return e && *e && *e != '0';
+        }();
+        if (!zero_fill && setSizeUninitialized(v, n))
+            return v;
     }
     v.resize(n);
     return v;

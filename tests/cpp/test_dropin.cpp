@@ -246,6 +246,21 @@ static void gpuCases() {
                        paganoLayup({0.0, 0.6, 1.2})};
         CHECK(frobeniusRelDiff(assembleFast(s), assembleStandard(s)) <= 1e-12);
     }
+    // arrays past the drop-in's large-array threshold (std::vectors sized without a
+    // zero fill, filled by the assembly's host threads): every element is written
+    {
+        ProblemSetup s{TensorProductSpace(KnotVector::uniform(2, 24), KnotVector::uniform(2, 24),
+                                          KnotVector::uniform(2, 8)),
+                       flat(1.0, 1.0, 0.1), paganoLayup({0.0, 1.5707963267948966, 0.7, -0.7, 0.0, 0.3, 1.2, 0.0})};
+        const StiffnessMatrix fa = assembleFast(s), st = assembleStandard(s);
+        CHECK(fa.nnz() > (std::int64_t(8) << 20) / 4); // the column array alone is past 8 MB
+        CHECK(fa.rowOffsets().size() == static_cast<std::size_t>(fa.dim()) + 1);
+        CHECK(fa.rowOffsets().back() == fa.nnz());
+        CHECK(fa.colIndices().size() == static_cast<std::size_t>(fa.nnz()));
+        CHECK(fa.values().size() == static_cast<std::size_t>(fa.nnz()));
+        CHECK(frobeniusRelDiff(fa, st) <= 1e-12);
+        CHECK(fa.symmetryRelError() <= 1e-12);
+    }
     // test_fast.cpp:335-352 work accounting
     {
         std::vector<double> angles;
