@@ -355,6 +355,73 @@ int eform_min_terms() {
     return 8;
 }
 
+/// Smallest term count that takes the slot form of the per-term combine
+/// (k_combine_slots; affine geometry, every thickness row seeing <= 3 terms).
+/// From 5 terms on the per-term kernel drops to one entry per thread
+/// (profiles/r2_coef_threshold.txt: C4 3.75 ms at 5 terms, 4.16 at 7) and the
+/// coefficient form takes 4.0 ms; the slot form keeps two entries per thread
+/// for any term count.  LAMFAST_SLOTS_MIN_TERMS overrides it (A/B runs, tests).
+int slots_min_terms() {
+    if (const char* e = std::getenv("LAMFAST_SLOTS_MIN_TERMS"))
+        return std::max(1, std::atoi(e));
+    return 5;
+}
+
+/// Slot schedule of the slot form: for every thickness row (absolute i_t) the
+/// term each of the n register slots holds, -1 where the row does not use the
+/// slot.  A row's terms are those switched on (lam_on) in a layer of a cell
+/// under its function.  Rows are walked in order; a term already in a slot
+/// keeps it, a new term takes the least recently used slot the row does not
+/// need, so with one element per ply each ply's term is formed once.
+/// Returns n (2 or 3), or 0 when some row sees more than max_slots terms.
+int slot_schedule(const lfb::Setup& s, int max_slots, std::vector<int32_t>& sched) {
+    const int T = s.n_terms, nt = s.n_t;
+    const int L = T > 0 ? static_cast<int>(s.lam_on.size() / static_cast<std::size_t>(T)) : 0;
+    std::vector<std::vector<int>> row_terms(static_cast<std::size_t>(nt));
+    {
+        std::vector<uint8_t> on(static_cast<std::size_t>(nt) * T, 0);
+        for (std::size_t c = 0; c < s.cell_first.size(); ++c)
+            for (int t = 0; t < T; ++t)
+                if (s.lam_on[static_cast<std::size_t>(t) * L + s.cell_layer[c]])
+                    for (int i = s.cell_first[c]; i <= s.cell_first[c] + s.kt.p && i < nt; ++i)
+                        on[static_cast<std::size_t>(i) * T + t] = 1;
+        for (int i = 0; i < nt; ++i)
+            for (int t = 0; t < T; ++t)
+                if (on[static_cast<std::size_t>(i) * T + t])
+                    row_terms[static_cast<std::size_t>(i)].push_back(t);
+    }
+    std::size_t most = 0;
+    for (const auto& r : row_terms)
+        most = std::max(most, r.size());
+    if (most > static_cast<std::size_t>(max_slots))
+        return 0;
+    const int n = most <= 2 ? 2 : 3;
+    sched.assign(static_cast<std::size_t>(nt) * n, -1);
+    std::vector<int> cur(static_cast<std::size_t>(n), -1), used(static_cast<std::size_t>(n), -1); // term, last row
+    for (int i = 0; i < nt; ++i) {
+        const auto& terms = row_terms[static_cast<std::size_t>(i)];
+        for (int t : terms) // terms that stay where they are
+            for (int k = 0; k < n; ++k)
+                if (cur[static_cast<std::size_t>(k)] == t)
+                    used[static_cast<std::size_t>(k)] = i;
+        for (int t : terms) {
+            if (std::find(cur.begin(), cur.end(), t) != cur.end())
+                continue;
+            int best = -1;
+            for (int k = 0; k < n; ++k)
+                if (used[static_cast<std::size_t>(k)] != i &&
+                    (best < 0 || used[static_cast<std::size_t>(k)] < used[static_cast<std::size_t>(best)]))
+                    best = k;
+            cur[static_cast<std::size_t>(best)] = t; // most <= n: a free slot exists
+            used[static_cast<std::size_t>(best)] = i;
+        }
+        for (int k = 0; k < n; ++k)
+            if (used[static_cast<std::size_t>(k)] == i)
+                sched[static_cast<std::size_t>(i) * n + k] = cur[static_cast<std::size_t>(k)];
+    }
+    return n;
+}
+
 /// Output-range fields of the device tables (row offsets slab-local).
 void set_range(const lfb::Range& r, lfb::DevTables& d) {
     d.t0 = r.t0;
@@ -451,11 +518,18 @@ void plan_init(lf_plan* plan, const lf_problem* p, int backend, int device, void
         if (!d.affine) {
             d.Pg = ar.alloc<double>(static_cast<std::size_t>(d.n_terms) * 4 * static_cast<std::size_t>(d.E));
             alloc_element_scratch(ar, d, d.n_terms);
+        } else if (std::vector<int32_t> sched;
+                   d.n_terms >= slots_min_terms() && (d.n_slots = slot_schedule(s, 3, sched)) > 0) {
+            // slot form of the per-term combine: rows see <= 3 terms each
+            d.slot_term = ar.upload(sched);
         } else if (d.n_terms >= eform_min_terms()) {
             // coefficient form of the combine: one pass for any term count
             d.Etab = ar.alloc<double>(static_cast<std::size_t>(std::max<long long>(1, d.n_pairs)) * lfb::kEPair);
         }
     }
+    if (backend != LF_BACKEND_STANDARD && std::getenv("LAMFAST_DEBUG_FORM"))
+        std::fprintf(stderr, "lamfast: combine form %s (%d terms, %d slots)\n",
+                     d.n_slots > 0 ? "slots" : d.Etab ? "coefficient" : "per-term", d.n_terms, d.n_slots);
     // graph replay for launch-bound plans (<= 64M values, or any standard plan:
     // its colour launches are many and short)
     const char* ge = std::getenv("LAMFAST_GRAPH");

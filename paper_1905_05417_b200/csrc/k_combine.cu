@@ -202,6 +202,226 @@ void combine_one(const DevTables& d, double* out, int pass, int t_chunk, int sta
 }
 
 // ---------------------------------------------------------------------------
+// Slot form of the per-term combine (affine geometry, 5 or more terms whose
+// thickness rows each see at most NS of them: laminates with many distinct
+// ply angles and one element per ply).  The per-term kernel above keeps the
+// entry's P of EVERY term in registers, so it drops to one entry per thread
+// at 5 terms and needs a read-modify-write pass per 8 terms; but a thickness
+// row only touches the terms of the plies under its function.  Here a thread
+// keeps the entry's nine term-independent 2D integrals I_xy and NS register
+// slots of P; the host assigns each row's terms to slots (capi.cu,
+// slot_schedule: a term keeps its slot while consecutive rows use it), and a
+// slot is refilled from I_xy and C~ of its new term (9 FMA) only when its
+// term changes -- once per ply.  Rows then run the same k-outer bodies as the
+// per-term kernel with NS "terms": 4 FMA per value and active slot, one
+// pass, two entries per thread for any term count.
+template <int NS>
+__device__ __forceinline__ void stage_rows_slots(const DevTables& d, int it0, int nrow, int lt_max, RowInfo* s_row,
+                                                 unsigned char* s_kr, int* s_term, double4* s_w, int tid,
+                                                 int nthreads) {
+    const long long pre0 = __ldg(d.pre_t + d.t0);
+    const long long preW = __ldg(d.pre_t + d.w_t0); // W / Wmask index base (the plan's rows)
+    const long long nine_S = 9 * d.S_s;
+    const int T = d.n_terms;
+    for (int rr = tid; rr < nrow; rr += nthreads) {
+        const int it = it0 + rr;
+        const long long pfx = __ldg(d.pre_t + it) - preW;
+        const int lt = __ldg(d.len_t + it);
+        unsigned m = 0;
+#pragma unroll
+        for (int sl = 0; sl < NS; ++sl) {
+            const int t = __ldg(d.slot_term + (long long)it * NS + sl);
+            int lo = 255, hi = 0;
+            if (t >= 0) {
+                // Wmask: one word per (pass of 8 terms, pair), k_prepare_affine
+                const unsigned* mk = d.Wmask + (long long)(t / 8) * d.n_pairs + pfx;
+                const unsigned bit = 1u << (t % 8);
+                for (int k = 0; k < lt; ++k)
+                    if (__ldg(mk + k) & bit) {
+                        lo = min(lo, k);
+                        hi = k + 1;
+                    }
+            }
+            if (hi > 0)
+                m |= 1u << sl;
+            s_kr[(rr * NS + sl) * 2] = (unsigned char)(lo == 255 ? 0 : lo);
+            s_kr[(rr * NS + sl) * 2 + 1] = (unsigned char)hi;
+            s_term[rr * NS + sl] = t;
+        }
+        s_row[rr].base = nine_S * (__ldg(d.pre_t + it) - pre0) - d.out_base;
+        s_row[rr].lt = lt | row_edge(d, it) << 8;
+        s_row[rr].mask = m;
+    }
+    const int nw = nrow * lt_max * NS;
+    for (int idx = tid; idx < nw; idx += nthreads) {
+        const int rr = idx / (lt_max * NS);
+        const int k = (idx / NS) % lt_max;
+        const int sl = idx % NS;
+        const int it = it0 + rr;
+        const int t = __ldg(d.slot_term + (long long)it * NS + sl);
+        double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
+        if (t >= 0 && k < __ldg(d.len_t + it)) {
+            const long long q = __ldg(d.pre_t + it) - preW + k;
+            const double2* src = reinterpret_cast<const double2*>(d.W + ((q * T) + t) * 4);
+            const double2 lo2 = __ldg(src), hi2 = __ldg(src + 1);
+            v = make_double4(lo2.x, lo2.y, hi2.x, hi2.y);
+        }
+        s_w[idx] = v;
+    }
+}
+
+template <int NS, int EPT, int BT, int MINB, bool CT_SMEM>
+__global__ void __launch_bounds__(BT, MINB) k_combine_slots(const DevTables d, double* __restrict__ out, int t_chunk,
+                                                            int stage_rows, int lt_max) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    RowInfo* s_row = reinterpret_cast<RowInfo*>(smem_raw);
+    unsigned char* s_kr = smem_raw + stage_rows * sizeof(RowInfo); // [row][NS][2]
+    int* s_term = reinterpret_cast<int*>(smem_raw + ((stage_rows * (sizeof(RowInfo) + 2 * NS) + 15) & ~15));
+    double4* s_w = reinterpret_cast<double4*>(
+        smem_raw + ((((stage_rows * (sizeof(RowInfo) + 2 * NS) + 15) & ~15) + stage_rows * NS * sizeof(int) + 31) & ~31));
+    // C~ of every term behind the weights (the slot refills read it; from
+    // global memory the refill's loads were the top stall), when it fits
+    double* s_ct = reinterpret_cast<double*>(s_w + (size_t)stage_rows * lt_max * NS);
+    if constexpr (CT_SMEM)
+        for (int idx = threadIdx.x; idx < d.n_terms * 81; idx += BT)
+            s_ct[idx] = __ldg(d.Ct + idx); // visible after the first staging barrier below
+
+    double I[EPT][9]; // I00 I01 I10 I11 | I02 I12 | I20 I21 | I22 (x, y: 0 d/du, 1 d/dv, 2 value)
+    int ab[EPT];
+    double P[EPT][NS][4];
+    double* o_thread[EPT];
+    long long A[EPT];
+    int B[EPT];
+    bool live[EPT], in_s0[EPT], in_s1[EPT];
+#pragma unroll
+    for (int x = 0; x < EPT; ++x) {
+        // the entry slots of combine_body: a warp's EPT stores per (row, k) are adjacent 256-byte runs
+        const long long e = (long long)blockIdx.x * BT * EPT + (threadIdx.x >> 5) * 32 * EPT + x * 32 +
+                            (threadIdx.x & 31);
+        live[x] = e < d.E;
+        const long long ec = live[x] ? e : d.E - 1;
+        int is = __ldg(d.blk_is + ec / kBlock);
+        while (__ldg(d.es_pre + is + 1) <= ec)
+            ++is;
+        const long long ebase = __ldg(d.es_pre + is);
+        const int r = (int)(ec - ebase);
+        in_s0[x] = is >= d.s0;
+        in_s1[x] = is < d.s1;
+        const int iu = is % d.nu, iv = is / d.nu;
+        const int Lu = __ldg(d.len_u + iu), Lv = __ldg(d.len_v + iv);
+        B[x] = 3 * Lu * Lv;
+        const int a = r / B[x];
+        const int rem = r - a * B[x];
+        A[x] = ebase + (long long)a * B[x];
+        o_thread[x] = out + (long long)rem;
+        const int sp = rem / 3, b = rem - 3 * sp;
+        const int sv = sp / Lu, su = sp - sv * Lu;
+        ab[x] = 3 * a + b;
+        const double* U = d.U + ((long long)iu * d.bu + su) * 4;
+        const double* V = d.V + ((long long)iv * d.bv + sv) * 4;
+        const double u0 = __ldg(U), u1 = __ldg(U + 1), u2 = __ldg(U + 2), u3 = __ldg(U + 3);
+        const double v0 = __ldg(V), v1 = __ldg(V + 1), v2 = __ldg(V + 2), v3 = __ldg(V + 3);
+        I[x][0] = u3 * v0, I[x][1] = u2 * v1, I[x][2] = u1 * v2, I[x][3] = u0 * v3;
+        I[x][4] = u2 * v0, I[x][5] = u0 * v2, I[x][6] = u1 * v0, I[x][7] = u0 * v1, I[x][8] = u0 * v0;
+#pragma unroll
+        for (int sl = 0; sl < NS; ++sl)
+#pragma unroll
+            for (int f = 0; f < 4; ++f)
+                P[x][sl][f] = 0.0;
+    }
+    int tag[NS]; // term whose P each slot holds (block-uniform)
+#pragma unroll
+    for (int sl = 0; sl < NS; ++sl)
+        tag[sl] = -1;
+
+    const int it_begin = d.t0 + blockIdx.y * t_chunk;
+    const int it_end = min(d.t1, it_begin + t_chunk);
+    bool any_live = false;
+#pragma unroll
+    for (int x = 0; x < EPT; ++x)
+        any_live |= live[x];
+
+    for (int it0 = it_begin; it0 < it_end; it0 += stage_rows) {
+        const int nrow = min(stage_rows, it_end - it0);
+        if (it0 != it_begin)
+            __syncthreads();
+        stage_rows_slots<NS>(d, it0, nrow, lt_max, s_row, s_kr, s_term, s_w, threadIdx.x, BT);
+        __syncthreads();
+        if (!any_live)
+            continue;
+        for (int rr = 0; rr < nrow; ++rr) {
+            const RowInfo ri = s_row[rr];
+            const int lt = ri.lt & 0xff, edge = ri.lt >> 8;
+            // slots whose term changes with this row: P of the new term from I_xy and C~ (affine_p's sums)
+#pragma unroll
+            for (int sl = 0; sl < NS; ++sl) {
+                const int t = s_term[rr * NS + sl];
+                if (t >= 0 && t != tag[sl]) {
+                    tag[sl] = t;
+#pragma unroll
+                    for (int x = 0; x < EPT; ++x) {
+                        double c[9];
+#pragma unroll
+                        for (int q = 0; q < 9; ++q)
+                            c[q] = CT_SMEM ? s_ct[t * 81 + 9 * q + ab[x]] : __ldg(d.Ct + t * 81 + 9 * q + ab[x]);
+                        P[x][sl][0] = c[0] * I[x][0] + c[1] * I[x][1] + c[3] * I[x][2] + c[4] * I[x][3];
+                        P[x][sl][1] = c[2] * I[x][4] + c[5] * I[x][5];
+                        P[x][sl][2] = c[6] * I[x][6] + c[7] * I[x][7];
+                        P[x][sl][3] = c[8] * I[x][8];
+                    }
+                }
+            }
+            bool lv[EPT];
+#pragma unroll
+            for (int x = 0; x < EPT; ++x)
+                lv[x] = edge ? live[x] && (!(edge & 1) || in_s0[x]) && (!(edge & 2) || in_s1[x]) : live[x];
+            double* o[EPT];
+#pragma unroll
+            for (int x = 0; x < EPT; ++x)
+                o[x] = o_thread[x] + ri.base + (long long)lt * A[x];
+#pragma unroll
+            for (int x = 0; x < EPT; ++x)
+                LF_CHECK(!lv[x] || (o[x] >= out && o[x] + (long long)(lt - 1) * B[x] < out + d.nnz_slab));
+            const double4* w = s_w + rr * lt_max * NS;
+            const unsigned char* kr = s_kr + rr * NS * 2;
+            switch (lt) {
+            case 1: row_dispatch<NS, EPT, 1, false>(P, w, ri.mask, kr, o, B, lv); break;
+            case 2: row_dispatch<NS, EPT, 2, false>(P, w, ri.mask, kr, o, B, lv); break;
+            case 3: row_dispatch<NS, EPT, 3, false>(P, w, ri.mask, kr, o, B, lv); break;
+            case 4: row_dispatch<NS, EPT, 4, false>(P, w, ri.mask, kr, o, B, lv); break;
+            case 5: row_dispatch<NS, EPT, 5, false>(P, w, ri.mask, kr, o, B, lv); break;
+            case 7: row_dispatch<NS, EPT, 7, false>(P, w, ri.mask, kr, o, B, lv); break;
+            default: combine_row_dyn<NS, EPT, false>(P, w, lt, ri.mask, o, B, lv); break;
+            }
+        }
+    }
+}
+
+template <int NS>
+int combine_slots_launch(const DevTables& d, double* out, int t_chunk, int lt_max, unsigned nchunk, cudaStream_t s) {
+    constexpr int EPT = 2, BT = 256, MINB = 2;
+    int stage_rows = (int)((24 * 1024) / ((size_t)lt_max * NS * sizeof(double4)));
+    stage_rows = std::max(1, std::min(stage_rows, t_chunk));
+    const size_t head = ((stage_rows * (sizeof(RowInfo) + 2 * NS) + 15) & ~size_t(15)) + (size_t)stage_rows * NS * sizeof(int);
+    size_t smem = ((head + 31) & ~size_t(31)) + (size_t)stage_rows * lt_max * NS * sizeof(double4);
+    const size_t ct_bytes = (size_t)d.n_terms * 81 * sizeof(double);
+    const int ct_smem = smem + ct_bytes <= 96 * 1024; // two blocks per SM keep their shared memory
+    if (ct_smem)
+        smem += ct_bytes;
+    const dim3 grid((unsigned)((d.E + (long long)BT * EPT - 1) / ((long long)BT * EPT)), nchunk);
+    auto launch = [&](auto kern) {
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, BT, smem, s>>>(d, out, t_chunk, stage_rows, lt_max);
+    };
+    if (ct_smem)
+        launch(k_combine_slots<NS, EPT, BT, MINB, true>);
+    else
+        launch(k_combine_slots<NS, EPT, BT, MINB, false>);
+    return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // Coefficient form of K4 for affine geometry with many operator terms
 // (decompose_angles: 5 per material; laminates with > 8 distinct angles).
 // With a constant frame every term's P is linear in the same nine 2D
@@ -489,6 +709,14 @@ int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t st
         if (launches)
             ++*launches;
         return (int)cudaGetLastError();
+    }
+    if (d.n_slots > 0 && d.slot_term && d.affine) {
+        // slot form: one pass for any term count (rows see <= n_slots terms each)
+        const int rc = d.n_slots <= 2 ? combine_slots_launch<2>(d, out, t_chunk, lt_max, nchunk, stream)
+                                      : combine_slots_launch<3>(d, out, t_chunk, lt_max, nchunk, stream);
+        if (launches)
+            ++*launches;
+        return rc;
     }
     for (int pass = 0; pass < d.n_passes; ++pass) {
         const int nterm = std::min(8, d.n_terms - 8 * pass);

@@ -95,6 +95,11 @@ struct DevTables {
     double* Ks;
     int ks_batch;
     const int* spt_first_h; // host copy of spt_first (the launcher's batch bounds)
+    // slot form of the per-term combine (k_combine_slots): per thickness row
+    // (absolute i_t) the term held by each of n_slots register slots, -1: slot
+    // not used by the row; n_slots = 0: per-term / coefficient forms
+    const int* slot_term;
+    int n_slots;
     // output range: the functions f = i_t * ns + i_s in [f0, f1), covering
     // thickness rows [t0, t1) -- row t0 from in-plane function s0, row t1 - 1
     // up to s1 (exclusive).  Entry (it, is, ...) of the range is written at

@@ -132,24 +132,32 @@ def test_c3_standard_slab_rows_are_bitwise_rows_of_the_full_matrix(gpu):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("case", ["decompose C4", "16 angles C3"])
+@pytest.mark.parametrize("case", ["decompose C4", "16 angles C3", "16 angles C3 slots", "6 angles C4 slots"])
 def test_full_size_coefficient_form_matches_per_term_form_and_oracle(gpu, oracle, monkeypatch, case):
-    """The coefficient form of the combine (default from 8 operator terms) at
-    full BASELINE size: C4 with decompose_angles (10 terms) and C3 with 16
-    distinct angles, against the per-term form with its read-modify-write
-    passes (LAMFAST_EFORM_MIN_TERMS=1000) on the device over the whole matrix
-    (same pattern; values within 1e-12 of max|K|), and the first, middle and
-    last thickness rows against the oracle."""
+    """The one-pass forms of the combine for many operator terms at full
+    BASELINE size -- the coefficient form (default from 8 terms where rows see
+    more than 3: C4 with decompose_angles, 10 terms; forced for C3 with 16
+    distinct angles) and the slot form (default from 5 terms where every row
+    sees <= 3: C3 with 16 distinct angles, C4 with 6) -- against the per-term
+    form with its read-modify-write passes (both thresholds at 1000) on the
+    device over the whole matrix (same pattern; values within 1e-12 of
+    max|K|), and the first, middle and last thickness rows against the
+    oracle."""
     import torch
+    slots = case.endswith("slots")
     if case == "decompose C4":
         prob = P.baseline_config("C4").replace(decompose_angles=True)
     else:
-        base = P.baseline_config("C3")
-        prob = base.replace(layers=[(P.baseline_orthotropic(), -1.5 + 3.0 * (k % 16) / 16)
+        base = P.baseline_config(case.split()[2])
+        n = int(case.split()[0])
+        prob = base.replace(layers=[(P.baseline_orthotropic(), -1.5 + 3.0 * (k % n) / n)
                                     for k in range(len(base.layers))])
+    one_pass = {"LAMFAST_SLOTS_MIN_TERMS": "5" if slots else "1000", "LAMFAST_EFORM_MIN_TERMS": "8"}
     vals = {}
     for mode in ("8", "1000"):
-        monkeypatch.setenv("LAMFAST_EFORM_MIN_TERMS", mode)
+        env = one_pass if mode == "8" else {"LAMFAST_SLOTS_MIN_TERMS": "1000", "LAMFAST_EFORM_MIN_TERMS": "1000"}
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
         plan = gpu.Plan(prob, "fast", 0)
         v = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
         plan.assemble(v.data_ptr())
@@ -161,7 +169,8 @@ def test_full_size_coefficient_form_matches_per_term_form_and_oracle(gpu, oracle
     assert float((vals["8"] - vals["1000"]).abs().max()) <= 1e-12 * scale
     del vals
     torch.cuda.empty_cache()
-    monkeypatch.setenv("LAMFAST_EFORM_MIN_TERMS", "8")
+    for k, v in one_pass.items():
+        monkeypatch.setenv(k, v)
     terms = oracle.fast_terms(prob)
     nt = prob.n_t
     for t in (0, nt // 2, nt - 1):

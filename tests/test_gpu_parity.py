@@ -141,6 +141,7 @@ def test_coefficient_form_matches_oracle(gpu, oracle, monkeypatch, min_terms, ca
     with C0 thickness knots, and a row slab cut inside a thickness row."""
     import torch
     monkeypatch.setenv("LAMFAST_EFORM_MIN_TERMS", min_terms)
+    monkeypatch.setenv("LAMFAST_SLOTS_MIN_TERMS", "1000")  # not the slot form (test_slot_form_matches_oracle)
     if case == "16 angles":
         prob = P.plate(2, 6, 5, [(P.baseline_orthotropic(), -1.5 + 0.2 * k) for k in range(16)], thickness=0.2)
     elif case == "decompose C2":
@@ -171,6 +172,77 @@ def test_coefficient_form_matches_oracle(gpu, oracle, monkeypatch, min_terms, ca
         plan.close()
         return
     got = gpu.assemble_fast(prob)
+    assert_csr_match(got.astuple(), oracle.assemble(prob, "fast"), RTOL)
+
+
+@pytest.mark.parametrize("min_terms", ["5", "1"])
+@pytest.mark.parametrize("case", ["16 angles", "6 angles C1", "mixed C0", "C2", "thick p3", "slab", "too many"])
+def test_slot_form_matches_oracle(gpu, oracle, monkeypatch, capfd, min_terms, case):
+    """The slot form of the per-term combine (k_combine_slots: the entry's nine
+    2D integrals and 2-3 register slots of P, refilled when a row brings a new
+    term; default from 5 terms where every thickness row sees <= 3, forced for
+    every term count with LAMFAST_SLOTS_MIN_TERMS=1) against the oracle:
+    16 distinct angles with one C0 element per ply (2 slots), 6 angles on C1
+    thickness splines (three plies under a function, 3 slots), mixed degrees
+    and materials, BASELINE C2, cubic thickness, a row slab cut inside
+    thickness rows, and a laminate whose rows see more than 3 terms (the plan
+    must fall back to another form)."""
+    import torch
+    monkeypatch.setenv("LAMFAST_SLOTS_MIN_TERMS", min_terms)
+    monkeypatch.setenv("LAMFAST_DEBUG_FORM", "1")
+    ortho = P.baseline_orthotropic()
+    expect = "slots"
+    if case == "16 angles":
+        prob = P.plate(2, 6, 5, [(ortho, -1.5 + 0.2 * k) for k in range(16)], thickness=0.2)
+    elif case == "6 angles C1":
+        prob = P.plate(2, 5, 4, [(ortho, -1.2 + 0.5 * (k % 6)) for k in range(9)], thickness=0.2,
+                       thickness_knots=P.uniform_knots(2, 9))
+    elif case == "mixed C0":
+        prob = P.LaminateProblem(
+            degree_u=2, degree_v=3, degree_t=2, knots_u=P.uniform_knots(2, 3),
+            knots_v=P.uniform_knots(3, 2), knots_t=P.c0_knots(2, 3), interfaces=P.equal_interfaces(3),
+            layers=[(ortho, 0.0), (P.isotropic(0.5, 0.3), 0.0), (ortho, 0.6)])
+        if min_terms == "5":
+            expect = "per-term"  # 3 terms: below the default threshold
+    elif case == "C2":
+        prob = P.baseline_config("C2")
+        if min_terms == "5":
+            expect = "per-term"
+    elif case == "thick p3":
+        prob = P.plate(2, 4, 4, [(ortho, 0.3 * k) for k in range(7)], thickness=0.3, thickness_degree=3,
+                       thickness_knots=P.c0_knots(3, 7))
+    elif case == "too many":
+        # cubic C2 thickness splines: four plies under a function, each at its own angle
+        prob = P.plate(2, 4, 4, [(ortho, 0.25 * k) for k in range(8)], thickness=0.2, thickness_degree=3,
+                       thickness_knots=P.uniform_knots(3, 8))
+        expect = "coefficient" if min_terms == "5" else None  # 8 terms: coefficient form by default
+    else:
+        prob = P.plate(2, 6, 5, [(ortho, -1.5 + 0.2 * k) for k in range(12)], thickness=0.2)
+        ns = prob.n_s
+        f0, f1 = ns + 5, 4 * ns - 7
+        plan = gpu.Plan(prob, "fast", 0, f_begin=f0, f_end=f1)
+        assert "combine form slots" in capfd.readouterr().err
+        rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
+        cols = torch.empty(plan.nnz, dtype=torch.int32, device="cuda")
+        vals = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
+        plan.build_pattern(rp.data_ptr(), cols.data_ptr())
+        plan.assemble(vals.data_ptr())
+        plan.synchronize()
+        trp, tc, tv = oracle.assemble(prob, "fast", 1, 4)
+        a, e = 3 * (f0 - ns), 3 * (f1 - ns)
+        want = (trp[a:e + 1] - trp[a], tc[trp[a]:trp[e]], tv[trp[a]:trp[e]])
+        assert_csr_match((rp.cpu().numpy(), cols.cpu().numpy(), vals.cpu().numpy()), want, RTOL)
+        plan.close()
+        return
+    capfd.readouterr()
+    got = gpu.assemble_fast(prob)
+    err = capfd.readouterr().err
+    if expect == "slots":
+        assert "combine form slots" in err, err
+    elif expect is not None:
+        assert f"combine form {expect}" in err and "combine form slots" not in err, err
+    else:
+        assert "combine form slots" not in err, err
     assert_csr_match(got.astuple(), oracle.assemble(prob, "fast"), RTOL)
 
 
