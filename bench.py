@@ -698,9 +698,10 @@ def measure_standard(args, prob, device, stream):
 def measure_many_terms(args, prob, device, stream, hbm):
     """Side measurement: the same workload with many operator terms, one
     launch whatever the term count: AssemblyOptions.decompose_angles (five
-    terms per material, ten under a vertex function: the coefficient form of
-    the combine, 9 FMA per value) and the orthotropic ply at 16 distinct
-    angles (two terms under any function: the slot form, k_combine_slots).
+    basis terms per material; on this affine map they are summed per distinct
+    ply configuration before the combine, so the per-term kernel runs with the
+    direct form's three terms) and the orthotropic ply at 16 distinct angles
+    (two terms under any function: the slot form, k_combine_slots).
     Device time per step (CUDA events) and the combine's HBM fraction, values
     in the same precomputed pattern."""
     import torch
@@ -718,7 +719,7 @@ def measure_many_terms(args, prob, device, stream, hbm):
         out[name] = {"ms_per_step": t["ms_per_step"], "value": plan.nnz / (t["ms_per_step"] / 1e3),
                      "unit": "nnz/s", "operator_builds": plan.stats().operator_builds,
                      "launches_per_step": plan.launch_count,
-                     "form": "coefficient (k_combine_coef)" if name == "decompose_angles" else "slots (k_combine_slots)",
+                     "form": plan.combine_form,
                      "combine_ms": k_ms, "combine_frac_of_hbm": plan.nnz * 8 / (k_ms / 1e3) / 1e9 / hbm}
         plan.close()
         del vals

@@ -208,6 +208,10 @@ int lf_plan_build_pattern(lf_plan* plan, int64_t* d_row_ptr, int32_t* d_cols);
 int lf_plan_assemble(lf_plan* plan, double* d_values);
 /* Kernels one lf_plan_assemble enqueues, and the dominant kernel's name. */
 int lf_plan_launch_count(const lf_plan* plan);
+/* Form of the combine kernel the plan chose for its operator terms (fast and
+ * Voigt-free backends): 0 per-term (k_combine), 1 slots (k_combine_slots),
+ * 2 coefficient (k_combine_coef); -1 for a standard plan or a null plan. */
+int lf_plan_combine_form(const lf_plan* plan);
 /* CUDA events around the dominant (combine) kernel of the most recent
  * lf_plan_assemble; cumulative milliseconds and launch count since reset. */
 int lf_plan_kernel_time(lf_plan* plan, int reset, double* ms_total, int64_t* launches);

@@ -115,6 +115,7 @@ SIGNATURES = [
     ("lf_plan_build_pattern", c_int, [c_void_p, c_void_p, c_void_p]),
     ("lf_plan_assemble", c_int, [c_void_p, c_void_p]),
     ("lf_plan_launch_count", c_int, [c_void_p]),
+    ("lf_plan_combine_form", c_int, [c_void_p]),
     ("lf_plan_kernel_time", c_int, [c_void_p, c_int, _P(c_double), _P(c_int64)]),
     ("lf_plan_stats", c_int, [c_void_p, _P(Stats)]),
     ("lf_plan_synchronize", c_int, [c_void_p]),

@@ -315,6 +315,11 @@ class Plan:
     def launch_count(self) -> int:
         return self.lib.lf_plan_launch_count(self.handle)
 
+    @property
+    def combine_form(self) -> str:
+        """Combine kernel form the plan chose: per-term, slots or coefficient."""
+        return {0: "per-term", 1: "slots", 2: "coefficient"}.get(self.lib.lf_plan_combine_form(self.handle), "none")
+
     def kernel_time(self, reset: bool = False) -> Tuple[float, int]:
         ms, n = c_double(), c_int64()
         abi.check(self.lib.lf_plan_kernel_time(self.handle, 1 if reset else 0, byref(ms), byref(n)))

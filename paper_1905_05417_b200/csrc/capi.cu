@@ -922,6 +922,11 @@ int lf_plan_assemble(lf_plan* plan, double* d_values) {
 }
 
 int lf_plan_launch_count(const lf_plan* plan) { return plan ? plan->launches : -1; }
+int lf_plan_combine_form(const lf_plan* plan) {
+    if (!plan || plan->setup.backend == LF_BACKEND_STANDARD)
+        return -1;
+    return plan->d.n_slots > 0 ? 1 : plan->d.Etab ? 2 : 0;
+}
 
 int lf_plan_kernel_time(lf_plan* plan, int reset, double* ms_total, int64_t* launches) {
     return guarded([&] {

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 namespace lfb {
@@ -780,6 +781,7 @@ Setup buildSetup(const lf_problem& p, int backend, int t0, int t1) {
 
     // operator terms
     const int nc_cfg = s.layup.n_configs;
+    int stat_terms = -1; // terms the work counters report when they differ from n_terms
     if (backend == LF_BACKEND_FAST && p.decompose_angles) {
         std::vector<int> groups; // representative layer per distinct constants, config order
         for (int c = 0; c < nc_cfg; ++c) {
@@ -810,6 +812,45 @@ Setup buildSetup(const lf_problem& p, int backend, int t0, int t1) {
                     s.lam_on[t * static_cast<std::size_t>(L) + static_cast<std::size_t>(l)] = 1;
                 }
             }
+        }
+        stat_terms = s.n_terms; // the five builds per material the option stands for (fast.cpp:285-336)
+        const char* fold = std::getenv("LAMFAST_FOLD_DECOMPOSE");
+        if (s.affine && !(fold && fold[0] == '0')) {
+            // Constant frame: the in-plane operators are never built (P is
+            // formed in registers from the 1D integrals and C~), and every
+            // term's contribution is linear in its contraction table.  The
+            // five basis tables of a material are therefore summed per
+            // distinct (material, angle) configuration with that ply's
+            // multipliers BEFORE the combine,
+            //     table(config) = sum_k w_k(angle) basis_k(material),
+            // which leaves one term per configuration -- the direct form's
+            // term count, with the decomposition's arithmetic for the ply
+            // stiffness -- instead of ten terms under a vertex function.
+            std::vector<double> tab(static_cast<std::size_t>(nc_cfg) * 81, 0.0);
+            std::vector<double> lam(static_cast<std::size_t>(nc_cfg) * L, 0.0);
+            std::vector<uint8_t> on(static_cast<std::size_t>(nc_cfg) * L, 0);
+            for (int c = 0; c < nc_cfg; ++c) {
+                const lf_layer& rep = p.layers[s.layup.rep_layer[static_cast<std::size_t>(c)]];
+                std::size_t g = 0;
+                while (g < groups.size() && !sameConstants(p.layers[groups[g]].constants, rep.constants))
+                    ++g;
+                const double cs = std::cos(rep.angle), sn = std::sin(rep.angle);
+                const double w[5] = {1.0, cs * cs * cs * cs, cs * cs * cs * sn, cs * cs, cs * sn};
+                for (int k = 0; k < 5; ++k)
+                    for (int e = 0; e < 81; ++e)
+                        tab[static_cast<std::size_t>(c) * 81 + e] +=
+                            w[k] * s.term_table[(5 * g + static_cast<std::size_t>(k)) * 81 + e];
+                for (int l = 0; l < L; ++l)
+                    if (s.layup.layer_config[static_cast<std::size_t>(l)] == c &&
+                        s.layer_active[static_cast<std::size_t>(l)]) {
+                        lam[static_cast<std::size_t>(c) * L + static_cast<std::size_t>(l)] = 1.0;
+                        on[static_cast<std::size_t>(c) * L + static_cast<std::size_t>(l)] = 1;
+                    }
+            }
+            s.n_terms = nc_cfg;
+            s.term_table = std::move(tab);
+            s.lam = std::move(lam);
+            s.lam_on = std::move(on);
         }
     } else {
         s.n_terms = nc_cfg;
@@ -857,9 +898,10 @@ Setup buildSetup(const lf_problem& p, int backend, int t0, int t1) {
         s.stats.qpoint_visits = per_build * static_cast<int64_t>(nc) * s.nqt;
         s.stats.frame_evaluations = per_build;
     } else {
-        s.stats.qpoint_visits = per_build * s.n_terms;
-        s.stats.frame_evaluations = per_build * s.n_terms;
-        s.stats.operator_builds = s.n_terms;
+        const int counted = stat_terms >= 0 ? stat_terms : s.n_terms;
+        s.stats.qpoint_visits = per_build * counted;
+        s.stats.frame_evaluations = per_build * counted;
+        s.stats.operator_builds = counted;
     }
     if (!standard && s.n_terms == 0)
         raise(LF_ERR_INVALID_ARGUMENT, "combineOperators: no operator terms");

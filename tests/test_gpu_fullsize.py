@@ -132,30 +132,36 @@ def test_c3_standard_slab_rows_are_bitwise_rows_of_the_full_matrix(gpu):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("case", ["decompose C4", "16 angles C3", "16 angles C3 slots", "6 angles C4 slots"])
+@pytest.mark.parametrize("case", ["decompose C4", "decompose C4 folded", "16 angles C3", "16 angles C3 slots",
+                                  "6 angles C4 slots"])
 def test_full_size_coefficient_form_matches_per_term_form_and_oracle(gpu, oracle, monkeypatch, case):
     """The one-pass forms of the combine for many operator terms at full
     BASELINE size -- the coefficient form (default from 8 terms where rows see
     more than 3: C4 with decompose_angles, 10 terms; forced for C3 with 16
     distinct angles) and the slot form (default from 5 terms where every row
-    sees <= 3: C3 with 16 distinct angles, C4 with 6) -- against the per-term
+    sees <= 3: C3 with 16 distinct angles, C4 with 6), and C4's
+    decompose_angles terms folded per ply configuration (the default on affine
+    maps: three terms, per-term kernel) -- against the unfolded per-term
     form with its read-modify-write passes (both thresholds at 1000) on the
     device over the whole matrix (same pattern; values within 1e-12 of
     max|K|), and the first, middle and last thickness rows against the
     oracle."""
     import torch
     slots = case.endswith("slots")
-    if case == "decompose C4":
+    folded = case.endswith("folded")
+    if case.startswith("decompose C4"):
         prob = P.baseline_config("C4").replace(decompose_angles=True)
     else:
         base = P.baseline_config(case.split()[2])
         n = int(case.split()[0])
         prob = base.replace(layers=[(P.baseline_orthotropic(), -1.5 + 3.0 * (k % n) / n)
                                     for k in range(len(base.layers))])
-    one_pass = {"LAMFAST_SLOTS_MIN_TERMS": "5" if slots else "1000", "LAMFAST_EFORM_MIN_TERMS": "8"}
+    one_pass = {"LAMFAST_SLOTS_MIN_TERMS": "5" if slots else "1000", "LAMFAST_EFORM_MIN_TERMS": "8",
+                "LAMFAST_FOLD_DECOMPOSE": "1" if folded else "0"}
     vals = {}
     for mode in ("8", "1000"):
-        env = one_pass if mode == "8" else {"LAMFAST_SLOTS_MIN_TERMS": "1000", "LAMFAST_EFORM_MIN_TERMS": "1000"}
+        env = one_pass if mode == "8" else {"LAMFAST_SLOTS_MIN_TERMS": "1000", "LAMFAST_EFORM_MIN_TERMS": "1000",
+                                            "LAMFAST_FOLD_DECOMPOSE": "0"}
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         plan = gpu.Plan(prob, "fast", 0)

@@ -142,6 +142,7 @@ def test_coefficient_form_matches_oracle(gpu, oracle, monkeypatch, min_terms, ca
     import torch
     monkeypatch.setenv("LAMFAST_EFORM_MIN_TERMS", min_terms)
     monkeypatch.setenv("LAMFAST_SLOTS_MIN_TERMS", "1000")  # not the slot form (test_slot_form_matches_oracle)
+    monkeypatch.setenv("LAMFAST_FOLD_DECOMPOSE", "0")  # keep the five terms per material (test_decompose_angles_folded)
     if case == "16 angles":
         prob = P.plate(2, 6, 5, [(P.baseline_orthotropic(), -1.5 + 0.2 * k) for k in range(16)], thickness=0.2)
     elif case == "decompose C2":
@@ -244,6 +245,37 @@ def test_slot_form_matches_oracle(gpu, oracle, monkeypatch, capfd, min_terms, ca
     else:
         assert "combine form slots" not in err, err
     assert_csr_match(got.astuple(), oracle.assemble(prob, "fast"), RTOL)
+
+
+@pytest.mark.parametrize("case", ["C2 with interlayers", "16 angles", "one ply active"])
+def test_decompose_angles_folded_on_affine_maps(gpu, oracle, case):
+    """decompose_angles on a constant frame: the five basis tables of a
+    material are summed per distinct ply configuration before the combine
+    (setup.cpp), so the combine runs with the direct form's terms (per-term
+    kernel for <= 4 configurations, slot form above) while the work counters
+    still report five builds per material (fast.cpp:285-336).  Values against
+    the oracle's decomposed assembly and against the direct assembly."""
+    ortho = P.baseline_orthotropic()
+    if case == "C2 with interlayers":
+        base = P.baseline_config("C2")
+        prob = base.replace(layers=[(P.isotropic(0.5, 0.3), 0.0) if k % 3 == 1 else l
+                                    for k, l in enumerate(base.layers)])
+        form, builds = "per-term", 10
+    elif case == "16 angles":
+        prob = P.plate(2, 6, 5, [(ortho, -1.5 + 0.2 * k) for k in range(16)], thickness=0.2)
+        form, builds = "slots", 5
+    else:
+        prob = P.plate(2, 5, 5, [(ortho, 0.4 * k) for k in range(6)], thickness=0.2).replace(active_layers=[2])
+        form, builds = "slots", 5
+    dec_prob = prob.replace(decompose_angles=True)
+    plan = gpu.Plan(dec_prob, "fast", 0)
+    assert plan.combine_form == form
+    assert plan.stats().operator_builds == builds
+    plan.close()
+    dec = gpu.assemble_fast(dec_prob)
+    assert dec.stats.operator_builds == builds
+    assert_csr_match(dec.astuple(), oracle.assemble(dec_prob, "fast"), RTOL)
+    assert csr_rel_diff(dec.astuple(), gpu.assemble_fast(prob).astuple()) <= 1e-12
 
 
 def test_stats_counters(gpu):
