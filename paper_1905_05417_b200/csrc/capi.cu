@@ -776,9 +776,20 @@ static bool host_columns_enabled() {
 /// (offset 0 = the first entry of f0), cut into equal-nnz pieces.
 struct HostColumns {
     std::vector<std::thread> th;
-    HostColumns(const lfb::Setup& s, int64_t f0, int64_t f1, int32_t* cols) {
+    /// background: the columns of a whole one-shot call, written while its
+    /// values cross PCIe into the same host memory.  They only have to finish
+    /// before the copy does, and every extra thread takes memory bandwidth
+    /// from the DMA: on the 16-core GPU box 4 threads give 273 ms per C4 call
+    /// (a plain D2H of the same bytes: 271 ms), 16 threads 288 ms, 2 threads
+    /// 403 ms (profiles/r2_e2e_col_threads.txt).  A quarter of the cores, at
+    /// least 4.  Otherwise (a chunk's columns that its sink waits for, or a
+    /// plain lf_pattern_columns call): up to 16 threads.
+    HostColumns(const lfb::Setup& s, int64_t f0, int64_t f1, int32_t* cols, bool background = false) {
         const int64_t base = lfb::functionOffset(s, f0), total = lfb::functionOffset(s, f1) - base;
-        const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        const unsigned cores = std::max(1u, std::thread::hardware_concurrency());
+        unsigned hw = background ? std::min(16u, std::max(4u, cores / 4)) : std::min(16u, cores);
+        if (const char* e = std::getenv("LAMFAST_COL_THREADS")) // A/B knob: host threads writing the columns
+            hw = static_cast<unsigned>(std::max(1, std::atoi(e)));
         const unsigned nt = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(hw, total >> 22)));
         std::vector<int64_t> cut{f0};
         for (unsigned t = 1; t < nt; ++t) { // first function whose offset reaches t/nt of the entries
@@ -1145,7 +1156,7 @@ static void run_one_shot(lf_plan& plan, OneShotStreams& st, int64_t chunk_nnz, c
     // cross PCIe (sinks)
     std::unique_ptr<HostColumns> hc, slot_hc[2];
     if (host_cols && !out.sink)
-        hc = std::make_unique<HostColumns>(s, s.f0, s.f1, out.cols);
+        hc = std::make_unique<HostColumns>(s, s.f0, s.f1, out.cols, /*background=*/true);
     plan_prepare(&plan, cs);
     auto finish = [&](std::size_t j) { // host side of chunk j (staged only)
         const int b = static_cast<int>(j % 2);
