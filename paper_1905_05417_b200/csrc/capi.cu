@@ -784,10 +784,18 @@ struct HostColumns {
     /// 403 ms (profiles/r2_e2e_col_threads.txt).  A quarter of the cores, at
     /// least 4.  Otherwise (a chunk's columns that its sink waits for, or a
     /// plain lf_pattern_columns call): up to 16 threads.
-    HostColumns(const lfb::Setup& s, int64_t f0, int64_t f1, int32_t* cols, bool background = false) {
+    /// chunk: one chunk's columns into its pinned staging slot while the
+    /// chunk's values cross PCIe (lf_assemble_stream); they must be there when
+    /// the chunk's copy ends.  3/8 of the cores, at least 6: C5's 203 GB CSR
+    /// streams in 2.39 s with 6 threads, 2.45 s with 8, 2.56 s with 16
+    /// (profiles/r2_c5_stream_threads.txt).
+    HostColumns(const lfb::Setup& s, int64_t f0, int64_t f1, int32_t* cols, bool background = false,
+                bool chunk = false) {
         const int64_t base = lfb::functionOffset(s, f0), total = lfb::functionOffset(s, f1) - base;
         const unsigned cores = std::max(1u, std::thread::hardware_concurrency());
-        unsigned hw = background ? std::min(16u, std::max(4u, cores / 4)) : std::min(16u, cores);
+        unsigned hw = background ? std::min(16u, std::max(4u, cores / 4))
+                      : chunk    ? std::min(16u, std::max(6u, 3 * cores / 8))
+                                 : std::min(16u, cores);
         if (const char* e = std::getenv("LAMFAST_COL_THREADS")) // A/B knob: host threads writing the columns
             hw = static_cast<unsigned>(std::max(1, std::atoi(e)));
         const unsigned nt = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(hw, total >> 22)));
@@ -1220,8 +1228,9 @@ static void run_one_shot(lf_plan& plan, OneShotStreams& st, int64_t chunk_nnz, c
         }
         CK(cudaEventRecord(drained[b], xs));
         if (host_cols && out.sink) // this chunk's columns, into its staging slot, while its values cross PCIe
-            slot_hc[b] = std::make_unique<HostColumns>(s, r.f0, r.f1,
-                                                       reinterpret_cast<int32_t*>(static_cast<char*>(stg->slot[b]) + so_cols));
+            slot_hc[b] = std::make_unique<HostColumns>(
+                s, r.f0, r.f1, reinterpret_cast<int32_t*>(static_cast<char*>(stg->slot[b]) + so_cols),
+                /*background=*/false, /*chunk=*/true);
         if (staged && k >= 1)
             finish(k - 1);
     }
