@@ -156,6 +156,18 @@ int lf_layup_configs(const lf_problem* p, int32_t* n_configs, int32_t* layer_con
                      double* config_stiffness);
 
 /* ---- closed-form CSR pattern ----------------------------------------- */
+/* Host-side view of the operator terms a plan of this problem combines (no
+ * device work): their number -- distinct ply configurations, or five per
+ * material with decompose_angles on a non-affine map; on an affine map the
+ * decomposition's basis tables are summed per configuration first --, their
+ * 81-entry contraction tables (tables, [n_terms][81], may be NULL), and the
+ * slot schedule of the slot form of the combine: n_slots = 2 or 3 and, per
+ * thickness function i_t, the term each slot holds or -1 (slot_term,
+ * [n_t][n_slots] with room for 3 per row, may be NULL); n_slots = 0 when some
+ * thickness row sees more than three terms.  fast.cpp:285-336 (the terms),
+ * fast.cpp:241-258 (which terms a thickness pair sums). */
+int lf_operator_terms(const lf_problem* p, int backend, int32_t* n_terms, double* tables, int32_t* n_slots,
+                      int32_t* slot_term);
 /* Matrix dimension (3 x number of functions) and number of stored entries
  * produced by `backend` (the standard backend drops thickness spans whose
  * cells are all masked by active_layers, assembly.cpp:184-186). */

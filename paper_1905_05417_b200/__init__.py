@@ -9,7 +9,7 @@ Python host layer over that ABI; see DESIGN.md.
 from .abi import LamfastError, library
 from .assembler import (CSR, Plan, assemble_fast, assemble_range, assemble_slab, assemble_stream, reference_bilinear, assemble_standard, assemble_voigt_free,
                         assemble_with, combine_operators, compute_inplane_operators,
-                        compute_thickness_operators, device_csr_stats, pattern_columns, pattern_size, release_memory,
+                        compute_thickness_operators, device_csr_stats, operator_terms, pattern_columns, pattern_size, release_memory,
                         slab_bounds, slab_bounds_functions)
 from .problem import (LaminateProblem, baseline_config, baseline_orthotropic, c0_knots,
                       cube_problem, equal_interfaces, isotropic, pagano, plate, sizes,
@@ -20,7 +20,7 @@ __all__ = [
     "assemble_slab", "assemble_range", "assemble_stream", "slab_bounds_functions",
     "LamfastError", "library", "CSR", "Plan", "assemble_fast", "assemble_standard",
     "assemble_voigt_free", "assemble_with", "combine_operators", "compute_inplane_operators",
-    "compute_thickness_operators", "device_csr_stats", "pattern_columns", "pattern_size", "release_memory", "slab_bounds",
+    "compute_thickness_operators", "device_csr_stats", "operator_terms", "pattern_columns", "pattern_size", "release_memory", "slab_bounds",
     "LaminateProblem", "baseline_config", "baseline_orthotropic", "c0_knots", "cube_problem",
     "equal_interfaces", "isotropic", "pagano", "plate", "sizes", "uniform_knots",
 ]

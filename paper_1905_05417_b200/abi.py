@@ -100,6 +100,7 @@ SIGNATURES = [
                               _P(c_double)]),
     ("lf_contraction_table", c_int, [_P(c_double), c_double, _P(c_double)]),
     ("lf_layup_configs", c_int, [_P(Problem), _P(c_int32), _P(c_int32), _P(c_double)]),
+    ("lf_operator_terms", c_int, [_P(Problem), c_int, _P(c_int32), _P(c_double), _P(c_int32), _P(c_int32)]),
     ("lf_pattern_size", c_int, [_P(Problem), c_int, _P(c_int64), _P(c_int64)]),
     ("lf_pattern_columns", c_int, [_P(Problem), c_int, c_int64, c_int64, _P(c_int32), _P(c_int64)]),
     ("lf_slab_bounds", c_int, [_P(Problem), c_int, c_int, c_int, _P(c_int32), _P(c_int32),

@@ -60,6 +60,23 @@ def pattern_size(prob: LaminateProblem, backend: str = "fast") -> Tuple[int, int
     return dim.value, nnz.value
 
 
+def operator_terms(prob: LaminateProblem, backend: str = "fast"):
+    """Host-side view of the operator terms a plan combines (lf_operator_terms):
+    (tables [n_terms, 81], slot_term [n_t, n_slots] or None when a thickness
+    row sees more than three terms)."""
+    lib = abi.library()
+    c = prob.to_c()
+    n, ns = c_int32(), c_int32()
+    abi.check(lib.lf_operator_terms(byref(c), abi.BACKENDS[backend], byref(n), None, byref(ns), None))
+    tables = np.empty((n.value, 81), dtype=np.float64)
+    sched = np.full((prob.n_t, 3), -1, dtype=np.int32)
+    abi.check(lib.lf_operator_terms(byref(c), abi.BACKENDS[backend], byref(n), _dp(tables), byref(ns),
+                                    sched.ctypes.data_as(POINTER(c_int32))))
+    if ns.value == 0:
+        return tables, None
+    return tables, sched.reshape(-1)[:prob.n_t * ns.value].reshape(prob.n_t, ns.value).copy()
+
+
 def pattern_columns(prob: LaminateProblem, f_begin: int = 0, f_end: int = -1, backend: str = "fast") -> np.ndarray:
     """Host-written CSR columns of the functions [f_begin, f_end)
     (lf_pattern_columns: the closed form k_pattern_cols writes on the device)."""

@@ -841,6 +841,24 @@ int lf_pattern_size(const lf_problem* p, int backend, int64_t* dim, int64_t* nnz
     });
 }
 
+int lf_operator_terms(const lf_problem* p, int backend, int32_t* n_terms, double* tables, int32_t* n_slots,
+                      int32_t* slot_term) {
+    return guarded([&] {
+        if (!p || !n_terms || !n_slots)
+            raise(LF_ERR_INVALID_ARGUMENT, "lf_operator_terms: null argument");
+        if (backend == LF_BACKEND_STANDARD)
+            raise(LF_ERR_INVALID_ARGUMENT, "lf_operator_terms: the standard backend has no operator terms");
+        const lfb::Setup s = lfb::buildSetup(*p, backend, 0, -1);
+        *n_terms = s.n_terms;
+        if (tables)
+            std::copy(s.term_table.begin(), s.term_table.end(), tables);
+        std::vector<int32_t> sched;
+        *n_slots = slot_schedule(s, 3, sched);
+        if (slot_term && *n_slots > 0)
+            std::copy(sched.begin(), sched.end(), slot_term);
+    });
+}
+
 int lf_pattern_columns(const lf_problem* p, int backend, int64_t f_begin, int64_t f_end, int32_t* cols,
                        int64_t* nnz) {
     return guarded([&] {

@@ -245,3 +245,83 @@ def test_host_pattern_columns_match_oracle(oracle, case):
     else:
         want = cols[rp[3 * f0]:rp[3 * f1]]
     assert got.dtype == np.int32 and np.array_equal(got, want)
+
+
+def _active_terms_per_row(prob, n_terms_of_layer):
+    """Terms under each thickness function: the layers of the cells (knot span
+    x ply) inside the function's support (fast.cpp:241-258)."""
+    kt = np.asarray(prob.knots_t, dtype=float)
+    p = prob.degree_t
+    itf = np.asarray(prob.interfaces, dtype=float)
+    n_t = len(kt) - p - 1
+    rows = [set() for _ in range(n_t)]
+    spans = [j for j in range(p, len(kt) - p - 1) if kt[j + 1] > kt[j]]
+    for j in spans:
+        for l in range(len(itf) - 1):
+            lo, hi = max(kt[j], itf[l]), min(kt[j + 1], itf[l + 1])
+            if hi - lo > 1e-14:
+                for i in range(j - p, j + 1):
+                    rows[i].add(n_terms_of_layer[l])
+    return rows
+
+
+@pytest.mark.parametrize("case", ["C2", "16 angles C0", "6 angles C1", "8 angles C2 cubic"])
+def test_slot_schedule_of_the_combine(case):
+    """lf_operator_terms' slot schedule (host logic of k_combine_slots): every
+    term under a thickness function holds exactly one slot in that row, no
+    other term is scheduled, and a term keeps its slot over consecutive rows
+    (one refill per ply with one C0 element per ply)."""
+    ortho = P.baseline_orthotropic()
+    if case == "C2":
+        prob, want_slots = P.baseline_config("C2"), 2
+    elif case == "16 angles C0":
+        prob, want_slots = P.plate(2, 3, 3, [(ortho, -1.5 + 0.2 * k) for k in range(16)]), 2
+    elif case == "6 angles C1":
+        prob = P.plate(2, 3, 3, [(ortho, -1.2 + 0.5 * (k % 6)) for k in range(9)], thickness_knots=P.uniform_knots(2, 9))
+        want_slots = 3
+    else:
+        prob = P.plate(2, 3, 3, [(ortho, 0.25 * k) for k in range(8)], thickness_degree=3,
+                       thickness_knots=P.uniform_knots(3, 8))
+        want_slots = None
+    tables, sched = lf.operator_terms(prob)
+    seen = []  # configurations in first-appearance order (materials.cpp:203-224), as distinct_configs counts
+    term_of_layer = []
+    for layer in prob.layers:
+        if layer not in seen:
+            seen.append(layer)
+        term_of_layer.append(seen.index(layer))
+    assert tables.shape == (prob.distinct_configs(), 81)
+    if want_slots is None:
+        assert sched is None
+        return
+    assert sched.shape == (prob.n_t, want_slots)
+    want = _active_terms_per_row(prob, term_of_layer)
+    refills = 0
+    held = [-1] * want_slots
+    for i in range(prob.n_t):
+        got = [t for t in sched[i] if t >= 0]
+        assert sorted(got) == sorted(want[i]), (i, got, want[i])
+        for k, t in enumerate(sched[i]):
+            if t >= 0 and held[k] != t:
+                held[k] = int(t)
+                refills += 1
+    if case == "16 angles C0":
+        assert refills == len(prob.layers)  # one per ply
+
+
+def test_decompose_angles_terms_fold_per_configuration_on_affine_maps():
+    """setup.cpp: with a constant frame the five basis tables per material are
+    summed per ply configuration, table(config) = sum_k w_k(angle) basis_k,
+    which equals the directly rotated configuration's table to rounding; a
+    non-affine map keeps five terms per material (fast.cpp:285-336)."""
+    base = P.baseline_config("C2")
+    prob = base.replace(layers=[(P.isotropic(0.5, 0.3), 0.0) if k % 3 == 1 else l for k, l in enumerate(base.layers)])
+    direct, _ = lf.operator_terms(prob)
+    folded, sched = lf.operator_terms(prob.replace(decompose_angles=True))
+    assert direct.shape == folded.shape == (3, 81) and sched is not None
+    assert np.abs(folded - direct).max() <= 1e-13 * np.abs(direct).max()
+    lx, ly = prob.geometry[0], prob.geometry[1]
+    skew = prob.replace(geometry_kind=1, geometry=(0, 0, 0, lx, 0.05 * ly, 0.0, -0.05 * lx, ly, 0.0,
+                                                   1.02 * lx, 1.03 * ly, 0.01), decompose_angles=True)
+    unfolded, _ = lf.operator_terms(skew)
+    assert unfolded.shape == (10, 81)
