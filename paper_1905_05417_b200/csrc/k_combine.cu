@@ -384,6 +384,16 @@ __global__ void __launch_bounds__(BT, MINB) k_combine_slots(const DevTables d, d
                 LF_CHECK(!lv[x] || (o[x] >= out && o[x] + (long long)(lt - 1) * B[x] < out + d.nnz_slab));
             const double4* w = s_w + rr * lt_max * NS;
             const unsigned char* kr = s_kr + rr * NS * 2;
+#ifndef LF_SLOTS_MASKED_LTS
+#define LF_SLOTS_MASKED_LTS 8 // bit L set: two-slot rows with L_t = L take the branch-free bodies; bubble rows
+                              // only (profiles/r2_slots_masked.txt: C4 16 angles 2.73 -> 2.67 ms, also L_t = 5: 2.72)
+#endif
+            if constexpr (NS == 2 && LF_SLOTS_MASKED_LTS != 0) {
+                if (((LF_SLOTS_MASKED_LTS >> 5) & 1) && lt == 5 && row_masked<NS, EPT, 5>(ri.mask, P, w, o, B, lv))
+                    continue;
+                if (((LF_SLOTS_MASKED_LTS >> 3) & 1) && lt == 3 && row_masked<NS, EPT, 3>(ri.mask, P, w, o, B, lv))
+                    continue;
+            }
             switch (lt) {
             case 1: row_dispatch<NS, EPT, 1, false>(P, w, ri.mask, kr, o, B, lv); break;
             case 2: row_dispatch<NS, EPT, 2, false>(P, w, ri.mask, kr, o, B, lv); break;
