@@ -49,17 +49,27 @@ plan.synchronize()
 st = lf.device_csr_stats(plan.rows, rp.data_ptr(), cols.data_ptr(), vals.data_ptr())
 out.append(st["fro_sq"])
 plan.close()
-# coefficient-form combine (12 terms) on a function range cut inside thickness rows
+# many-term combines (12 terms) on a function range cut inside thickness rows: the slot form
+# (default: two terms under any function), the coefficient form, and the slot form with three
+# slots (C1 thickness splines: three plies under a function)
 many12 = P.plate(2, 6, 5, [(P.baseline_orthotropic(), -1.5 + 0.2 * k) for k in range(12)], thickness=0.2)
-plan = lf.Plan(many12, "fast", 0, f_begin=many12.n_s + 5, f_end=4 * many12.n_s - 7)
-rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
-cols = torch.empty(plan.nnz, dtype=torch.int32, device="cuda")
-vals = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
-plan.build_pattern(rp.data_ptr(), cols.data_ptr())
-plan.assemble(vals.data_ptr())
-plan.synchronize()
-out.append(float(vals.sum()))
-plan.close()
+many_c1 = P.plate(2, 5, 4, [(P.baseline_orthotropic(), -1.2 + 0.5 * (k % 6)) for k in range(9)], thickness=0.2,
+                  thickness_knots=P.uniform_knots(2, 9))
+for prob, env, form in ((many12, {}, "slots"), (many12, {"LAMFAST_SLOTS_MIN_TERMS": "1000"}, "coefficient"),
+                        (many_c1, {}, "slots")):
+    os.environ.update(env)
+    plan = lf.Plan(prob, "fast", 0, f_begin=prob.n_s + 5, f_end=4 * prob.n_s - 7)
+    for k in env:
+        os.environ.pop(k)
+    assert plan.combine_form == form, (plan.combine_form, form)
+    rp = torch.empty(plan.rows + 1, dtype=torch.int64, device="cuda")
+    cols = torch.empty(plan.nnz, dtype=torch.int32, device="cuda")
+    vals = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
+    plan.build_pattern(rp.data_ptr(), cols.data_ptr())
+    plan.assemble(vals.data_ptr())
+    plan.synchronize()
+    out.append(float(vals.sum()))
+    plan.close()
 # a BASELINE-size plan (C3): the large-slab pattern kernel (16 entries per thread) and the
 # 4-term combine with the branch-free bodies
 c3 = P.baseline_config("C3")
