@@ -278,6 +278,19 @@ def test_decompose_angles_folded_on_affine_maps(gpu, oracle, case):
     assert csr_rel_diff(dec.astuple(), gpu.assemble_fast(prob).astuple()) <= 1e-12
 
 
+def test_slot_form_voigt_free_backend(gpu, oracle):
+    """The Voigt-free backend (contraction tables from the bracket fit,
+    voigt_free.cpp:142-298) runs the same combine kernels: 16 distinct angles
+    take the slot form there too."""
+    prob = P.plate(2, 5, 4, [(P.baseline_orthotropic(), -1.5 + 0.2 * k) for k in range(16)], thickness=0.2)
+    plan = gpu.Plan(prob, "voigt_free", 0)
+    assert plan.combine_form == "slots"
+    plan.close()
+    got = gpu.assemble_with("voigt_free", prob)
+    assert_csr_match(got.astuple(), oracle.assemble(prob, "voigt_free"), RTOL)
+    assert csr_rel_diff(got.astuple(), gpu.assemble_fast(prob).astuple()) <= 1e-12
+
+
 def test_stats_counters(gpu):
     """test_fast.cpp:335-352 work accounting."""
     angles = [0.0 if l % 2 == 0 else 1.5707963267948966 for l in range(32)]
