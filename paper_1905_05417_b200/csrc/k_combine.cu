@@ -51,6 +51,13 @@ __device__ __forceinline__ void combine_body(const DevTables& d, double* __restr
         const int rem = r - a * B[x];
         A[x] = ebase + (long long)a * B[x];
         o_thread[x] = out + (long long)rem;
+#ifdef LF_STORE_ONLY_NOP // diagnostic: no P at all (the store pattern at the occupancy the launch bounds allow)
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+#pragma unroll
+            for (int f = 0; f < 4; ++f)
+                P[x][t][f] = 0.0;
+#else
         if constexpr (AFFINE) {
             const int s = rem / 3, b = rem - 3 * (rem / 3);
             const int sv = s / Lu, su = s - sv * Lu;
@@ -62,6 +69,7 @@ __device__ __forceinline__ void combine_body(const DevTables& d, double* __restr
                 for (int f = 0; f < 4; ++f)
                     P[x][t][f] = __ldg(d.Pg + ((long long)(t_first + t) * 4 + f) * d.E + ec);
         }
+#endif
     }
 
     const int it_begin = d.t0 + blockIdx.y * t_chunk;
