@@ -13,6 +13,24 @@ namespace lfb {
 
 namespace {
 
+// block -> (entry block, row chunk).  The row chunks run fastest in the
+// launch order (grid x = chunk) where the entry blocks fit grid y: the blocks
+// in flight then cover every chunk of a narrow entry window instead of one
+// chunk of a wide one, which the store pattern likes better (C3 1.314 ->
+// 1.275 ms, C4 2.50 -> 2.47 ms, profiles/r2_grid_order.txt).
+#define LF_BLOCK_ENTRY (d.grid_swap ? blockIdx.y : blockIdx.x)
+#define LF_BLOCK_CHUNK (d.grid_swap ? blockIdx.x : blockIdx.y)
+
+/// grid of `nblk` entry blocks x `nchunk` row chunks, and the order flag for the kernel
+inline dim3 combine_grid(long long nblk, unsigned nchunk, DevTables& d) {
+#ifdef LF_NO_GRID_SWAP
+    d.grid_swap = 0;
+#else
+    d.grid_swap = nblk <= 65535 ? 1 : 0;
+#endif
+    return d.grid_swap ? dim3(nchunk, (unsigned)nblk) : dim3((unsigned)nblk, nchunk);
+}
+
 template <int NT, int EPT, bool AFFINE, bool ACCUM, int BT>
 __device__ __forceinline__ void combine_body(const DevTables& d, double* __restrict__ out, int pass, int t_chunk,
                                              int stage_rows, int lt_max) {
@@ -33,7 +51,7 @@ __device__ __forceinline__ void combine_body(const DevTables& d, double* __restr
         // entry of slot x: e = blockIdx*256*EPT + warp*32*EPT + x*32 + lane, so
         // a warp's EPT stores per (row, k) are adjacent 256-byte runs (these
         // warp-contiguous slots measured C4 2.79 -> 2.66 ms against strided ones)
-        const long long e = (long long)blockIdx.x * BT * EPT + (threadIdx.x >> 5) * 32 * EPT + x * 32 +
+        const long long e = (long long)LF_BLOCK_ENTRY * BT * EPT + (threadIdx.x >> 5) * 32 * EPT + x * 32 +
                             (threadIdx.x & 31);
         live[x] = e < d.E;
         const long long ec = live[x] ? e : d.E - 1;
@@ -72,7 +90,7 @@ __device__ __forceinline__ void combine_body(const DevTables& d, double* __restr
 #endif
     }
 
-    const int it_begin = d.t0 + blockIdx.y * t_chunk;
+    const int it_begin = d.t0 + LF_BLOCK_CHUNK * t_chunk;
     const int it_end = min(d.t1, it_begin + t_chunk);
     bool any_live = false;
 #pragma unroll
@@ -176,11 +194,12 @@ void combine_one_ept(const DevTables& d, double* out, int pass, int t_chunk, int
     constexpr bool bounded = EPT >= 2;
     const size_t smem = ((stage_rows * (sizeof(RowInfo) + 2 * NT) + 31) & ~size_t(31)) +
                         (size_t)stage_rows * lt_max * NT * sizeof(double4);
-    const dim3 grid((unsigned)((d.E + (long long)BT * EPT - 1) / ((long long)BT * EPT)), nchunk);
+    DevTables dl = d;
+    const dim3 grid = combine_grid((d.E + (long long)BT * EPT - 1) / ((long long)BT * EPT), nchunk, dl);
     auto launch = [&](auto kern) {
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<grid, BT, smem, s>>>(d, out, pass, t_chunk, stage_rows, lt_max);
+        kern<<<grid, BT, smem, s>>>(dl, out, pass, t_chunk, stage_rows, lt_max);
     };
     if constexpr (!bounded) {
         if (d.affine)
@@ -304,7 +323,7 @@ __global__ void __launch_bounds__(BT, MINB) k_combine_slots(const DevTables d, d
 #pragma unroll
     for (int x = 0; x < EPT; ++x) {
         // the entry slots of combine_body: a warp's EPT stores per (row, k) are adjacent 256-byte runs
-        const long long e = (long long)blockIdx.x * BT * EPT + (threadIdx.x >> 5) * 32 * EPT + x * 32 +
+        const long long e = (long long)LF_BLOCK_ENTRY * BT * EPT + (threadIdx.x >> 5) * 32 * EPT + x * 32 +
                             (threadIdx.x & 31);
         live[x] = e < d.E;
         const long long ec = live[x] ? e : d.E - 1;
@@ -342,7 +361,7 @@ __global__ void __launch_bounds__(BT, MINB) k_combine_slots(const DevTables d, d
     for (int sl = 0; sl < NS; ++sl)
         tag[sl] = -1;
 
-    const int it_begin = d.t0 + blockIdx.y * t_chunk;
+    const int it_begin = d.t0 + LF_BLOCK_CHUNK * t_chunk;
     const int it_end = min(d.t1, it_begin + t_chunk);
     bool any_live = false;
 #pragma unroll
@@ -426,11 +445,12 @@ int combine_slots_launch(const DevTables& d, double* out, int t_chunk, int lt_ma
     const int ct_smem = smem + ct_bytes <= 96 * 1024; // two blocks per SM keep their shared memory
     if (ct_smem)
         smem += ct_bytes;
-    const dim3 grid((unsigned)((d.E + (long long)BT * EPT - 1) / ((long long)BT * EPT)), nchunk);
+    DevTables dl = d;
+    const dim3 grid = combine_grid((d.E + (long long)BT * EPT - 1) / ((long long)BT * EPT), nchunk, dl);
     auto launch = [&](auto kern) {
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<grid, BT, smem, s>>>(d, out, t_chunk, stage_rows, lt_max);
+        kern<<<grid, BT, smem, s>>>(dl, out, t_chunk, stage_rows, lt_max);
     };
     if (ct_smem)
         launch(k_combine_slots<NS, EPT, BT, MINB, true>);
@@ -687,7 +707,10 @@ int launch_combine(const DevTables& d, double* out, int t_chunk, cudaStream_t st
         // general geometry loads P from HBM once per block: whole-slab chunks
         // (measured C3 bilinear 1.47 -> 1.38 ms); affine P is recomputed, so
         // shorter chunks balance better (profiles/r1_tchunk_sweep.txt)
-        t_chunk = d.affine ? std::min(nt, 48) : nt;
+        // (C5 family, 32 k entry blocks of p = 3 four-term entries: ~100-row chunks amortise the
+        // heavier entry prologue, 193 rows 18.63 -> 17.88 ms, profiles/r2_grid_order.txt; C3 / C4
+        // with 3.7 k entry blocks keep 48)
+        t_chunk = d.affine ? std::min(nt, blocks_x >= 16384 ? 112 : 48) : nt;
         while (!d.affine && t_chunk > 64 && blocks_x * ((nt + t_chunk - 1) / t_chunk) < 148LL * 2 * 4)
             t_chunk = (t_chunk + 1) / 2;
         while (t_chunk > 32 && blocks_x * ((nt + t_chunk - 1) / t_chunk) < 148LL * 2 * 4)

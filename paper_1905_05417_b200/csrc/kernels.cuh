@@ -95,6 +95,8 @@ struct DevTables {
     double* Ks;
     int ks_batch;
     const int* spt_first_h; // host copy of spt_first (the launcher's batch bounds)
+    // combine launches: 1 = grid x runs over the row chunks, y over the entry blocks (k_combine.cu)
+    int grid_swap;
     // slot form of the per-term combine (k_combine_slots): per thickness row
     // (absolute i_t) the term held by each of n_slots register slots, -1: slot
     // not used by the row; n_slots = 0: per-term / coefficient forms
