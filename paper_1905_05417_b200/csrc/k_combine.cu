@@ -26,7 +26,7 @@ inline dim3 combine_grid(long long nblk, unsigned nchunk, DevTables& d) {
 #ifdef LF_NO_GRID_SWAP
     d.grid_swap = 0;
 #else
-    d.grid_swap = nblk <= 65535 ? 1 : 0;
+    d.grid_swap = nblk >= 2048 && nblk <= 65535 ? 1 : 0; // small plans (C2: 473 entry blocks) ran 5% slower swapped
 #endif
     return d.grid_swap ? dim3(nchunk, (unsigned)nblk) : dim3((unsigned)nblk, nchunk);
 }
